@@ -1,0 +1,120 @@
+/* shearlet_b200.h -- C ABI of the B200-native shearlet dec/rec hot path.
+ *
+ * A drop-in for the reference's public C++ API for this path
+ * (/root/reference/proj/core/include/shearlet/...), exported as plain C so any
+ * host (C++, Python ctypes, cgo, JNI) can bind it. Plain pointers and sizes
+ * only; no CUDA, torch or C++ types cross the boundary (streams are void*).
+ *
+ * Conventions (mirroring the reference):
+ *  - row-major grids, last axis fastest, axis 0 the "horizontal" filter-bank
+ *    axis (grid.hpp:12-13, 41);
+ *  - coefficient stacks are contiguous [R][dims...] float64, bands in the
+ *    system's filter order (enumerate_filters_2d/3d, system2d.cpp:59-73,
+ *    system3d.cpp:58-80);
+ *  - forward = unnormalised periodic cross-correlation with each filter:
+ *    band_i = Re IDFT(conj(psi_i) .* DFT(f)) (transform.hpp:27-31);
+ *  - inverse = Re IDFT(sum_i DFT(c_i) .* psi_i / W) (transform.hpp:33-37);
+ *  - hard threshold keeps |x| >= K[scale - j0] * sigma (* RMS_i when scaled),
+ *    lowpass untouched (apps.hpp:31-44, apps.cpp:57-81);
+ *  - every error is an int code (below) mapping 1:1 to the reference's
+ *    exception classes (errors.hpp:9-56); sl_last_error() gives the message.
+ *
+ * "_dev" entry points take device pointers on the handle's device and run on
+ * the given CUDA stream (NULL = legacy default stream); "_host" entry points
+ * take host pointers and include the H2D/D2H copies (synchronous).
+ * A handle owns its device memory; calls on one handle are serialised.
+ */
+#ifndef SHEARLET_B200_H
+#define SHEARLET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sl_status {
+    SL_OK = 0,
+    SL_ERR_GENERIC = 1,          /* shearlet::Error (e.g. residue guard)        */
+    SL_ERR_SHAPE = 2,            /* shearlet::ShapeError                         */
+    SL_ERR_CONFIG = 3,           /* shearlet::ConfigError                        */
+    SL_ERR_DOMAIN = 4,           /* shearlet::DomainError                        */
+    SL_ERR_SINGULAR_FRAME = 5,   /* shearlet::SingularFrameError                 */
+    SL_ERR_UNSUPPORTED_SIZE = 6, /* shearlet::UnsupportedSizeError               */
+    SL_ERR_ASSET = 7,            /* shearlet::AssetError                         */
+    SL_ERR_FORMAT = 8,           /* shearlet::FormatError                        */
+    SL_ERR_CUDA = 20,            /* CUDA runtime failure                         */
+    SL_ERR_INVALID = 22,         /* null handle / bad argument at the ABI        */
+};
+
+typedef struct sl_system sl_system;
+
+/* Library / device queries. */
+const char* sl_version(void);
+const char* sl_last_error(void);
+int sl_device_count(int* count);
+
+/* ---- system construction ------------------------------------------------
+ * Replaces build_system_2d (system2d.hpp:66-69) / build_system_3d
+ * (system3d.hpp:68-71) with ScaleProfile::from_levels(levels, j0)
+ * (filters.hpp:88), QmfPair::maximally_flat_9tap() (filters.hpp:21) and
+ * default_fan_filter() (filters.hpp:58) or FanFilter::impulse()
+ * (impulse_fan != 0, filters.hpp:51).  The filter spectra, W and RMS are
+ * computed on `device`.  shard_lo/shard_hi restrict the handle to bands
+ * [lo, hi) of the full system (multi-GPU shearlet-index sharding); pass 0, -1
+ * for the whole system. */
+int sl_system_create_2d(int rows, int cols, const int* levels, int n_scales, int j0, int full_system,
+                        int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out);
+int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
+                        int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out);
+int sl_system_destroy(sl_system* sys);
+
+/* ---- system queries (ShearletSystem2D/3D members) ------------------------ */
+int sl_ndim(const sl_system* sys, int* ndim, int64_t dims[3]);
+int sl_redundancy(const sl_system* sys, int* R);          /* redundancy(): full system */
+int sl_shard(const sl_system* sys, int* lo, int* hi);      /* bands held by this handle */
+/* index records, 4 x int32 per filter: kind, scale, k1 (2D: shear), k2 (2D: 0);
+ * kinds as FilterKind2D/3D (system2d.hpp:12-16, system3d.hpp:12-17). */
+int sl_index(const sl_system* sys, int32_t* records);
+int sl_filter_norms(const sl_system* sys, double* rms);    /* filter_norms: R doubles */
+int sl_frame_weight(const sl_system* sys, double* w);      /* frame_weight: full grid (host) */
+int sl_frame_bounds(const sl_system* sys, double* A, double* B);
+/* psi_hat_i on the full grid, interleaved (re, im) (filters[i] / filter_freq(i)). */
+int sl_filter_spectrum(sl_system* sys, int i, double* out);
+
+/* ---- hot path, device pointers ------------------------------------------- */
+/* forward(): f [dims] -> coeffs [hi-lo][dims] (this handle's bands). */
+int sl_sheardec_dev(sl_system* sys, const double* f, double* coeffs, void* stream);
+/* forward() + hard_threshold() fused into the dec epilogue. */
+int sl_sheardec_threshold_dev(sl_system* sys, const double* f, double* coeffs, const double* K, int nK,
+                              double sigma, int scale_by_rms, void* stream);
+/* inverse(): coeffs [nbands][dims] -> f [dims]; nbands must equal the
+ * handle's band count (ShapeError otherwise). On a shard the result is that
+ * shard's partial sum (linear in the coefficients; sum over shards = full). */
+int sl_shearrec_dev(sl_system* sys, const double* coeffs, int nbands, double* f, void* stream);
+/* hard_threshold(): in -> out (may alias), nK must equal n_scales. */
+int sl_hard_threshold_dev(sl_system* sys, const double* in, double* out, int nbands, const double* K, int nK,
+                          double sigma, int scale_by_rms, void* stream);
+/* denoise(): inverse(hard_threshold(forward(in))) with the stack kept in the
+ * handle's device scratch. */
+int sl_denoise_dev(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
+                   int scale_by_rms, void* stream);
+
+/* ---- hot path, host pointers (value semantics like the reference) -------- */
+int sl_sheardec_host(sl_system* sys, const double* f, double* coeffs);
+int sl_shearrec_host(sl_system* sys, const double* coeffs, int nbands, double* f);
+int sl_hard_threshold_host(sl_system* sys, const double* in, double* out, int nbands, const double* K, int nK,
+                           double sigma, int scale_by_rms);
+int sl_denoise_host(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
+                    int scale_by_rms);
+
+/* ---- synthetic inputs (phantoms.hpp / apps.hpp generators, host) ---------- */
+int sl_phantom_cartoon(int n, double* out);            /* phantoms::cartoon        */
+int sl_phantom_cartoon_volume(int n, double* out);     /* phantoms::cartoon_volume */
+int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double sigma, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHEARLET_B200_H */

@@ -1,0 +1,152 @@
+"""oracle/gen_golden.py -- TEST INFRASTRUCTURE ONLY.
+
+Generates the committed golden fixtures under tests/golden/ from the
+UNMODIFIED reference library (oracle/_ref/libshearlet_ref.so, built from
+/root/reference by `make -C oracle ref`). Run here, in the container that has
+/root/reference; the GPU box only reads the committed .npz files.
+
+    python oracle/gen_golden.py [--big]
+
+Each fixture stores the inputs (or the recipe to regenerate them with the
+reference's own generators), and the reference's outputs either in full
+(small grids) or as per-band statistics plus a fixed strided sample
+(large grids), so the files stay small.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import ref  # noqa: E402
+from oracle import shearlet_np as O  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden")
+
+
+def sample_idx(n, k=257):
+    """Fixed strided sample of k flat indices in [0, n)."""
+    return (np.arange(k, dtype=np.int64) * 7919) % n
+
+
+def band_stats(bands):
+    flat = bands.reshape(bands.shape[0], -1)
+    return {
+        "band_l2": np.sqrt(np.sum(flat * flat, axis=1)),
+        "band_sum": np.sum(flat, axis=1),
+        "band_sample": flat[:, sample_idx(flat.shape[1])],
+    }
+
+
+def save(name, **kw):
+    os.makedirs(OUT, exist_ok=True)
+    path = os.path.join(OUT, name + ".npz")
+    np.savez_compressed(path, **kw)
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)")
+
+
+def gen_2d_full(name, n, levels, f, j0=0):
+    s = ref.RefSystem2D(n, n, levels, j0=j0)
+    bands = s.forward(f)
+    rec = s.inverse(bands)
+    save(name, f=f, levels=np.array(levels), j0=j0, index=s.index(), filter_norms=s.filter_norms(),
+         frame_weight=s.frame_weight(), bands=bands, rec=rec)
+
+
+def gen_2d_stats(name, n, levels, f, K=None, sigma=None, j0=0):
+    s = ref.RefSystem2D(n, n, levels, j0=j0)
+    bands = s.forward(f)
+    rec = s.inverse(bands)
+    W = s.frame_weight()
+    kw = dict(levels=np.array(levels), j0=j0, index=s.index(), filter_norms=s.filter_norms(),
+              W_min=W.min(), W_max=W.max(), W_sample=W.reshape(-1)[sample_idx(W.size)],
+              f_sum=f.sum(), f_l2=np.sqrt((f * f).sum()),
+              rec_sample=rec.reshape(-1)[sample_idx(rec.size)],
+              rec_relerr=np.linalg.norm(rec - f) / np.linalg.norm(f), **band_stats(bands))
+    if K is not None:
+        thr = s.hard_threshold(bands, K, sigma)
+        kept = np.count_nonzero(thr.reshape(thr.shape[0], -1), axis=1)
+        den = s.inverse(thr)
+        kw.update(K=np.array(K), sigma=sigma, kept=kept,
+                  den_sample=den.reshape(-1)[sample_idx(den.size)], den_sum=den.sum(),
+                  den_l2=np.sqrt((den * den).sum()))
+    save(name, **kw)
+    return s, bands
+
+
+def gen_3d(name, dims, levels, f, K=None, sigma=None, full=False, threads=0):
+    t = time.time()
+    s = ref.RefSystem3D(dims, levels, threads=threads)
+    W = s.frame_weight()
+    kw = dict(dims=np.array(dims), levels=np.array(levels), index=s.index(),
+              filter_norms=s.filter_norms(), W_min=W.min(), W_max=W.max(),
+              W_sample=W.reshape(-1)[sample_idx(W.size)], f_sum=f.sum())
+    print(f"  built {dims} {levels} R={s.R} in {time.time() - t:.1f}s")
+    # a few filters, sampled, to pin the on-the-fly synthesis
+    fi = [0, 1, s.R // 3, s.R // 2, s.R - 1]
+    kw["filter_ids"] = np.array(fi)
+    kw["filter_samples"] = np.stack([s.filter(i).reshape(-1)[sample_idx(W.size)] for i in fi])
+    if K is not None and not full:
+        si = sample_idx(W.size)
+        den, kept, l2, smp = s.denoise_stats(f, K, sigma, si, threads=threads)
+        kw.update(K=np.array(K), sigma=sigma, kept=kept, band_l2=l2, band_sample=smp,
+                  den_sample=den.reshape(-1)[si], den_sum=den.sum(), den_l2=np.sqrt((den * den).sum()))
+    elif full:
+        bands = s.forward(f, threads=threads)
+        rec = s.inverse(bands, threads=threads)
+        kw.update(f=f, bands=bands, rec=rec)
+    else:
+        bands = s.forward(f, threads=threads)
+        rec = s.inverse(bands, threads=threads)
+        kw.update(rec_sample=rec.reshape(-1)[sample_idx(rec.size)],
+                  rec_relerr=np.linalg.norm(rec - f) / np.linalg.norm(f), **band_stats(bands))
+    print(f"  done in {time.time() - t:.1f}s")
+    save(name, **kw)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
+    a = ap.parse_args()
+    if not ref.available():
+        sys.exit("build the reference first: make -C oracle ref")
+
+    # test_transform.cpp:55-64 (naive-correlation pin): 16^2 [0,1] seed 21
+    gen_2d_full("t2d_16_01_seed21", 16, [0, 1], O.random_grid((16, 16), 21))
+    # test_transform.cpp:26-40 impulse at 16^2 [0,1]
+    imp = np.zeros((16, 16)); imp[0, 0] = 1.0
+    gen_2d_full("t2d_16_01_impulse", 16, [0, 1], imp)
+    # test_transform.cpp:66-72 round trip 64^2 [0,0,1,1] seed 22
+    gen_2d_full("t2d_64_0011_seed22", 64, [0, 0, 1, 1], O.random_grid((64, 64), 22))
+    # non-square grid (drop-in generality): 40 x 24 [0,1], seed 5
+    s = ref.RefSystem2D(40, 24, [0, 1])
+    f = O.random_grid((40, 24), 5)
+    b = s.forward(f)
+    save("t2d_40x24_01_seed5", f=f, levels=np.array([0, 1]), j0=0, index=s.index(),
+         filter_norms=s.filter_norms(), frame_weight=s.frame_weight(), bands=b, rec=s.inverse(b))
+    # cfg1: cartoon 256^2 [1,1] round trip
+    gen_2d_stats("cfg1_cartoon256_11", 256, [1, 1], ref.cartoon(256))
+    # cfg2: cartoon 512 + noise(sigma 40, seed 7), [1,1,2,2], defaults_2d(40)
+    noisy = ref.add_noise(ref.cartoon(512), 40.0, 7)
+    s2, _ = gen_2d_stats("cfg2_denoise512_1122", 512, [1, 1, 2, 2], noisy, K=[2.5, 2.5, 2.5, 3.8], sigma=40.0)
+    # 3D: test_transform.cpp:150-189 16^3 [0,1]; 8^3 [0] seed 80 (naive pin)
+    gen_3d("t3d_8_0_seed80", (8, 8, 8), [0], np.random.default_rng(80).uniform(-1, 1, (8, 8, 8)), full=True)
+    gen_3d("t3d_16_01_rand", (16, 16, 16), [0, 1], np.random.default_rng(70).uniform(-1, 1, (16, 16, 16)))
+    gen_3d("t3d_12x16x20_01", (12, 16, 20), [0, 1], np.random.default_rng(3).uniform(-1, 1, (12, 16, 20)))
+    # acceptance crit.1 3D shape 32^3 [0,0,1]
+    gen_3d("t3d_32_001", (32, 32, 32), [0, 0, 1], np.random.default_rng(2).uniform(-1, 1, (32, 32, 32)),
+           K=[3.0, 3.0, 4.0], sigma=0.3)
+    if a.big:
+        # cfg4: cartoon_volume(128), [1,1]
+        gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))
+        # cfg5: cartoon_volume(192) + noise(40, seed 3), SL3D_2 [1,1,2], defaults_3d(40)
+        noisy3 = ref.add_noise(ref.cartoon_volume(192), 40.0, 3)
+        gen_3d("cfg5_denoise192_112", (192, 192, 192), [1, 1, 2], noisy3, K=[3.0, 3.0, 4.0], sigma=40.0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,340 @@
+// oracle/ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A flat C wrapper over the UNMODIFIED reference library, compiled from
+// /root/reference/proj/core/src/*.cpp by oracle/Makefile into
+// oracle/_ref/libshearlet_ref.so. It exists so Python tests, the golden
+// generator (oracle/gen_golden.py) and bench.py's cpu_baseline leg can drive
+// the reference's own public API (system2d.hpp:66-69, system3d.hpp:68-71,
+// transform.hpp:27-37, apps.hpp:16-44) through ctypes. Only the call
+// plumbing lives here; every number comes from the reference code.
+#include <cstdint>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "shearlet/apps.hpp"
+#include "shearlet/fft.hpp"
+#include "shearlet/phantoms.hpp"
+#include "shearlet/system2d.hpp"
+#include "shearlet/system3d.hpp"
+#include "shearlet/transform.hpp"
+
+using namespace shearlet;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ShapeError& e) { g_err = e.what(); return 2; }
+    catch (const ConfigError& e) { g_err = e.what(); return 3; }
+    catch (const DomainError& e) { g_err = e.what(); return 4; }
+    catch (const SingularFrameError& e) { g_err = e.what(); return 5; }
+    catch (const UnsupportedSizeError& e) { g_err = e.what(); return 6; }
+    catch (const Error& e) { g_err = e.what(); return 1; }
+    catch (const std::exception& e) { g_err = e.what(); return 99; }
+}
+
+const QmfPair& qmf() {
+    static const QmfPair q = QmfPair::maximally_flat_9tap();
+    return q;
+}
+FanFilter fan_for(int impulse_fan) {
+    return impulse_fan ? FanFilter::impulse() : default_fan_filter();
+}
+ScaleProfile profile_of(const int* levels, int n, int j0) {
+    return ScaleProfile::from_levels(std::vector<int>(levels, levels + n), j0);
+}
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- 2D
+int ref_build_2d(int rows, int cols, const int* levels, int n_scales, int j0, int full,
+                 int impulse_fan, int threads, void** out) {
+    return guard([&] {
+        auto* s = new ShearletSystem2D(build_system_2d(
+            static_cast<std::size_t>(rows), static_cast<std::size_t>(cols),
+            profile_of(levels, n_scales, j0), fan_for(impulse_fan), qmf(), full != 0, threads));
+        *out = s;
+    });
+}
+void ref_free_2d(void* h) { delete static_cast<ShearletSystem2D*>(h); }
+int ref_redundancy_2d(void* h) { return static_cast<int>(static_cast<ShearletSystem2D*>(h)->redundancy()); }
+
+// index records: kind, scale, shear (3 ints per filter)
+void ref_index_2d(void* h, int* rec) {
+    const auto& s = *static_cast<ShearletSystem2D*>(h);
+    for (std::size_t i = 0; i < s.index.size(); ++i) {
+        rec[3 * i] = static_cast<int>(s.index[i].kind);
+        rec[3 * i + 1] = s.index[i].scale;
+        rec[3 * i + 2] = static_cast<int>(s.index[i].shear);
+    }
+}
+void ref_filter_norms_2d(void* h, double* out) {
+    const auto& s = *static_cast<ShearletSystem2D*>(h);
+    std::memcpy(out, s.filter_norms.data(), sizeof(double) * s.filter_norms.size());
+}
+void ref_frame_weight_2d(void* h, double* out) {
+    const auto& s = *static_cast<ShearletSystem2D*>(h);
+    std::memcpy(out, s.frame_weight.data(), sizeof(double) * s.frame_weight.size());
+}
+// full complex spectrum of filter i, interleaved re/im
+void ref_filter_2d(void* h, int i, double* out) {
+    const auto& s = *static_cast<ShearletSystem2D*>(h);
+    std::memcpy(out, s.filters[static_cast<std::size_t>(i)].data(),
+                sizeof(double) * 2 * s.filters[static_cast<std::size_t>(i)].size());
+}
+
+int ref_forward_2d(void* h, const double* f, double* bands, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem2D*>(h);
+        Signal2D in(s.rows, s.cols);
+        std::memcpy(in.data(), f, sizeof(double) * in.size());
+        const auto c = forward(in, s, threads);
+        const std::size_t n = in.size();
+        for (std::size_t i = 0; i < c.bands.size(); ++i)
+            std::memcpy(bands + i * n, c.bands[i].data(), sizeof(double) * n);
+    });
+}
+
+namespace {
+CoefficientStack2D stack2_of(const ShearletSystem2D& s, const double* bands, int nb) {
+    CoefficientStack2D c;
+    c.rows = s.rows;
+    c.cols = s.cols;
+    c.index = s.index;
+    c.bands.assign(static_cast<std::size_t>(nb), RealGrid2(s.rows, s.cols));
+    const std::size_t n = s.rows * s.cols;
+    for (std::size_t i = 0; i < c.bands.size(); ++i)
+        std::memcpy(c.bands[i].data(), bands + i * n, sizeof(double) * n);
+    return c;
+}
+CoefficientStack3D stack3_of(const ShearletSystem3D& s, const double* bands, int nb) {
+    CoefficientStack3D c;
+    c.dims = s.dims;
+    c.index = s.index;
+    c.bands.assign(static_cast<std::size_t>(nb), RealGrid3(s.dims[0], s.dims[1], s.dims[2]));
+    const std::size_t n = s.dims[0] * s.dims[1] * s.dims[2];
+    for (std::size_t i = 0; i < c.bands.size(); ++i)
+        std::memcpy(c.bands[i].data(), bands + i * n, sizeof(double) * n);
+    return c;
+}
+} // namespace
+
+int ref_inverse_2d(void* h, const double* bands, int nb, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem2D*>(h);
+        const auto r = inverse(stack2_of(s, bands, nb), s, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+
+int ref_hard_threshold_2d(void* h, const double* bands, int nb, const double* K, int nK,
+                          double sigma, int scaled, double* out) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem2D*>(h);
+        ThresholdSchedule sch{std::vector<double>(K, K + nK), sigma, scaled != 0};
+        const auto r = hard_threshold(stack2_of(s, bands, nb), sch, s);
+        const std::size_t n = s.rows * s.cols;
+        for (std::size_t i = 0; i < r.bands.size(); ++i)
+            std::memcpy(out + i * n, r.bands[i].data(), sizeof(double) * n);
+    });
+}
+
+int ref_denoise_2d(void* h, const double* in, const double* K, int nK, double sigma,
+                   int scaled, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem2D*>(h);
+        Signal2D f(s.rows, s.cols);
+        std::memcpy(f.data(), in, sizeof(double) * f.size());
+        ThresholdSchedule sch{std::vector<double>(K, K + nK), sigma, scaled != 0};
+        const auto r = denoise(f, s, sch, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+
+// ---------------------------------------------------------------- 3D
+int ref_build_3d(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full,
+                 int impulse_fan, int threads, void** out) {
+    return guard([&] {
+        auto* s = new ShearletSystem3D(build_system_3d(
+            {static_cast<std::size_t>(n0), static_cast<std::size_t>(n1),
+             static_cast<std::size_t>(n2)},
+            profile_of(levels, n_scales, j0), fan_for(impulse_fan), qmf(), full != 0, threads));
+        *out = s;
+    });
+}
+void ref_free_3d(void* h) { delete static_cast<ShearletSystem3D*>(h); }
+int ref_redundancy_3d(void* h) { return static_cast<int>(static_cast<ShearletSystem3D*>(h)->redundancy()); }
+void ref_index_3d(void* h, int* rec) {
+    const auto& s = *static_cast<ShearletSystem3D*>(h);
+    for (std::size_t i = 0; i < s.index.size(); ++i) {
+        rec[4 * i] = static_cast<int>(s.index[i].kind);
+        rec[4 * i + 1] = s.index[i].scale;
+        rec[4 * i + 2] = static_cast<int>(s.index[i].k1);
+        rec[4 * i + 3] = static_cast<int>(s.index[i].k2);
+    }
+}
+void ref_filter_norms_3d(void* h, double* out) {
+    const auto& s = *static_cast<ShearletSystem3D*>(h);
+    std::memcpy(out, s.filter_norms.data(), sizeof(double) * s.filter_norms.size());
+}
+void ref_frame_weight_3d(void* h, double* out) {
+    const auto& s = *static_cast<ShearletSystem3D*>(h);
+    std::memcpy(out, s.frame_weight.data(), sizeof(double) * s.frame_weight.size());
+}
+int ref_filter_3d(void* h, int i, double* out) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        const auto g = s.filter_freq(static_cast<std::size_t>(i));
+        std::memcpy(out, g.data(), sizeof(double) * 2 * g.size());
+    });
+}
+// per-scale factor tables (taps): highpass length/center, phi shapes
+int ref_scale_info_3d(void* h, int s, int* info) {
+    return guard([&] {
+        const auto& sys = *static_cast<ShearletSystem3D*>(h);
+        const auto& sc = sys.scales.at(static_cast<std::size_t>(s));
+        info[0] = sc.d;
+        info[1] = static_cast<int>(sc.highpass.size());
+        info[2] = static_cast<int>(sc.highpass.center);
+        info[3] = static_cast<int>(sc.phi.size());
+    });
+}
+
+int ref_forward_3d(void* h, const double* f, double* bands, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        Signal3D in(s.dims[0], s.dims[1], s.dims[2]);
+        std::memcpy(in.data(), f, sizeof(double) * in.size());
+        const auto c = forward(in, s, threads);
+        const std::size_t n = in.size();
+        for (std::size_t i = 0; i < c.bands.size(); ++i)
+            std::memcpy(bands + i * n, c.bands[i].data(), sizeof(double) * n);
+    });
+}
+int ref_inverse_3d(void* h, const double* bands, int nb, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        const auto r = inverse(stack3_of(s, bands, nb), s, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+int ref_hard_threshold_3d(void* h, const double* bands, int nb, const double* K, int nK,
+                          double sigma, int scaled, double* out) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        ThresholdSchedule sch{std::vector<double>(K, K + nK), sigma, scaled != 0};
+        const auto r = hard_threshold(stack3_of(s, bands, nb), sch, s);
+        const std::size_t n = s.dims[0] * s.dims[1] * s.dims[2];
+        for (std::size_t i = 0; i < r.bands.size(); ++i)
+            std::memcpy(out + i * n, r.bands[i].data(), sizeof(double) * n);
+    });
+}
+int ref_denoise_3d(void* h, const double* in, const double* K, int nK, double sigma,
+                   int scaled, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        Signal3D f(s.dims[0], s.dims[1], s.dims[2]);
+        std::memcpy(f.data(), in, sizeof(double) * f.size());
+        ThresholdSchedule sch{std::vector<double>(K, K + nK), sigma, scaled != 0};
+        const auto r = denoise(f, s, sch, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+
+
+// forward -> hard_threshold -> inverse, also reporting per-band L2 norms of the
+// forward stack and kept counts of the thresholded stack (for big fixtures
+// where the stack itself is too large to hand back).
+int ref_denoise_3d_stats(void* h, const double* in, const double* K, int nK, double sigma,
+                         int scaled, double* out, long long* kept, double* band_l2,
+                         double* band_sample, const long long* sample_idx, int n_sample,
+                         int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        Signal3D f(s.dims[0], s.dims[1], s.dims[2]);
+        std::memcpy(f.data(), in, sizeof(double) * f.size());
+        ThresholdSchedule sch{std::vector<double>(K, K + nK), sigma, scaled != 0};
+        CoefficientStack3D c = forward(f, s, threads);
+        for (std::size_t i = 0; i < c.bands.size(); ++i) {
+            double e = 0.0;
+            for (double x : c.bands[i].raw()) e += x * x;
+            band_l2[i] = std::sqrt(e);
+            for (int q = 0; q < n_sample; ++q)
+                band_sample[i * static_cast<std::size_t>(n_sample) + static_cast<std::size_t>(q)] =
+                    c.bands[i].raw()[static_cast<std::size_t>(sample_idx[q])];
+        }
+        CoefficientStack3D t = hard_threshold(c, sch, s);
+        c = CoefficientStack3D{};
+        for (std::size_t i = 0; i < t.bands.size(); ++i) {
+            long long k = 0;
+            for (double x : t.bands[i].raw()) k += (x != 0.0);
+            kept[i] = k;
+        }
+        const auto r = inverse(t, s, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+
+// ---------------------------------------------------------------- inputs
+void ref_cartoon(int n, double* out) {
+    const auto g = phantoms::cartoon(static_cast<std::size_t>(n));
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+}
+void ref_cartoon_volume(int n, double* out) {
+    const auto g = phantoms::cartoon_volume(static_cast<std::size_t>(n));
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+}
+void ref_add_noise_2d(int rows, int cols, const double* in, double sigma, std::uint64_t seed,
+                      double* out) {
+    Signal2D s(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols));
+    std::memcpy(s.data(), in, sizeof(double) * s.size());
+    const auto r = add_gaussian_noise(s, sigma, seed);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+}
+void ref_add_noise_3d(int n0, int n1, int n2, const double* in, double sigma, std::uint64_t seed,
+                      double* out) {
+    Signal3D s(static_cast<std::size_t>(n0), static_cast<std::size_t>(n1), static_cast<std::size_t>(n2));
+    std::memcpy(s.data(), in, sizeof(double) * s.size());
+    const auto r = add_gaussian_noise(s, sigma, seed);
+    std::memcpy(out, r.data(), sizeof(double) * r.size());
+}
+double ref_psnr_2d(int rows, int cols, const double* a, const double* b) {
+    Signal2D x(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols)), y(x);
+    std::memcpy(x.data(), a, sizeof(double) * x.size());
+    std::memcpy(y.data(), b, sizeof(double) * y.size());
+    return psnr(x, y);
+}
+// raw 1D/2D/3D complex FFT through the reference wrapper (validates the shim)
+void ref_fft_forward(int rank, const int* dims, double* data) {
+    std::size_t n = 1;
+    for (int a = 0; a < rank; ++a) n *= static_cast<std::size_t>(dims[a]);
+    if (rank == 1) {
+        std::vector<std::complex<double>> v(n);
+        std::memcpy(v.data(), data, 16 * n);
+        fft::forward(v);
+        std::memcpy(data, v.data(), 16 * n);
+    } else if (rank == 2) {
+        ComplexGrid2 g(static_cast<std::size_t>(dims[0]), static_cast<std::size_t>(dims[1]));
+        std::memcpy(g.data(), data, 16 * n);
+        fft::forward(g);
+        std::memcpy(data, g.data(), 16 * n);
+    } else {
+        ComplexGrid3 g(static_cast<std::size_t>(dims[0]), static_cast<std::size_t>(dims[1]),
+                       static_cast<std::size_t>(dims[2]));
+        std::memcpy(g.data(), data, 16 * n);
+        fft::forward(g);
+        std::memcpy(data, g.data(), 16 * n);
+    }
+}
+
+} // extern "C"

@@ -1,0 +1,477 @@
+"""paper_1402_5670_b200 -- B200-native digital shearlet dec/rec hot path.
+
+Python host mirror of the reference's C++ API for this path
+(/root/reference/proj/core/include/shearlet/{system2d,system3d,transform,apps}.hpp),
+bound through the C ABI in include/shearlet_b200.h (libshearlet_b200.so, built
+in-tree by __graft_entry__.build()). Names, argument meaning and error classes
+follow the reference:
+
+    build_system_2d(rows, cols, ScaleProfile, fan, full_system)  system2d.hpp:66-69
+    build_system_3d(dims, ScaleProfile, fan, full_system)        system3d.hpp:68-71
+    forward(f, sys) / inverse(coeffs, sys)                       transform.hpp:27-37
+    hard_threshold(coeffs, schedule, sys), denoise(...)          apps.hpp:31-44
+    ThresholdSchedule.defaults_2d / defaults_3d                  apps.hpp:19-29
+    sys.filter_norms (RMS), sys.frame_weight, sys.frame_bounds() system2d.hpp:29-51
+
+Arrays: numpy float64 arrays run the host-pointer entry points (value
+semantics, like the reference); CUDA torch tensors run the device-pointer
+entry points on the current torch stream and return CUDA tensors. There is
+no CPU fallback: without the built library every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libshearlet_b200.so")
+
+# ------------------------------------------------------------------ errors
+# errors.hpp:9-56
+
+
+class Error(RuntimeError):
+    pass
+
+
+class DomainError(Error):
+    pass
+
+
+class ShapeError(Error):
+    pass
+
+
+class ConfigError(Error):
+    pass
+
+
+class AssetError(Error):
+    pass
+
+
+class FormatError(Error):
+    pass
+
+
+class SingularFrameError(Error):
+    pass
+
+
+class UnsupportedSizeError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class InvalidArgument(Error):
+    pass
+
+
+_CODES = {1: Error, 2: ShapeError, 3: ConfigError, 4: DomainError, 5: SingularFrameError,
+          6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 20: CudaError, 22: InvalidArgument}
+
+# ------------------------------------------------------------------ library
+_lib = None
+
+
+def lib():
+    """Load libshearlet_b200.so; raises loudly if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(there is no CPU fallback for the shearlet hot path)")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    i = C.c_int
+    dp = C.POINTER(C.c_double)
+    ip = C.POINTER(C.c_int)
+    L.sl_version.restype = C.c_char_p
+    L.sl_last_error.restype = C.c_char_p
+    L.sl_device_count.argtypes = [ip]
+    L.sl_system_create_2d.argtypes = [i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
+    L.sl_system_create_3d.argtypes = [i, i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
+    L.sl_system_destroy.argtypes = [P]
+    L.sl_ndim.argtypes = [P, ip, C.POINTER(C.c_int64)]
+    L.sl_redundancy.argtypes = [P, ip]
+    L.sl_shard.argtypes = [P, ip, ip]
+    L.sl_index.argtypes = [P, C.POINTER(C.c_int32)]
+    L.sl_filter_norms.argtypes = [P, dp]
+    L.sl_frame_weight.argtypes = [P, dp]
+    L.sl_frame_bounds.argtypes = [P, dp, dp]
+    L.sl_filter_spectrum.argtypes = [P, i, dp]
+    L.sl_sheardec_dev.argtypes = [P, P, P, P]
+    L.sl_sheardec_threshold_dev.argtypes = [P, P, P, dp, i, C.c_double, i, P]
+    L.sl_shearrec_dev.argtypes = [P, P, i, P, P]
+    L.sl_hard_threshold_dev.argtypes = [P, P, P, i, dp, i, C.c_double, i, P]
+    L.sl_denoise_dev.argtypes = [P, P, P, dp, i, C.c_double, i, P]
+    L.sl_sheardec_host.argtypes = [P, dp, dp]
+    L.sl_shearrec_host.argtypes = [P, dp, i, dp]
+    L.sl_hard_threshold_host.argtypes = [P, dp, dp, i, dp, i, C.c_double, i]
+    L.sl_denoise_host.argtypes = [P, dp, dp, dp, i, C.c_double, i]
+    L.sl_phantom_cartoon.argtypes = [i, dp]
+    L.sl_phantom_cartoon_volume.argtypes = [i, dp]
+    L.sl_add_gaussian_noise.argtypes = [dp, dp, C.c_int64, C.c_double, C.c_uint64]
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = [
+    "sl_version", "sl_last_error", "sl_device_count", "sl_system_create_2d", "sl_system_create_3d",
+    "sl_system_destroy", "sl_ndim", "sl_redundancy", "sl_shard", "sl_index", "sl_filter_norms",
+    "sl_frame_weight", "sl_frame_bounds", "sl_filter_spectrum", "sl_sheardec_dev", "sl_sheardec_threshold_dev",
+    "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_sheardec_host", "sl_shearrec_host",
+    "sl_hard_threshold_host", "sl_denoise_host", "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
+    "sl_add_gaussian_noise",
+]
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().sl_last_error().decode()
+        raise _CODES.get(rc, Error)(msg)
+
+
+def _dp(a: np.ndarray):
+    if a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise InvalidArgument("expected a C-contiguous float64 array")
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _is_cuda_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _stream_ptr(device: int):
+    import torch
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+# ------------------------------------------------------------------ profiles
+@dataclass
+class ScaleProfile:
+    """filters.hpp:79-92."""
+    shear_levels: List[int]
+    coarsest_scale_offset: int = 0
+
+    @property
+    def n_scales(self) -> int:
+        return len(self.shear_levels)
+
+    def top_level(self) -> int:
+        return self.coarsest_scale_offset + self.n_scales
+
+    def validate(self):  # filters.cpp:168-176
+        if self.coarsest_scale_offset < 0:
+            raise ConfigError("ScaleProfile: coarsest scale offset must be >= 0")
+        if any(d < 0 for d in self.shear_levels):
+            raise ConfigError("ScaleProfile: shear levels must be >= 0")
+
+    @staticmethod
+    def from_levels(levels: Sequence[int], j0: int = 0) -> "ScaleProfile":
+        p = ScaleProfile(list(int(x) for x in levels), int(j0))
+        p.validate()
+        return p
+
+    @staticmethod
+    def parabolic(n_scales: int, j0: int = 1) -> "ScaleProfile":  # d_j = ceil(j/2)
+        return ScaleProfile.from_levels([(j0 + i + 1) // 2 for i in range(n_scales)], j0)
+
+
+@dataclass
+class ThresholdSchedule:
+    """apps.hpp:19-29."""
+    per_scale_factors: List[float]
+    sigma: float = 0.0
+    scale_by_filter_norm: bool = True
+
+    @staticmethod
+    def defaults_2d(sigma: float, n_scales: int = 4) -> "ThresholdSchedule":
+        k = [2.5] * n_scales
+        if n_scales > 0:
+            k[-1] = 3.8
+        return ThresholdSchedule(k, sigma, True)
+
+    @staticmethod
+    def defaults_3d(sigma: float, n_scales: int = 3) -> "ThresholdSchedule":
+        k = [3.0] * n_scales
+        if n_scales > 0:
+            k[-1] = 4.0
+        return ThresholdSchedule(k, sigma, True)
+
+
+# ------------------------------------------------------------------ systems
+class _System:
+    ndim = 0
+
+    def __init__(self, handle, profile: ScaleProfile, full_system: bool, device: int):
+        self._h = handle
+        self.profile = profile
+        self.full_system = full_system
+        self.device = device
+        L = lib()
+        R = C.c_int()
+        _check(L.sl_redundancy(self._h, C.byref(R)))
+        self._R = R.value
+        lo, hi = C.c_int(), C.c_int()
+        _check(L.sl_shard(self._h, C.byref(lo), C.byref(hi)))
+        self.shard = (lo.value, hi.value)
+        rec = np.zeros((self._R, 4), dtype=np.int32)
+        _check(L.sl_index(self._h, rec.ctypes.data_as(C.POINTER(C.c_int32))))
+        self.index_records = rec
+        rms = np.zeros(self._R)
+        _check(L.sl_filter_norms(self._h, _dp(rms)))
+        self.filter_norms = rms
+        self._W = None
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().sl_system_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def redundancy(self) -> int:
+        return self._R
+
+    @property
+    def n_bands(self) -> int:
+        return self.shard[1] - self.shard[0]
+
+    @property
+    def frame_weight(self) -> np.ndarray:
+        if self._W is None:
+            w = np.zeros(self.shape)
+            _check(lib().sl_frame_weight(self._h, _dp(w)))
+            self._W = w
+        return self._W
+
+    def frame_bounds(self):
+        a, b = C.c_double(), C.c_double()
+        _check(lib().sl_frame_bounds(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def filter_freq(self, i: int) -> np.ndarray:
+        out = np.zeros(self.shape + (2,))
+        _check(lib().sl_filter_spectrum(self._h, int(i), _dp(out)))
+        return out[..., 0] + 1j * out[..., 1]
+
+
+class ShearletSystem2D(_System):
+    """system2d.hpp:29-51 (filters live on the GPU as real Hermitian halves)."""
+    ndim = 2
+
+    def __init__(self, handle, rows, cols, profile, full_system, device):
+        self.rows, self.cols = rows, cols
+        self.shape = (rows, cols)
+        super().__init__(handle, profile, full_system, device)
+        # FilterIndex2D records: (kind, scale, shear)
+        self.index = [(int(k), int(s), int(sh)) for k, s, sh, _ in self.index_records]
+
+
+class ShearletSystem3D(_System):
+    """system3d.hpp:32-61 (filters synthesised on the fly from factor tables)."""
+    ndim = 3
+
+    def __init__(self, handle, dims, profile, full_system, device):
+        self.dims = tuple(dims)
+        self.shape = tuple(dims)
+        super().__init__(handle, profile, full_system, device)
+        self.index = [(int(k), int(s), int(a), int(b)) for k, s, a, b in self.index_records]
+
+
+def _levels_arg(profile: ScaleProfile):
+    lv = np.asarray(profile.shear_levels, dtype=np.int32)
+    return lv, lv.ctypes.data_as(C.POINTER(C.c_int))
+
+
+def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan: str = "dmaxflat4",
+                    full_system: bool = False, device: int = 0, shard=None) -> ShearletSystem2D:
+    """build_system_2d (system2d.hpp:66-69). fan: "dmaxflat4" (default_fan_filter) or "impulse"."""
+    profile.validate()
+    lv, lvp = _levels_arg(profile)
+    h = C.c_void_p()
+    lo, hi = (0, -1) if shard is None else shard
+    _check(lib().sl_system_create_2d(int(rows), int(cols), lvp, len(lv), profile.coarsest_scale_offset,
+                                     int(full_system), int(fan == "impulse"), int(device), int(lo), int(hi),
+                                     C.byref(h)))
+    return ShearletSystem2D(h, rows, cols, profile, full_system, device)
+
+
+def build_system_3d(dims, profile: ScaleProfile, fan: str = "dmaxflat4", full_system: bool = False,
+                    device: int = 0, shard=None) -> ShearletSystem3D:
+    """build_system_3d (system3d.hpp:68-71)."""
+    profile.validate()
+    lv, lvp = _levels_arg(profile)
+    h = C.c_void_p()
+    n0, n1, n2 = (int(x) for x in dims)
+    lo, hi = (0, -1) if shard is None else shard
+    _check(lib().sl_system_create_3d(n0, n1, n2, lvp, len(lv), profile.coarsest_scale_offset,
+                                     int(full_system), int(fan == "impulse"), int(device), int(lo), int(hi),
+                                     C.byref(h)))
+    return ShearletSystem3D(h, (n0, n1, n2), profile, full_system, device)
+
+
+def redundancy_2d(profile: ScaleProfile, full_system: bool = False) -> int:  # system2d.cpp:49-57
+    profile.validate()
+    r = 1
+    for d in profile.shear_levels:
+        per = 2 * (1 << d) + 1
+        r += 2 * per if full_system else 2 * per - 2
+    return r
+
+
+def redundancy_3d(profile: ScaleProfile, full_system: bool = False) -> int:  # system3d.cpp:27-35
+    profile.validate()
+    r = 1
+    for d in profile.shear_levels:
+        q = 2 * (1 << d) + 1
+        r += 3 * q * q if full_system else 3 * q * q - 6 * q + 4
+    return r
+
+
+# ------------------------------------------------------------------ transforms
+def _check_signal(f, sys: _System, what: str):
+    if tuple(f.shape) != tuple(sys.shape):
+        raise ShapeError(f"{what}: signal dims do not match the system grid")
+
+
+def _k_arg(schedule: ThresholdSchedule):
+    K = np.ascontiguousarray(schedule.per_scale_factors, dtype=np.float64)
+    return K, K.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def forward(f, sys: _System, threads: int = 0):
+    """Undecimated analysis band_i = Re IDFT(conj(psi_i) DFT(f)) (transform.hpp:27-31).
+
+    Returns the coefficient stack [n_bands, *dims] (numpy or CUDA tensor, like f).
+    `threads` is accepted for API parity; the GPU grid replaces host threads."""
+    _check_signal(f, sys, "forward")
+    L = lib()
+    if _is_cuda_tensor(f):
+        import torch
+        f = f.contiguous().to(torch.float64)
+        out = torch.empty((sys.n_bands,) + tuple(sys.shape), dtype=torch.float64, device=f.device)
+        _check(L.sl_sheardec_dev(sys.handle, C.c_void_p(f.data_ptr()), C.c_void_p(out.data_ptr()),
+                                 _stream_ptr(f.device.index)))
+        return out
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    out = np.empty((sys.n_bands,) + tuple(sys.shape))
+    _check(L.sl_sheardec_host(sys.handle, _dp(f), _dp(out)))
+    return out
+
+
+def inverse(coeffs, sys: _System, threads: int = 0):
+    """Exact synthesis f = Re IDFT(sum_i DFT(c_i) psi_i / W) (transform.hpp:33-37)."""
+    if tuple(coeffs.shape[1:]) != tuple(sys.shape) or coeffs.shape[0] != sys.n_bands:
+        raise ShapeError("inverse: coefficient stack does not match the system")
+    L = lib()
+    if _is_cuda_tensor(coeffs):
+        import torch
+        coeffs = coeffs.contiguous().to(torch.float64)
+        out = torch.empty(tuple(sys.shape), dtype=torch.float64, device=coeffs.device)
+        _check(L.sl_shearrec_dev(sys.handle, C.c_void_p(coeffs.data_ptr()), int(coeffs.shape[0]),
+                                 C.c_void_p(out.data_ptr()), _stream_ptr(coeffs.device.index)))
+        return out
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    out = np.empty(tuple(sys.shape))
+    _check(L.sl_shearrec_host(sys.handle, _dp(coeffs), int(coeffs.shape[0]), _dp(out)))
+    return out
+
+
+def hard_threshold(coeffs, schedule: ThresholdSchedule, sys: _System):
+    """Zero |x| < K_j sigma (RMS_i); lowpass untouched; returns a new stack (apps.hpp:31-38)."""
+    K, Kp = _k_arg(schedule)
+    L = lib()
+    if _is_cuda_tensor(coeffs):
+        import torch
+        coeffs = coeffs.contiguous()
+        out = torch.empty_like(coeffs)
+        _check(L.sl_hard_threshold_dev(sys.handle, C.c_void_p(coeffs.data_ptr()), C.c_void_p(out.data_ptr()),
+                                       int(coeffs.shape[0]), Kp, len(K), float(schedule.sigma),
+                                       int(schedule.scale_by_filter_norm), _stream_ptr(coeffs.device.index)))
+        return out
+    coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+    out = np.empty_like(coeffs)
+    _check(L.sl_hard_threshold_host(sys.handle, _dp(coeffs), _dp(out), int(coeffs.shape[0]), Kp, len(K),
+                                    float(schedule.sigma), int(schedule.scale_by_filter_norm)))
+    return out
+
+
+def forward_thresholded(f, sys: _System, schedule: ThresholdSchedule):
+    """forward() with hard_threshold() fused into the dec epilogue (CUDA tensors)."""
+    _check_signal(f, sys, "forward")
+    import torch
+    K, Kp = _k_arg(schedule)
+    f = f.contiguous().to(torch.float64)
+    out = torch.empty((sys.n_bands,) + tuple(sys.shape), dtype=torch.float64, device=f.device)
+    _check(lib().sl_sheardec_threshold_dev(sys.handle, C.c_void_p(f.data_ptr()), C.c_void_p(out.data_ptr()),
+                                           Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm),
+                                           _stream_ptr(f.device.index)))
+    return out
+
+
+def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0):
+    """inverse(hard_threshold(forward(noisy))) (apps.hpp:40-43, apps.cpp:114-121)."""
+    _check_signal(noisy, sys, "forward")
+    K, Kp = _k_arg(schedule)
+    L = lib()
+    if _is_cuda_tensor(noisy):
+        import torch
+        noisy = noisy.contiguous().to(torch.float64)
+        out = torch.empty_like(noisy)
+        _check(L.sl_denoise_dev(sys.handle, C.c_void_p(noisy.data_ptr()), C.c_void_p(out.data_ptr()), Kp, len(K),
+                                float(schedule.sigma), int(schedule.scale_by_filter_norm),
+                                _stream_ptr(noisy.device.index)))
+        return out
+    noisy = np.ascontiguousarray(noisy, dtype=np.float64)
+    out = np.empty_like(noisy)
+    _check(L.sl_denoise_host(sys.handle, _dp(noisy), _dp(out), Kp, len(K), float(schedule.sigma),
+                             int(schedule.scale_by_filter_norm)))
+    return out
+
+
+# ------------------------------------------------------------------ inputs
+def cartoon(n: int) -> np.ndarray:
+    """phantoms::cartoon (phantoms.cpp:14-36)."""
+    out = np.empty((n, n))
+    _check(lib().sl_phantom_cartoon(int(n), _dp(out)))
+    return out
+
+
+def cartoon_volume(n: int) -> np.ndarray:
+    """phantoms::cartoon_volume (phantoms.cpp:91-108)."""
+    out = np.empty((n, n, n))
+    _check(lib().sl_phantom_cartoon_volume(int(n), _dp(out)))
+    return out
+
+
+def add_gaussian_noise(x: np.ndarray, sigma: float, seed: int) -> np.ndarray:
+    """add_gaussian_noise (apps.cpp:47-55): mt19937_64 + Box-Muller."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(lib().sl_add_gaussian_noise(_dp(x), _dp(out), x.size, float(sigma), int(seed)))
+    return out
+
+
+def psnr(reference: np.ndarray, test: np.ndarray) -> float:
+    """20 log10(255 sqrt(N) / ||ref - test||) (apps.cpp:125-135)."""
+    if reference.shape != test.shape:
+        raise ShapeError("psnr: dimension mismatch")
+    e2 = float(np.sum((reference - test) ** 2))
+    if e2 == 0.0:
+        return float("inf")
+    return 20.0 * np.log10(255.0 * np.sqrt(reference.size) / np.sqrt(e2))
