@@ -100,6 +100,22 @@ int sl_hard_threshold_dev(sl_system* sys, const double* in, double* out, int nba
 int sl_denoise_dev(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
                    int scale_by_rms, void* stream);
 
+/* ---- batched hot path (device pointers) ----------------------------------
+ * nframes independent signals, contiguous [nframes][dims]; stacks
+ * [nframes][nbands][dims]. Frames are spread over up to sl_set_streams()
+ * internal streams (default 4) that fork from and join back into `stream`,
+ * so concurrent frames overlap on the GPU; results are identical to
+ * per-frame calls. sl_sheardec_batch_dev thresholds when K != NULL. */
+int sl_set_streams(sl_system* sys, int nstreams);
+int sl_sheardec_batch_dev(sl_system* sys, const double* f, int nframes, double* coeffs, const double* K, int nK,
+                          double sigma, int scale_by_rms, void* stream);
+int sl_shearrec_batch_dev(sl_system* sys, const double* coeffs, int nframes, double* f, void* stream);
+int sl_denoise_batch_dev(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
+                         double sigma, int scale_by_rms, void* stream);
+/* host in/out: H2D of all frames + batched denoise + D2H, synchronous */
+int sl_denoise_batch_host(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
+                          double sigma, int scale_by_rms);
+
 /* ---- hot path, host pointers (value semantics like the reference) -------- */
 int sl_sheardec_host(sl_system* sys, const double* f, double* coeffs);
 int sl_shearrec_host(sl_system* sys, const double* coeffs, int nbands, double* f);
@@ -107,6 +123,18 @@ int sl_hard_threshold_host(sl_system* sys, const double* in, double* out, int nb
                            double sigma, int scale_by_rms);
 int sl_denoise_host(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
                     int scale_by_rms);
+
+/* ---- instrumentation ---------------------------------------------------
+ * sl_profile(enable) clears the per-pass statistics and turns CUDA-event timing
+ * of every kernel launch on/off; sl_pass_stats returns, per pass name (32-byte
+ * NUL-padded slots), the summed device time in ms, the launch count and the
+ * number of bands/spectra those launches processed since the last sl_profile
+ * call. sl_launch_count is the cumulative number of kernels this handle has
+ * launched (construction included). */
+int sl_profile(sl_system* sys, int enable);
+int sl_pass_stats(sl_system* sys, int max_passes, char* names, double* ms_total, int64_t* launches, int64_t* units,
+                  int* n_passes);
+int sl_launch_count(const sl_system* sys, int64_t* count);
 
 /* ---- synthetic inputs (phantoms.hpp / apps.hpp generators, host) ---------- */
 int sl_phantom_cartoon(int n, double* out);            /* phantoms::cartoon        */

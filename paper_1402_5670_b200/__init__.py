@@ -28,7 +28,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libshearlet_b200.so")
+LIB_PATH = os.environ.get("SLB_LIB", os.path.join(_HERE, "libshearlet_b200.so"))  # SLB_LIB: dev variants
 
 # ------------------------------------------------------------------ errors
 # errors.hpp:9-56
@@ -117,6 +117,14 @@ def lib():
     L.sl_shearrec_host.argtypes = [P, dp, i, dp]
     L.sl_hard_threshold_host.argtypes = [P, dp, dp, i, dp, i, C.c_double, i]
     L.sl_denoise_host.argtypes = [P, dp, dp, dp, i, C.c_double, i]
+    L.sl_set_streams.argtypes = [P, i]
+    L.sl_sheardec_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
+    L.sl_shearrec_batch_dev.argtypes = [P, P, i, P, P]
+    L.sl_denoise_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
+    L.sl_denoise_batch_host.argtypes = [P, dp, i, dp, dp, i, C.c_double, i]
+    L.sl_profile.argtypes = [P, i]
+    L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
+    L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
     L.sl_phantom_cartoon.argtypes = [i, dp]
     L.sl_phantom_cartoon_volume.argtypes = [i, dp]
     L.sl_add_gaussian_noise.argtypes = [dp, dp, C.c_int64, C.c_double, C.c_uint64]
@@ -129,7 +137,10 @@ EXPORTED_SYMBOLS = [
     "sl_system_destroy", "sl_ndim", "sl_redundancy", "sl_shard", "sl_index", "sl_filter_norms",
     "sl_frame_weight", "sl_frame_bounds", "sl_filter_spectrum", "sl_sheardec_dev", "sl_sheardec_threshold_dev",
     "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_sheardec_host", "sl_shearrec_host",
-    "sl_hard_threshold_host", "sl_denoise_host", "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
+    "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
+    "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
+    "sl_denoise_batch_host",
+    "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
 ]
 
@@ -263,6 +274,31 @@ class _System:
         a, b = C.c_double(), C.c_double()
         _check(lib().sl_frame_bounds(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    # ---- instrumentation (bench.py) ----
+    def set_profiling(self, enable: bool = True):
+        _check(lib().sl_profile(self._h, int(enable)))
+
+    def pass_stats(self):
+        n = C.c_int()
+        names = C.create_string_buffer(32 * 64)
+        ms = np.zeros(64)
+        cnt = np.zeros(64, dtype=np.int64)
+        units = np.zeros(64, dtype=np.int64)
+        _check(lib().sl_pass_stats(self._h, 64, names, _dp(ms), cnt.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   units.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(n)))
+        raw = names.raw
+        return {raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i]), int(units[i]))
+                for i in range(n.value)}
+
+    def set_streams(self, n: int):
+        """Concurrent internal streams used by the batched entry points."""
+        _check(lib().sl_set_streams(self._h, int(n)))
+
+    def launch_count(self) -> int:
+        c = C.c_int64()
+        _check(lib().sl_launch_count(self._h, C.byref(c)))
+        return c.value
 
     def filter_freq(self, i: int) -> np.ndarray:
         out = np.zeros(self.shape + (2,))
@@ -441,6 +477,58 @@ def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0):
     out = np.empty_like(noisy)
     _check(L.sl_denoise_host(sys.handle, _dp(noisy), _dp(out), Kp, len(K), float(schedule.sigma),
                              int(schedule.scale_by_filter_norm)))
+    return out
+
+
+def _check_batch(x, sys: _System):
+    if x.ndim != sys.ndim + 1 or tuple(x.shape[1:]) != tuple(sys.shape):
+        raise ShapeError("batch: expected [nframes, *dims] matching the system grid")
+
+
+def forward_batch(frames, sys: _System, schedule: Optional[ThresholdSchedule] = None):
+    """forward() (optionally + fused hard_threshold) of [nframes, *dims] CUDA frames -> [nframes, nb, *dims]."""
+    _check_batch(frames, sys)
+    import torch
+    frames = frames.contiguous().to(torch.float64)
+    out = torch.empty((frames.shape[0], sys.n_bands) + tuple(sys.shape), dtype=torch.float64, device=frames.device)
+    if schedule is None:
+        Kp, nK, sg, sc = None, 0, 0.0, 0
+    else:
+        K, Kp = _k_arg(schedule)
+        nK, sg, sc = len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm)
+    _check(lib().sl_sheardec_batch_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
+                                       C.c_void_p(out.data_ptr()), Kp, nK, sg, sc, _stream_ptr(frames.device.index)))
+    return out
+
+
+def inverse_batch(coeffs, sys: _System):
+    """inverse() of [nframes, nb, *dims] CUDA stacks -> [nframes, *dims]."""
+    if coeffs.ndim != sys.ndim + 2 or coeffs.shape[1] != sys.n_bands or tuple(coeffs.shape[2:]) != tuple(sys.shape):
+        raise ShapeError("inverse_batch: coefficient stacks do not match the system")
+    import torch
+    coeffs = coeffs.contiguous().to(torch.float64)
+    out = torch.empty((coeffs.shape[0],) + tuple(sys.shape), dtype=torch.float64, device=coeffs.device)
+    _check(lib().sl_shearrec_batch_dev(sys.handle, C.c_void_p(coeffs.data_ptr()), int(coeffs.shape[0]),
+                                       C.c_void_p(out.data_ptr()), _stream_ptr(coeffs.device.index)))
+    return out
+
+
+def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule):
+    """denoise() of [nframes, *dims] frames; CUDA tensors stay on the device, numpy
+    arrays go through the host entry point (H2D + dec/thr/rec + D2H)."""
+    _check_batch(frames, sys)
+    K, Kp = _k_arg(schedule)
+    args = (Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm))
+    if _is_cuda_tensor(frames):
+        import torch
+        frames = frames.contiguous().to(torch.float64)
+        out = torch.empty_like(frames)
+        _check(lib().sl_denoise_batch_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
+                                          C.c_void_p(out.data_ptr()), *args, _stream_ptr(frames.device.index)))
+        return out
+    frames = np.ascontiguousarray(frames, dtype=np.float64)
+    out = np.empty_like(frames)
+    _check(lib().sl_denoise_batch_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))
     return out
 
 

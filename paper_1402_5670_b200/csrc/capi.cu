@@ -1,0 +1,610 @@
+// B200 shearlet engine: system construction on the GPU, dec/rec orchestration
+// and the C ABI declared in include/shearlet_b200.h.
+//
+// Reference mapping (under /root/reference/proj/core):
+//   build_system_2d   src/system2d.cpp:75-116   -> System::build_2d
+//   build_system_3d   src/system3d.cpp:82-142   -> System::build_3d
+//   forward 2D/3D     src/transform.cpp:13-61   -> dec_2d / dec_3d
+//   inverse 2D/3D     src/transform.cpp:63-125  -> rec_2d / rec_3d
+//   hard_threshold    src/apps.cpp:57-112       -> deltas() + k_threshold / fused epilogue
+//   denoise           src/apps.cpp:114-121      -> sl_denoise_dev
+#include "build.cuh"
+#include "transform.cuh"
+#include "phantoms.cuh"
+
+// ====================================================================== C ABI
+using namespace slb;
+
+struct sl_system {
+    System s;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return SL_OK;
+    } catch (const SlError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return SL_ERR_DOMAIN;
+    } catch (const std::bad_alloc& e) {
+        g_err = "host allocation failed";
+        return SL_ERR_GENERIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SL_ERR_GENERIC;
+    }
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) SL_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+System& sys_of(sl_system* h) {
+    if (!h) throw SlError(SL_ERR_INVALID, "null system handle");
+    return h->s;
+}
+const System& sys_of(const sl_system* h) {
+    if (!h) throw SlError(SL_ERR_INVALID, "null system handle");
+    return h->s;
+}
+cudaStream_t stream_of(void* st) { return static_cast<cudaStream_t>(st); }
+
+void require_dev_ptr(const void* p, const char* what) {
+    if (!p) throw SlError(SL_ERR_INVALID, std::string(what) + ": null pointer");
+}
+
+int create(int ndim, const int* n, const int* levels, int n_scales, int j0, int full, int impulse_fan, int device,
+           int lo, int hi, sl_system** out) {
+    return guard([&] {
+        if (!out) throw SlError(SL_ERR_INVALID, "null output handle");
+        *out = nullptr;
+        if (n_scales < 0) throw SlError(SL_ERR_CONFIG, "ScaleProfile: n_scales must be >= 0");
+        if (n_scales > 0 && !levels) throw SlError(SL_ERR_INVALID, "null levels");
+        for (int a = 0; a < ndim; ++a)
+            if (n[a] < 8)
+                throw SlError(SL_ERR_UNSUPPORTED_SIZE, ndim == 2 ? "build_system_2d: grid must be at least 8x8"
+                                                                 : "build_system_3d: each dim must be >= 8");
+        DeviceGuard dg(device);
+        auto h = std::make_unique<sl_system>();
+        System& s = h->s;
+        s.ndim = ndim;
+        for (int a = 0; a < ndim; ++a) s.n[a] = n[a];
+        s.prof.levels.assign(levels, levels + n_scales);
+        s.prof.j0 = j0;
+        s.full = full != 0;
+        s.device = device;
+        init_geometry(s);
+        cudaStream_t st;
+        SL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        try {
+            if (ndim == 2)
+                build_2d(s, impulse_fan, st);
+            else
+                build_3d(s, impulse_fan, st);
+            SL_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaStreamDestroy(st);
+        set_shard(s, lo, hi);
+        *out = h.release();
+    });
+}
+}  // namespace
+
+extern "C" {
+
+const char* sl_version(void) { return "shearlet_b200 0.1 (sm_100a fp64)"; }
+const char* sl_last_error(void) { return g_err.c_str(); }
+
+int sl_device_count(int* count) {
+    return guard([&] {
+        if (!count) throw SlError(SL_ERR_INVALID, "null count");
+        SL_CUDA(cudaGetDeviceCount(count));
+    });
+}
+
+int sl_system_create_2d(int rows, int cols, const int* levels, int n_scales, int j0, int full_system, int impulse_fan,
+                        int device, int shard_lo, int shard_hi, sl_system** out) {
+    const int n[2] = {rows, cols};
+    return create(2, n, levels, n_scales, j0, full_system, impulse_fan, device, shard_lo, shard_hi, out);
+}
+
+int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
+                        int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out) {
+    const int n[3] = {n0, n1, n2};
+    return create(3, n, levels, n_scales, j0, full_system, impulse_fan, device, shard_lo, shard_hi, out);
+}
+
+int sl_system_destroy(sl_system* sys) {
+    return guard([&] {
+        if (!sys) return;
+        DeviceGuard dg(sys->s.device);
+        delete sys;
+    });
+}
+
+int sl_ndim(const sl_system* h, int* ndim, int64_t dims[3]) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (ndim) *ndim = s.ndim;
+        if (dims)
+            for (int a = 0; a < 3; ++a) dims[a] = a < s.ndim ? s.n[a] : 1;
+    });
+}
+
+int sl_redundancy(const sl_system* h, int* R) {
+    return guard([&] {
+        if (!R) throw SlError(SL_ERR_INVALID, "null R");
+        *R = sys_of(h).R;
+    });
+}
+
+int sl_shard(const sl_system* h, int* lo, int* hi) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (lo) *lo = s.lo;
+        if (hi) *hi = s.hi;
+    });
+}
+
+int sl_index(const sl_system* h, int32_t* rec) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (!rec) throw SlError(SL_ERR_INVALID, "null records");
+        for (int i = 0; i < s.R; ++i) {
+            const Record& r = s.index[static_cast<size_t>(i)];
+            rec[4 * i] = r.kind;
+            rec[4 * i + 1] = r.scale;
+            rec[4 * i + 2] = r.k1;
+            rec[4 * i + 3] = r.k2;
+        }
+    });
+}
+
+int sl_filter_norms(const sl_system* h, double* rms) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (!rms) throw SlError(SL_ERR_INVALID, "null output");
+        std::memcpy(rms, s.rms.data(), s.rms.size() * sizeof(double));
+    });
+}
+
+int sl_frame_bounds(const sl_system* h, double* A, double* B) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (A) *A = s.Wmin;
+        if (B) *B = s.Wmax;
+    });
+}
+
+int sl_frame_weight(const sl_system* h, double* w) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (!w) throw SlError(SL_ERR_INVALID, "null output");
+        DeviceGuard dg(s.device);
+        std::vector<double> half(static_cast<size_t>(s.nhalf));
+        SL_CUDA(cudaMemcpy(half.data(), s.W.p, half.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        // expand the Hermitian half: W(-xi) = W(xi)
+        const long long rows = s.nrows;
+        const int L = s.L_last;
+        for (long long r = 0; r < rows; ++r) {
+            long long rr = 0;  // index of the negated leading coordinates
+            if (s.ndim == 2) {
+                rr = (s.n[0] - r) % s.n[0];
+            } else {
+                const long long i0 = r / s.n[1], i1 = r % s.n[1];
+                rr = ((s.n[0] - i0) % s.n[0]) * s.n[1] + (s.n[1] - i1) % s.n[1];
+            }
+            for (int k = 0; k < L; ++k)
+                w[r * L + k] = k < s.H ? half[static_cast<size_t>(r * s.ldh + k)]
+                                       : half[static_cast<size_t>(rr * s.ldh + (L - k))];
+        }
+    });
+}
+
+int sl_filter_spectrum(sl_system* h, int i, double* out) {
+    return guard([&] {
+        System& s = sys_of(h);
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (i < 0 || i >= s.R) throw SlError(SL_ERR_DOMAIN, "filter index out of range");
+        if (!out) throw SlError(SL_ERR_INVALID, "null output");
+        DeviceGuard dg(s.device);
+        std::vector<double> half(static_cast<size_t>(s.nhalf));
+        if (s.ndim == 2) {
+            SL_CUDA(cudaMemcpy(half.data(), s.psi.p + static_cast<size_t>(i) * s.nhalf, half.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+        } else {
+            // synthesise on the device through the same energy kernel path
+            DBuf<double> tmp;
+            tmp.alloc(static_cast<size_t>(s.nhalf));
+            FiltSynth3DFlat f{s.synth, s.ldh};
+            k_synth_band<<<1024, 256>>>(f, i, s.nhalf, tmp.p);
+            check_launch("k_synth_band");
+            SL_CUDA(cudaMemcpy(half.data(), tmp.p, half.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+        const long long rows = s.nrows;
+        const int L = s.L_last;
+        for (long long r = 0; r < rows; ++r) {
+            long long rr;
+            if (s.ndim == 2) {
+                rr = (s.n[0] - r) % s.n[0];
+            } else {
+                const long long i0 = r / s.n[1], i1 = r % s.n[1];
+                rr = ((s.n[0] - i0) % s.n[0]) * s.n[1] + (s.n[1] - i1) % s.n[1];
+            }
+            for (int k = 0; k < L; ++k) {
+                out[2 * (r * L + k)] = k < s.H ? half[static_cast<size_t>(r * s.ldh + k)]
+                                               : half[static_cast<size_t>(rr * s.ldh + (L - k))];
+                out[2 * (r * L + k) + 1] = 0.0;
+            }
+        }
+    });
+}
+
+int sl_sheardec_dev(sl_system* h, const double* f, double* coeffs, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(f, "sheardec input");
+        require_dev_ptr(coeffs, "sheardec output");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        dec(s, f, coeffs, nullptr, stream_of(stream));
+    });
+}
+
+int sl_sheardec_threshold_dev(sl_system* h, const double* f, double* coeffs, const double* K, int nK, double sigma,
+                              int scaled, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(f, "sheardec input");
+        require_dev_ptr(coeffs, "sheardec output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        dec(s, f, coeffs, s.delta.p, stream_of(stream));
+    });
+}
+
+int sl_shearrec_dev(sl_system* h, const double* coeffs, int nbands, double* f, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "inverse: coefficient stack does not match the system");
+        require_dev_ptr(coeffs, "shearrec input");
+        require_dev_ptr(f, "shearrec output");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        rec(s, coeffs, f, stream_of(stream));
+    });
+}
+
+int sl_hard_threshold_dev(sl_system* h, const double* in, double* out, int nbands, const double* K, int nK,
+                          double sigma, int scaled, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "hard_threshold: stack does not match the system");
+        require_dev_ptr(in, "hard_threshold input");
+        require_dev_ptr(out, "hard_threshold output");
+        dim3 grid(static_cast<unsigned>(std::min<long long>(1024, (s.nreal + 255) / 256)), s.nb());
+        LaunchScope ls(s, "threshold", stream_of(stream), s.nb());
+        k_threshold<<<grid, 256, 0, stream_of(stream)>>>(in, out, s.nreal, s.delta.p + s.lo);
+        check_launch("k_threshold");
+    });
+}
+
+int sl_denoise_dev(sl_system* h, const double* in, double* out, const double* K, int nK, double sigma, int scaled,
+                   void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(in, "denoise input");
+        require_dev_ptr(out, "denoise output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        dec(s, in, s.stack.p, s.delta.p, stream_of(stream));
+        rec(s, s.stack.p, out, stream_of(stream));
+    });
+}
+
+// ---- batched variants: frames fanned out over the handle's workspaces ----
+}  // extern "C"
+namespace {
+// Runs per_frame(frame, stream) for every frame, spreading frames round-robin
+// over min(nstreams, nframes) workspaces whose streams fork from / join into
+// the caller's stream (workspace 0 runs on the caller's stream itself).
+template <class Fn>
+void fan_out(System& s, int nframes, cudaStream_t user, Fn&& per_frame) {
+    const int K = std::max(1, std::min(s.nstreams, nframes));
+    s.ensure_workspaces(K);
+    if (K > 1) {
+        SL_CUDA(cudaEventRecord(s.fork_ev, user));
+        for (int k = 1; k < K; ++k) SL_CUDA(cudaStreamWaitEvent(s.ws[static_cast<size_t>(k)]->st, s.fork_ev, 0));
+    }
+    try {
+        for (int f = 0; f < nframes; ++f) {
+            const int k = f % K;
+            s.w = s.ws[static_cast<size_t>(k)].get();
+            per_frame(f, k == 0 ? user : s.w->st);
+        }
+    } catch (...) {
+        s.w = s.ws[0].get();
+        throw;
+    }
+    s.w = s.ws[0].get();
+    for (int k = 1; k < K; ++k) {
+        System::Workspace& wk = *s.ws[static_cast<size_t>(k)];
+        SL_CUDA(cudaEventRecord(wk.ev, wk.st));
+        SL_CUDA(cudaStreamWaitEvent(user, wk.ev, 0));
+    }
+}
+}  // namespace
+extern "C" {
+
+int sl_set_streams(sl_system* h, int nstreams) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (nstreams < 1 || nstreams > 16) throw SlError(SL_ERR_CONFIG, "nstreams must be in [1, 16]");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        s.nstreams = nstreams;
+    });
+}
+
+int sl_sheardec_batch_dev(sl_system* h, const double* f, int nframes, double* coeffs, const double* K, int nK,
+                          double sigma, int scaled, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(f, "sheardec input");
+        require_dev_ptr(coeffs, "sheardec output");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        cudaStream_t st = stream_of(stream);
+        if (K) deltas(s, K, nK, sigma, scaled, st);
+        const double* dl = K ? s.delta.p : nullptr;
+        fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+            dec(s, f + static_cast<size_t>(fr) * s.nreal, coeffs + static_cast<size_t>(fr) * s.nb() * s.nreal, dl, fst);
+        });
+    });
+}
+
+int sl_shearrec_batch_dev(sl_system* h, const double* coeffs, int nframes, double* f, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(coeffs, "shearrec input");
+        require_dev_ptr(f, "shearrec output");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        fan_out(s, nframes, stream_of(stream), [&](int fr, cudaStream_t fst) {
+            rec(s, coeffs + static_cast<size_t>(fr) * s.nb() * s.nreal, f + static_cast<size_t>(fr) * s.nreal, fst);
+        });
+    });
+}
+
+int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* out, const double* K, int nK,
+                         double sigma, int scaled, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(in, "denoise input");
+        require_dev_ptr(out, "denoise output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        cudaStream_t st = stream_of(stream);
+        deltas(s, K, nK, sigma, scaled, st);
+        fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+            s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+            dec(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, s.delta.p, fst);
+            rec(s, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal, fst);
+        });
+    });
+}
+
+// Host in/out (e2e): H2D of all frames, batched dec/thr/rec, D2H of the results.
+int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* out, const double* K, int nK,
+                          double sigma, int scaled) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!in || !out) throw SlError(SL_ERR_INVALID, "null host pointer");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        const size_t n = static_cast<size_t>(nframes) * s.nreal;
+        s.io_in.alloc(n);
+        s.io_out.alloc(n);
+        cudaStream_t st = 0;
+        SL_CUDA(cudaMemcpyAsync(s.io_in.p, in, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        deltas(s, K, nK, sigma, scaled, st);
+        fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+            s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+            dec(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, s.delta.p, fst);
+            rec(s, s.w->stack.p, s.io_out.p + static_cast<size_t>(fr) * s.nreal, fst);
+        });
+        SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SL_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// ---- host-pointer variants ----------------------------------------------
+int sl_sheardec_host(sl_system* h, const double* f, double* coeffs) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!f || !coeffs) throw SlError(SL_ERR_INVALID, "null host pointer");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        s.io_in.alloc(static_cast<size_t>(s.nreal));
+        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        SL_CUDA(cudaMemcpy(s.io_in.p, f, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
+        dec(s, s.io_in.p, s.stack.p, nullptr, 0);
+        SL_CUDA(cudaMemcpy(coeffs, s.stack.p, static_cast<size_t>(s.nb()) * s.nreal * sizeof(double),
+                           cudaMemcpyDeviceToHost));
+    });
+}
+
+int sl_shearrec_host(sl_system* h, const double* coeffs, int nbands, double* f) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "inverse: coefficient stack does not match the system");
+        if (!f || !coeffs) throw SlError(SL_ERR_INVALID, "null host pointer");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        s.io_out.alloc(static_cast<size_t>(s.nreal));
+        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        SL_CUDA(cudaMemcpy(s.stack.p, coeffs, static_cast<size_t>(s.nb()) * s.nreal * sizeof(double),
+                           cudaMemcpyHostToDevice));
+        rec(s, s.stack.p, s.io_out.p, 0);
+        SL_CUDA(cudaMemcpy(f, s.io_out.p, s.nreal * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int sl_hard_threshold_host(sl_system* h, const double* in, double* out, int nbands, const double* K, int nK,
+                           double sigma, int scaled) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!in || !out) throw SlError(SL_ERR_INVALID, "null host pointer");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        deltas(s, K, nK, sigma, scaled, 0);
+        if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "hard_threshold: stack does not match the system");
+        const size_t n = static_cast<size_t>(s.nb()) * s.nreal;
+        s.stack.alloc(n);
+        SL_CUDA(cudaMemcpy(s.stack.p, in, n * sizeof(double), cudaMemcpyHostToDevice));
+        dim3 grid(static_cast<unsigned>(std::min<long long>(1024, (s.nreal + 255) / 256)), s.nb());
+        k_threshold<<<grid, 256>>>(s.stack.p, s.stack.p, s.nreal, s.delta.p + s.lo);
+        check_launch("k_threshold");
+        SL_CUDA(cudaMemcpy(out, s.stack.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int sl_denoise_host(sl_system* h, const double* in, double* out, const double* K, int nK, double sigma, int scaled) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!in || !out) throw SlError(SL_ERR_INVALID, "null host pointer");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        deltas(s, K, nK, sigma, scaled, 0);
+        s.io_in.alloc(static_cast<size_t>(s.nreal));
+        s.io_out.alloc(static_cast<size_t>(s.nreal));
+        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        SL_CUDA(cudaMemcpy(s.io_in.p, in, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
+        dec(s, s.io_in.p, s.stack.p, s.delta.p, 0);
+        rec(s, s.stack.p, s.io_out.p, 0);
+        SL_CUDA(cudaMemcpy(out, s.io_out.p, s.nreal * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int sl_profile(sl_system* h, int enable) {
+    return guard([&] {
+        System& s = sys_of(h);
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        collect_profile(s);
+        s.stats.clear();
+        s.profiling = enable != 0;
+    });
+}
+
+int sl_pass_stats(sl_system* h, int max_passes, char* names, double* ms_total, int64_t* launches, int64_t* units,
+                  int* n_passes) {
+    return guard([&] {
+        System& s = sys_of(h);
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        collect_profile(s);
+        int i = 0;
+        for (const auto& kv : s.stats) {
+            if (i >= max_passes) break;
+            if (names) {
+                std::memset(names + 32 * i, 0, 32);
+                std::strncpy(names + 32 * i, kv.first.c_str(), 31);
+            }
+            if (ms_total) ms_total[i] = kv.second.ms;
+            if (launches) launches[i] = kv.second.n;
+            if (units) units[i] = kv.second.units;
+            ++i;
+        }
+        if (n_passes) *n_passes = i;
+    });
+}
+
+int sl_launch_count(const sl_system* h, int64_t* count) {
+    return guard([&] {
+        if (!count) throw SlError(SL_ERR_INVALID, "null count");
+        *count = sys_of(h).launches;
+    });
+}
+
+int sl_phantom_cartoon(int n, double* out) {
+    return guard([&] {
+        if (n <= 0 || !out) throw SlError(SL_ERR_INVALID, "bad cartoon arguments");
+        cartoon(n, out);
+    });
+}
+
+int sl_phantom_cartoon_volume(int n, double* out) {
+    return guard([&] {
+        if (n <= 0 || !out) throw SlError(SL_ERR_INVALID, "bad cartoon_volume arguments");
+        cartoon_volume(n, out);
+    });
+}
+
+int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double sigma, uint64_t seed) {
+    return guard([&] {
+        if (sigma < 0.0) throw SlError(SL_ERR_DOMAIN, "add_gaussian_noise: sigma must be >= 0");
+        if (!in || !out) throw SlError(SL_ERR_INVALID, "null pointer");
+        if (in != out) std::memcpy(out, in, static_cast<size_t>(count) * sizeof(double));
+        if (sigma == 0.0) return;
+        Mt64 rng(seed);
+        bool have = false;
+        double spare = 0.0;
+        auto uni = [&rng] { return static_cast<double>(rng()) * 0x1.0p-64; };
+        for (int64_t i = 0; i < count; ++i) {
+            double g;
+            if (have) {
+                have = false;
+                g = spare;
+            } else {
+                double u1;
+                do {
+                    u1 = uni();
+                } while (u1 <= 0.0);
+                const double u2 = uni();
+                const double r = std::sqrt(-2.0 * std::log(u1));
+                const double a = 2.0 * M_PI * u2;
+                spare = r * std::sin(a);
+                have = true;
+                g = r * std::cos(a);
+            }
+            out[i] += sigma * g;
+        }
+    });
+}
+
+}  // extern "C"

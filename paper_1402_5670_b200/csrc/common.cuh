@@ -1,0 +1,283 @@
+// Shared host-side infrastructure of the engine: errors, device buffers,
+// FFT plans, launch configuration and the System handle.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/shearlet_b200.h"
+#include "kernels.cuh"
+#include "taps.hpp"
+
+namespace slb {
+
+// ------------------------------------------------------------------ errors
+struct SlError : std::runtime_error {
+    int code;
+    SlError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define SL_CUDA(x)                                                                                  \
+    do {                                                                                            \
+        cudaError_t e_ = (x);                                                                       \
+        if (e_ != cudaSuccess)                                                                      \
+            throw SlError(SL_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+static void check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw SlError(SL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ device buffers
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count <= n && p) return;
+        release();
+        if (count == 0) return;
+        SL_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    // Synchronous upload (construction time only). The copy is ordered on the
+    // stream that consumes it and completed before returning: a pageable
+    // cudaMemcpy may return before its DMA lands, and kernels on a non-blocking
+    // stream are not ordered after the legacy stream.
+    void upload(const T* h, size_t count, cudaStream_t st) {
+        SL_CUDA(cudaStreamSynchronize(st));
+        alloc(count);
+        SL_CUDA(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+        SL_CUDA(cudaStreamSynchronize(st));
+    }
+};
+
+// ------------------------------------------------------------------ FFT plans
+struct PlanHolder {
+    FftPlan plan;
+    DBuf<double2> tw;
+};
+
+static std::vector<int> factor_radices(int L) {
+    std::vector<int> r;
+    int m = L;
+    while (m % 8 == 0) { r.push_back(8); m /= 8; }
+    while (m % 4 == 0) { r.push_back(4); m /= 4; }
+    while (m % 2 == 0) { r.push_back(2); m /= 2; }
+    while (m % 3 == 0) { r.push_back(3); m /= 3; }
+    while (m % 5 == 0) { r.push_back(5); m /= 5; }
+    for (int f = 7; m > 1; f += 2)
+        while (m % f == 0) { r.push_back(f); m /= f; }
+    return r;
+}
+
+static void make_plan(int L, PlanHolder& ph, cudaStream_t st) {
+    const std::vector<int> r = factor_radices(L);
+    if (static_cast<int>(r.size()) > kMaxStages) throw SlError(SL_ERR_UNSUPPORTED_SIZE, "FFT length has too many factors");
+    for (int x : r)
+        if (x > 64) throw SlError(SL_ERR_UNSUPPORTED_SIZE, "FFT length has a prime factor > 64");
+    ph.plan.L = L;
+    ph.plan.nst = static_cast<int>(r.size());
+    int ns = 1;
+    for (size_t s = 0; s < r.size(); ++s) {
+        ph.plan.radix[s] = r[s];
+        ph.plan.ns[s] = ns;
+        ns *= r[s];
+    }
+    std::vector<double2> tw(static_cast<size_t>(L));
+    for (int k = 0; k < L; ++k) {
+        const long double a = -2.0L * 3.141592653589793238462643383279502884L * k / L;
+        tw[static_cast<size_t>(k)] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(sinl(a)));
+    }
+    ph.tw.upload(tw.data(), tw.size(), st);
+    ph.plan.tw = ph.tw.p;
+}
+
+// ------------------------------------------------------------------ launch helpers
+static constexpr int kMaxLen = 4096;  // per-line FFT length limit (shared-memory tile)
+
+struct LineCfg {
+    int V;
+    size_t smem;
+    int threads;
+};
+
+// Lines per CTA so that a tile is ~4096 complex (64 KiB per ping-pong buffer).
+static LineCfg line_cfg(int L, bool strided) {
+    int V = std::max(1, 4096 / L);
+    if (strided) V = std::max(V, 8);
+    V = std::min(V, 64);
+    while (V > 1 && 2ull * V * (L + 1) * sizeof(double2) > 200 * 1024) V /= 2;
+    LineCfg c;
+    c.V = V;
+    c.smem = 2ull * V * (L + 1) * sizeof(double2);
+    c.threads = 256;
+    return c;
+}
+
+template <class K>
+static void set_smem(K kern, size_t smem) {
+    static std::mutex mu;
+    static std::map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(reinterpret_cast<const void*>(kern));
+    if (it != done.end() && it->second >= smem) return;
+    SL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    done[reinterpret_cast<const void*>(kern)] = smem;
+}
+
+// ------------------------------------------------------------------ system
+struct System {
+    int ndim = 2;
+    int n[3] = {1, 1, 1};
+    int L_last = 0, H = 0, ldh = 0;
+    long long nreal = 0, nhalf = 0;
+    int nrows = 0;  // product of the leading dims
+    Profile prof;
+    bool full = false;
+    int device = 0;
+    std::vector<Record> index;
+    int R = 0;
+    int lo = 0, hi = 0;  // shard
+    std::vector<double> rms;
+    double Wmin = 0, Wmax = 0;
+
+    std::map<int, std::unique_ptr<PlanHolder>> plans;
+    DBuf<double> psi;   // 2D: [R][nhalf] real
+    // 2D fast path (fast2d.cuh): column-major halves psi^T [R][H][n0], W^T [H][n0]
+    bool fast2d = false;
+    DBuf<double> psiT, WT;
+    DBuf<double> W;     // [nhalf]
+    // 3D synthesis tables
+    DBuf<BandDesc3D> bands3;
+    DBuf<double> tab1, tab2;
+    FiltSynth3D synth{};
+    // scratch: one workspace per concurrent stream (batched calls fan frames
+    // out over several workspaces); `w` is the workspace the next pass uses.
+    struct Workspace {
+        DBuf<double2> F, inter, acc, slots;
+        DBuf<double> stack;
+        cudaStream_t st = nullptr;  // owned stream (workspaces > 0)
+        cudaEvent_t ev = nullptr;
+        ~Workspace() {
+            if (ev) cudaEventDestroy(ev);
+            if (st) cudaStreamDestroy(st);
+        }
+    };
+    std::vector<std::unique_ptr<Workspace>> ws;
+    Workspace* w = nullptr;
+    int nstreams = 4;               // workspaces used by batched calls
+    cudaEvent_t fork_ev = nullptr;
+    DBuf<double> delta, stack, io_in, io_out;
+    int chunk = 1;
+    std::mutex mu;
+
+    // instrumentation: kernel launch count (always) and optional per-pass
+    // CUDA-event timing (sl_profile); events are recorded on the launch stream.
+    long long launches = 0;
+    bool profiling = false;
+    struct PendingEv {
+        std::string name;
+        cudaEvent_t a, b;
+        long long units;
+    };
+    std::vector<PendingEv> pending;
+    struct PassStat {
+        double ms = 0;
+        long long n = 0;
+        long long units = 0;  // bands (or spectra) processed
+    };
+    std::map<std::string, PassStat> stats;
+
+    int nb() const { return hi - lo; }
+
+    System() {
+        ws.emplace_back(new Workspace());
+        w = ws[0].get();
+    }
+    ~System() {
+        if (fork_ev) cudaEventDestroy(fork_ev);
+    }
+    // Ensure n workspaces exist (1..n-1 with their own non-blocking streams).
+    void ensure_workspaces(int n) {
+        if (!fork_ev) SL_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+        while (static_cast<int>(ws.size()) < n) {
+            auto p = std::make_unique<Workspace>();
+            SL_CUDA(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+            SL_CUDA(cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming));
+            ws.push_back(std::move(p));
+        }
+    }
+
+    const FftPlan& plan(int L, cudaStream_t st) {
+        auto it = plans.find(L);
+        if (it != plans.end()) return it->second->plan;
+        auto ph = std::make_unique<PlanHolder>();
+        make_plan(L, *ph, st);
+        const FftPlan& p = ph->plan;
+        plans[L] = std::move(ph);
+        return p;
+    }
+};
+
+// Brackets one kernel launch: counts it and, when profiling, records a
+// start/stop event pair on the launch stream.
+struct LaunchScope {
+    System& s;
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaStream_t st;
+    const char* name;
+    long long units;
+    LaunchScope(System& sys, const char* nm, cudaStream_t stream, long long u = 1)
+        : s(sys), st(stream), name(nm), units(u) {
+        ++s.launches;
+        if (s.profiling) {
+            SL_CUDA(cudaEventCreate(&a));
+            SL_CUDA(cudaEventCreate(&b));
+            SL_CUDA(cudaEventRecord(a, st));
+        }
+    }
+    ~LaunchScope() {
+        if (a) {
+            cudaEventRecord(b, st);
+            s.pending.push_back({name, a, b, units});
+        }
+    }
+};
+
+static void collect_profile(System& s) {
+    for (auto& p : s.pending) {
+        SL_CUDA(cudaEventSynchronize(p.b));
+        float ms = 0;
+        SL_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto& st = s.stats[p.name];
+        st.ms += ms;
+        st.n += 1;
+        st.units += p.units;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    s.pending.clear();
+}
+
+}  // namespace slb

@@ -1,0 +1,293 @@
+// Specialised 2D dec / rec kernels (register-resident FFT lines, compile-time
+// lengths) for grids whose n0 and n1 both have a RegPlan.
+//
+// Layout: every half spectrum is stored column-major, X^T[k1][k0] with
+// k1 < H = n1/2 + 1 and k0 < n0, so an axis-0 line is contiguous. The filter
+// bank psi^T[b][k1][k0] (real) and W^T share that layout.
+//
+//   dec : cols_dec  (F^T * psi_b -> IFFT_0 -> inter^T[b])         per band group
+//         rows_c2r  (inter^T -> pair-packed IFFT_1 -> 1/N, threshold -> band)
+//   rec : rows_r2c  (band -> pair-packed FFT_1 -> inter^T[b])
+//         cols_rec  (sum_{b in group} FFT_0(inter^T[b]) * psi_b -> slot)
+//         cols_final(sum_slots / W -> IFFT_0 -> inter^T[0]) ; rows_c2r -> f
+// The rows kernels stage the column-major intermediate through a
+// [2V rows][H] shared tile (coalesced 2V*16-byte runs per k1); the pair's
+// rows of that tile double as the line's FFT exchange buffer.
+#pragma once
+
+#include "fft_reg.cuh"
+
+namespace slb {
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// CTA shapes: rows kernels take V = 256 / T row pairs (256 threads, a ~66 KB
+// [2V][H] tile); column kernels take 128 / T lines (128 threads, L * 16 B each).
+template <int L>
+struct RowCfg {
+    static constexpr int T = RegPlan<L>::T;
+    static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
+    static constexpr int THREADS = V * T;
+};
+template <int L>
+struct ColCfg {
+    static constexpr int T = RegPlan<L>::T;
+    static constexpr int LINES = (128 / T) > 0 ? 128 / T : 1;
+    static constexpr int THREADS = LINES * T;
+    static constexpr int MIN_BLOCKS = 65536 / (THREADS * 88) > 0 ? 65536 / (THREADS * 88) : 1;  // <= ~88 regs
+};
+
+// ---------------------------------------------------------------- rows c2r
+// In : src[k1 * n0 + r] (column-major half spectrum), bands strided by sbs.
+// Out: dst[r * L + i] real rows, scaled, optionally thresholded (delta >= 0).
+template <int L>
+__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+    k2_rows_c2r(const double2* __restrict__ src, long long sbs, double* __restrict__ dst, long long dbs, int n0,
+                int H, double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    extern __shared__ double2 tile[];  // [2V][H]
+    const int r0 = blockIdx.x * 2 * V;
+    src += blockIdx.y * sbs;
+    dst += blockIdx.y * dbs;
+    const int nrows = min(2 * V, n0 - r0);
+    // all tile loads in flight at once (cp.async, 16 B each, L2 only)
+    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
+        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+        if (rr < nrows)
+            cp_async16(tile + rr * H + k, src + (long long)k * n0 + r0 + rr);
+        else
+            tile[rr * H + k] = make_double2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int q = threadIdx.x / T, t = threadIdx.x - q * T;
+    const double2* Xr = tile + (2 * q) * H;
+    const double2* Yr = Xr + H;
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k = t + T * m;
+        double2 X, Y;
+        if (k < H) {
+            X = Xr[k];
+            Y = Yr[k];
+            if (k == 0 || 2 * k == L) {
+                X.y = 0.0;
+                Y.y = 0.0;
+            }
+            x[m] = make_double2(X.x - Y.y, X.y + Y.x);  // X + iY
+        } else {
+            X = Xr[L - k];
+            Y = Yr[L - k];
+            x[m] = make_double2(X.x + Y.y, Y.x - X.y);  // conj(X) + i conj(Y)
+        }
+    }
+    double2* lb = tile + (2 * q) * H;  // this pair's rows double as its exchange buffer (2H >= L)
+    line_sync<T>();
+    reg_fft<L, +1>(x, lb, t, tw);
+    const double dl = delta ? delta[band0 + blockIdx.y] : -1.0;
+    const int ra = r0 + 2 * q;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        double a = x[m].x * scale, b = x[m].y * scale;
+        if (dl >= 0.0) {
+            if (fabs(a) < dl) a = 0.0;
+            if (fabs(b) < dl) b = 0.0;
+        }
+        const int i = t + T * m;
+        if (ra < n0) dst[(long long)ra * L + i] = a;
+        if (ra + 1 < n0) dst[(long long)(ra + 1) * L + i] = b;
+    }
+}
+
+// ---------------------------------------------------------------- rows r2c
+// In : real rows src[r * L + i]; Out: column-major half spectrum dst[k1 * n0 + r].
+template <int L>
+__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+    k2_rows_r2c(const double* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int n0,
+                int H, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    constexpr int KPT = (L / 2 + 1 + T - 1) / T;  // split outputs per thread
+    extern __shared__ double2 tile[];            // [2V][H]
+    const int r0 = blockIdx.x * 2 * V;
+    src += blockIdx.y * sbs;
+    dst += blockIdx.y * dbs;
+    const int q = threadIdx.x / T, t = threadIdx.x - q * T;
+    const int ra = r0 + 2 * q;
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int i = t + T * m;
+        const double a = ra < n0 ? __ldg(src + (long long)ra * L + i) : 0.0;
+        const double b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : 0.0;
+        x[m] = make_double2(a, b);
+    }
+    double2* lb = tile + (2 * q) * H;
+    reg_fft<L, -1>(x, lb, t, tw);
+    // Z in registers (element t + T m); publish to the line buffer, then split
+#pragma unroll
+    for (int m = 0; m < E; ++m) lb[swz(t + T * m)] = x[m];
+    line_sync<T>();
+    double2 zk[KPT], zm[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            zk[u] = lb[swz(k)];
+            zm[u] = lb[swz(k == 0 ? 0 : L - k)];
+        }
+    }
+    line_sync<T>();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            lb[k] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));          // X
+            lb[H + k] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));      // Y
+        }
+    }
+    __syncthreads();
+    const int nrows = min(2 * V, n0 - r0);
+    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
+        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+        if (rr < nrows) __stcg(dst + (long long)k * n0 + r0 + rr, tile[rr * H + k]);
+    }
+}
+
+// ---------------------------------------------------------------- column lines
+// Column k1 of a column-major half spectrum is the contiguous line src[k1 * L ...].
+
+// dec: inter[b] = IFFT_0(F * psi_b) for the G bands of this CTA's group.
+template <int L>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
+    k2_cols_dec(const double2* __restrict__ FT, const double* __restrict__ psiT, long long pbs,
+                double2* __restrict__ inter, long long ibs, int H, int band0, int G, int nb,
+                const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    extern __shared__ double2 lbuf[];  // per line: [exchange L][F column L]
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
+    const bool valid = k1 < H;
+    double2* sm = lbuf + li * 2 * L;
+    double2* fs = sm + L;
+#ifndef SLB_NO_CPASYNC
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        if (valid)
+            cp_async16(fs + t + T * m, FT + (long long)k1 * L + t + T * m);
+        else
+            fs[t + T * m] = make_double2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+#else
+#pragma unroll
+    for (int m = 0; m < E; ++m) fs[t + T * m] = valid ? __ldg(FT + (long long)k1 * L + t + T * m) : make_double2(0.0, 0.0);
+#endif
+    const int g0 = blockIdx.y * G;
+    const int gn = min(G, nb - g0);
+    for (int bb = 0; bb < gn; ++bb) {
+        const int b = g0 + bb;
+        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+        double2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const double p = valid ? __ldg(ps + t + T * m) : 0.0;
+            const double2 fv = fs[t + T * m];
+            x[m] = make_double2(fv.x * p, fv.y * p);  // conj(psi) * F, psi real
+        }
+        reg_fft<L, +1>(x, sm, t, tw);
+        if (valid) {
+            double2* o = inter + (long long)b * ibs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) __stcg(o + t + T * m, x[m]);
+        }
+        line_sync<T>();
+    }
+}
+
+// rec: slot[g] = sum_{b in group g} FFT_0(inter[b]) * psi_b.
+template <int L>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
+    k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
+                double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
+                const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    extern __shared__ double2 lbuf[];  // per line: [exchange L][accumulator L]
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
+    const bool valid = k1 < H;
+    double2* sm = lbuf + li * 2 * L;
+    double2* acc = sm + L;  // thread t owns acc[t + T m]
+#pragma unroll
+    for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
+    const int g0 = blockIdx.y * G;
+    const int gn = min(G, nb - g0);
+    for (int bb = 0; bb < gn; ++bb) {
+        const int b = g0 + bb;
+        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
+        double2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : make_double2(0.0, 0.0);
+        reg_fft<L, -1>(x, sm, t, tw);
+        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const double p = valid ? __ldg(ps + t + T * m) : 0.0;
+            double2 a = acc[t + T * m];
+            a.x = fma(x[m].x, p, a.x);
+            a.y = fma(x[m].y, p, a.y);
+            acc[t + T * m] = a;
+        }
+        line_sync<T>();
+    }
+    if (valid) {
+        double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, acc[t + T * m]);
+    }
+}
+
+// final rec column pass: IFFT_0((sum_s slot[s]) / W) -> out; also the plain
+// forward column FFT (F = FFT_0 of the rows pass) when W == nullptr && DIR < 0.
+template <int L, int DIR>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+    k2_cols_sum(const double2* __restrict__ slots, long long sbs, int nslots, const double* __restrict__ WT,
+                double2* __restrict__ out, int H, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    extern __shared__ double2 lbuf[];
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
+    const bool valid = k1 < H;
+    double2* sm = lbuf + li * L;
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) x[m] = make_double2(0.0, 0.0);
+    if (valid) {
+        for (int s = 0; s < nslots; ++s) {
+            const double2* in = slots + (long long)s * sbs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) x[m] = cadd(x[m], __ldcg(in + t + T * m));
+        }
+        if (WT) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const double w = __ldg(WT + (long long)k1 * L + t + T * m);
+                x[m] = make_double2(x[m].x / w, x[m].y / w);
+            }
+        }
+    }
+    reg_fft<L, DIR>(x, sm, t, tw);
+    if (valid) {
+        double2* o = out + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, x[m]);
+    }
+}
+
+}  // namespace slb

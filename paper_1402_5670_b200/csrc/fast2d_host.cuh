@@ -1,0 +1,161 @@
+// Host orchestration of the specialised 2D path (kernels in fast2d.cuh).
+#pragma once
+#include <cstdlib>
+
+#include "fast2d.cuh"
+#include "launch.cuh"
+
+namespace slb {
+
+static bool fast2d_supported(int n0, int n1) {
+    if (std::getenv("SLB_DISABLE_FAST2D")) return false;
+    if (n0 != n1) return false;
+    switch (n0) {
+        case 64: case 128: case 192: case 256: case 512: case 1024: case 2048: return true;
+        default: return false;
+    }
+}
+
+static int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::max(1, std::atoi(e)) : dflt;
+}
+
+// Band grouping: G bands per column-pass CTA (F / accumulator reuse), C bands
+// per chunk (intermediate kept around 32 MiB so it stays L2-resident).
+struct Fast2DCfg {
+    int G, C;
+};
+static Fast2DCfg fast2d_cfg(const System& s) {
+    const int G = env_int("SLB_GROUP", 2);
+    const double per = static_cast<double>(s.H) * s.n[0] * sizeof(double2);
+    int C = env_int("SLB_CHUNK", std::max(1, static_cast<int>((32.0 * 1024 * 1024) / per)));
+    C = std::max(G, (C / G) * G);
+    return {G, C};
+}
+
+template <int L0, int L1>
+static void dec2d_fast_t(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    const int n0 = s.n[0], H = s.H;
+    const long long nhT = static_cast<long long>(H) * n0;  // column-major half spectrum
+    const Fast2DCfg cfg = fast2d_cfg(s);
+    const int nb = s.nb();
+    const int C = std::min(cfg.C, nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * nhT);
+    s.w->F.alloc(static_cast<size_t>(nhT));
+    const double2* tw0 = s.plan(L0, st).tw;
+    const double2* tw1 = s.plan(L1, st).tw;
+    using RC = RowCfg<L1>;
+    using CC = ColCfg<L0>;
+    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);
+    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    set_smem(k2_rows_r2c<L1>, row_smem);
+    set_smem(k2_rows_c2r<L1>, row_smem);
+    set_smem(k2_cols_sum<L0, -1>, col_smem);
+    set_smem(k2_cols_dec<L0>, 2 * col_smem);
+    const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
+    const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
+    {  // F^T = FFT_0(FFT_1(f))
+        LaunchScope ls(s, "f2_rows_r2c", st, 1);
+        k2_rows_r2c<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(f, 0, s.w->inter.p, 0, n0, H, tw1);
+        check_launch("k2_rows_r2c");
+    }
+    {
+        LaunchScope ls(s, "f2_cols_fwd", st, 1);
+        k2_cols_sum<L0, -1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->inter.p, 0, 1, nullptr, s.w->F.p, H, tw0);
+        check_launch("k2_cols_sum");
+    }
+    const double scale = 1.0 / static_cast<double>(s.nreal);
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        const int groups = (cb + cfg.G - 1) / cfg.G;
+        {
+            LaunchScope ls(s, "f2_cols_dec", st, cb);
+            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+                s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0);
+            check_launch("k2_cols_dec");
+        }
+        {
+            LaunchScope ls(s, delta ? "f2_rows_c2r_thr" : "f2_rows_c2r", st, cb);
+            k2_rows_c2r<L1><<<dim3(row_blocks, cb), RC::THREADS, row_smem, st>>>(
+                s.w->inter.p, nhT, out + static_cast<size_t>(b0) * s.nreal, s.nreal, n0, H, scale, delta, s.lo + b0, tw1);
+            check_launch("k2_rows_c2r");
+        }
+    }
+}
+
+template <int L0, int L1>
+static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    const int n0 = s.n[0], H = s.H;
+    const long long nhT = static_cast<long long>(H) * n0;
+    const Fast2DCfg cfg = fast2d_cfg(s);
+    const int nb = s.nb();
+    const int C = std::min(cfg.C, nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * nhT);
+    int nslots = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) nslots += (std::min(C, nb - b0) + cfg.G - 1) / cfg.G;
+    s.w->slots.alloc(static_cast<size_t>(nslots) * nhT);
+    const double2* tw0 = s.plan(L0, st).tw;
+    const double2* tw1 = s.plan(L1, st).tw;
+    using RC = RowCfg<L1>;
+    using CC = ColCfg<L0>;
+    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);
+    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    set_smem(k2_rows_r2c<L1>, row_smem);
+    set_smem(k2_rows_c2r<L1>, row_smem);
+    set_smem(k2_cols_rec<L0>, 2 * col_smem);
+    set_smem(k2_cols_sum<L0, +1>, col_smem);
+    const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
+    const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
+    int slot0 = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        const int groups = (cb + cfg.G - 1) / cfg.G;
+        {
+            LaunchScope ls(s, "f2_rows_r2c", st, cb);
+            k2_rows_r2c<L1><<<dim3(row_blocks, cb), RC::THREADS, row_smem, st>>>(
+                coeffs + static_cast<size_t>(b0) * s.nreal, s.nreal, s.w->inter.p, nhT, n0, H, tw1);
+            check_launch("k2_rows_r2c");
+        }
+        {
+            LaunchScope ls(s, "f2_cols_rec", st, cb);
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0);
+            check_launch("k2_cols_rec");
+        }
+        slot0 += groups;
+    }
+    {
+        LaunchScope ls(s, "f2_cols_final", st, 1);
+        k2_cols_sum<L0, +1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->slots.p, nhT, nslots, s.WT.p, s.w->inter.p, H,
+                                                                        tw0);
+        check_launch("k2_cols_sum");
+    }
+    {
+        LaunchScope ls(s, "f2_rows_c2r", st, 1);
+        k2_rows_c2r<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(
+            s.w->inter.p, 0, out, 0, n0, H, 1.0 / static_cast<double>(s.nreal), nullptr, 0, tw1);
+        check_launch("k2_rows_c2r");
+    }
+}
+
+#define SLB_FAST2D_DISPATCH(FN, ...)                       \
+    switch (s.n[0]) {                                      \
+        case 64: FN<64, 64>(__VA_ARGS__); break;           \
+        case 128: FN<128, 128>(__VA_ARGS__); break;        \
+        case 192: FN<192, 192>(__VA_ARGS__); break;        \
+        case 256: FN<256, 256>(__VA_ARGS__); break;        \
+        case 512: FN<512, 512>(__VA_ARGS__); break;        \
+        case 1024: FN<1024, 1024>(__VA_ARGS__); break;     \
+        case 2048: FN<2048, 2048>(__VA_ARGS__); break;     \
+        default: throw SlError(SL_ERR_GENERIC, "fast2d: unsupported size"); \
+    }
+
+static void dec2d_fast(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    SLB_FAST2D_DISPATCH(dec2d_fast_t, s, f, out, delta, st)
+}
+static void rec2d_fast(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    SLB_FAST2D_DISPATCH(rec2d_fast_t, s, coeffs, out, st)
+}
+
+}  // namespace slb

@@ -1,0 +1,181 @@
+// Register-resident fp64 Stockham FFT with compile-time radix plans.
+//
+// One line of length L is transformed by T threads, each holding E = L / T
+// complex values in registers. Thread t holds elements t + T*m (m < E) both on
+// entry and on exit, so global loads/stores of a line are coalesced across
+// the T threads without any staging. Between radix stages the line goes
+// through a private shared-memory buffer of L double2 with an XOR swizzle
+// (e ^ ((e >> 3) & 7)) that makes both the strided Stockham writes and the
+// contiguous reads bank-conflict free; lines of T <= 32 threads synchronise
+// with __syncwarp, wider lines with a named barrier per line.
+//
+// Stage s (radix R, Ns = product of earlier radices) performs the Stockham
+// butterfly j: inputs j + r*L/R (times w^{r*(j%Ns)}, w = e^{DIR 2 pi i/(Ns R)}),
+// outputs (j - j%Ns)*R + j%Ns + r*Ns; thread t owns butterflies j = t + T*q.
+#pragma once
+
+#include "fft.cuh"
+
+namespace slb {
+
+template <int L>
+struct RegPlan;  // T, E, NST, R[]
+
+#define SLB_REG_PLAN(L_, T_, ...)                                     \
+    template <>                                                       \
+    struct RegPlan<L_> {                                              \
+        static constexpr int T = T_;                                  \
+        static constexpr int E = L_ / T_;                             \
+        static constexpr int R[] = {__VA_ARGS__};                     \
+        static constexpr int NST = sizeof(R) / sizeof(int);           \
+    };
+
+// E = 8 complex per thread (16 doubles) keeps kernels near 64-80 registers.
+#ifndef SLB_WIDE_E
+SLB_REG_PLAN(64, 8, 8, 8)
+SLB_REG_PLAN(128, 16, 8, 4, 4)
+SLB_REG_PLAN(256, 32, 8, 8, 4)
+SLB_REG_PLAN(512, 64, 8, 8, 8)
+SLB_REG_PLAN(1024, 128, 8, 8, 4, 4)
+SLB_REG_PLAN(2048, 256, 8, 8, 8, 4)
+SLB_REG_PLAN(192, 16, 4, 4, 4, 3)
+#else
+SLB_REG_PLAN(64, 8, 8, 8)
+SLB_REG_PLAN(128, 16, 8, 4, 4)
+SLB_REG_PLAN(256, 16, 16, 16)
+SLB_REG_PLAN(512, 32, 8, 8, 8)
+SLB_REG_PLAN(1024, 64, 16, 8, 8)
+SLB_REG_PLAN(2048, 128, 16, 16, 8)
+SLB_REG_PLAN(192, 8, 8, 8, 3)
+#endif
+#undef SLB_REG_PLAN
+
+template <int L>
+constexpr int plan_ns(int s) {
+    int ns = 1;
+    for (int i = 0; i < s; ++i) ns *= RegPlan<L>::R[i];
+    return ns;
+}
+
+__device__ __forceinline__ int swz(int e) { return e ^ ((e >> 3) & 7); }
+
+template <int T>
+__device__ __forceinline__ void line_sync() {
+    if constexpr (T <= 32) {
+        __syncwarp();
+    } else {
+        // one named barrier per line (ids 1..15), T threads each
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / T)), "r"(T) : "memory");
+    }
+}
+
+// radix-16 = 4 x 4 with internal twiddles w16^{n1 k2}
+template <int DIR>
+__device__ __forceinline__ void bfly16(double2* a) {
+    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, r2 = 0.70710678118654752440;
+    // stage 1: four radix-4 over n2 (stride 4), n1 = 0..3
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) bfly4<DIR>(a[n1], a[n1 + 4], a[n1 + 8], a[n1 + 12]);
+    // a[n1 + 4 k1] now holds sum_n2 x[n1 + 4 n2] w4^{n2 k1}; twiddle by w16^{n1 k1}
+    auto tw = [](double2 v, double c, double s) {  // v * (c + DIR i s)
+        return make_double2(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
+    };
+    a[5] = tw(a[5], c1, s1);     // n1=1,k1=1: w^1
+    a[9] = tw(a[9], r2, r2);     // n1=1,k1=2: w^2
+    a[13] = tw(a[13], s1, c1);   // n1=1,k1=3: w^3
+    a[6] = tw(a[6], r2, r2);     // n1=2,k1=1: w^2
+    a[10] = mul_di<DIR>(a[10]);  // n1=2,k1=2: w^4
+    a[14] = tw(a[14], -r2, r2);  // n1=2,k1=3: w^6
+    a[7] = tw(a[7], s1, c1);     // n1=3,k1=1: w^3
+    a[11] = tw(a[11], -r2, r2);  // n1=3,k1=2: w^6
+    a[15] = tw(a[15], -c1, -s1); // n1=3,k1=3: w^9
+    // stage 2: radix-4 over n1 for each k1; output index k1 + 4 k2
+    double2 o[16];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        double2 b0 = a[4 * k1], b1 = a[4 * k1 + 1], b2 = a[4 * k1 + 2], b3 = a[4 * k1 + 3];
+        bfly4<DIR>(b0, b1, b2, b3);
+        o[k1] = b0;
+        o[k1 + 4] = b1;
+        o[k1 + 8] = b2;
+        o[k1 + 12] = b3;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = o[i];
+}
+
+// Butterfly of radix R on x[q + B*r], r < R.
+template <int R, int DIR, int E>
+__device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = x[q + B * r];
+    if constexpr (R == 2) {
+        bfly2<DIR>(v[0], v[1]);
+    } else if constexpr (R == 3) {
+        bfly3<DIR>(v[0], v[1], v[2]);
+    } else if constexpr (R == 4) {
+        bfly4<DIR>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (R == 8) {
+        bfly8<DIR>(v);
+    } else if constexpr (R == 16) {
+        bfly16<DIR>(v);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[q + B * r] = v[r];
+}
+
+template <int L, int DIR, int S>
+struct RegStage {
+    using P = RegPlan<L>;
+    static constexpr int R = P::R[S];
+    static constexpr int E = P::E;
+    static constexpr int T = P::T;
+    static constexpr int B = E / R;
+    static constexpr int NS = plan_ns<L>(S);
+    static_assert(E % R == 0, "radix must divide the per-thread element count");
+
+    __device__ __forceinline__ static void run(double2 (&x)[E], double2* sm, int t, const double2* __restrict__ tw) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+            const int j = t + T * q;
+            const int jm = j % NS;
+            if constexpr (NS > 1) {
+#pragma unroll
+                for (int r = 1; r < R; ++r)
+                    x[q + B * r] = cmul(x[q + B * r], twiddle<DIR>(tw, r * jm * (L / (NS * R))));
+            }
+            bfly_strided<R, DIR>(x, q, B);
+        }
+        if constexpr (S + 1 < P::NST) {
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int j = t + T * q;
+                const int jm = j % NS;
+                const int base = (j - jm) * R + jm;
+#pragma unroll
+                for (int r = 0; r < R; ++r) sm[swz(base + r * NS)] = x[q + B * r];
+            }
+            line_sync<T>();
+            constexpr int R2 = P::R[S + 1];
+            constexpr int B2 = E / R2;
+#pragma unroll
+            for (int q = 0; q < B2; ++q) {
+                const int j = t + T * q;
+#pragma unroll
+                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz(j + r * (L / R2))];
+            }
+            line_sync<T>();
+            RegStage<L, DIR, S + 1>::run(x, sm, t, tw);
+        }
+    }
+};
+
+// In/out: x[m] = element t + T*m of the line. sm: the line's L-element buffer.
+template <int L, int DIR>
+__device__ __forceinline__ void reg_fft(double2 (&x)[RegPlan<L>::E], double2* sm, int t,
+                                        const double2* __restrict__ tw) {
+    RegStage<L, DIR, 0>::run(x, sm, t, tw);
+}
+
+}  // namespace slb

@@ -1,0 +1,121 @@
+// dec / rec orchestration and threshold deltas.
+#pragma once
+#include "launch.cuh"
+#include "fast2d_host.cuh"
+
+namespace slb {
+
+// ------------------------------------------------------------------ thresholds
+// delta_i = K[scale - j0] * sigma (* RMS_i) for this handle's bands; -1 for the
+// lowpass (untouched). Validation as hard_threshold_impl (apps.cpp:59-67).
+static void deltas(System& s, const double* K, int nK, double sigma, int scaled, cudaStream_t st) {
+    if (nK != s.prof.n_scales()) throw SlError(SL_ERR_CONFIG, "hard_threshold: schedule length must equal n_scales");
+    if (sigma < 0.0) throw SlError(SL_ERR_CONFIG, "hard_threshold: sigma must be >= 0");
+    for (int i = 0; i < nK; ++i)
+        if (!(K[i] > 0.0)) throw SlError(SL_ERR_CONFIG, "hard_threshold: factors must be positive");
+    std::vector<double> d(static_cast<size_t>(s.R), -1.0);
+    for (int i = 0; i < s.R; ++i) {
+        const Record& r = s.index[static_cast<size_t>(i)];
+        if (r.scale < 0) continue;
+        double dl = K[r.scale - s.prof.j0] * sigma;
+        if (scaled) dl *= s.rms[static_cast<size_t>(i)];
+        d[static_cast<size_t>(i)] = dl;
+    }
+    s.delta.alloc(d.size());
+    SL_CUDA(cudaMemcpyAsync(s.delta.p, d.data(), d.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+
+// ------------------------------------------------------------------ transforms
+static void forward_spectrum(System& s, const double* f, cudaStream_t st) {
+    s.w->F.alloc(static_cast<size_t>(s.nhalf));
+    rows_r2c(s, f, 0, s.w->F.p, 0, s.nrows, s.L_last, s.H, s.ldh, 1, st);
+    if (s.ndim == 3) {
+        int outer;
+        LineGeom g1 = geom_axis(s, 1, &outer);
+        lines<-1, kPlain>(s, s.w->F.p, 0, s.w->F.p, 0, g1, outer, 1, NoFilt{}, 0, nullptr, st);
+    }
+    int outer;
+    LineGeom g0 = geom_axis(s, 0, &outer);
+    lines<-1, kPlain>(s, s.w->F.p, 0, s.w->F.p, 0, g0, outer, 1, NoFilt{}, 0, nullptr, st);
+}
+
+template <class Filt>
+static void dec_bands(System& s, const Filt& filt, double* out, const double* delta, cudaStream_t st) {
+    const int nb = s.nb();
+    const int C = std::min(s.chunk, nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * s.nhalf);
+    const double scale = 1.0 / static_cast<double>(s.nreal);
+    int outer0, outer1 = 1;
+    LineGeom g0 = geom_axis(s, 0, &outer0);
+    LineGeom g1{};
+    if (s.ndim == 3) g1 = geom_axis(s, 1, &outer1);
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        lines<+1, kDecMul>(s, s.w->F.p, 0, s.w->inter.p, s.nhalf, g0, outer0, cb, filt, s.lo + b0, nullptr, st);
+        if (s.ndim == 3)
+            lines<+1, kPlain>(s, s.w->inter.p, s.nhalf, s.w->inter.p, s.nhalf, g1, outer1, cb, NoFilt{}, 0, nullptr, st);
+        rows_c2r(s, s.w->inter.p, s.nhalf, out + static_cast<size_t>(b0) * s.nreal, s.nreal, s.nrows, s.L_last, s.H,
+                 s.ldh, cb, scale, delta, s.lo + b0, st);
+    }
+}
+
+template <class Filt>
+static void rec_bands(System& s, const Filt& filt, const double* coeffs, double* out, cudaStream_t st) {
+    const int nb = s.nb();
+    const int C = std::min(s.chunk, nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * s.nhalf);
+    s.w->acc.alloc(static_cast<size_t>(s.nhalf));
+    int outer0, outer1 = 1;
+    LineGeom g0 = geom_axis(s, 0, &outer0);
+    LineGeom g1{};
+    if (s.ndim == 3) g1 = geom_axis(s, 1, &outer1);
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        rows_r2c(s, coeffs + static_cast<size_t>(b0) * s.nreal, s.nreal, s.w->inter.p, s.nhalf, s.nrows, s.L_last, s.H,
+                 s.ldh, cb, st);
+        if (s.ndim == 3)
+            lines<-1, kPlain>(s, s.w->inter.p, s.nhalf, s.w->inter.p, s.nhalf, g1, outer1, cb, NoFilt{}, 0, nullptr, st);
+        lines<-1, kRecMul>(s, s.w->inter.p, s.nhalf, s.w->inter.p, s.nhalf, g0, outer0, cb, filt, s.lo + b0, nullptr, st);
+        LaunchScope ls(s, "reduce_bands", st, cb);
+        k_reduce_bands<<<1184, 256, 0, st>>>(s.w->acc.p, s.w->inter.p, s.nhalf, cb, b0 > 0);
+        check_launch("k_reduce_bands");
+    }
+    // acc / W, then the inverse transform of the single accumulated spectrum
+    lines<+1, kDivW>(s, s.w->acc.p, 0, s.w->acc.p, 0, g0, outer0, 1, NoFilt{}, 0, s.W.p, st);
+    if (s.ndim == 3) lines<+1, kPlain>(s, s.w->acc.p, 0, s.w->acc.p, 0, g1, outer1, 1, NoFilt{}, 0, nullptr, st);
+    rows_c2r(s, s.w->acc.p, 0, out, 0, s.nrows, s.L_last, s.H, s.ldh, 1, 1.0 / static_cast<double>(s.nreal), nullptr, 0,
+             st);
+}
+
+static void dec(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    if (s.fast2d) {
+        dec2d_fast(s, f, out, delta, st);
+        return;
+    }
+    forward_spectrum(s, f, st);
+    if (s.ndim == 2)
+        dec_bands(s, FiltTable2DGet{FiltTable2D{s.psi.p, s.nhalf}}, out, delta, st);
+    else
+        dec_bands(s, FiltSynth3DFlat{s.synth, s.ldh}, out, delta, st);
+}
+
+static void rec(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+    if (s.fast2d) {
+        rec2d_fast(s, coeffs, out, st);
+        return;
+    }
+    if (s.ndim == 2)
+        rec_bands(s, FiltTable2DGet{FiltTable2D{s.psi.p, s.nhalf}}, coeffs, out, st);
+    else
+        rec_bands(s, FiltSynth3DFlat{s.synth, s.ldh}, coeffs, out, st);
+}
+
+// materialise one synthesised 3D filter (half spectrum) for API queries
+__global__ void k_synth_band(FiltSynth3DFlat f, int band, long long nhalf, double* out) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nhalf; e += (long long)gridDim.x * blockDim.x)
+        out[e] = ((e % f.ldh) < f.s.n[2] / 2 + 1) ? f.get(band, e) : 0.0;
+}
+
+
+}  // namespace slb

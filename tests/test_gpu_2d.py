@@ -255,3 +255,25 @@ def test_shards_sum_to_full(cuda):
         np.testing.assert_array_equal(c, cf[lo:hi])
         parts += P.inverse(c, s)
     assert rel_l2(parts, f) <= 1e-10
+
+
+def test_batched_api_matches_per_frame(cuda):
+    import torch
+    s = system(256, 256, [1, 1])
+    sch = P.ThresholdSchedule.defaults_2d(30.0, 2)
+    frames = np.stack([P.add_gaussian_noise(P.cartoon(256), 30.0, i) for i in range(5)])
+    ft = torch.from_numpy(frames).to(cuda)
+    s.set_streams(3)
+    den_b = P.denoise_batch(ft, s, sch)
+    dec_b = P.forward_batch(ft, s, sch)
+    rec_b = P.inverse_batch(dec_b, s)
+    host_b = P.denoise_batch(frames, s, sch)
+    torch.cuda.synchronize()
+    for i in range(5):
+        one = P.denoise(ft[i], s, sch)
+        assert torch.equal(den_b[i], one)
+        assert torch.equal(rec_b[i], one)
+        assert torch.equal(dec_b[i], P.forward_thresholded(ft[i], s, sch))
+        np.testing.assert_array_equal(host_b[i], one.cpu().numpy())
+    with pytest.raises(P.ShapeError):
+        P.denoise_batch(ft[:, :128], s, sch)
