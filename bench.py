@@ -395,6 +395,7 @@ def pass_bytes(name, dims):
     N = int(np.prod(dims))
     Nh = N // dims[-1] * (dims[-1] // 2 + 1)
     return None if name == "none" else {
+        # generic path
         "rows_c2r_thr": 16 * Nh + 8 * N,          # intermediate read + band write, per band
         "rows_c2r": 16 * Nh + 8 * N,
         "rows_r2c": 8 * N + 16 * Nh,
@@ -403,6 +404,23 @@ def pass_bytes(name, dims):
         "lines_plain": 32 * Nh,
         "lines_divw": 32 * Nh + 8 * Nh,
         "reduce_bands": 16 * Nh,
+        # fast 2D path (fast2d.cuh)
+        "f2_rows_r2c": 8 * N + 16 * Nh,           # band rows read + column-major half write
+        "f2_rows_c2r_thr": 16 * Nh + 8 * N,       # half read + thresholded band write
+        "f2_rows_c2r": 16 * Nh + 8 * N,
+        "f2_cols_dec": 8 * Nh + 16 * Nh,          # real psi + half write (F re-reads hit L2)
+        "f2_cols_rec": 16 * Nh + 8 * Nh,          # half read + real psi (slot writes amortised)
+        "f2_cols_fwd": 32 * Nh,
+        "f2_cols_final": 32 * Nh + 8 * Nh,
+        # fast 3D path (fast3d.cuh); psi synthesised from L2-resident tables
+        "f3_rows_r2c": 8 * N + 16 * Nh,
+        "f3_rows_c2r_thr": 16 * Nh + 8 * N,
+        "f3_rows_c2r": 16 * Nh + 8 * N,
+        "f3_axis1": 32 * Nh,
+        "f3_ax0_dec": 32 * Nh,                    # F read + rotated write
+        "f3_ax0_rec": 48 * Nh,                    # rotated read + accumulator read-modify-write
+        "f3_ax0_fwd": 32 * Nh,
+        "f3_ax0_final": 40 * Nh,
     }.get(name, None)
 
 

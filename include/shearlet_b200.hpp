@@ -1,0 +1,172 @@
+// shearlet_b200.hpp -- header-only C++ host API over the C ABI.
+//
+// Mirrors the reference's C++ interface for the hot path
+// (/root/reference/proj/core/include/shearlet/{system2d,system3d,transform,apps,errors}.hpp):
+// same function names and argument meaning, the same exception hierarchy, and
+// value semantics on host containers. Signals are row-major std::vector<double>
+// (axis 0 slowest), stacks are contiguous [R][dims...].
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "shearlet_b200.h"
+
+namespace shearlet_b200 {
+
+// errors.hpp:9-56
+struct Error : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DomainError : Error { using Error::Error; };
+struct ShapeError : Error { using Error::Error; };
+struct ConfigError : Error { using Error::Error; };
+struct AssetError : Error { using Error::Error; };
+struct FormatError : Error { using Error::Error; };
+struct SingularFrameError : Error { using Error::Error; };
+struct UnsupportedSizeError : Error { using Error::Error; };
+struct CudaError : Error { using Error::Error; };
+
+inline void check(int rc) {
+    if (rc == SL_OK) return;
+    const std::string m = sl_last_error();
+    switch (rc) {
+        case SL_ERR_SHAPE: throw ShapeError(m);
+        case SL_ERR_CONFIG: throw ConfigError(m);
+        case SL_ERR_DOMAIN: throw DomainError(m);
+        case SL_ERR_SINGULAR_FRAME: throw SingularFrameError(m);
+        case SL_ERR_UNSUPPORTED_SIZE: throw UnsupportedSizeError(m);
+        case SL_ERR_ASSET: throw AssetError(m);
+        case SL_ERR_FORMAT: throw FormatError(m);
+        case SL_ERR_CUDA: throw CudaError(m);
+        default: throw Error(m);
+    }
+}
+
+// ScaleProfile::from_levels (filters.hpp:79-92)
+struct ScaleProfile {
+    std::vector<int> shear_levels;
+    int coarsest_scale_offset = 0;
+    static ScaleProfile from_levels(std::vector<int> levels, int j0 = 0) { return {std::move(levels), j0}; }
+    int n_scales() const { return static_cast<int>(shear_levels.size()); }
+};
+
+// ThresholdSchedule (apps.hpp:19-29)
+struct ThresholdSchedule {
+    std::vector<double> per_scale_factors;
+    double sigma = 0.0;
+    bool scale_by_filter_norm = true;
+    static ThresholdSchedule defaults_2d(double sigma, int n_scales = 4) {
+        std::vector<double> k(static_cast<size_t>(n_scales), 2.5);
+        if (n_scales > 0) k.back() = 3.8;
+        return {k, sigma, true};
+    }
+    static ThresholdSchedule defaults_3d(double sigma, int n_scales = 3) {
+        std::vector<double> k(static_cast<size_t>(n_scales), 3.0);
+        if (n_scales > 0) k.back() = 4.0;
+        return {k, sigma, true};
+    }
+};
+
+struct FilterIndex {  // kind, scale, k1 (2D shear), k2
+    int kind, scale, k1, k2;
+};
+
+// ShearletSystem2D / 3D: owns the device-resident filter bank.
+class ShearletSystem {
+  public:
+    explicit ShearletSystem(sl_system* h) : h_(h, &sl_system_destroy) {
+        int nd = 0;
+        int64_t d[3];
+        check(sl_ndim(h, &nd, d));
+        ndim_ = nd;
+        for (int a = 0; a < 3; ++a) dims_[static_cast<size_t>(a)] = static_cast<size_t>(d[a]);
+        int R = 0, lo = 0, hi = 0;
+        check(sl_redundancy(h, &R));
+        check(sl_shard(h, &lo, &hi));
+        R_ = R;
+        nb_ = hi - lo;
+        std::vector<int32_t> rec(static_cast<size_t>(4 * R));
+        check(sl_index(h, rec.data()));
+        for (int i = 0; i < R; ++i)
+            index.push_back({rec[4 * i], rec[4 * i + 1], rec[4 * i + 2], rec[4 * i + 3]});
+        filter_norms.resize(static_cast<size_t>(R));
+        check(sl_filter_norms(h, filter_norms.data()));
+    }
+    sl_system* handle() const { return h_.get(); }
+    std::size_t redundancy() const { return static_cast<std::size_t>(R_); }
+    std::size_t n_bands() const { return static_cast<std::size_t>(nb_); }
+    std::size_t size() const { return ndim_ == 2 ? dims_[0] * dims_[1] : dims_[0] * dims_[1] * dims_[2]; }
+    int ndim() const { return ndim_; }
+    std::pair<double, double> frame_bounds() const {
+        double a, b;
+        check(sl_frame_bounds(h_.get(), &a, &b));
+        return {a, b};
+    }
+    std::vector<double> frame_weight() const {
+        std::vector<double> w(size());
+        check(sl_frame_weight(h_.get(), w.data()));
+        return w;
+    }
+    std::vector<FilterIndex> index;
+    std::vector<double> filter_norms;  // RMS
+
+  private:
+    std::unique_ptr<sl_system, int (*)(sl_system*)> h_;
+    int ndim_ = 0, R_ = 0, nb_ = 0;
+    std::array<std::size_t, 3> dims_{1, 1, 1};
+};
+
+// build_system_2d / build_system_3d (system2d.hpp:66-69, system3d.hpp:68-71)
+inline ShearletSystem build_system_2d(std::size_t rows, std::size_t cols, const ScaleProfile& p,
+                                      bool impulse_fan = false, bool full_system = false, int device = 0) {
+    sl_system* h = nullptr;
+    check(sl_system_create_2d(static_cast<int>(rows), static_cast<int>(cols), p.shear_levels.data(), p.n_scales(),
+                              p.coarsest_scale_offset, full_system, impulse_fan, device, 0, -1, &h));
+    return ShearletSystem(h);
+}
+inline ShearletSystem build_system_3d(std::array<std::size_t, 3> d, const ScaleProfile& p, bool impulse_fan = false,
+                                      bool full_system = false, int device = 0) {
+    sl_system* h = nullptr;
+    check(sl_system_create_3d(static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]),
+                              p.shear_levels.data(), p.n_scales(), p.coarsest_scale_offset, full_system, impulse_fan,
+                              device, 0, -1, &h));
+    return ShearletSystem(h);
+}
+
+// forward / inverse (transform.hpp:27-37), value semantics
+inline std::vector<double> forward(const std::vector<double>& f, const ShearletSystem& s) {
+    if (f.size() != s.size()) throw ShapeError("forward: signal dims do not match the system grid");
+    std::vector<double> c(s.n_bands() * s.size());
+    check(sl_sheardec_host(s.handle(), f.data(), c.data()));
+    return c;
+}
+inline std::vector<double> inverse(const std::vector<double>& coeffs, const ShearletSystem& s) {
+    if (coeffs.size() != s.n_bands() * s.size())
+        throw ShapeError("inverse: coefficient stack does not match the system");
+    std::vector<double> f(s.size());
+    check(sl_shearrec_host(s.handle(), coeffs.data(), static_cast<int>(s.n_bands()), f.data()));
+    return f;
+}
+// hard_threshold / denoise (apps.hpp:31-44)
+inline std::vector<double> hard_threshold(const std::vector<double>& coeffs, const ThresholdSchedule& sch,
+                                          const ShearletSystem& s) {
+    std::vector<double> out(coeffs.size());
+    check(sl_hard_threshold_host(s.handle(), coeffs.data(), out.data(),
+                                 static_cast<int>(coeffs.size() / std::max<std::size_t>(1, s.size())),
+                                 sch.per_scale_factors.data(), static_cast<int>(sch.per_scale_factors.size()),
+                                 sch.sigma, sch.scale_by_filter_norm));
+    return out;
+}
+inline std::vector<double> denoise(const std::vector<double>& noisy, const ShearletSystem& s,
+                                   const ThresholdSchedule& sch) {
+    if (noisy.size() != s.size()) throw ShapeError("forward: signal dims do not match the system grid");
+    std::vector<double> out(s.size());
+    check(sl_denoise_host(s.handle(), noisy.data(), out.data(), sch.per_scale_factors.data(),
+                          static_cast<int>(sch.per_scale_factors.size()), sch.sigma, sch.scale_by_filter_norm));
+    return out;
+}
+
+}  // namespace shearlet_b200

@@ -1,7 +1,9 @@
 // System construction on the GPU (2D filter bank, 3D factor tables, W, RMS).
 #pragma once
 #include "launch.cuh"
+#include "gpu_taps.cuh"
 #include "fast2d_host.cuh"
+#include "fast3d_host.cuh"
 
 namespace slb {
 
@@ -113,14 +115,22 @@ __global__ void k_half_to_colmajor(const double* __restrict__ in, double* __rest
 // ------------------------------------------------------------------ build helpers
 // Embed centred taps into an n0 x n1 periodic grid on the device and return
 // its Hermitian-half spectrum [n0][ldh] in `spec` (GPU FFT).
+static void spectrum_2d_of_dtaps(System& s, const double* dt, long t0, long t1, long c0, long c1, int n0, int n1,
+                                 DBuf<double>& grid, DBuf<double2>& spec, cudaStream_t st);
 static void spectrum_2d_of_taps(System& s, const Taps2& t, int n0, int n1, DBuf<double>& dtaps, DBuf<double>& grid,
                                 DBuf<double2>& spec, cudaStream_t st) {
-    const int H = n1 / 2 + 1, ldh = (H + 7) / 8 * 8;
     dtaps.upload(t.v.data(), t.v.size(), st);
+    spectrum_2d_of_dtaps(s, dtaps.p, static_cast<long>(t.n0), static_cast<long>(t.n1), t.c0, t.c1, n0, n1, grid, spec,
+                         st);
+}
+// Embed device-resident centred taps into an n0 x n1 grid and r2c it (GPU).
+static void spectrum_2d_of_dtaps(System& s, const double* dt, long t0, long t1, long c0, long c1, int n0, int n1,
+                                 DBuf<double>& grid, DBuf<double2>& spec, cudaStream_t st) {
+    const int H = n1 / 2 + 1, ldh = (H + 7) / 8 * 8;
     grid.alloc(static_cast<size_t>(n0) * n1);
     spec.alloc(static_cast<size_t>(n0) * ldh);
     k_embed2d<<<std::min<long long>(4096, ((long long)n0 * n1 + 255) / 256), 256, 0, st>>>(
-        dtaps.p, static_cast<int>(t.n0), static_cast<int>(t.n1), t.c0, t.c1, grid.p, n0, n1);
+        dt, static_cast<int>(t0), static_cast<int>(t1), c0, c1, grid.p, n0, n1);
     check_launch("k_embed2d");
     rows_r2c(s, grid.p, 0, spec.p, 0, n0, n1, H, ldh, 1, st);
     if (n0 > 1) {
@@ -139,11 +149,11 @@ static void spectrum_2d_of_taps(System& s, const Taps2& t, int n0, int n1, DBuf<
 
 // Full real spectrum (n0 x n1) of centred taps, expanded from the half by the
 // even symmetry of symmetric taps; also returns max|im| / max|re| of the half.
-static std::vector<double> real_spectrum_full(System& s, const Taps2& t, int n0, int n1, double* im_ratio,
+static std::vector<double> real_spectrum_full(System& s, const DTaps2& t, int n0, int n1, double* im_ratio,
                                               cudaStream_t st) {
-    DBuf<double> dtaps, grid;
+    DBuf<double> grid;
     DBuf<double2> spec;
-    spectrum_2d_of_taps(s, t, n0, n1, dtaps, grid, spec, st);
+    spectrum_2d_of_dtaps(s, t.p(), t.n0, t.n1, t.c0, t.c1, n0, n1, grid, spec, st);
     const int H = n1 / 2 + 1, ldh = (H + 7) / 8 * 8;
     std::vector<double2> h(static_cast<size_t>(n0) * ldh);
     SL_CUDA(cudaMemcpyAsync(h.data(), spec.p, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, st));
@@ -244,25 +254,32 @@ static void build_2d(System& s, int impulse_fan, cudaStream_t st) {
     const int J = s.prof.top();
     const int n0 = s.n[0], n1 = s.n[1];
     s.psi.alloc(static_cast<size_t>(s.R) * s.nhalf);
-    DBuf<double> dtaps, grid;
+    DBuf<double> dtaps, grid, tbuf;
     DBuf<double2> spec;
     DBuf<unsigned long long> mx;
     mx.alloc(2);
+    const bool host_taps = std::getenv("SLB_HOST_TAPS") != nullptr;  // cross-check path
+    const DTaps2 dfan = d_upload(fan, st);
     double worst = 0.0;
     int worst_i = -1;
     for (int i = 0; i < s.R; ++i) {
         const Record& r = s.index[static_cast<size_t>(i)];
-        Taps2 t;
         if (r.kind == 0) {
             Taps1 hJ;
             cascade(q, J, &hJ, nullptr);
-            t = outer(hJ, hJ);
-        } else {
+            spectrum_2d_of_taps(s, outer(hJ, hJ), n0, n1, dtaps, grid, spec, st);
+        } else if (host_taps) {
             const int d = s.prof.levels[static_cast<size_t>(r.scale - s.prof.j0)];
-            t = cone_taps(r.scale, r.k1, d, J, fan, q);
+            Taps2 t = cone_taps(r.scale, r.k1, d, J, fan, q);
             if (r.kind == 2) t = transposed(t);
+            spectrum_2d_of_taps(s, t, n0, n1, dtaps, grid, spec, st);
+        } else {
+            // upsampling, separable convolutions and the digital shear on the GPU
+            const int d = s.prof.levels[static_cast<size_t>(r.scale - s.prof.j0)];
+            DTaps2 t = d_cone_taps(r.scale, r.k1, d, J, dfan, q, tbuf, st);
+            if (r.kind == 2) t = d_transposed(t, st);
+            spectrum_2d_of_dtaps(s, t.p(), t.n0, t.n1, t.c0, t.c1, n0, n1, grid, spec, st);
         }
-        spectrum_2d_of_taps(s, t, n0, n1, dtaps, grid, spec, st);
         SL_CUDA(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), st));
         k_take_real<<<256, 256, 0, st>>>(spec.p, s.psi.p + static_cast<size_t>(i) * s.nhalf, s.nhalf, s.ldh, s.H, mx.p);
         check_launch("k_take_real");
@@ -324,14 +341,14 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
         Taps2 t2 = Taps2::zeros(1, t.size(), 0, t.c);
         std::memcpy(t2.v.data(), t.v.data(), t.size() * sizeof(double));
         double r;
-        std::vector<double> full = real_spectrum_full(s, t2, 1, n, &r, st);
+        std::vector<double> full = real_spectrum_full(s, d_upload(t2, st), 1, n, &r, st);
         worst = std::max(worst, r);
         const int off = static_cast<int>(tab1.size());
         tab1.insert(tab1.end(), full.begin(), full.end());
         return off;
     };
     std::map<std::pair<int, int>, int> cache2;  // (taps id, n_p * 65536 + n_s) -> off
-    auto add_2d = [&](const Taps2& t, int tid, int np, int ns) {
+    auto add_2d = [&](const DTaps2& t, int tid, int np, int ns) {
         const auto key = std::make_pair(tid, np * 65536 + ns);
         auto it = cache2.find(key);
         if (it != cache2.end()) return it->second;
@@ -343,6 +360,8 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
         cache2[key] = off;
         return off;
     };
+    DBuf<double> tbuf;
+    const DTaps2 dfan = d_upload(fan, st);
     Taps1 hJ;
     cascade(q, J, &hJ, nullptr);
     FiltSynth3D syn{};
@@ -353,7 +372,7 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
     struct ScaleTabs {
         int d;
         Taps1 g;
-        std::vector<Taps2> phi;
+        std::vector<DTaps2> phi;  // device-built component taps
         std::map<int, int> goff;  // axis length -> offset
     };
     std::vector<ScaleTabs> sc(static_cast<size_t>(s.prof.n_scales()));
@@ -367,7 +386,10 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
         cascade(q, J - j, nullptr, &S.g);
         const int K = 1 << d;
         for (int k = -K; k <= K; ++k) {
-            S.phi.push_back(phi_taps(j, k, d, J, fan, q));
+            if (std::getenv("SLB_HOST_TAPS"))
+                S.phi.push_back(d_upload(phi_taps(j, k, d, J, fan, q), st));
+            else
+                S.phi.push_back(d_phi_taps(j, k, d, J, dfan, q, tbuf, st));
             phi_id[static_cast<size_t>(si)].push_back(tid++);
         }
     }
@@ -416,6 +438,15 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
     SL_CUDA(cudaStreamSynchronize(st));
     finish_rms(s, hp.data(), nblk, s.R);
     finish_W(s, st);
+    if (fast3d_supported(s.n)) {
+        s.fast3d = true;
+        const int n = s.n[0];
+        const long long tot = static_cast<long long>(s.H) * n * n;
+        s.WN.alloc(static_cast<size_t>(tot));
+        k3_half_to_natural<<<std::min<long long>(8192, (tot + 255) / 256), 256, 0, st>>>(s.W.p, s.WN.p, n, s.H, s.ldh);
+        check_launch("k3_half_to_natural");
+        SL_CUDA(cudaStreamSynchronize(st));
+    }
 }
 
 

@@ -167,6 +167,9 @@ struct System {
     // 2D fast path (fast2d.cuh): column-major halves psi^T [R][H][n0], W^T [H][n0]
     bool fast2d = false;
     DBuf<double> psiT, WT;
+    // 3D fast path (fast3d.cuh): W in the natural [k2][k1][k0] layout
+    bool fast3d = false;
+    DBuf<double> WN;
     DBuf<double> W;     // [nhalf]
     // 3D synthesis tables
     DBuf<BandDesc3D> bands3;

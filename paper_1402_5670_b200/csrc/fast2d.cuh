@@ -27,8 +27,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-// CTA shapes: rows kernels take V = 256 / T row pairs (256 threads, a ~66 KB
-// [2V][H] tile); column kernels take 128 / T lines (128 threads, L * 16 B each).
+// Slot of (k, rr) in a [H][2V] tile: the rr index is XOR-swizzled with k so
+// that both the dense global-order fills (consecutive rr) and the per-line
+// reads (consecutive k, fixed rr) are bank-conflict free. 2V is a power of two.
+template <int V>
+__device__ __forceinline__ int tslot(int k, int rr) {
+    return k * (2 * V) + (rr ^ (k & (2 * V - 1)));
+}
+
+// CTA shapes: rows kernels take V = 256 / T row pairs (256 threads; smem =
+// [H][2V] tile + V line buffers); column kernels take 128 / T lines
+// (128 threads, L * 16 B each).
 template <int L>
 struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
@@ -51,45 +60,43 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     k2_rows_c2r(const double2* __restrict__ src, long long sbs, double* __restrict__ dst, long long dbs, int n0,
                 int H, double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
-    extern __shared__ double2 tile[];  // [2V][H]
+    extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers of L
     const int r0 = blockIdx.x * 2 * V;
     src += blockIdx.y * sbs;
     dst += blockIdx.y * dbs;
     const int nrows = min(2 * V, n0 - r0);
-    // all tile loads in flight at once (cp.async, 16 B each, L2 only)
+    // all tile loads in flight at once (cp.async, 16 B each, L2 only); the
+    // smem slot order follows the global order so each warp's writes are dense
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
         if (rr < nrows)
-            cp_async16(tile + rr * H + k, src + (long long)k * n0 + r0 + rr);
+            cp_async16(tile + tslot<V>(k, rr), src + (long long)k * n0 + r0 + rr);
         else
-            tile[rr * H + k] = make_double2(0.0, 0.0);
+            tile[tslot<V>(k, rr)] = make_double2(0.0, 0.0);
     }
     cp_async_wait_all();
     __syncthreads();
     const int q = threadIdx.x / T, t = threadIdx.x - q * T;
-    const double2* Xr = tile + (2 * q) * H;
-    const double2* Yr = Xr + H;
     double2 x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int k = t + T * m;
         double2 X, Y;
         if (k < H) {
-            X = Xr[k];
-            Y = Yr[k];
+            X = tile[tslot<V>(k, 2 * q)];
+            Y = tile[tslot<V>(k, 2 * q + 1)];
             if (k == 0 || 2 * k == L) {
                 X.y = 0.0;
                 Y.y = 0.0;
             }
             x[m] = make_double2(X.x - Y.y, X.y + Y.x);  // X + iY
         } else {
-            X = Xr[L - k];
-            Y = Yr[L - k];
+            X = tile[tslot<V>(L - k, 2 * q)];
+            Y = tile[tslot<V>(L - k, 2 * q + 1)];
             x[m] = make_double2(X.x + Y.y, Y.x - X.y);  // conj(X) + i conj(Y)
         }
     }
-    double2* lb = tile + (2 * q) * H;  // this pair's rows double as its exchange buffer (2H >= L)
-    line_sync<T>();
+    double2* lb = tile + H * 2 * V + q * L;
     reg_fft<L, +1>(x, lb, t, tw);
     const double dl = delta ? delta[band0 + blockIdx.y] : -1.0;
     const int ra = r0 + 2 * q;
@@ -114,7 +121,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
                 int H, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;  // split outputs per thread
-    extern __shared__ double2 tile[];            // [2V][H]
+    extern __shared__ double2 tile[];            // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
     src += blockIdx.y * sbs;
     dst += blockIdx.y * dbs;
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
         const double b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : 0.0;
         x[m] = make_double2(a, b);
     }
-    double2* lb = tile + (2 * q) * H;
+    double2* lb = tile + H * 2 * V + q * L;
     reg_fft<L, -1>(x, lb, t, tw);
     // Z in registers (element t + T m); publish to the line buffer, then split
 #pragma unroll
@@ -143,20 +150,19 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
             zm[u] = lb[swz(k == 0 ? 0 : L - k)];
         }
     }
-    line_sync<T>();
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            lb[k] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));          // X
-            lb[H + k] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));      // Y
+            tile[tslot<V>(k, 2 * q)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));      // X
+            tile[tslot<V>(k, 2 * q + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));  // Y
         }
     }
     __syncthreads();
     const int nrows = min(2 * V, n0 - r0);
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
-        if (rr < nrows) __stcg(dst + (long long)k * n0 + r0 + rr, tile[rr * H + k]);
+        if (rr < nrows) __stcg(dst + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
     }
 }
 

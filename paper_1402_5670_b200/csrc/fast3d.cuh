@@ -1,0 +1,184 @@
+// Specialised 3D dec / rec kernels for cubic grids with a RegPlan length.
+//
+// Half spectra (H = n2/2 + 1) live in two layouts, both without padding:
+//   rotated  R[k2][i0][k1]  (k1 fastest) -- what the rows pass (axis 2,
+//            pair-packed, reused from fast2d.cuh with n0*n1 rows) reads/writes
+//   natural  N[k2][k1][k0]  (k0 fastest) -- F, the accumulator and W
+// Passes:
+//   axis 1 : contiguous lines of R, in place                     (k3_lines_contig)
+//   axis 0 : N -> R  (contiguous load, rotated staged store)      (k3_ax0_to_rot)
+//            R -> N  (rotated staged load, contiguous store/RMW)  (k3_ax0_from_rot)
+// The 3D filter psi_b(k0, k1, k2) is synthesised in registers from the
+// per-scale factor tables (system3d.cpp:144-186), so no filter bank is read.
+#pragma once
+
+#include "fast2d.cuh"
+#include "kernels.cuh"
+
+namespace slb {
+
+// [L][V] staging tile, v XOR-swizzled with i0 (dense fills, conflict-free line reads)
+template <int V>
+__device__ __forceinline__ int aslot(int i0, int v) {
+    return i0 * V + (v ^ (i0 & (V - 1)));
+}
+
+template <int L>
+struct Ax0Cfg {
+    static constexpr int T = RegPlan<L>::T;
+    static constexpr int V = 8;  // lines (consecutive k1) per CTA -> 128-byte rotated runs
+    static constexpr int THREADS = V * T;
+};
+
+// ---------------------------------------------------------------- axis 1 (contiguous lines, in place)
+template <int L, int DIR>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+    k3_lines_contig(double2* __restrict__ data, long long bstride, long long nlines, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    extern __shared__ double2 lbuf[];
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const long long line = (long long)blockIdx.x * ColCfg<L>::LINES + li;
+    const bool valid = line < nlines;
+    double2* d = data + blockIdx.y * bstride + line * L;
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(d + t + T * m) : make_double2(0.0, 0.0);
+    reg_fft<L, DIR>(x, lbuf + li * L, t, tw);
+    if (valid) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcg(d + t + T * m, x[m]);
+    }
+}
+
+enum Ax0Mode : int {
+    kAx0Plain = 0,   // no filter
+    kAx0DecMul = 1,  // prologue x *= conj(psi) (psi real)
+    kAx0RecAcc = 2,  // epilogue acc (+)= x * psi
+    kAx0DivW = 3,    // prologue x /= W
+};
+
+// ---------------------------------------------------------------- axis 0: N -> R
+// Line (k2, k1) = contiguous N[(k2*n + k1)*n + k0]; output element (k2, i0, k1)
+// goes to R[(k2*n + i0)*n + k1], staged through the tile so each i0 writes V
+// consecutive k1 (a 128-byte run).
+template <int L, int DIR, int MODE>
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
+    k3_ax0_to_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int H,
+                  FiltSynth3D filt, int band0, const double* __restrict__ WN, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
+    constexpr int n = L;
+    extern __shared__ double2 tile[];  // [L][V] tile + V line buffers
+    const int lines_per_k2 = n / V;
+    const int k2 = blockIdx.x / lines_per_k2;
+    const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
+    const int band = band0 + blockIdx.y;
+    src += blockIdx.y * sbs;
+    dst += blockIdx.y * dbs;
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = k1_0 + li;
+    const double2* s = src + ((long long)k2 * n + k1) * n;
+    BandDesc3D bd{};
+    if (MODE == kAx0DecMul) bd = filt.bands[band];
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k0 = t + T * m;
+        double2 z = __ldcg(s + k0);
+        if (MODE == kAx0DecMul) {
+            const double p = filt.get_d(bd, k0, k1, k2);
+            z = make_double2(z.x * p, z.y * p);
+        } else if (MODE == kAx0DivW) {
+            const double w = __ldg(WN + ((long long)k2 * n + k1) * n + k0);
+            z = make_double2(z.x / w, z.y / w);
+        }
+        x[m] = z;
+    }
+    double2* lb = tile + V * L + li * L;  // line exchange buffer (separate from the tile)
+    reg_fft<L, DIR>(x, lb, t, tw);
+    // publish into the [i0][v] tile, then write 128-byte rotated runs
+#pragma unroll
+    for (int m = 0; m < E; ++m) tile[aslot<V>(t + T * m, li)] = x[m];
+    __syncthreads();
+    double2* o = dst + (long long)k2 * n * n + k1_0;
+    for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+        const int i0 = idx / V, v = idx - i0 * V;
+        __stcg(o + (long long)i0 * n + v, tile[aslot<V>(i0, v)]);
+    }
+    (void)H;
+}
+
+// ---------------------------------------------------------------- axis 0: R -> N
+// Non-accumulating modes: one spectrum per blockIdx.y. kAx0RecAcc: the CTA
+// walks the chunk's `nbands` bands in order, accumulating FFT_0(x) * psi_b in
+// registers, and read-modify-writes the accumulator once (deterministic).
+template <int L, int DIR, int MODE>
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
+    k3_ax0_from_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int nbands,
+                    FiltSynth3D filt, int band0, int accumulate, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
+    constexpr int n = L;
+    extern __shared__ double2 tile[];  // [L][V] tile + V line buffers
+    const int lines_per_k2 = n / V;
+    const int k2 = blockIdx.x / lines_per_k2;
+    const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = k1_0 + li;
+    double2* lb = tile + V * L + li * L;  // line exchange buffer
+    const int nb = MODE == kAx0RecAcc ? nbands : 1;
+    if (MODE != kAx0RecAcc) {
+        src += blockIdx.y * sbs;
+        dst += blockIdx.y * dbs;
+    }
+    double2 acc[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) acc[m] = make_double2(0.0, 0.0);
+    double2 x[E];
+    for (int bb = 0; bb < nb; ++bb) {
+        const double2* si = src + bb * sbs + (long long)k2 * n * n + k1_0;
+        __syncthreads();  // previous band's line buffers are free
+        for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+            const int i0 = idx / V, v = idx - i0 * V;
+            cp_async16(tile + aslot<V>(i0, v), si + (long long)i0 * n + v);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
+        reg_fft<L, DIR>(x, lb, t, tw);
+        if (MODE == kAx0RecAcc) {
+            const BandDesc3D bd = filt.bands[band0 + bb];
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const double p = filt.get_d(bd, t + T * m, k1, k2);
+                acc[m].x = fma(x[m].x, p, acc[m].x);
+                acc[m].y = fma(x[m].y, p, acc[m].y);
+            }
+        }
+    }
+    double2* d = dst + ((long long)k2 * n + k1) * n;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k0 = t + T * m;
+        if (MODE == kAx0RecAcc) {
+            double2 a = acc[m];
+            if (accumulate) a = cadd(__ldcg(d + k0), a);
+            __stcg(d + k0, a);
+        } else {
+            __stcg(d + k0, x[m]);
+        }
+    }
+}
+
+// [i0][i1][ldh] row-major half (build layout) -> natural N[k2][k1][k0]
+__global__ void k3_half_to_natural(const double* __restrict__ in, double* __restrict__ out, int n, int H, int ldh) {
+    const long long tot = (long long)H * n * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int k0 = (int)(e % n);
+        const long long r = e / n;
+        const int k1 = (int)(r % n);
+        const int k2 = (int)(r / n);
+        out[e] = in[((long long)k0 * n + k1) * ldh + k2];
+    }
+}
+
+}  // namespace slb

@@ -1,0 +1,139 @@
+// Host orchestration of the specialised 3D path (kernels in fast3d.cuh).
+#pragma once
+#include "fast2d_host.cuh"
+#include "fast3d.cuh"
+
+namespace slb {
+
+static bool fast3d_supported(const int* n) {
+    if (std::getenv("SLB_DISABLE_FAST3D")) return false;
+    if (n[0] != n[1] || n[1] != n[2]) return false;
+    switch (n[0]) {
+        case 64: case 128: case 192: case 256: return true;
+        default: return false;
+    }
+}
+
+// bands per chunk: the rotated intermediate of a chunk stays around 64 MiB
+static int fast3d_chunk(const System& s) {
+    const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
+    return env_int("SLB_CHUNK3", std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
+}
+
+template <int n>
+struct Fast3DLaunch {
+    using RC = RowCfg<n>;
+    using CC = ColCfg<n>;
+    using AC = Ax0Cfg<n>;
+    System& s;
+    cudaStream_t st;
+    int H;
+    long long nT;
+    const double2* tw;
+    size_t row_smem, col_smem, ax_smem;
+    int row_blocks, line_blocks, ax_blocks;
+    Fast3DLaunch(System& sys, cudaStream_t stream) : s(sys), st(stream) {
+        H = s.H;
+        nT = static_cast<long long>(H) * n * n;
+        tw = s.plan(n, st).tw;
+        row_smem = (static_cast<size_t>(2 * RC::V) * H + static_cast<size_t>(RC::V) * n) * sizeof(double2);
+        col_smem = static_cast<size_t>(CC::LINES) * n * sizeof(double2);
+        ax_smem = 2 * static_cast<size_t>(AC::V) * n * sizeof(double2);
+        row_blocks = (n * n + 2 * RC::V - 1) / (2 * RC::V);
+        line_blocks = static_cast<int>((static_cast<long long>(H) * n + CC::LINES - 1) / CC::LINES);
+        ax_blocks = H * (n / AC::V);
+    }
+    void rows_r2c(const double* src, long long sbs, double2* dst, int nb) {
+        set_smem(k2_rows_r2c<n>, row_smem);
+        LaunchScope ls(s, "f3_rows_r2c", st, nb);
+        k2_rows_r2c<n><<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(src, sbs, dst, nT, n * n, H, tw);
+        check_launch("k2_rows_r2c");
+    }
+    void rows_c2r(const double2* src, double* dst, long long dbs, int nb, const double* delta, int band0) {
+        set_smem(k2_rows_c2r<n>, row_smem);
+        LaunchScope ls(s, delta ? "f3_rows_c2r_thr" : "f3_rows_c2r", st, nb);
+        k2_rows_c2r<n><<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(
+            src, nT, dst, dbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
+        check_launch("k2_rows_c2r");
+    }
+    template <int DIR>
+    void axis1(double2* data, int nb) {
+        set_smem(k3_lines_contig<n, DIR>, col_smem);
+        LaunchScope ls(s, "f3_axis1", st, nb);
+        k3_lines_contig<n, DIR><<<dim3(line_blocks, nb), CC::THREADS, col_smem, st>>>(data, nT, static_cast<long long>(H) * n,
+                                                                                      tw);
+        check_launch("k3_lines_contig");
+    }
+    template <int DIR, int MODE>
+    void to_rot(const double2* src, long long sbs, double2* dst, int nb, int band0, const double* WN, const char* nm) {
+        set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
+        LaunchScope ls(s, nm, st, nb);
+        k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, nb), AC::THREADS, ax_smem, st>>>(src, sbs, dst, nT, H, s.synth,
+                                                                                        band0, WN, tw);
+        check_launch("k3_ax0_to_rot");
+    }
+    template <int DIR, int MODE>
+    void from_rot(const double2* src, double2* dst, int nb, int band0, int accumulate, const char* nm) {
+        set_smem(k3_ax0_from_rot<n, DIR, MODE>, ax_smem);
+        LaunchScope ls(s, nm, st, nb);
+        const int grid_y = MODE == kAx0RecAcc ? 1 : nb;
+        k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, grid_y), AC::THREADS, ax_smem, st>>>(
+            src, nT, dst, nT, nb, s.synth, band0, accumulate, tw);
+        check_launch("k3_ax0_from_rot");
+    }
+};
+
+template <int n>
+static void dec3d_fast_t(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    s.w->F.alloc(static_cast<size_t>(K.nT));
+    // F (natural layout) = FFT_0 FFT_1 R2C_2 f
+    K.rows_r2c(f, 0, s.w->inter.p, 1);
+    K.template axis1<-1>(s.w->inter.p, 1);
+    K.template from_rot<-1, kAx0Plain>(s.w->inter.p, s.w->F.p, 1, 0, 0, "f3_ax0_fwd");
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        K.template to_rot<+1, kAx0DecMul>(s.w->F.p, 0, s.w->inter.p, cb, s.lo + b0, nullptr, "f3_ax0_dec");
+        K.template axis1<+1>(s.w->inter.p, cb);
+        K.rows_c2r(s.w->inter.p, out + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+    }
+}
+
+template <int n>
+static void rec3d_fast_t(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    s.w->acc.alloc(static_cast<size_t>(K.nT));
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        K.rows_r2c(coeffs + static_cast<size_t>(b0) * s.nreal, s.nreal, s.w->inter.p, cb);
+        K.template axis1<-1>(s.w->inter.p, cb);
+        K.template from_rot<-1, kAx0RecAcc>(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, "f3_ax0_rec");
+    }
+    K.template to_rot<+1, kAx0DivW>(s.w->acc.p, 0, s.w->inter.p, 1, 0, s.WN.p, "f3_ax0_final");
+    K.template axis1<+1>(s.w->inter.p, 1);
+    K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
+}
+
+#define SLB_FAST3D_DISPATCH(FN, ...)                                        \
+    switch (s.n[0]) {                                                       \
+        case 64: FN<64>(__VA_ARGS__); break;                                \
+        case 128: FN<128>(__VA_ARGS__); break;                              \
+        case 192: FN<192>(__VA_ARGS__); break;                              \
+        case 256: FN<256>(__VA_ARGS__); break;                              \
+        default: throw SlError(SL_ERR_GENERIC, "fast3d: unsupported size"); \
+    }
+
+static void dec3d_fast(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    SLB_FAST3D_DISPATCH(dec3d_fast_t, s, f, out, delta, st)
+}
+static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    SLB_FAST3D_DISPATCH(rec3d_fast_t, s, coeffs, out, st)
+}
+
+}  // namespace slb

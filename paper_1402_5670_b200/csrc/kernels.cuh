@@ -52,11 +52,14 @@ struct FiltSynth3D {
     int n[3];
     int lp_off[3];         // lowpass hJ spectra per axis in tab1d
     __device__ __forceinline__ double get(int band, int i0, int i1, int i2) const {
-        const BandDesc3D d = bands[band];
+        return get_d(bands[band], i0, i1, i2);
+    }
+    // descriptor already loaded (hoisted out of per-element loops)
+    __device__ __forceinline__ double get_d(const BandDesc3D& d, int i0, int i1, int i2) const {
         if (d.kind == 0)
             return __ldg(tab1d + lp_off[0] + i0) * __ldg(tab1d + lp_off[1] + i1) * __ldg(tab1d + lp_off[2] + i2);
-        const int id[3] = {i0, i1, i2};
-        const int p = id[d.pa], a = id[d.s1], b = id[d.s2];
+        auto pick = [=](int ax) { return ax == 0 ? i0 : (ax == 1 ? i1 : i2); };  // no local-memory array
+        const int p = pick(d.pa), a = pick(d.s1), b = pick(d.s2);
         return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + p * n[d.s1] + a) *
                __ldg(tab2d + d.p2_off + p * n[d.s2] + b);
     }

@@ -2,6 +2,7 @@
 #pragma once
 #include "launch.cuh"
 #include "fast2d_host.cuh"
+#include "fast3d_host.cuh"
 
 namespace slb {
 
@@ -92,6 +93,10 @@ static void dec(System& s, const double* f, double* out, const double* delta, cu
         dec2d_fast(s, f, out, delta, st);
         return;
     }
+    if (s.fast3d) {
+        dec3d_fast(s, f, out, delta, st);
+        return;
+    }
     forward_spectrum(s, f, st);
     if (s.ndim == 2)
         dec_bands(s, FiltTable2DGet{FiltTable2D{s.psi.p, s.nhalf}}, out, delta, st);
@@ -103,6 +108,10 @@ static void rec(System& s, const double* coeffs, double* out, cudaStream_t st) {
     if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
     if (s.fast2d) {
         rec2d_fast(s, coeffs, out, st);
+        return;
+    }
+    if (s.fast3d) {
+        rec3d_fast(s, coeffs, out, st);
         return;
     }
     if (s.ndim == 2)

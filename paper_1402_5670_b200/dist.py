@@ -1,0 +1,56 @@
+"""Multi-GPU plumbing for the shearlet hot path (torch.distributed).
+
+* 3D (and large 2D) systems shard the filter bank by shearlet index: rank r
+  owns the contiguous band range shard_range(R, r, world) (balanced by count:
+  every band costs the same FFT work). The input volume is broadcast from the
+  root, each rank decomposes / thresholds / reconstructs its own bands, and
+  the reconstruction partial sums -- linear in the coefficients -- are
+  combined with a sum-reduce (NCCL over NVLink on the GPU box).
+* Batched 2D frames shard by image (frame_range): no collective.
+The reference has no distributed code; its
+parallel_for over the filter index (parallel.hpp:20-46) is the axis sharded
+here.
+"""
+from __future__ import annotations
+
+from typing import Callable, Tuple
+
+
+def shard_range(R: int, rank: int, world: int) -> Tuple[int, int]:
+    """Contiguous balanced band range [lo, hi) of rank `rank`."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank / world size")
+    return R * rank // world, R * (rank + 1) // world
+
+
+def frame_range(nframes: int, rank: int, world: int) -> Tuple[int, int]:
+    """Frames of a batch handled by `rank` (shard by image)."""
+    return shard_range(nframes, rank, world)
+
+
+def sharded_denoise(x, local_partial: Callable, group=None, root: int = 0):
+    """Broadcast x from `root`, run local_partial(x) -> partial reconstruction
+    (this rank's bands only), and sum-reduce the partials onto `root`.
+    Returns the full reconstruction on `root` (the partial elsewhere)."""
+    import torch.distributed as dist
+    dist.broadcast(x, src=root, group=group)
+    part = local_partial(x)
+    dist.reduce(part, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return part
+
+
+def sharded_forward_thresholded(x, sys, schedule, group=None, root: int = 0):
+    """Device path: broadcast then this rank's thresholded bands."""
+    import torch.distributed as dist
+    from . import forward_thresholded
+    dist.broadcast(x, src=root, group=group)
+    return forward_thresholded(x, sys, schedule)
+
+
+def sharded_inverse(coeffs, sys, group=None, root: int = 0):
+    """Partial reconstruction of this rank's bands, sum-reduced to `root`."""
+    import torch.distributed as dist
+    from . import inverse
+    part = inverse(coeffs, sys)
+    dist.reduce(part, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return part

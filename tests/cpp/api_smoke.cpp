@@ -1,0 +1,43 @@
+// C++ host API smoke test (built and run by tests/test_cpp_api.py on the GPU).
+// Mirrors test_transform.cpp:66-72 (round trip) and test_apps.cpp:53-95.
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+#include "shearlet_b200.hpp"
+
+using namespace shearlet_b200;
+
+int main() {
+    auto sys = build_system_2d(64, 64, ScaleProfile::from_levels({0, 0, 1, 1}));
+    std::mt19937_64 rng(22);
+    std::vector<double> f(64 * 64);
+    for (double& x : f) x = 2.0 * (static_cast<double>(rng()) * 0x1.0p-64) - 1.0;
+    const auto c = forward(f, sys);
+    const auto r = inverse(c, sys);
+    double num = 0, den = 0;
+    for (size_t i = 0; i < f.size(); ++i) {
+        num += (r[i] - f[i]) * (r[i] - f[i]);
+        den += f[i] * f[i];
+    }
+    const double err = std::sqrt(num / den);
+    int fails = 0;
+    if (!(err <= 1e-10)) { std::printf("round trip %g\n", err); ++fails; }
+    if (sys.redundancy() != 25) { std::printf("R %zu\n", sys.redundancy()); ++fails; }
+    try {
+        (void)forward(std::vector<double>(16 * 16), sys);
+        ++fails;
+    } catch (const ShapeError&) {
+    }
+    try {
+        (void)hard_threshold(c, ThresholdSchedule{{1.0}, 0.1, true}, sys);
+        ++fails;
+    } catch (const ConfigError&) {
+    }
+    const auto same = hard_threshold(c, ThresholdSchedule{{1, 1, 1, 1}, 0.0, true}, sys);
+    if (same != c) { std::printf("sigma 0 not identity\n"); ++fails; }
+    const auto [A, B] = sys.frame_bounds();
+    if (!(A > 0 && B >= A)) ++fails;
+    std::printf("cpp api: err %.2e R %zu A %.6f B %.6f fails %d\n", err, sys.redundancy(), A, B, fails);
+    return fails;
+}

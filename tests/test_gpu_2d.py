@@ -277,3 +277,17 @@ def test_batched_api_matches_per_frame(cuda):
         np.testing.assert_array_equal(host_b[i], one.cpu().numpy())
     with pytest.raises(P.ShapeError):
         P.denoise_batch(ft[:, :128], s, sch)
+
+
+@pytest.mark.parametrize("shape,levels", [((64, 64), [0, 0, 1, 1]), ((128, 128), [1, 1, 2]), ((48, 80), [0, 1])])
+def test_gpu_tap_construction_matches_host_taps(cuda, shape, levels, monkeypatch):
+    # upsampling, separable convolutions and the digital shear run on the GPU
+    # (csrc/gpu_taps.cuh); the host tap algebra (csrc/taps.cpp) is the cross-check
+    prof = P.ScaleProfile.from_levels(levels)
+    dev = P.build_system_2d(*shape, prof)
+    monkeypatch.setenv("SLB_HOST_TAPS", "1")
+    host = P.build_system_2d(*shape, prof)
+    monkeypatch.delenv("SLB_HOST_TAPS")
+    np.testing.assert_allclose(dev.filter_norms, host.filter_norms, rtol=1e-14)
+    for i in range(dev.redundancy()):
+        assert np.abs(dev.filter_freq(i) - host.filter_freq(i)).max() <= 1e-14

@@ -157,3 +157,14 @@ def test_shards_sum_to_full(cuda):
         np.testing.assert_array_equal(c, cf[lo:hi])
         parts += P.inverse(c, s)
     assert rel_l2(parts, f) <= 1e-10
+
+
+def test_gpu_tap_construction_matches_host_taps(cuda, monkeypatch):
+    prof = P.ScaleProfile.from_levels([0, 0, 1])
+    dev = P.build_system_3d((32, 32, 32), prof)
+    monkeypatch.setenv("SLB_HOST_TAPS", "1")
+    host = P.build_system_3d((32, 32, 32), prof)
+    monkeypatch.delenv("SLB_HOST_TAPS")
+    np.testing.assert_allclose(dev.filter_norms, host.filter_norms, rtol=1e-14)
+    for i in (0, 1, 20, 40, 75):
+        assert np.abs(dev.filter_freq(i) - host.filter_freq(i)).max() <= 1e-14
