@@ -141,9 +141,16 @@ struct RegStage {
             const int j = t + T * q;
             const int jm = j % NS;
             if constexpr (NS > 1) {
+                // one table load per butterfly; w^2..w^(R-1) by complex products
+                // (error ~3 ulp, far inside the 1e-10 budget) instead of R-1
+                // loads through the L1 data pipe
+                const double2 w1 = twiddle<DIR>(tw, jm * (L / (NS * R)));
+                double2 wp[R];
+                wp[1] = w1;
 #pragma unroll
-                for (int r = 1; r < R; ++r)
-                    x[q + B * r] = cmul(x[q + B * r], twiddle<DIR>(tw, r * jm * (L / (NS * R))));
+                for (int r = 2; r < R; ++r) wp[r] = (r & 1) ? cmul(wp[r - 1], w1) : cmul(wp[r / 2], wp[r / 2]);
+#pragma unroll
+                for (int r = 1; r < R; ++r) x[q + B * r] = cmul(x[q + B * r], wp[r]);
             }
             bfly_strided<R, DIR>(x, q, B);
         }

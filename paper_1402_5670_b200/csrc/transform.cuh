@@ -3,8 +3,16 @@
 #include "launch.cuh"
 #include "fast2d_host.cuh"
 #include "fast3d_host.cuh"
+#include "fast2d_p_host.cuh"
 
 namespace slb {
+
+// persistent pipelined 2D kernels by default; SLB_FAST2D_V=1 selects the
+// one-tile-per-CTA kernels (kept for A/B measurements)
+static bool fast2d_persistent() {
+    const char* e = std::getenv("SLB_FAST2D_V");
+    return !(e && std::atoi(e) == 1);
+}
 
 // ------------------------------------------------------------------ thresholds
 // delta_i = K[scale - j0] * sigma (* RMS_i) for this handle's bands; -1 for the
@@ -90,7 +98,10 @@ static void rec_bands(System& s, const Filt& filt, const double* coeffs, double*
 
 static void dec(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
     if (s.fast2d) {
-        dec2d_fast(s, f, out, delta, st);
+        if (fast2d_persistent())
+            dec2d_fastp(s, f, out, delta, st);
+        else
+            dec2d_fast(s, f, out, delta, st);
         return;
     }
     if (s.fast3d) {
@@ -107,7 +118,10 @@ static void dec(System& s, const double* f, double* out, const double* delta, cu
 static void rec(System& s, const double* coeffs, double* out, cudaStream_t st) {
     if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
     if (s.fast2d) {
-        rec2d_fast(s, coeffs, out, st);
+        if (fast2d_persistent())
+            rec2d_fastp(s, coeffs, out, st);
+        else
+            rec2d_fast(s, coeffs, out, st);
         return;
     }
     if (s.fast3d) {
