@@ -323,8 +323,7 @@ int sl_denoise_dev(sl_system* h, const double* in, double* out, const double* K,
         DeviceGuard dg(s.device);
         deltas(s, K, nK, sigma, scaled, stream_of(stream));
         s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-        dec(s, in, s.stack.p, s.delta.p, stream_of(stream));
-        rec(s, s.stack.p, out, stream_of(stream));
+        denoise(s, in, s.stack.p, out, s.delta.p, stream_of(stream));
     });
 }
 
@@ -418,8 +417,8 @@ int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* ou
         deltas(s, K, nK, sigma, scaled, st);
         fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
             s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-            dec(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, s.delta.p, fst);
-            rec(s, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal, fst);
+            denoise(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal,
+                    s.delta.p, fst);
         });
     });
 }
@@ -442,8 +441,8 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         deltas(s, K, nK, sigma, scaled, st);
         fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
             s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-            dec(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, s.delta.p, fst);
-            rec(s, s.w->stack.p, s.io_out.p + static_cast<size_t>(fr) * s.nreal, fst);
+            denoise(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p,
+                    s.io_out.p + static_cast<size_t>(fr) * s.nreal, s.delta.p, fst);
         });
         SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
         SL_CUDA(cudaStreamSynchronize(st));
@@ -514,8 +513,7 @@ int sl_denoise_host(sl_system* h, const double* in, double* out, const double* K
         s.io_out.alloc(static_cast<size_t>(s.nreal));
         s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
         SL_CUDA(cudaMemcpy(s.io_in.p, in, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
-        dec(s, s.io_in.p, s.stack.p, s.delta.p, 0);
-        rec(s, s.stack.p, s.io_out.p, 0);
+        denoise(s, s.io_in.p, s.stack.p, s.io_out.p, s.delta.p, 0);
         SL_CUDA(cudaMemcpy(out, s.io_out.p, s.nreal * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }

@@ -96,7 +96,10 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
             x[m] = make_double2(X.x + Y.y, Y.x - X.y);  // conj(X) + i conj(Y)
         }
     }
-    double2* lb = tile + H * 2 * V + q * L;
+    // the tile is dead once every line has gathered its inputs: the line
+    // exchange buffers alias it (H*2V >= V*L), halving shared memory per CTA
+    __syncthreads();
+    double2* lb = tile + q * L;
     reg_fft<L, +1>(x, lb, t, tw);
     const double dl = delta ? delta[band0 + blockIdx.y] : -1.0;
     const int ra = r0 + 2 * q;
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
         const double b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : 0.0;
         x[m] = make_double2(a, b);
     }
-    double2* lb = tile + H * 2 * V + q * L;
+    double2* lb = tile + q * L;  // line buffers alias the (not yet used) output tile
     reg_fft<L, -1>(x, lb, t, tw);
     // Z in registers (element t + T m); publish to the line buffer, then split
 #pragma unroll
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
             zm[u] = lb[swz(k == 0 ? 0 : L - k)];
         }
     }
+    __syncthreads();  // all line buffers read before the tile is written
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;

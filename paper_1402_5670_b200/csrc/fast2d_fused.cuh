@@ -1,0 +1,186 @@
+// Fused 2D denoise pipeline: dec rows pass + hard threshold + rec rows pass in
+// one kernel, so a thresholded band is written once (the materialised stack)
+// and never read back: 3 passes per band instead of 4.
+//
+//   cols_dec  : inter[b] = IFFT_0(F psi_b)                       (fast2d.cuh)
+//   rows_fused: band_b = thr(IFFT_1(inter[b]) / N) -> stack;
+//               inter[b] = FFT_1(band_b)  (in place, same tile)
+//   cols_rec  : slot += FFT_0(inter[b]) psi_b                     (fast2d.cuh)
+// Semantics = inverse(hard_threshold(forward(f))) (apps.cpp:114-121).
+#pragma once
+
+#include "fast2d_host.cuh"
+
+namespace slb {
+
+template <int L>
+__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+    k2_rows_fused(double2* __restrict__ inter, long long ibs, double* __restrict__ band, long long bbs, int n0, int H,
+                  double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    constexpr int KPT = (L / 2 + 1 + T - 1) / T;
+    extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers
+    const int r0 = blockIdx.x * 2 * V;
+    inter += blockIdx.y * ibs;
+    band += blockIdx.y * bbs;
+    const int nrows = min(2 * V, n0 - r0);
+    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
+        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+        if (rr < nrows)
+            cp_async16(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
+        else
+            tile[tslot<V>(k, rr)] = make_double2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int q = threadIdx.x / T, t = threadIdx.x - q * T;
+    double2 x[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const int k = t + T * m;
+        double2 X, Y;
+        if (k < H) {
+            X = tile[tslot<V>(k, 2 * q)];
+            Y = tile[tslot<V>(k, 2 * q + 1)];
+            if (k == 0 || 2 * k == L) {
+                X.y = 0.0;
+                Y.y = 0.0;
+            }
+            x[m] = make_double2(X.x - Y.y, X.y + Y.x);
+        } else {
+            X = tile[tslot<V>(L - k, 2 * q)];
+            Y = tile[tslot<V>(L - k, 2 * q + 1)];
+            x[m] = make_double2(X.x + Y.y, Y.x - X.y);
+        }
+    }
+    __syncthreads();              // every line has gathered: the tile is dead
+    double2* lb = tile + q * L;   // line buffers alias it (H*2V >= V*L)
+    reg_fft<L, +1>(x, lb, t, tw);
+    const double dl = delta[band0 + blockIdx.y];
+    const int ra = r0 + 2 * q;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        double a = x[m].x * scale, c = x[m].y * scale;
+        if (dl >= 0.0) {
+            if (fabs(a) < dl) a = 0.0;
+            if (fabs(c) < dl) c = 0.0;
+        }
+        const int i = t + T * m;
+        if (ra < n0) band[(long long)ra * L + i] = a;
+        if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
+        x[m] = make_double2(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : 0.0);  // rec input: the thresholded rows
+    }
+    reg_fft<L, -1>(x, lb, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) lb[swz(t + T * m)] = x[m];
+    line_sync<T>();
+    double2 zk[KPT], zm[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            zk[u] = lb[swz(k)];
+            zm[u] = lb[swz(k == 0 ? 0 : L - k)];
+        }
+    }
+    __syncthreads();  // all line buffers read before the tile is rewritten
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            tile[tslot<V>(k, 2 * q)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));
+            tile[tslot<V>(k, 2 * q + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));
+        }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
+        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+        if (rr < nrows) __stcg(inter + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
+    }
+}
+
+// denoise with the stack materialised in `stack` ([nb][n0][n1]).
+template <int L0, int L1>
+static void denoise2d_fast_t(System& s, const double* f, double* stack, double* out, const double* delta,
+                             cudaStream_t st) {
+    const int n0 = s.n[0], H = s.H;
+    const long long nhT = static_cast<long long>(H) * n0;
+    const Fast2DCfg cfg = fast2d_cfg(s);
+    const int nb = s.nb();
+    const int C = std::min(cfg.C, nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * nhT);
+    s.w->F.alloc(static_cast<size_t>(nhT));
+    int nslots = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) nslots += (std::min(C, nb - b0) + cfg.G - 1) / cfg.G;
+    s.w->slots.alloc(static_cast<size_t>(nslots) * nhT);
+    const double2* tw0 = s.plan(L0, st).tw;
+    const double2* tw1 = s.plan(L1, st).tw;
+    using RC = RowCfg<L1>;
+    using CC = ColCfg<L0>;
+    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
+    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    set_smem(k2_rows_r2c<L1>, row_smem);
+    set_smem(k2_rows_c2r<L1>, row_smem);
+    set_smem(k2_rows_fused<L1>, row_smem);
+    set_smem(k2_cols_sum<L0, -1>, col_smem);
+    set_smem(k2_cols_sum<L0, +1>, col_smem);
+    set_smem(k2_cols_dec<L0>, 2 * col_smem);
+    set_smem(k2_cols_rec<L0>, 2 * col_smem);
+    const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
+    const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
+    {
+        LaunchScope ls(s, "f2_rows_r2c", st, 1);
+        k2_rows_r2c<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(f, 0, s.w->inter.p, 0, n0, H, tw1);
+        check_launch("k2_rows_r2c");
+    }
+    {
+        LaunchScope ls(s, "f2_cols_fwd", st, 1);
+        k2_cols_sum<L0, -1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->inter.p, 0, 1, nullptr, s.w->F.p, H, tw0);
+        check_launch("k2_cols_sum");
+    }
+    const double scale = 1.0 / static_cast<double>(s.nreal);
+    int slot0 = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        const int groups = (cb + cfg.G - 1) / cfg.G;
+        {
+            LaunchScope ls(s, "f2_cols_dec", st, cb);
+            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+                s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0);
+            check_launch("k2_cols_dec");
+        }
+        {
+            LaunchScope ls(s, "f2_rows_fused", st, cb);
+            k2_rows_fused<L1><<<dim3(row_blocks, cb), RC::THREADS, row_smem, st>>>(
+                s.w->inter.p, nhT, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, n0, H, scale, delta,
+                s.lo + b0, tw1);
+            check_launch("k2_rows_fused");
+        }
+        {
+            LaunchScope ls(s, "f2_cols_rec", st, cb);
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0);
+            check_launch("k2_cols_rec");
+        }
+        slot0 += groups;
+    }
+    {
+        LaunchScope ls(s, "f2_cols_final", st, 1);
+        k2_cols_sum<L0, +1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->slots.p, nhT, nslots, s.WT.p,
+                                                                        s.w->inter.p, H, tw0);
+        check_launch("k2_cols_sum");
+    }
+    {
+        LaunchScope ls(s, "f2_rows_c2r", st, 1);
+        k2_rows_c2r<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(s.w->inter.p, 0, out, 0, n0, H, scale,
+                                                                            nullptr, 0, tw1);
+        check_launch("k2_rows_c2r");
+    }
+}
+
+static void denoise2d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
+                           cudaStream_t st) {
+    SLB_FAST2D_DISPATCH(denoise2d_fast_t, s, f, stack, out, delta, st)
+}
+
+}  // namespace slb

@@ -47,7 +47,7 @@ static void dec2d_fast_t(System& s, const double* f, double* out, const double* 
     const double2* tw1 = s.plan(L1, st).tw;
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = (static_cast<size_t>(2 * RC::V) * H + static_cast<size_t>(RC::V) * L1) * sizeof(double2);
+    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
     const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
@@ -99,7 +99,7 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
     const double2* tw1 = s.plan(L1, st).tw;
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = (static_cast<size_t>(2 * RC::V) * H + static_cast<size_t>(RC::V) * L1) * sizeof(double2);
+    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
     const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);

@@ -36,7 +36,7 @@ struct Fast3DLaunch {
         H = s.H;
         nT = static_cast<long long>(H) * n * n;
         tw = s.plan(n, st).tw;
-        row_smem = (static_cast<size_t>(2 * RC::V) * H + static_cast<size_t>(RC::V) * n) * sizeof(double2);
+        row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
         col_smem = static_cast<size_t>(CC::LINES) * n * sizeof(double2);
         ax_smem = 2 * static_cast<size_t>(AC::V) * n * sizeof(double2);
         row_blocks = (n * n + 2 * RC::V - 1) / (2 * RC::V);

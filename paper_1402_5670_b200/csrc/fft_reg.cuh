@@ -35,7 +35,11 @@ struct RegPlan;  // T, E, NST, R[]
 SLB_REG_PLAN(64, 8, 8, 8)
 SLB_REG_PLAN(128, 16, 8, 4, 4)
 SLB_REG_PLAN(256, 32, 8, 8, 4)
+#ifndef SLB_PLAN512
 SLB_REG_PLAN(512, 64, 8, 8, 8)
+#else
+SLB_PLAN512
+#endif
 SLB_REG_PLAN(1024, 128, 8, 8, 4, 4)
 SLB_REG_PLAN(2048, 256, 8, 8, 8, 4)
 SLB_REG_PLAN(192, 16, 4, 4, 4, 3)
@@ -104,6 +108,45 @@ __device__ __forceinline__ void bfly16(double2* a) {
     for (int i = 0; i < 16; ++i) a[i] = o[i];
 }
 
+// radix-32 = radix-2 over two radix-16 halves (decimation in time):
+// X[k] = E[k] + w32^k O[k], X[k+16] = E[k] - w32^k O[k].
+template <int DIR>
+__device__ __forceinline__ void bfly32(double2* a) {
+    double2 e[16], o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        e[i] = a[2 * i];
+        o[i] = a[2 * i + 1];
+    }
+    bfly16<DIR>(e);
+    bfly16<DIR>(o);
+    constexpr double c[16] = {1.0,
+                              0.98078528040323044913,
+                              0.92387953251128675613,
+                              0.83146961230254523708,
+                              0.70710678118654752440,
+                              0.55557023301960222474,
+                              0.38268343236508977173,
+                              0.19509032201612826785,
+                              0.0,
+                              -0.19509032201612826785,
+                              -0.38268343236508977173,
+                              -0.55557023301960222474,
+                              -0.70710678118654752440,
+                              -0.83146961230254523708,
+                              -0.92387953251128675613,
+                              -0.98078528040323044913};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        // w32^k = cos(2 pi k/32) + DIR i sin(2 pi k/32); sin(2 pi k/32) = cos(2 pi (8-k)/32)
+        const double cs = c[k];
+        const double sn = k <= 8 ? c[8 - k] : c[k - 8];
+        const double2 t = k == 0 ? o[0] : make_double2(o[k].x * cs - DIR * o[k].y * sn, o[k].y * cs + DIR * o[k].x * sn);
+        a[k] = cadd(e[k], t);
+        a[k + 16] = csub(e[k], t);
+    }
+}
+
 // Butterfly of radix R on x[q + B*r], r < R.
 template <int R, int DIR, int E>
 __device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
@@ -120,6 +163,8 @@ __device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
         bfly8<DIR>(v);
     } else if constexpr (R == 16) {
         bfly16<DIR>(v);
+    } else if constexpr (R == 32) {
+        bfly32<DIR>(v);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) x[q + B * r] = v[r];

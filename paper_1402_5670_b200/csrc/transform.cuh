@@ -4,6 +4,7 @@
 #include "fast2d_host.cuh"
 #include "fast3d_host.cuh"
 #include "fast2d_p_host.cuh"
+#include "fast2d_fused.cuh"
 
 namespace slb {
 
@@ -140,5 +141,18 @@ __global__ void k_synth_band(FiltSynth3DFlat f, int band, long long nhalf, doubl
         out[e] = ((e % f.ldh) < f.s.n[2] / 2 + 1) ? f.get(band, e) : 0.0;
 }
 
+
+// denoise = inverse(hard_threshold(forward(f))) with the stack materialised in
+// `stack`; the 2D fast path fuses the dec rows pass, the threshold and the rec
+// rows pass (fast2d_fused.cuh). SLB_DENOISE_UNFUSED=1 forces dec + rec.
+static void denoise(System& s, const double* f, double* stack, double* out, const double* delta, cudaStream_t st) {
+    if (s.fast2d && !std::getenv("SLB_DENOISE_UNFUSED")) {
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        denoise2d_fast(s, f, stack, out, delta, st);
+        return;
+    }
+    dec(s, f, stack, delta, st);
+    rec(s, stack, out, st);
+}
 
 }  // namespace slb
