@@ -415,6 +415,8 @@ int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* ou
         DeviceGuard dg(s.device);
         cudaStream_t st = stream_of(stream);
         deltas(s, K, nK, sigma, scaled, st);
+        s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
+        if (denoise_batch_mega(s, in, nframes, s.stack.p, out, s.delta.p, st)) return;
         fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
             s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
             denoise(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal,
@@ -439,11 +441,13 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         cudaStream_t st = 0;
         SL_CUDA(cudaMemcpyAsync(s.io_in.p, in, n * sizeof(double), cudaMemcpyHostToDevice, st));
         deltas(s, K, nK, sigma, scaled, st);
-        fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
-            s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-            denoise(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p,
-                    s.io_out.p + static_cast<size_t>(fr) * s.nreal, s.delta.p, fst);
-        });
+        s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
+        if (!denoise_batch_mega(s, s.io_in.p, nframes, s.stack.p, s.io_out.p, s.delta.p, st))
+            fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+                s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+                denoise(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p,
+                        s.io_out.p + static_cast<size_t>(fr) * s.nreal, s.delta.p, fst);
+            });
         SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
         SL_CUDA(cudaStreamSynchronize(st));
     });

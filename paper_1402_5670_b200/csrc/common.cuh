@@ -192,6 +192,7 @@ struct System {
     int nstreams = 4;               // workspaces used by batched calls
     cudaEvent_t fork_ev = nullptr;
     DBuf<double> delta, stack, io_in, io_out;
+    std::shared_ptr<void> mega;  // MegaState of the 2D megakernel (mega2d_host.cuh)
     int chunk = 1;
     std::mutex mu;
 

@@ -5,6 +5,7 @@
 #include "fast3d_host.cuh"
 #include "fast2d_p_host.cuh"
 #include "fast2d_fused.cuh"
+#include "mega2d_host.cuh"
 
 namespace slb {
 
@@ -153,6 +154,18 @@ static void denoise(System& s, const double* f, double* stack, double* out, cons
     }
     dec(s, f, stack, delta, st);
     rec(s, stack, out, st);
+}
+
+// Batched denoise of nframes contiguous frames with per-frame stacks in
+// `stacks` ([nframes][nb][dims]). The 2D fast path runs one persistent
+// megakernel for the whole batch; otherwise frames go through denoise().
+static bool denoise_batch_mega(System& s, const double* in, int nframes, double* stacks, double* out,
+                               const double* delta, cudaStream_t st) {
+    if (!mega2d_enabled(s) || nframes < 1) return false;
+    if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+    if (!s.mega) s.mega = std::make_shared<MegaState>();
+    mega_denoise(s, *static_cast<MegaState*>(s.mega.get()), in, nframes, stacks, out, delta, st);
+    return true;
 }
 
 }  // namespace slb

@@ -271,10 +271,11 @@ def test_batched_api_matches_per_frame(cuda):
     torch.cuda.synchronize()
     for i in range(5):
         one = P.denoise(ft[i], s, sch)
-        assert torch.equal(den_b[i], one)
+        # the batched path may sum bands in a different association (megakernel)
+        assert (torch.linalg.norm(den_b[i] - one) / torch.linalg.norm(one)).item() <= 1e-12
         assert torch.equal(rec_b[i], one)
         assert torch.equal(dec_b[i], P.forward_thresholded(ft[i], s, sch))
-        np.testing.assert_array_equal(host_b[i], one.cpu().numpy())
+        assert np.linalg.norm(host_b[i] - one.cpu().numpy()) <= 1e-12 * np.linalg.norm(host_b[i])
     with pytest.raises(P.ShapeError):
         P.denoise_batch(ft[:, :128], s, sch)
 
