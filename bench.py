@@ -266,8 +266,12 @@ def main():
             return
         for i in range(frames):
             x = d_in[i]
-            if world > 1:
-                dist.broadcast(x, src=0)
+            if world == 1:
+                # fused denoise (dec rows + threshold + rec rows in one pass), stack materialised
+                P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(d_out[i].data_ptr()),
+                                          Kp, len(K), float(sch.sigma), 1, stream_ptr()))
+                continue
+            dist.broadcast(x, src=0)
             P._check(L.sl_sheardec_threshold_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(stack.data_ptr()),
                                                  Kp, len(K), float(sch.sigma), 1, stream_ptr()))
             P._check(L.sl_shearrec_dev(sysg.handle, C.c_void_p(stack.data_ptr()), sysg.n_bands,

@@ -357,6 +357,10 @@ static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
         worst = std::max(worst, r);
         const int off = static_cast<int>(tab2.size());
         tab2.insert(tab2.end(), full.begin(), full.end());
+        // transposed copy right after the plane (ns x np): coalesced lookups
+        // when the principal index runs along axis 0 (FiltSynth3D::get_d)
+        for (int a = 0; a < ns; ++a)
+            for (int p = 0; p < np; ++p) tab2.push_back(full[static_cast<size_t>(p) * ns + a]);
         cache2[key] = off;
         return off;
     };

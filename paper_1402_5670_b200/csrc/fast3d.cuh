@@ -26,7 +26,11 @@ __device__ __forceinline__ int aslot(int i0, int v) {
 template <int L>
 struct Ax0Cfg {
     static constexpr int T = RegPlan<L>::T;
+#ifndef SLB_AX0_V
     static constexpr int V = 8;  // lines (consecutive k1) per CTA -> 128-byte rotated runs
+#else
+    static constexpr int V = SLB_AX0_V;
+#endif
     static constexpr int THREADS = V * T;
 };
 
@@ -62,7 +66,7 @@ enum Ax0Mode : int {
 // goes to R[(k2*n + i0)*n + k1], staged through the tile so each i0 writes V
 // consecutive k1 (a 128-byte run).
 template <int L, int DIR, int MODE>
-__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
     k3_ax0_to_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int H,
                   FiltSynth3D filt, int band0, const double* __restrict__ WN, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
@@ -108,11 +112,11 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
 }
 
 // ---------------------------------------------------------------- axis 0: R -> N
-// Non-accumulating modes: one spectrum per blockIdx.y. kAx0RecAcc: the CTA
-// walks the chunk's `nbands` bands in order, accumulating FFT_0(x) * psi_b in
-// registers, and read-modify-writes the accumulator once (deterministic).
+// One spectrum per blockIdx.y. kAx0RecAcc: blockIdx.y walks nothing -- the
+// host launches one band at a time and the epilogue read-modify-writes the
+// accumulator (acc (+)= FFT_0(x) psi_b, band order = launch order, deterministic).
 template <int L, int DIR, int MODE>
-__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
     k3_ax0_from_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int nbands,
                     FiltSynth3D filt, int band0, int accumulate, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
@@ -124,49 +128,37 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
     double2* lb = tile + V * L + li * L;  // line exchange buffer
-    const int nb = MODE == kAx0RecAcc ? nbands : 1;
-    if (MODE != kAx0RecAcc) {
-        src += blockIdx.y * sbs;
-        dst += blockIdx.y * dbs;
+    src += blockIdx.y * sbs;
+    if (MODE != kAx0RecAcc) dst += blockIdx.y * dbs;
+    const double2* si = src + (long long)k2 * n * n + k1_0;
+    for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+        const int i0 = idx / V, v = idx - i0 * V;
+        cp_async16(tile + aslot<V>(i0, v), si + (long long)i0 * n + v);
     }
-    double2 acc[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) acc[m] = make_double2(0.0, 0.0);
+    cp_async_wait_all();
+    __syncthreads();
     double2 x[E];
-    for (int bb = 0; bb < nb; ++bb) {
-        const double2* si = src + bb * sbs + (long long)k2 * n * n + k1_0;
-        __syncthreads();  // previous band's line buffers are free
-        for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
-            const int i0 = idx / V, v = idx - i0 * V;
-            cp_async16(tile + aslot<V>(i0, v), si + (long long)i0 * n + v);
-        }
-        cp_async_wait_all();
-        __syncthreads();
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
-        reg_fft<L, DIR>(x, lb, t, tw);
-        if (MODE == kAx0RecAcc) {
-            const BandDesc3D bd = filt.bands[band0 + bb];
-#pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const double p = filt.get_d(bd, t + T * m, k1, k2);
-                acc[m].x = fma(x[m].x, p, acc[m].x);
-                acc[m].y = fma(x[m].y, p, acc[m].y);
-            }
-        }
-    }
+    for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
+    reg_fft<L, DIR>(x, lb, t, tw);
     double2* d = dst + ((long long)k2 * n + k1) * n;
+    if (MODE == kAx0RecAcc) {
+        const BandDesc3D bd = filt.bands[band0 + blockIdx.y];
+        double2 a[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k0 = t + T * m;
-        if (MODE == kAx0RecAcc) {
-            double2 a = acc[m];
-            if (accumulate) a = cadd(__ldcg(d + k0), a);
-            __stcg(d + k0, a);
-        } else {
-            __stcg(d + k0, x[m]);
+        for (int m = 0; m < E; ++m) a[m] = accumulate ? __ldcg(d + t + T * m) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const double p = filt.get_d(bd, t + T * m, k1, k2);
+            a[m].x = fma(x[m].x, p, a[m].x);
+            a[m].y = fma(x[m].y, p, a[m].y);
+            __stcg(d + t + T * m, a[m]);
         }
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcg(d + t + T * m, x[m]);
     }
+    (void)nbands;
 }
 
 // [i0][i1][ldh] row-major half (build layout) -> natural N[k2][k1][k0]

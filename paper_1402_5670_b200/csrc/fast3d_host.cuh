@@ -2,6 +2,7 @@
 #pragma once
 #include "fast2d_host.cuh"
 #include "fast3d.cuh"
+#include "fast2d_fused.cuh"
 
 namespace slb {
 
@@ -56,6 +57,14 @@ struct Fast3DLaunch {
             src, nT, dst, dbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
         check_launch("k2_rows_c2r");
     }
+    // dec rows pass + threshold + rec rows pass (fast2d_fused.cuh) over n*n rows
+    void rows_fused(double2* inter, double* band, long long bbs, int nb, const double* delta, int band0) {
+        set_smem(k2_rows_fused<n>, row_smem);
+        LaunchScope ls(s, "f3_rows_fused", st, nb);
+        k2_rows_fused<n><<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(
+            inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
+        check_launch("k2_rows_fused");
+    }
     template <int DIR>
     void axis1(double2* data, int nb) {
         set_smem(k3_lines_contig<n, DIR>, col_smem);
@@ -76,8 +85,16 @@ struct Fast3DLaunch {
     void from_rot(const double2* src, double2* dst, int nb, int band0, int accumulate, const char* nm) {
         set_smem(k3_ax0_from_rot<n, DIR, MODE>, ax_smem);
         LaunchScope ls(s, nm, st, nb);
-        const int grid_y = MODE == kAx0RecAcc ? 1 : nb;
-        k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, grid_y), AC::THREADS, ax_smem, st>>>(
+        if (MODE == kAx0RecAcc) {
+            // bands one launch at a time: the accumulator RMW stays in band order
+            for (int b = 0; b < nb; ++b) {
+                k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, 1), AC::THREADS, ax_smem, st>>>(
+                    src + b * nT, nT, dst, nT, 1, s.synth, band0 + b, accumulate || b > 0, tw);
+                check_launch("k3_ax0_from_rot");
+            }
+            return;
+        }
+        k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, nb), AC::THREADS, ax_smem, st>>>(
             src, nT, dst, nT, nb, s.synth, band0, accumulate, tw);
         check_launch("k3_ax0_from_rot");
     }
@@ -120,6 +137,33 @@ static void rec3d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
     K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
 }
 
+// denoise with the stack materialised: 5 passes per band instead of 6 and no
+// band read-back (the thresholded rows feed the rec r2c in the same kernel)
+template <int n>
+static void denoise3d_fast_t(System& s, const double* f, double* stack, double* out, const double* delta,
+                             cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    s.w->F.alloc(static_cast<size_t>(K.nT));
+    s.w->acc.alloc(static_cast<size_t>(K.nT));
+    K.rows_r2c(f, 0, s.w->inter.p, 1);
+    K.template axis1<-1>(s.w->inter.p, 1);
+    K.template from_rot<-1, kAx0Plain>(s.w->inter.p, s.w->F.p, 1, 0, 0, "f3_ax0_fwd");
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        K.template to_rot<+1, kAx0DecMul>(s.w->F.p, 0, s.w->inter.p, cb, s.lo + b0, nullptr, "f3_ax0_dec");
+        K.template axis1<+1>(s.w->inter.p, cb);
+        K.rows_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+        K.template axis1<-1>(s.w->inter.p, cb);
+        K.template from_rot<-1, kAx0RecAcc>(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, "f3_ax0_rec");
+    }
+    K.template to_rot<+1, kAx0DivW>(s.w->acc.p, 0, s.w->inter.p, 1, 0, s.WN.p, "f3_ax0_final");
+    K.template axis1<+1>(s.w->inter.p, 1);
+    K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
+}
+
 #define SLB_FAST3D_DISPATCH(FN, ...)                                        \
     switch (s.n[0]) {                                                       \
         case 64: FN<64>(__VA_ARGS__); break;                                \
@@ -134,6 +178,11 @@ static void dec3d_fast(System& s, const double* f, double* out, const double* de
 }
 static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_t st) {
     SLB_FAST3D_DISPATCH(rec3d_fast_t, s, coeffs, out, st)
+}
+
+static void denoise3d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
+                           cudaStream_t st) {
+    SLB_FAST3D_DISPATCH(denoise3d_fast_t, s, f, stack, out, delta, st)
 }
 
 }  // namespace slb

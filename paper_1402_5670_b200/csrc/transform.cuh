@@ -152,6 +152,11 @@ static void denoise(System& s, const double* f, double* stack, double* out, cons
         denoise2d_fast(s, f, stack, out, delta, st);
         return;
     }
+    if (s.fast3d && !std::getenv("SLB_DENOISE_UNFUSED")) {
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        denoise3d_fast(s, f, stack, out, delta, st);
+        return;
+    }
     dec(s, f, stack, delta, st);
     rec(s, stack, out, st);
 }
