@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
         }
         x[m] = z;
     }
-    double2* lb = tile + V * L + li * L;  // line exchange buffer (separate from the tile)
+    double2* lb = tile + li * L;  // line exchange buffers alias the output tile
     reg_fft<L, DIR>(x, lb, t, tw);
+    __syncthreads();              // every line's FFT is done with the aliased buffers
     // publish into the [i0][v] tile, then write 128-byte rotated runs
 #pragma unroll
     for (int m = 0; m < E; ++m) tile[aslot<V>(t + T * m, li)] = x[m];
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
     const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
-    double2* lb = tile + V * L + li * L;  // line exchange buffer
+    double2* lb = tile + li * L;  // line exchange buffers alias the input tile (after the gather)
     src += blockIdx.y * sbs;
     if (MODE != kAx0RecAcc) dst += blockIdx.y * dbs;
     const double2* si = src + (long long)k2 * n * n + k1_0;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
     double2 x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
+    __syncthreads();  // all lines gathered: the tile becomes the line buffers
     reg_fft<L, DIR>(x, lb, t, tw);
     double2* d = dst + ((long long)k2 * n + k1) * n;
     if (MODE == kAx0RecAcc) {

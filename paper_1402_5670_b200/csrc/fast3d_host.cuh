@@ -39,7 +39,7 @@ struct Fast3DLaunch {
         tw = s.plan(n, st).tw;
         row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
         col_smem = static_cast<size_t>(CC::LINES) * n * sizeof(double2);
-        ax_smem = 2 * static_cast<size_t>(AC::V) * n * sizeof(double2);
+        ax_smem = static_cast<size_t>(AC::V) * n * sizeof(double2);  // tile; line buffers alias it
         row_blocks = (n * n + 2 * RC::V - 1) / (2 * RC::V);
         line_blocks = static_cast<int>((static_cast<long long>(H) * n + CC::LINES - 1) / CC::LINES);
         ax_blocks = H * (n / AC::V);
