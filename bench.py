@@ -99,7 +99,12 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            # wait for the first sample so the timed region is covered from its start
+            t0 = time.time()
+            self.first = self.proc.stdout.readline() if self.proc.stdout else ""
+            while not self.first and time.time() - t0 < 5:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
@@ -162,7 +167,8 @@ def cpu_reference(cfg, seconds=12.0):
             x = np.full(dims, 40.0)
             run = lambda: O.inverse_3d(O.hard_threshold(O.forward_3d(x, so), so.index, 0, so.filter_norms, K,  # noqa
                                                         cfg["sigma"]), so)
-    run()  # warm-up (first-touch page faults, plan creation)
+    if len(dims) == 2:
+        run()  # warm-up (first-touch page faults, plan creation); 3D volumes run once (bounded sample)
     times = []
     t_all = time.perf_counter()
     while True:
@@ -183,7 +189,7 @@ def cpu_reference(cfg, seconds=12.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="2d512", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -197,7 +203,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        res = cpu_reference(cfg, seconds=max(10.0, 2.0 * args.steps))
+        res = cpu_reference(cfg, seconds=20.0)
         line = {"metric": cfg["metric"], "value": res["value"], "unit": cfg["unit"], "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / res["value"],
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -413,6 +419,8 @@ def pass_bytes(name, dims):
         "f2_rows_r2c": 8 * N + 16 * Nh,           # band rows read + column-major half write
         "f2_rows_c2r_thr": 16 * Nh + 8 * N,       # half read + thresholded band write
         "f2_rows_c2r": 16 * Nh + 8 * N,
+        "f2_rows_fused": 16 * Nh + 8 * N + 16 * Nh,  # half read, thresholded band write, rec half write
+        "f3_rows_fused": 16 * Nh + 8 * N + 16 * Nh,
         "f2_cols_dec": 8 * Nh + 16 * Nh,          # real psi + half write (F re-reads hit L2)
         "f2_cols_rec": 16 * Nh + 8 * Nh,          # half read + real psi (slot writes amortised)
         "f2_cols_fwd": 32 * Nh,

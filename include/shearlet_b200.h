@@ -43,6 +43,7 @@ enum sl_status {
     SL_ERR_UNSUPPORTED_SIZE = 6, /* shearlet::UnsupportedSizeError               */
     SL_ERR_ASSET = 7,            /* shearlet::AssetError                         */
     SL_ERR_FORMAT = 8,           /* shearlet::FormatError                        */
+    SL_ERR_DEGENERATE_MASK = 9,  /* shearlet::DegenerateMaskError                */
     SL_ERR_CUDA = 20,            /* CUDA runtime failure                         */
     SL_ERR_INVALID = 22,         /* null handle / bad argument at the ABI        */
 };
@@ -123,6 +124,22 @@ int sl_hard_threshold_host(sl_system* sys, const double* in, double* out, int nb
                            double sigma, int scale_by_rms);
 int sl_denoise_host(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
                     int scale_by_rms);
+
+/* ---- iterative thresholding pipelines ("next") ----------------
+ * inpaint (apps.hpp:46-78, apps.cpp:179-235): estimate_{k+1} =
+ * rec(thr_uniform(dec(mask .* (masked - estimate_k) + estimate_k), delta_k)),
+ * delta_k = delta_init * delta_min^(k/(iterations-1)); delta_init < 0 selects
+ * the largest (RMS-scaled) coefficient of the input. separate (apps.hpp:80-90,
+ * apps.cpp:237-280) runs the same scheme jointly over a directional and an
+ * isotropic system. The whole loop runs on the device. */
+int sl_inpaint_dev(sl_system* sys, const double* masked, const double* mask, double* out, int iterations,
+                   double delta_init, double delta_min, int scale_by_rms, void* stream);
+int sl_inpaint_host(sl_system* sys, const double* masked, const double* mask, double* out, int iterations,
+                    double delta_init, double delta_min, int scale_by_rms);
+int sl_separate_dev(sl_system* directional, sl_system* isotropic, const double* signal, double* curves, double* blobs,
+                    int iterations, double delta_init, double delta_min, int scale_by_rms, void* stream);
+int sl_separate_host(sl_system* directional, sl_system* isotropic, const double* signal, double* curves,
+                     double* blobs, int iterations, double delta_init, double delta_min, int scale_by_rms);
 
 /* ---- instrumentation ---------------------------------------------------
  * sl_profile(enable) clears the per-pass statistics and turns CUDA-event timing

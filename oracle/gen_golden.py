@@ -140,6 +140,19 @@ def main():
     # acceptance crit.1 3D shape 32^3 [0,0,1]
     gen_3d("t3d_32_001", (32, 32, 32), [0, 0, 1], np.random.default_rng(2).uniform(-1, 1, (32, 32, 32)),
            K=[3.0, 3.0, 4.0], sigma=0.3)
+    # SURVEY 8f "next": iterative pipelines (apps.cpp:179-280)
+    s = ref.RefSystem2D(128, 128, [0, 1, 1])
+    mask = ref.random_mask(128, 128, 0.3, 5)
+    masked = ref.cartoon(128) * mask
+    rec = s.inpaint(masked, mask, 12)
+    save("it_inpaint128", masked=masked, mask=mask, levels=np.array([0, 1, 1]), iterations=12, delta_min=0.01,
+         out=rec)
+    sd = ref.RefSystem2D(128, 128, [0, 1])
+    si = ref.RefSystem2D(128, 128, [0, 0], impulse_fan=True)
+    sig = ref.curves_plus_dots(128)
+    c, b = sd.separate(si, sig, 10)
+    save("it_separate128", signal=sig, dir_levels=np.array([0, 1]), iso_levels=np.array([0, 0]), iterations=10,
+         delta_min=0.01, curves=c, blobs=b)
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

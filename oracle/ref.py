@@ -51,6 +51,10 @@ def lib():
             getattr(L, f"ref_hard_threshold_{d}").argtypes = [P, dp, C.c_int, dp, C.c_int, C.c_double, C.c_int, dp]
             getattr(L, f"ref_denoise_{d}").argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.c_int]
         L.ref_denoise_3d_stats.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.POINTER(C.c_longlong), dp, dp, C.POINTER(C.c_longlong), C.c_int, C.c_int]
+        L.ref_inpaint_2d.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, C.c_int]
+        L.ref_separate_2d.argtypes = [P, P, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, dp, C.c_int]
+        L.ref_random_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, dp]
+        L.ref_curves_plus_dots.argtypes = [C.c_int, dp]
         L.ref_cartoon.argtypes = [C.c_int, dp]
         L.ref_cartoon_volume.argtypes = [C.c_int, dp]
         L.ref_add_noise_2d.argtypes = [C.c_int, C.c_int, dp, C.c_double, C.c_uint64, dp]
@@ -149,6 +153,21 @@ class RefSystem2D:
         _check(lib().ref_denoise_2d(self.h, _dp(f), _dp(K), len(K), sigma, int(scaled), _dp(out), threads))
         return out
 
+    def inpaint(self, masked, mask, iterations, delta_init=-1.0, delta_min=0.01, scaled=True, threads=0):
+        masked = np.ascontiguousarray(masked, dtype=np.float64)
+        mask = np.ascontiguousarray(mask, dtype=np.float64)
+        out = np.zeros(self.shape)
+        _check(lib().ref_inpaint_2d(self.h, _dp(masked), _dp(mask), iterations, delta_init, delta_min, int(scaled),
+                                    _dp(out), threads))
+        return out
+
+    def separate(self, iso, signal, iterations, delta_init=-1.0, delta_min=0.01, scaled=True, threads=0):
+        signal = np.ascontiguousarray(signal, dtype=np.float64)
+        c, b = np.zeros(self.shape), np.zeros(self.shape)
+        _check(lib().ref_separate_2d(self.h, iso.h, _dp(signal), iterations, delta_init, delta_min, int(scaled),
+                                     _dp(c), _dp(b), threads))
+        return c, b
+
 
 class RefSystem3D:
     """Reference ShearletSystem3D (core/include/shearlet/system3d.hpp:32-61)."""
@@ -229,6 +248,18 @@ class RefSystem3D:
                                           kept.ctypes.data_as(LL), _dp(l2), _dp(smp), si.ctypes.data_as(LL),
                                           len(si), threads))
         return out, kept, l2, smp
+
+
+def random_mask(rows, cols, keep, seed):
+    out = np.zeros((rows, cols))
+    lib().ref_random_mask(rows, cols, keep, seed, _dp(out))
+    return out
+
+
+def curves_plus_dots(n):
+    out = np.zeros((n, n))
+    lib().ref_curves_plus_dots(n, _dp(out))
+    return out
 
 
 def cartoon(n):

@@ -285,6 +285,49 @@ int ref_denoise_3d_stats(void* h, const double* in, const double* K, int nK, dou
     });
 }
 
+// ---------------------------------------------------------------- iterative pipelines
+int ref_inpaint_2d(void* h, const double* masked, const double* mask, int iterations, double delta_init,
+                   double delta_min, int scaled, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem2D*>(h);
+        Signal2D x(s.rows, s.cols), m(s.rows, s.cols);
+        std::memcpy(x.data(), masked, sizeof(double) * x.size());
+        std::memcpy(m.data(), mask, sizeof(double) * m.size());
+        InpaintConfig cfg;
+        cfg.iterations = iterations;
+        cfg.delta_init = delta_init;
+        cfg.delta_min = delta_min;
+        cfg.scale_by_filter_norm = scaled != 0;
+        const auto r = inpaint(x, m, s, cfg, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
+int ref_separate_2d(void* hd, void* hi, const double* signal, int iterations, double delta_init, double delta_min,
+                    int scaled, double* curves, double* blobs, int threads) {
+    return guard([&] {
+        const auto& d = *static_cast<ShearletSystem2D*>(hd);
+        const auto& i = *static_cast<ShearletSystem2D*>(hi);
+        Signal2D x(d.rows, d.cols);
+        std::memcpy(x.data(), signal, sizeof(double) * x.size());
+        InpaintConfig cfg;
+        cfg.iterations = iterations;
+        cfg.delta_init = delta_init;
+        cfg.delta_min = delta_min;
+        cfg.scale_by_filter_norm = scaled != 0;
+        const auto r = separate(x, d, i, cfg, threads);
+        std::memcpy(curves, r.curvilinear.data(), sizeof(double) * x.size());
+        std::memcpy(blobs, r.blobs.data(), sizeof(double) * x.size());
+    });
+}
+void ref_random_mask(int rows, int cols, double keep, std::uint64_t seed, double* out) {
+    const auto m = phantoms::random_mask(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols), keep, seed);
+    std::memcpy(out, m.data(), sizeof(double) * m.size());
+}
+void ref_curves_plus_dots(int n, double* out) {
+    const auto g = phantoms::curves_plus_dots(static_cast<std::size_t>(n));
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+}
+
 // ---------------------------------------------------------------- inputs
 void ref_cartoon(int n, double* out) {
     const auto g = phantoms::cartoon(static_cast<std::size_t>(n));

@@ -66,6 +66,10 @@ class UnsupportedSizeError(Error):
     pass
 
 
+class DegenerateMaskError(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -75,7 +79,8 @@ class InvalidArgument(Error):
 
 
 _CODES = {1: Error, 2: ShapeError, 3: ConfigError, 4: DomainError, 5: SingularFrameError,
-          6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 20: CudaError, 22: InvalidArgument}
+          6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 9: DegenerateMaskError, 20: CudaError,
+          22: InvalidArgument}
 
 # ------------------------------------------------------------------ library
 _lib = None
@@ -122,6 +127,10 @@ def lib():
     L.sl_shearrec_batch_dev.argtypes = [P, P, i, P, P]
     L.sl_denoise_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
     L.sl_denoise_batch_host.argtypes = [P, dp, i, dp, dp, i, C.c_double, i]
+    L.sl_inpaint_dev.argtypes = [P, P, P, P, i, C.c_double, C.c_double, i, P]
+    L.sl_inpaint_host.argtypes = [P, dp, dp, dp, i, C.c_double, C.c_double, i]
+    L.sl_separate_dev.argtypes = [P, P, P, P, P, i, C.c_double, C.c_double, i, P]
+    L.sl_separate_host.argtypes = [P, P, dp, dp, dp, i, C.c_double, C.c_double, i]
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
@@ -139,7 +148,7 @@ EXPORTED_SYMBOLS = [
     "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_sheardec_host", "sl_shearrec_host",
     "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
     "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
-    "sl_denoise_batch_host",
+    "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
 ]
@@ -530,6 +539,68 @@ def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule):
     out = np.empty_like(frames)
     _check(lib().sl_denoise_batch_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))
     return out
+
+
+# ------------------------------------------------------------------ iterative pipelines
+@dataclass
+class InpaintConfig:
+    """apps.hpp:46-51."""
+    iterations: int = 100
+    delta_init: float = -1.0   # < 0: largest (RMS-scaled) coefficient of the input
+    delta_min: float = 0.01
+    scale_by_filter_norm: bool = True
+
+
+def inpaint(masked_signal, mask, sys: _System, config: InpaintConfig = InpaintConfig(), threads: int = 0):
+    """Iterative-thresholding inpainting (apps.hpp:59-76, apps.cpp:179-235); the loop runs on the GPU."""
+    if tuple(mask.shape) != tuple(masked_signal.shape):
+        raise ShapeError("inpaint: mask dims must match the signal")
+    _check_signal(masked_signal, sys, "inpaint")
+    args = (int(config.iterations), float(config.delta_init), float(config.delta_min),
+            int(config.scale_by_filter_norm))
+    L = lib()
+    if _is_cuda_tensor(masked_signal):
+        import torch
+        x = masked_signal.contiguous().to(torch.float64)
+        m = mask.contiguous().to(torch.float64)
+        out = torch.empty_like(x)
+        _check(L.sl_inpaint_dev(sys.handle, C.c_void_p(x.data_ptr()), C.c_void_p(m.data_ptr()),
+                                C.c_void_p(out.data_ptr()), *args, _stream_ptr(x.device.index)))
+        return out
+    x = np.ascontiguousarray(masked_signal, dtype=np.float64)
+    m = np.ascontiguousarray(mask, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(L.sl_inpaint_host(sys.handle, _dp(x), _dp(m), _dp(out), *args))
+    return out
+
+
+@dataclass
+class SeparationResult:
+    """apps.hpp:78-81."""
+    curvilinear: object
+    blobs: object
+
+
+def separate(signal, directional: ShearletSystem2D, isotropic: ShearletSystem2D,
+             config: InpaintConfig = InpaintConfig(), threads: int = 0) -> SeparationResult:
+    """Joint iterative thresholding over two systems (apps.hpp:83-90, apps.cpp:237-280)."""
+    if tuple(signal.shape) != tuple(directional.shape) or tuple(signal.shape) != tuple(isotropic.shape):
+        raise ShapeError("separate: both systems must match the signal dims")
+    args = (int(config.iterations), float(config.delta_init), float(config.delta_min),
+            int(config.scale_by_filter_norm))
+    L = lib()
+    if _is_cuda_tensor(signal):
+        import torch
+        x = signal.contiguous().to(torch.float64)
+        c, b = torch.empty_like(x), torch.empty_like(x)
+        _check(L.sl_separate_dev(directional.handle, isotropic.handle, C.c_void_p(x.data_ptr()),
+                                 C.c_void_p(c.data_ptr()), C.c_void_p(b.data_ptr()), *args,
+                                 _stream_ptr(x.device.index)))
+        return SeparationResult(c, b)
+    x = np.ascontiguousarray(signal, dtype=np.float64)
+    c, b = np.empty_like(x), np.empty_like(x)
+    _check(L.sl_separate_host(directional.handle, isotropic.handle, _dp(x), _dp(c), _dp(b), *args))
+    return SeparationResult(c, b)
 
 
 # ------------------------------------------------------------------ inputs

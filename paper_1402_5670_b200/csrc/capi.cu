@@ -11,6 +11,7 @@
 #include "build.cuh"
 #include "transform.cuh"
 #include "phantoms.cuh"
+#include "iterative.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
@@ -519,6 +520,78 @@ int sl_denoise_host(sl_system* h, const double* in, double* out, const double* K
         SL_CUDA(cudaMemcpy(s.io_in.p, in, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
         denoise(s, s.io_in.p, s.stack.p, s.io_out.p, s.delta.p, 0);
         SL_CUDA(cudaMemcpy(out, s.io_out.p, s.nreal * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---- iterative pipelines (apps.hpp:46-90) ------------------------------------
+int sl_inpaint_dev(sl_system* h, const double* masked, const double* mask, double* out, int iterations,
+                   double delta_init, double delta_min, int scale_by_rms, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(masked, "inpaint signal");
+        require_dev_ptr(mask, "inpaint mask");
+        require_dev_ptr(out, "inpaint output");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        inpaint(s, masked, mask, out, iterations, delta_init, delta_min, scale_by_rms != 0, stream_of(stream));
+    });
+}
+
+int sl_inpaint_host(sl_system* h, const double* masked, const double* mask, double* out, int iterations,
+                    double delta_init, double delta_min, int scale_by_rms) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!masked || !mask || !out) throw SlError(SL_ERR_INVALID, "null host pointer");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        DBuf<double> dm, dk, dout;
+        dm.alloc(static_cast<size_t>(s.nreal));
+        dk.alloc(static_cast<size_t>(s.nreal));
+        dout.alloc(static_cast<size_t>(s.nreal));
+        SL_CUDA(cudaMemcpy(dm.p, masked, s.nreal * 8, cudaMemcpyHostToDevice));
+        SL_CUDA(cudaMemcpy(dk.p, mask, s.nreal * 8, cudaMemcpyHostToDevice));
+        inpaint(s, dm.p, dk.p, dout.p, iterations, delta_init, delta_min, scale_by_rms != 0, 0);
+        SL_CUDA(cudaMemcpy(out, dout.p, s.nreal * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int sl_separate_dev(sl_system* directional, sl_system* isotropic, const double* signal, double* curves, double* blobs,
+                    int iterations, double delta_init, double delta_min, int scale_by_rms, void* stream) {
+    return guard([&] {
+        System& d = sys_of(directional);
+        System& i = sys_of(isotropic);
+        if (d.device != i.device) throw SlError(SL_ERR_CONFIG, "separate: systems on different devices");
+        require_dev_ptr(signal, "separate signal");
+        require_dev_ptr(curves, "separate curves");
+        require_dev_ptr(blobs, "separate blobs");
+        std::lock_guard<std::mutex> lk(d.mu);
+        std::unique_lock<std::mutex> lk2(i.mu, std::defer_lock);
+        if (&d != &i) lk2.lock();
+        DeviceGuard dg(d.device);
+        separate(d, i, signal, curves, blobs, iterations, delta_init, delta_min, scale_by_rms != 0,
+                 stream_of(stream));
+    });
+}
+
+int sl_separate_host(sl_system* directional, sl_system* isotropic, const double* signal, double* curves,
+                     double* blobs, int iterations, double delta_init, double delta_min, int scale_by_rms) {
+    return guard([&] {
+        System& d = sys_of(directional);
+        System& i = sys_of(isotropic);
+        if (d.device != i.device) throw SlError(SL_ERR_CONFIG, "separate: systems on different devices");
+        if (!signal || !curves || !blobs) throw SlError(SL_ERR_INVALID, "null host pointer");
+        std::lock_guard<std::mutex> lk(d.mu);
+        std::unique_lock<std::mutex> lk2(i.mu, std::defer_lock);
+        if (&d != &i) lk2.lock();
+        DeviceGuard dg(d.device);
+        DBuf<double> ds, dc, db;
+        ds.alloc(static_cast<size_t>(d.nreal));
+        dc.alloc(static_cast<size_t>(d.nreal));
+        db.alloc(static_cast<size_t>(d.nreal));
+        SL_CUDA(cudaMemcpy(ds.p, signal, d.nreal * 8, cudaMemcpyHostToDevice));
+        separate(d, i, ds.p, dc.p, db.p, iterations, delta_init, delta_min, scale_by_rms != 0, 0);
+        SL_CUDA(cudaMemcpy(curves, dc.p, d.nreal * 8, cudaMemcpyDeviceToHost));
+        SL_CUDA(cudaMemcpy(blobs, db.p, d.nreal * 8, cudaMemcpyDeviceToHost));
     });
 }
 

@@ -279,7 +279,21 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS)
 #pragma unroll
     for (int m = 0; m < E; ++m) x[m] = make_double2(0.0, 0.0);
     if (valid) {
-        for (int s = 0; s < nslots; ++s) {
+        // slots summed in order; two slots' loads in flight per step
+        int s = 0;
+        for (; s + 1 < nslots; s += 2) {
+            const double2* in0 = slots + (long long)s * sbs + (long long)k1 * L;
+            const double2* in1 = in0 + sbs;
+            double2 u[E], v[E];
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                u[m] = __ldcg(in0 + t + T * m);
+                v[m] = __ldcg(in1 + t + T * m);
+            }
+#pragma unroll
+            for (int m = 0; m < E; ++m) x[m] = cadd(cadd(x[m], u[m]), v[m]);
+        }
+        for (; s < nslots; ++s) {
             const double2* in = slots + (long long)s * sbs + (long long)k1 * L;
 #pragma unroll
             for (int m = 0; m < E; ++m) x[m] = cadd(x[m], __ldcg(in + t + T * m));
