@@ -27,6 +27,7 @@
 #ifndef SHEARLET_B200_H
 #define SHEARLET_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -140,6 +141,14 @@ int sl_separate_dev(sl_system* directional, sl_system* isotropic, const double* 
                     int iterations, double delta_init, double delta_min, int scale_by_rms, void* stream);
 int sl_separate_host(sl_system* directional, sl_system* isotropic, const double* signal, double* curves,
                      double* blobs, int iterations, double delta_init, double delta_min, int scale_by_rms);
+
+/* ---- SHCF coefficient files (transform.hpp:39-52, transform.cpp:127-269) --
+ * Host buffers; byte-identical to the reference's serialize(). The records
+ * are the handle's bands; deserialize checks magic, version, dims, band
+ * count and index records against the system (FormatError / ShapeError). */
+int sl_shcf_size(const sl_system* sys, int nbands, size_t* bytes);
+int sl_shcf_serialize(const sl_system* sys, const double* coeffs, int nbands, unsigned char* out, size_t cap);
+int sl_shcf_deserialize(const sl_system* sys, const unsigned char* in, size_t len, double* coeffs, int nbands);
 
 /* ---- instrumentation ---------------------------------------------------
  * sl_profile(enable) clears the per-pass statistics and turns CUDA-event timing

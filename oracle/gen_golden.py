@@ -153,6 +153,15 @@ def main():
     c, b = sd.separate(si, sig, 10)
     save("it_separate128", signal=sig, dir_levels=np.array([0, 1]), iso_levels=np.array([0, 0]), iterations=10,
          delta_min=0.01, curves=c, blobs=b)
+    # SURVEY 8f "next": SHCF coefficient files (transform.cpp:127-269), bytes from the reference serialize()
+    s = ref.RefSystem2D(16, 16, [0, 1])
+    b = s.forward(O.random_grid((16, 16), 21))
+    save("shcf_2d_16_01", levels=np.array([0, 1]), bands=b,
+         shcf=np.frombuffer(ref.serialize(s, b), dtype=np.uint8))
+    s3 = ref.RefSystem3D((8, 12, 10), [0])
+    b3 = s3.forward(np.random.default_rng(11).uniform(-1, 1, (8, 12, 10)))
+    save("shcf_3d_8x12x10_0", levels=np.array([0]), bands=b3,
+         shcf=np.frombuffer(ref.serialize(s3, b3), dtype=np.uint8))
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

@@ -62,6 +62,11 @@ def lib():
         L.ref_psnr_2d.argtypes = [C.c_int, C.c_int, dp, dp]
         L.ref_psnr_2d.restype = C.c_double
         L.ref_fft_forward.argtypes = [C.c_int, ip, dp]
+        for d in ("2d", "3d"):
+            getattr(L, f"ref_serialize_{d}").argtypes = [P, dp, C.c_int, C.c_char_p, C.c_longlong]
+            getattr(L, f"ref_serialize_{d}").restype = C.c_longlong
+        L.ref_deserialize.argtypes = [C.c_char_p, C.c_longlong, ip, ip, dp, C.c_longlong]
+        L.ref_deserialize.restype = C.c_int
         _lib = L
     return _lib
 
@@ -248,6 +253,34 @@ class RefSystem3D:
                                           kept.ctypes.data_as(LL), _dp(l2), _dp(smp), si.ctypes.data_as(LL),
                                           len(si), threads))
         return out, kept, l2, smp
+
+
+def _serialize(fn, h, bands):
+    bands = np.ascontiguousarray(bands, dtype=np.float64)
+    n = fn(h, _dp(bands), bands.shape[0], None, 0)
+    if n < 0:
+        _check(int(-n))
+    buf = C.create_string_buffer(int(n))
+    fn(h, _dp(bands), bands.shape[0], buf, n)
+    return buf.raw
+
+
+def serialize(system, bands) -> bytes:
+    """Reference serialize() (transform.cpp:185-213) of a stack on `system`."""
+    fn = lib().ref_serialize_2d if isinstance(system, RefSystem2D) else lib().ref_serialize_3d
+    return _serialize(fn, system.h, bands)
+
+
+def deserialize(data: bytes):
+    """Reference deserialize_2d/3d (transform.cpp:216-269) -> bands [count][dims]."""
+    nd, dims = C.c_int(), np.zeros(3, dtype=np.int32)
+    nb = lib().ref_deserialize(data, len(data), C.byref(nd), _ip(dims), None, 0)
+    if nb < 0:
+        _check(-nb)
+    shape = tuple(int(d) for d in dims[: nd.value])
+    out = np.zeros((nb,) + shape)
+    lib().ref_deserialize(data, len(data), C.byref(nd), _ip(dims), _dp(out), out.size)
+    return out
 
 
 def random_mask(rows, cols, keep, seed):

@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,9 @@ int guard(F&& f) {
     catch (const DomainError& e) { g_err = e.what(); return 4; }
     catch (const SingularFrameError& e) { g_err = e.what(); return 5; }
     catch (const UnsupportedSizeError& e) { g_err = e.what(); return 6; }
+    catch (const AssetError& e) { g_err = e.what(); return 7; }
+    catch (const FormatError& e) { g_err = e.what(); return 8; }
+    catch (const DegenerateMaskError& e) { g_err = e.what(); return 9; }
     catch (const Error& e) { g_err = e.what(); return 1; }
     catch (const std::exception& e) { g_err = e.what(); return 99; }
 }
@@ -319,6 +323,62 @@ int ref_separate_2d(void* hd, void* hi, const double* signal, int iterations, do
         std::memcpy(blobs, r.blobs.data(), sizeof(double) * x.size());
     });
 }
+// ---------------------------------------------------------------- SHCF files
+// serialize() (transform.hpp:44-45) into a caller buffer; returns the byte
+// count (call with out == nullptr to size), or -code on error.
+long long ref_serialize_2d(void* h, const double* bands, int nb, unsigned char* out, long long cap) {
+    std::string bytes;
+    const int rc = guard([&] {
+        std::ostringstream os(std::ios::binary);
+        serialize(stack2_of(*static_cast<ShearletSystem2D*>(h), bands, nb), os);
+        bytes = os.str();
+    });
+    if (rc) return -rc;
+    if (out && cap >= static_cast<long long>(bytes.size())) std::memcpy(out, bytes.data(), bytes.size());
+    return static_cast<long long>(bytes.size());
+}
+long long ref_serialize_3d(void* h, const double* bands, int nb, unsigned char* out, long long cap) {
+    std::string bytes;
+    const int rc = guard([&] {
+        std::ostringstream os(std::ios::binary);
+        serialize(stack3_of(*static_cast<ShearletSystem3D*>(h), bands, nb), os);
+        bytes = os.str();
+    });
+    if (rc) return -rc;
+    if (out && cap >= static_cast<long long>(bytes.size())) std::memcpy(out, bytes.data(), bytes.size());
+    return static_cast<long long>(bytes.size());
+}
+// deserialize_2d/3d (transform.hpp:50-51): bands out (nb*size doubles), dims
+// out, returns band count or -code.
+int ref_deserialize(const unsigned char* in, long long len, int* ndim, int* dims, double* bands, long long cap) {
+    int nb = 0;
+    const int rc = guard([&] {
+        std::istringstream is(std::string(reinterpret_cast<const char*>(in), static_cast<std::size_t>(len)),
+                              std::ios::binary);
+        const int d = shcf_dimensionality(is);
+        is.seekg(0);
+        *ndim = d;
+        if (d == 2) {
+            const auto c = deserialize_2d(is);
+            dims[0] = static_cast<int>(c.rows); dims[1] = static_cast<int>(c.cols); dims[2] = 1;
+            nb = static_cast<int>(c.bands.size());
+            const std::size_t n = c.rows * c.cols;
+            if (bands && cap >= static_cast<long long>(n * c.bands.size()))
+                for (std::size_t i = 0; i < c.bands.size(); ++i)
+                    std::memcpy(bands + i * n, c.bands[i].data(), sizeof(double) * n);
+        } else {
+            const auto c = deserialize_3d(is);
+            for (int a = 0; a < 3; ++a) dims[a] = static_cast<int>(c.dims[a]);
+            nb = static_cast<int>(c.bands.size());
+            const std::size_t n = c.dims[0] * c.dims[1] * c.dims[2];
+            if (bands && cap >= static_cast<long long>(n * c.bands.size()))
+                for (std::size_t i = 0; i < c.bands.size(); ++i)
+                    std::memcpy(bands + i * n, c.bands[i].data(), sizeof(double) * n);
+        }
+    });
+    return rc ? -rc : nb;
+}
+
 void ref_random_mask(int rows, int cols, double keep, std::uint64_t seed, double* out) {
     const auto m = phantoms::random_mask(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols), keep, seed);
     std::memcpy(out, m.data(), sizeof(double) * m.size());

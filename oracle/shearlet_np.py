@@ -534,6 +534,21 @@ class MT19937_64:
         return y & 0xFFFFFFFFFFFFFFFF
 
 
+
+def serialize_shcf(bands, index) -> bytes:  # src/transform.cpp:185-213
+    """SHCF bytes: "SHCF", u16 1, u8 ndim, u32 dims, u32 count, records
+    (u8 kind, i32 scale, i32 k1/shear, i32 k2/0), then f64 LE row-major."""
+    import struct
+    bands = np.ascontiguousarray(bands, dtype="<f8")
+    nd = bands.ndim - 1
+    out = [b"SHCF", struct.pack("<HB", 1, nd), struct.pack("<%dI" % nd, *bands.shape[1:]),
+           struct.pack("<I", bands.shape[0])]
+    for r in index:
+        out.append(struct.pack("<Biii", r[0], r[1], r[2], r[3] if len(r) > 3 else 0))
+    out.append(bands.tobytes())
+    return b"".join(out)
+
+
 def random_grid(shape, seed):
     """U[-1,1) grid, tests/oracles.hpp:175-190 (pure Python: small sizes only)."""
     rng = MT19937_64(seed)

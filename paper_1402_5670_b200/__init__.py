@@ -131,6 +131,9 @@ def lib():
     L.sl_inpaint_host.argtypes = [P, dp, dp, dp, i, C.c_double, C.c_double, i]
     L.sl_separate_dev.argtypes = [P, P, P, P, P, i, C.c_double, C.c_double, i, P]
     L.sl_separate_host.argtypes = [P, P, dp, dp, dp, i, C.c_double, C.c_double, i]
+    L.sl_shcf_size.argtypes = [P, i, C.POINTER(C.c_size_t)]
+    L.sl_shcf_serialize.argtypes = [P, dp, i, C.c_char_p, C.c_size_t]
+    L.sl_shcf_deserialize.argtypes = [P, C.c_char_p, C.c_size_t, dp, i]
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
@@ -149,6 +152,7 @@ EXPORTED_SYMBOLS = [
     "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
     "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
+    "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
 ]
@@ -538,6 +542,26 @@ def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule):
     frames = np.ascontiguousarray(frames, dtype=np.float64)
     out = np.empty_like(frames)
     _check(lib().sl_denoise_batch_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))
+    return out
+
+
+# ------------------------------------------------------------------ SHCF files
+def serialize(coeffs, sys: _System) -> bytes:
+    """SHCF bytes of a coefficient stack (transform.hpp:45-46), identical to the reference."""
+    c = np.ascontiguousarray(coeffs.cpu().numpy() if _is_cuda_tensor(coeffs) else coeffs, dtype=np.float64)
+    if c.ndim != sys.ndim + 1 or tuple(c.shape[1:]) != tuple(sys.shape):
+        raise ShapeError(f"serialize: stack shape {c.shape} does not match the system {sys.shape}")
+    n = C.c_size_t()
+    _check(lib().sl_shcf_size(sys.handle, int(c.shape[0]), C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(lib().sl_shcf_serialize(sys.handle, _dp(c), int(c.shape[0]), buf, n.value))
+    return buf.raw
+
+
+def deserialize(data: bytes, sys: _System) -> np.ndarray:
+    """Coefficient stack from SHCF bytes, validated against the system (transform.hpp:50-52)."""
+    out = np.empty((sys.n_bands,) + tuple(sys.shape))
+    _check(lib().sl_shcf_deserialize(sys.handle, data, len(data), _dp(out), sys.n_bands))
     return out
 
 

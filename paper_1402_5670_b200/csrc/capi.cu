@@ -12,6 +12,7 @@
 #include "transform.cuh"
 #include "phantoms.cuh"
 #include "iterative.cuh"
+#include "shcf.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
@@ -592,6 +593,31 @@ int sl_separate_host(sl_system* directional, sl_system* isotropic, const double*
         separate(d, i, ds.p, dc.p, db.p, iterations, delta_init, delta_min, scale_by_rms != 0, 0);
         SL_CUDA(cudaMemcpy(curves, dc.p, d.nreal * 8, cudaMemcpyDeviceToHost));
         SL_CUDA(cudaMemcpy(blobs, db.p, d.nreal * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---- SHCF coefficient files (transform.hpp:39-52) --------------------------
+int sl_shcf_size(const sl_system* h, int nbands, size_t* bytes) {
+    return guard([&] {
+        if (!bytes) throw SlError(SL_ERR_INVALID, "null size");
+        *bytes = shcf_bytes(sys_of(h), nbands);
+    });
+}
+
+int sl_shcf_serialize(const sl_system* h, const double* coeffs, int nbands, unsigned char* out, size_t cap) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (!coeffs || !out) throw SlError(SL_ERR_INVALID, "null pointer");
+        if (cap < shcf_bytes(s, nbands)) throw SlError(SL_ERR_INVALID, "output buffer too small");
+        shcf_serialize(s, coeffs, nbands, out);
+    });
+}
+
+int sl_shcf_deserialize(const sl_system* h, const unsigned char* in, size_t len, double* coeffs, int nbands) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        if (!in || !coeffs) throw SlError(SL_ERR_INVALID, "null pointer");
+        shcf_deserialize(s, in, len, coeffs, nbands);
     });
 }
 

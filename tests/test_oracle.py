@@ -123,3 +123,16 @@ def test_reference_library_matches_golden():
     g = golden("t2d_64_0011_seed22")
     r = ref.RefSystem2D(64, 64, [0, 0, 1, 1])
     assert rel_l2(r.forward(g["f"]), g["bands"]) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["shcf_2d_16_01", "shcf_3d_8x12x10_0"])
+def test_oracle_shcf_bytes_golden(name):
+    # transform.cpp:185-213: the restated writer reproduces the reference's bytes
+    g = golden(name)
+    b = g["bands"]
+    if b.ndim == 3:
+        s = O.build_system_2d(b.shape[1], b.shape[2], list(g["levels"]))
+        idx = [tuple(r) + (0,) for r in s.index]
+    else:
+        idx = O.enumerate_filters_3d(O.Profile(list(g["levels"]), 0))
+    assert O.serialize_shcf(b, idx) == g["shcf"].tobytes()
