@@ -69,6 +69,24 @@ int sl_system_create_2d(int rows, int cols, const int* levels, int n_scales, int
                         int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out);
 int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
                         int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out);
+/* Same with an explicit filter bank: build_system_2d/3d(..., fan, qmf, ...)
+ * with a user FanFilter (row-major fan_rows x fan_cols taps, centre
+ * (fan_c0, fan_c1); load_fan_filter / maxflat_fan(order), filters.hpp:54-67,
+ * fan_design.cpp:70-108) and QmfPair (1D taps + centre index; filters.hpp:14-21).
+ * lowpass NULL = maximally_flat_9tap(); highpass NULL = mirror_highpass(lowpass)
+ * (QmfPair::from_lowpass); fan NULL = default_fan_filter(). The filter spectra
+ * must come out real (centrally symmetric taps), else SL_ERR_DOMAIN. */
+int sl_system_create_2d_ex(int rows, int cols, const int* levels, int n_scales, int j0, int full_system,
+                           const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
+                           int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
+                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out);
+int sl_system_create_3d_ex(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
+                           const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
+                           int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
+                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out);
+/* fan_design::maxflat_fan(order) (fan_design.cpp:70-108), host: dims/centre
+ * always written; taps written when non-NULL (cap doubles). */
+int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1);
 int sl_system_destroy(sl_system* sys);
 
 /* ---- system queries (ShearletSystem2D/3D members) ------------------------ */

@@ -27,6 +27,7 @@ struct AssetError : Error { using Error::Error; };
 struct FormatError : Error { using Error::Error; };
 struct SingularFrameError : Error { using Error::Error; };
 struct UnsupportedSizeError : Error { using Error::Error; };
+struct DegenerateMaskError : Error { using Error::Error; };
 struct CudaError : Error { using Error::Error; };
 
 inline void check(int rc) {
@@ -40,6 +41,7 @@ inline void check(int rc) {
         case SL_ERR_UNSUPPORTED_SIZE: throw UnsupportedSizeError(m);
         case SL_ERR_ASSET: throw AssetError(m);
         case SL_ERR_FORMAT: throw FormatError(m);
+        case SL_ERR_DEGENERATE_MASK: throw DegenerateMaskError(m);
         case SL_ERR_CUDA: throw CudaError(m);
         default: throw Error(m);
     }
@@ -136,6 +138,51 @@ inline ShearletSystem build_system_3d(std::array<std::size_t, 3> d, const ScaleP
     return ShearletSystem(h);
 }
 
+// Explicit filter bank (filters.hpp:14-67): 1D QMF taps and a 2D fan, each with a centre.
+struct Taps1d {
+    std::vector<double> v;
+    int center = 0;
+};
+struct QmfPair {
+    Taps1d lowpass, highpass;  // highpass empty = mirror_highpass(lowpass)
+    static QmfPair from_lowpass(Taps1d low) { return QmfPair{std::move(low), {}}; }
+};
+struct FanFilter {
+    std::vector<double> taps;  // row-major rows x cols
+    int rows = 0, cols = 0, center0 = 0, center1 = 0;
+    static FanFilter impulse() { return FanFilter{{1.0}, 1, 1, 0, 0}; }
+    static FanFilter maxflat(int order) {  // fan_design::maxflat_fan
+        FanFilter f;
+        check(sl_maxflat_fan(order, nullptr, 0, &f.rows, &f.cols, &f.center0, &f.center1));
+        f.taps.resize(static_cast<std::size_t>(f.rows) * f.cols);
+        check(sl_maxflat_fan(order, f.taps.data(), static_cast<int64_t>(f.taps.size()), nullptr, nullptr, nullptr,
+                             nullptr));
+        return f;
+    }
+};
+inline ShearletSystem build_system_2d(std::size_t rows, std::size_t cols, const ScaleProfile& p, const FanFilter& fan,
+                                      const QmfPair& qmf, bool full_system = false, int device = 0) {
+    sl_system* h = nullptr;
+    const bool hp = !qmf.highpass.v.empty();
+    check(sl_system_create_2d_ex(
+        static_cast<int>(rows), static_cast<int>(cols), p.shear_levels.data(), p.n_scales(), p.coarsest_scale_offset,
+        full_system, qmf.lowpass.v.empty() ? nullptr : qmf.lowpass.v.data(), static_cast<int>(qmf.lowpass.v.size()), qmf.lowpass.center,
+        hp ? qmf.highpass.v.data() : nullptr, static_cast<int>(qmf.highpass.v.size()), qmf.highpass.center,
+        fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1, device, 0, -1, &h));
+    return ShearletSystem(h);
+}
+inline ShearletSystem build_system_3d(std::array<std::size_t, 3> d, const ScaleProfile& p, const FanFilter& fan,
+                                      const QmfPair& qmf, bool full_system = false, int device = 0) {
+    sl_system* h = nullptr;
+    const bool hp = !qmf.highpass.v.empty();
+    check(sl_system_create_3d_ex(
+        static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]), p.shear_levels.data(), p.n_scales(),
+        p.coarsest_scale_offset, full_system, qmf.lowpass.v.empty() ? nullptr : qmf.lowpass.v.data(), static_cast<int>(qmf.lowpass.v.size()),
+        qmf.lowpass.center, hp ? qmf.highpass.v.data() : nullptr, static_cast<int>(qmf.highpass.v.size()),
+        qmf.highpass.center, fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1, device, 0, -1, &h));
+    return ShearletSystem(h);
+}
+
 // forward / inverse (transform.hpp:27-37), value semantics
 inline std::vector<double> forward(const std::vector<double>& f, const ShearletSystem& s) {
     if (f.size() != s.size()) throw ShapeError("forward: signal dims do not match the system grid");
@@ -167,6 +214,21 @@ inline std::vector<double> denoise(const std::vector<double>& noisy, const Shear
     check(sl_denoise_host(s.handle(), noisy.data(), out.data(), sch.per_scale_factors.data(),
                           static_cast<int>(sch.per_scale_factors.size()), sch.sigma, sch.scale_by_filter_norm));
     return out;
+}
+
+// SHCF coefficient files (transform.hpp:39-52): bytes of serialize() / deserialize_2d/3d
+inline std::vector<unsigned char> serialize(const std::vector<double>& coeffs, const ShearletSystem& s) {
+    if (coeffs.size() != s.n_bands() * s.size()) throw ShapeError("serialize: stack does not match the system");
+    std::size_t n = 0;
+    check(sl_shcf_size(s.handle(), static_cast<int>(s.n_bands()), &n));
+    std::vector<unsigned char> out(n);
+    check(sl_shcf_serialize(s.handle(), coeffs.data(), static_cast<int>(s.n_bands()), out.data(), n));
+    return out;
+}
+inline std::vector<double> deserialize(const std::vector<unsigned char>& bytes, const ShearletSystem& s) {
+    std::vector<double> c(s.n_bands() * s.size());
+    check(sl_shcf_deserialize(s.handle(), bytes.data(), bytes.size(), c.data(), static_cast<int>(s.n_bands())));
+    return c;
 }
 
 }  // namespace shearlet_b200

@@ -108,6 +108,36 @@ def gen_3d(name, dims, levels, f, K=None, sigma=None, full=False, threads=0):
     save(name, **kw)
 
 
+LEGALL_LOWPASS = np.array([-0.125, 0.25, 0.75, 0.25, -0.125])  # symmetric 5-tap, sums to 1
+
+
+def gen_banks():
+    """Custom FanFilter / QmfPair systems (build_system_2d/3d with explicit fan, qmf)."""
+    fan2 = ref.maxflat_fan(2)
+    q = (LEGALL_LOWPASS, 2)
+    s = ref.RefSystem2D(32, 32, [0, 1], fan=fan2, qmf=q)
+    f = O.random_grid((32, 32), 9)
+    b = s.forward(f)
+    save("bank_2d_32_fan2_legall", f=f, levels=np.array([0, 1]), fan=fan2[0], fan_c=np.array(fan2[1:]),
+         lowpass=LEGALL_LOWPASS, lowpass_c=2, index=s.index(), filter_norms=s.filter_norms(),
+         frame_weight=s.frame_weight(), bands=b, rec=s.inverse(b))
+    fan3 = ref.maxflat_fan(3)
+    s = ref.RefSystem2D(48, 40, [1, 1], fan=fan3)
+    f = O.random_grid((48, 40), 10)
+    b = s.forward(f)
+    save("bank_2d_48x40_fan3", f=f, levels=np.array([1, 1]), fan=fan3[0], fan_c=np.array(fan3[1:]),
+         index=s.index(), filter_norms=s.filter_norms(), frame_weight=s.frame_weight(), bands=b,
+         rec=s.inverse(b))
+    s3 = ref.RefSystem3D((16, 16, 16), [0, 1], fan=fan2, qmf=q)
+    f = np.random.default_rng(12).uniform(-1, 1, (16, 16, 16))
+    b = s3.forward(f)
+    save("bank_3d_16_fan2_legall", f=f, levels=np.array([0, 1]), fan=fan2[0], fan_c=np.array(fan2[1:]),
+         lowpass=LEGALL_LOWPASS, lowpass_c=2, index=s3.index(), filter_norms=s3.filter_norms(),
+         W_sample=s3.frame_weight().reshape(-1)[sample_idx(f.size)], rec=s3.inverse(b), **band_stats(b))
+    # fan_design::maxflat_fan(order), orders 1..6 (fan_design.cpp:70-108)
+    save("maxflat_fans", **{f"order{o}": ref.maxflat_fan(o)[0] for o in range(1, 7)})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
@@ -162,6 +192,7 @@ def main():
     b3 = s3.forward(np.random.default_rng(11).uniform(-1, 1, (8, 12, 10)))
     save("shcf_3d_8x12x10_0", levels=np.array([0]), bands=b3,
          shcf=np.frombuffer(ref.serialize(s3, b3), dtype=np.uint8))
+    gen_banks()
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

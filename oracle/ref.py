@@ -62,6 +62,10 @@ def lib():
         L.ref_psnr_2d.argtypes = [C.c_int, C.c_int, dp, dp]
         L.ref_psnr_2d.restype = C.c_double
         L.ref_fft_forward.argtypes = [C.c_int, ip, dp]
+        bank = [dp, C.c_int, C.c_int, dp, C.c_int, C.c_int, dp, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_build_2d_bank.argtypes = [C.c_int] * 2 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
+        L.ref_build_3d_bank.argtypes = [C.c_int] * 3 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
+        L.ref_maxflat_fan.argtypes = [C.c_int, dp, C.c_longlong, ip]
         for d in ("2d", "3d"):
             getattr(L, f"ref_serialize_{d}").argtypes = [P, dp, C.c_int, C.c_char_p, C.c_longlong]
             getattr(L, f"ref_serialize_{d}").restype = C.c_longlong
@@ -81,6 +85,37 @@ def _ip(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_int))
 
 
+def _bank_args(fan, qmf):
+    """fan = (taps2d, c0, c1) or None (default fan); qmf = (lowpass, c) or (lowpass, c, highpass, hc) or None."""
+    keep = []
+    if qmf is None:
+        q = [None, 0, 0, None, 0, 0]
+    else:
+        lp = np.ascontiguousarray(qmf[0], dtype=np.float64)
+        keep.append(lp)
+        q = [_dp(lp), len(lp), int(qmf[1]), None, 0, 0]
+        if len(qmf) > 2:
+            hp = np.ascontiguousarray(qmf[2], dtype=np.float64)
+            keep.append(hp)
+            q[3:] = [_dp(hp), len(hp), int(qmf[3])]
+    if fan is None:
+        f = [None, 0, 0, 0, 0]
+    else:
+        t = np.ascontiguousarray(fan[0], dtype=np.float64)
+        keep.append(t)
+        f = [_dp(t), t.shape[0], t.shape[1], int(fan[1]), int(fan[2])]
+    return q + f, keep
+
+
+def maxflat_fan(order):
+    """fan_design::maxflat_fan(order) from the reference -> (taps, c0, c1)."""
+    dims = np.zeros(4, dtype=np.int32)
+    _check(lib().ref_maxflat_fan(order, None, 0, _ip(dims)))
+    t = np.zeros((dims[0], dims[1]))
+    _check(lib().ref_maxflat_fan(order, _dp(t), t.size, _ip(dims)))
+    return t, int(dims[2]), int(dims[3])
+
+
 class RefError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"reference error {code}: {msg}")
@@ -95,11 +130,15 @@ def _check(rc):
 class RefSystem2D:
     """Reference ShearletSystem2D (core/include/shearlet/system2d.hpp:29-51)."""
 
-    def __init__(self, rows, cols, levels, j0=0, full=False, impulse_fan=False, threads=0):
+    def __init__(self, rows, cols, levels, j0=0, full=False, impulse_fan=False, threads=0, fan=None, qmf=None):
         L = lib()
         lv = np.asarray(levels, dtype=np.int32)
         h = C.c_void_p()
-        _check(L.ref_build_2d(rows, cols, _ip(lv), len(lv), j0, int(full), int(impulse_fan), threads, C.byref(h)))
+        if fan is None and qmf is None:
+            _check(L.ref_build_2d(rows, cols, _ip(lv), len(lv), j0, int(full), int(impulse_fan), threads, C.byref(h)))
+        else:
+            args, self._keep = _bank_args(fan, qmf)
+            _check(L.ref_build_2d_bank(rows, cols, _ip(lv), len(lv), j0, int(full), *args, threads, C.byref(h)))
         self.h = h
         self.rows, self.cols = rows, cols
         self.shape = (rows, cols)
@@ -177,12 +216,17 @@ class RefSystem2D:
 class RefSystem3D:
     """Reference ShearletSystem3D (core/include/shearlet/system3d.hpp:32-61)."""
 
-    def __init__(self, dims, levels, j0=0, full=False, impulse_fan=False, threads=0):
+    def __init__(self, dims, levels, j0=0, full=False, impulse_fan=False, threads=0, fan=None, qmf=None):
         L = lib()
         lv = np.asarray(levels, dtype=np.int32)
         h = C.c_void_p()
         n0, n1, n2 = dims
-        _check(L.ref_build_3d(n0, n1, n2, _ip(lv), len(lv), j0, int(full), int(impulse_fan), threads, C.byref(h)))
+        if fan is None and qmf is None:
+            _check(L.ref_build_3d(n0, n1, n2, _ip(lv), len(lv), j0, int(full), int(impulse_fan), threads,
+                                  C.byref(h)))
+        else:
+            args, self._keep = _bank_args(fan, qmf)
+            _check(L.ref_build_3d_bank(n0, n1, n2, _ip(lv), len(lv), j0, int(full), *args, threads, C.byref(h)))
         self.h = h
         self.shape = tuple(dims)
         self.n_scales = len(lv)

@@ -51,6 +51,21 @@ const QmfPair& qmf() {
 FanFilter fan_for(int impulse_fan) {
     return impulse_fan ? FanFilter::impulse() : default_fan_filter();
 }
+QmfPair qmf_of(const double* lp, int lpn, int lpc, const double* hp, int hpn, int hpc) {
+    if (!lp) return qmf();
+    QmfPair q = QmfPair::from_lowpass(Taps1d{std::vector<double>(lp, lp + lpn), lpc});
+    if (hp) q.highpass = Taps1d{std::vector<double>(hp, hp + hpn), hpc};
+    return q;
+}
+FanFilter fan_of(const double* f, int fr, int fc, int fc0, int fc1) {
+    if (!f) return default_fan_filter();
+    Taps2d t;
+    t.v = RealGrid2(static_cast<std::size_t>(fr), static_cast<std::size_t>(fc));
+    std::memcpy(t.v.data(), f, sizeof(double) * static_cast<std::size_t>(fr * fc));
+    t.center0 = fc0;
+    t.center1 = fc1;
+    return FanFilter{t, "custom"};
+}
 ScaleProfile profile_of(const int* levels, int n, int j0) {
     return ScaleProfile::from_levels(std::vector<int>(levels, levels + n), j0);
 }
@@ -70,6 +85,41 @@ int ref_build_2d(int rows, int cols, const int* levels, int n_scales, int j0, in
         *out = s;
     });
 }
+// build_system_2d/3d with an explicit FanFilter + QmfPair (system2d.hpp:66-69)
+int ref_build_2d_bank(int rows, int cols, const int* levels, int n_scales, int j0, int full, const double* lp, int lpn,
+                      int lpc, const double* hp, int hpn, int hpc, const double* fan, int fr, int fc, int fc0, int fc1,
+                      int threads, void** out) {
+    return guard([&] {
+        auto* s = new ShearletSystem2D(build_system_2d(
+            static_cast<std::size_t>(rows), static_cast<std::size_t>(cols), profile_of(levels, n_scales, j0),
+            fan_of(fan, fr, fc, fc0, fc1), qmf_of(lp, lpn, lpc, hp, hpn, hpc), full != 0, threads));
+        *out = s;
+    });
+}
+int ref_build_3d_bank(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full, const double* lp,
+                      int lpn, int lpc, const double* hp, int hpn, int hpc, const double* fan, int fr, int fc, int fc0,
+                      int fc1, int threads, void** out) {
+    return guard([&] {
+        auto* s = new ShearletSystem3D(build_system_3d(
+            {static_cast<std::size_t>(n0), static_cast<std::size_t>(n1), static_cast<std::size_t>(n2)},
+            profile_of(levels, n_scales, j0), fan_of(fan, fr, fc, fc0, fc1), qmf_of(lp, lpn, lpc, hp, hpn, hpc),
+            full != 0, threads));
+        *out = s;
+    });
+}
+// fan_design::maxflat_fan(order) -> taps (cap doubles), dims and centres
+int ref_maxflat_fan(int order, double* out, long long cap, int* dims) {
+    return guard([&] {
+        const Taps2d t = fan_design::maxflat_fan(order);
+        dims[0] = static_cast<int>(t.size0());
+        dims[1] = static_cast<int>(t.size1());
+        dims[2] = static_cast<int>(t.center0);
+        dims[3] = static_cast<int>(t.center1);
+        if (out && cap >= static_cast<long long>(t.size0() * t.size1()))
+            std::memcpy(out, t.v.data(), sizeof(double) * t.size0() * t.size1());
+    });
+}
+
 void ref_free_2d(void* h) { delete static_cast<ShearletSystem2D*>(h); }
 int ref_redundancy_2d(void* h) { return static_cast<int>(static_cast<ShearletSystem2D*>(h)->redundancy()); }
 

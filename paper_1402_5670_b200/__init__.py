@@ -21,6 +21,7 @@ no CPU fallback: without the built library every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -104,6 +105,10 @@ def lib():
     L.sl_device_count.argtypes = [ip]
     L.sl_system_create_2d.argtypes = [i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
     L.sl_system_create_3d.argtypes = [i, i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
+    bank = [dp, i, i, dp, i, i, dp, i, i, i, i]
+    L.sl_system_create_2d_ex.argtypes = [i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
+    L.sl_system_create_3d_ex.argtypes = [i, i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
+    L.sl_maxflat_fan.argtypes = [i, dp, C.c_int64, ip, ip, ip, ip]
     L.sl_system_destroy.argtypes = [P]
     L.sl_ndim.argtypes = [P, ip, C.POINTER(C.c_int64)]
     L.sl_redundancy.argtypes = [P, ip]
@@ -153,6 +158,7 @@ EXPORTED_SYMBOLS = [
     "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
+    "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
 ]
@@ -347,30 +353,159 @@ def _levels_arg(profile: ScaleProfile):
     return lv, lv.ctypes.data_as(C.POINTER(C.c_int))
 
 
-def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan: str = "dmaxflat4",
+def alpha_to_shear_levels(alpha: Sequence[float], j0: int) -> List[int]:  # filters.cpp:196-207
+    out = []
+    for i, a in enumerate(alpha):
+        if not (0.0 < a < 2.0):
+            raise DomainError("alpha_to_shear_levels: alpha must lie in (0, 2)")
+        out.append(int(math.ceil((2.0 - a) * (j0 + i) / 2.0)))
+    return out
+
+
+@dataclass
+class QmfPair:
+    """Quadrature-mirror pair (filters.hpp:14-21): 1D taps with a centre index."""
+    lowpass: np.ndarray
+    highpass: np.ndarray
+    lowpass_center: int
+    highpass_center: int
+
+    @staticmethod
+    def from_lowpass(taps: Sequence[float], center: Optional[int] = None) -> "QmfPair":
+        """g(n) = (-1)^n h(n), n counted from the centre (filters.cpp:22-34)."""
+        h = np.asarray(taps, dtype=np.float64).copy()
+        c = len(h) // 2 if center is None else int(center)
+        g = np.array([(-v if (i - c) % 2 else v) for i, v in enumerate(h)], dtype=np.float64)
+        return QmfPair(h, g, c, c)
+
+    @staticmethod
+    def maximally_flat_9tap() -> Optional["QmfPair"]:
+        return None  # the library's built-in default (filters.cpp:12-20, 36-38)
+
+
+@dataclass
+class FanFilter:
+    """2D directional fan filter with provenance (filters.hpp:51-67)."""
+    taps: np.ndarray
+    center0: int
+    center1: int
+    provenance: str = ""
+
+    @staticmethod
+    def impulse() -> "FanFilter":
+        return FanFilter(np.ones((1, 1)), 0, 0, "impulse")
+
+    @staticmethod
+    def maxflat(order: int) -> "FanFilter":
+        """fan_design::maxflat_fan(order) (fan_design.cpp:70-108), computed by the library."""
+        r, c, c0, c1 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().sl_maxflat_fan(int(order), None, 0, C.byref(r), C.byref(c), C.byref(c0), C.byref(c1)))
+        t = np.zeros((r.value, c.value))
+        _check(lib().sl_maxflat_fan(int(order), _dp(t), t.size, None, None, None, None))
+        return FanFilter(t, c0.value, c1.value, f"dmaxflat{order}")
+
+    @staticmethod
+    def default() -> "FanFilter":
+        """default_fan_filter() (filters.cpp:114-122), checksum-verified."""
+        f = FanFilter.maxflat(4)
+        if fan_checksum(f) != DEFAULT_FAN_CHECKSUM:
+            raise AssetError("default_fan_filter: checksum mismatch on bundled fan filter")
+        return f
+
+    @staticmethod
+    def load(path: str) -> "FanFilter":
+        """load_fan_filter (filters.cpp:124-140): "rows cols c0 c1" then rows of taps."""
+        try:
+            with open(path) as fh:
+                words = fh.read().split()
+        except OSError:
+            raise AssetError("fan filter asset not readable: " + path)
+        try:
+            rows, cols, c0, c1 = int(words[0]), int(words[1]), int(words[2]), int(words[3])
+        except (IndexError, ValueError):
+            raise AssetError("fan filter asset header corrupt: " + path)
+        if rows <= 0 or cols <= 0:
+            raise AssetError("fan filter asset header corrupt: " + path)
+        try:
+            vals = [float(w) for w in words[4:4 + rows * cols]]
+        except ValueError:
+            raise AssetError("fan filter asset truncated: " + path)
+        if len(vals) < rows * cols:
+            raise AssetError("fan filter asset truncated: " + path)
+        return FanFilter(np.array(vals).reshape(rows, cols), c0, c1, "file:" + path)
+
+    def save(self, path: str):
+        """save_fan_filter (filters.cpp:142-156)."""
+        try:
+            with open(path, "w") as fh:
+                fh.write(f"{self.taps.shape[0]} {self.taps.shape[1]} {self.center0} {self.center1}\n")
+                for row in self.taps:
+                    fh.write(" ".join(repr(float(v)) for v in row) + "\n")
+        except OSError:
+            raise AssetError("cannot write fan filter asset: " + path)
+
+
+DEFAULT_FAN_CHECKSUM = 0xB942F71DC884B1BA  # filters.cpp:113-116
+
+
+def fan_checksum(fan: "FanFilter") -> int:
+    """FNV-1a 64 over dims, centres and little-endian tap bytes (filters.cpp:89-110)."""
+    h = 1469598103934665603
+    meta = np.array([fan.taps.shape[0], fan.taps.shape[1], fan.center0 & 0xFFFFFFFFFFFFFFFF,
+                     fan.center1 & 0xFFFFFFFFFFFFFFFF], dtype="<u8").tobytes()
+    for b in meta + np.ascontiguousarray(fan.taps, dtype="<f8").tobytes():
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def _bank_args(fan, qmf):
+    """(lowpass, len, c, highpass, len, c, fan, rows, cols, c0, c1) ctypes args; keeps arrays alive."""
+    keep = []
+    if qmf is None:
+        q = [None, 0, 0, None, 0, 0]
+    else:
+        lp = np.ascontiguousarray(qmf.lowpass, dtype=np.float64)
+        hp = np.ascontiguousarray(qmf.highpass, dtype=np.float64)
+        keep += [lp, hp]
+        q = [_dp(lp), len(lp), int(qmf.lowpass_center), _dp(hp), len(hp), int(qmf.highpass_center)]
+    if fan is None or isinstance(fan, str):
+        if fan not in (None, "dmaxflat4", "impulse"):
+            raise ConfigError(f"unknown fan filter {fan!r}")
+        fan = FanFilter.impulse() if fan == "impulse" else None
+    if fan is None:
+        f = [None, 0, 0, 0, 0]
+    else:
+        t = np.ascontiguousarray(fan.taps, dtype=np.float64)
+        keep.append(t)
+        f = [_dp(t), t.shape[0], t.shape[1], int(fan.center0), int(fan.center1)]
+    return q + f, keep
+
+
+def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair] = None,
                     full_system: bool = False, device: int = 0, shard=None) -> ShearletSystem2D:
-    """build_system_2d (system2d.hpp:66-69). fan: "dmaxflat4" (default_fan_filter) or "impulse"."""
+    """build_system_2d (system2d.hpp:66-69). fan: None/"dmaxflat4" (default_fan_filter), "impulse" or a
+    FanFilter; qmf: None (maximally_flat_9tap) or a QmfPair."""
     profile.validate()
     lv, lvp = _levels_arg(profile)
     h = C.c_void_p()
     lo, hi = (0, -1) if shard is None else shard
-    _check(lib().sl_system_create_2d(int(rows), int(cols), lvp, len(lv), profile.coarsest_scale_offset,
-                                     int(full_system), int(fan == "impulse"), int(device), int(lo), int(hi),
-                                     C.byref(h)))
+    args, _keep = _bank_args(fan, qmf)
+    _check(lib().sl_system_create_2d_ex(int(rows), int(cols), lvp, len(lv), profile.coarsest_scale_offset,
+                                        int(full_system), *args, int(device), int(lo), int(hi), C.byref(h)))
     return ShearletSystem2D(h, rows, cols, profile, full_system, device)
 
 
-def build_system_3d(dims, profile: ScaleProfile, fan: str = "dmaxflat4", full_system: bool = False,
-                    device: int = 0, shard=None) -> ShearletSystem3D:
-    """build_system_3d (system3d.hpp:68-71)."""
+def build_system_3d(dims, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair] = None,
+                    full_system: bool = False, device: int = 0, shard=None) -> ShearletSystem3D:
+    """build_system_3d (system3d.hpp:68-71); fan / qmf as build_system_2d."""
     profile.validate()
     lv, lvp = _levels_arg(profile)
     h = C.c_void_p()
     n0, n1, n2 = (int(x) for x in dims)
     lo, hi = (0, -1) if shard is None else shard
-    _check(lib().sl_system_create_3d(n0, n1, n2, lvp, len(lv), profile.coarsest_scale_offset,
-                                     int(full_system), int(fan == "impulse"), int(device), int(lo), int(hi),
-                                     C.byref(h)))
+    args, _keep = _bank_args(fan, qmf)
+    _check(lib().sl_system_create_3d_ex(n0, n1, n2, lvp, len(lv), profile.coarsest_scale_offset,
+                                        int(full_system), *args, int(device), int(lo), int(hi), C.byref(h)))
     return ShearletSystem3D(h, (n0, n1, n2), profile, full_system, device)
 
 

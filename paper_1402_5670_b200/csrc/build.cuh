@@ -238,6 +238,13 @@ static Taps2 fan_of(int impulse_fan) {
     return f;
 }
 
+// The filter bank a system is built from: FanFilter + QmfPair (system2d.hpp:66-69).
+struct Bank {
+    Taps2 fan;
+    Qmf qmf;
+};
+static Bank default_bank(int impulse_fan) { return Bank{fan_of(impulse_fan), qmf_from_lowpass(maxflat9_lowpass())}; }
+
 static void set_shard(System& s, int lo, int hi) {
     if (hi < 0) hi = s.R;
     if (lo < 0 || hi > s.R || lo >= hi) throw SlError(SL_ERR_CONFIG, "shard range outside the filter bank");
@@ -245,10 +252,10 @@ static void set_shard(System& s, int lo, int hi) {
     s.hi = hi;
 }
 
-static void build_2d(System& s, int impulse_fan, cudaStream_t st) {
+static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     validate_profile(s.prof);
-    const Taps2 fan = fan_of(impulse_fan);
-    const Qmf q = qmf_from_lowpass(maxflat9_lowpass());
+    const Taps2& fan = bank.fan;
+    const Qmf& q = bank.qmf;
     s.index = enumerate_2d(s.prof, s.full);
     s.R = static_cast<int>(s.index.size());
     const int J = s.prof.top();
@@ -327,10 +334,10 @@ static void build_2d(System& s, int impulse_fan, cudaStream_t st) {
     }
 }
 
-static void build_3d(System& s, int impulse_fan, cudaStream_t st) {
+static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
     validate_profile(s.prof);
-    const Taps2 fan = fan_of(impulse_fan);
-    const Qmf q = qmf_from_lowpass(maxflat9_lowpass());
+    const Taps2& fan = bank.fan;
+    const Qmf& q = bank.qmf;
     s.index = enumerate_3d(s.prof, s.full);
     s.R = static_cast<int>(s.index.size());
     const int J = s.prof.top();

@@ -69,7 +69,31 @@ void require_dev_ptr(const void* p, const char* what) {
     if (!p) throw SlError(SL_ERR_INVALID, std::string(what) + ": null pointer");
 }
 
-int create(int ndim, const int* n, const int* levels, int n_scales, int j0, int full, int impulse_fan, int device,
+// Explicit taps -> Bank; NULL lowpass = QmfPair::maximally_flat_9tap(), NULL
+// highpass = mirror_highpass(lowpass) (QmfPair::from_lowpass), NULL fan =
+// default_fan_filter() (filters.cpp:32-38, 114-122).
+Bank bank_of(const double* lp, int lp_len, int lp_c, const double* hp, int hp_len, int hp_c, const double* fan, int fr,
+             int fc, int fc0, int fc1) {
+    Bank b = default_bank(0);
+    if (lp) {
+        if (lp_len < 1) throw SlError(SL_ERR_INVALID, "QmfPair: empty lowpass");
+        b.qmf.lowpass = Taps1{std::vector<double>(lp, lp + lp_len), lp_c};
+        b.qmf.highpass = mirror_highpass(b.qmf.lowpass);
+    }
+    if (hp) {
+        if (hp_len < 1) throw SlError(SL_ERR_INVALID, "QmfPair: empty highpass");
+        b.qmf.highpass = Taps1{std::vector<double>(hp, hp + hp_len), hp_c};
+    }
+    if (fan) {
+        if (fr < 1 || fc < 1) throw SlError(SL_ERR_INVALID, "FanFilter: empty taps");
+        Taps2 t = Taps2::zeros(static_cast<size_t>(fr), static_cast<size_t>(fc), fc0, fc1);
+        std::memcpy(t.v.data(), fan, sizeof(double) * t.v.size());
+        b.fan = std::move(t);
+    }
+    return b;
+}
+
+int create(int ndim, const int* n, const int* levels, int n_scales, int j0, int full, const Bank* bank_in, int device,
            int lo, int hi, sl_system** out) {
     return guard([&] {
         if (!out) throw SlError(SL_ERR_INVALID, "null output handle");
@@ -94,9 +118,9 @@ int create(int ndim, const int* n, const int* levels, int n_scales, int j0, int 
         SL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         try {
             if (ndim == 2)
-                build_2d(s, impulse_fan, st);
+                build_2d(s, *bank_in, st);
             else
-                build_3d(s, impulse_fan, st);
+                build_3d(s, *bank_in, st);
             SL_CUDA(cudaStreamSynchronize(st));
         } catch (...) {
             cudaStreamDestroy(st);
@@ -124,13 +148,62 @@ int sl_device_count(int* count) {
 int sl_system_create_2d(int rows, int cols, const int* levels, int n_scales, int j0, int full_system, int impulse_fan,
                         int device, int shard_lo, int shard_hi, sl_system** out) {
     const int n[2] = {rows, cols};
-    return create(2, n, levels, n_scales, j0, full_system, impulse_fan, device, shard_lo, shard_hi, out);
+    Bank bank;
+    const int rc = guard([&] { bank = default_bank(impulse_fan); });
+    if (rc) return rc;
+    return create(2, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
 }
 
 int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
                         int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out) {
     const int n[3] = {n0, n1, n2};
-    return create(3, n, levels, n_scales, j0, full_system, impulse_fan, device, shard_lo, shard_hi, out);
+    Bank bank;
+    const int rc = guard([&] { bank = default_bank(impulse_fan); });
+    if (rc) return rc;
+    return create(3, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
+}
+
+int sl_system_create_2d_ex(int rows, int cols, const int* levels, int n_scales, int j0, int full_system,
+                           const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
+                           int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
+                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out) {
+    const int n[2] = {rows, cols};
+    Bank bank;
+    const int rc = guard([&] {
+        bank = bank_of(lowpass, lowpass_len, lowpass_center, highpass, highpass_len, highpass_center, fan, fan_rows,
+                       fan_cols, fan_c0, fan_c1);
+    });
+    if (rc) return rc;
+    return create(2, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
+}
+
+int sl_system_create_3d_ex(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
+                           const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
+                           int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
+                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out) {
+    const int n[3] = {n0, n1, n2};
+    Bank bank;
+    const int rc = guard([&] {
+        bank = bank_of(lowpass, lowpass_len, lowpass_center, highpass, highpass_len, highpass_center, fan, fan_rows,
+                       fan_cols, fan_c0, fan_c1);
+    });
+    if (rc) return rc;
+    return create(3, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
+}
+
+int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1) {
+    return guard([&] {
+        if (order < 1) throw SlError(SL_ERR_DOMAIN, "maxflat_fan: order must be >= 1");
+        const Taps2 f = maxflat_fan(order);
+        if (rows) *rows = static_cast<int>(f.n0);
+        if (cols) *cols = static_cast<int>(f.n1);
+        if (c0) *c0 = static_cast<int>(f.c0);
+        if (c1) *c1 = static_cast<int>(f.c1);
+        if (taps) {
+            if (cap < static_cast<int64_t>(f.v.size())) throw SlError(SL_ERR_INVALID, "maxflat_fan: buffer too small");
+            std::memcpy(taps, f.v.data(), sizeof(double) * f.v.size());
+        }
+    });
 }
 
 int sl_system_destroy(sl_system* sys) {

@@ -38,6 +38,27 @@ int main() {
     if (same != c) { std::printf("sigma 0 not identity\n"); ++fails; }
     const auto [A, B] = sys.frame_bounds();
     if (!(A > 0 && B >= A)) ++fails;
+    // SHCF round trip and a custom filter bank (maxflat_fan(2) + a 5-tap QMF)
+    const auto bytes = serialize(c, sys);
+    if (deserialize(bytes, sys) != c) { std::printf("shcf round trip\n"); ++fails; }
+    auto bytes_bad = bytes;
+    bytes_bad[0] = 'X';
+    try {
+        (void)deserialize(bytes_bad, sys);
+        ++fails;
+    } catch (const FormatError&) {
+    }
+    auto sys2 = build_system_2d(32, 32, ScaleProfile::from_levels({0, 1}), FanFilter::maxflat(2),
+                                QmfPair::from_lowpass(Taps1d{{-0.125, 0.25, 0.75, 0.25, -0.125}, 2}));
+    std::vector<double> g(32 * 32);
+    for (double& x : g) x = 2.0 * (static_cast<double>(rng()) * 0x1.0p-64) - 1.0;
+    const auto r2 = inverse(forward(g, sys2), sys2);
+    double n2 = 0, d2 = 0;
+    for (size_t i = 0; i < g.size(); ++i) {
+        n2 += (r2[i] - g[i]) * (r2[i] - g[i]);
+        d2 += g[i] * g[i];
+    }
+    if (!(std::sqrt(n2 / d2) <= 1e-10)) { std::printf("custom bank round trip %g\n", std::sqrt(n2 / d2)); ++fails; }
     std::printf("cpp api: err %.2e R %zu A %.6f B %.6f fails %d\n", err, sys.redundancy(), A, B, fails);
     return fails;
 }

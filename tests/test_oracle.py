@@ -136,3 +136,78 @@ def test_oracle_shcf_bytes_golden(name):
     else:
         idx = O.enumerate_filters_3d(O.Profile(list(g["levels"]), 0))
     assert O.serialize_shcf(b, idx) == g["shcf"].tobytes()
+
+
+def test_oracle_maxflat_fans_golden():
+    # fan_design.cpp:70-108, bit-exact for every order
+    g = golden("maxflat_fans")
+    for o in range(1, 7):
+        np.testing.assert_array_equal(O.maxflat_fan(o).v, g[f"order{o}"])
+
+
+def _bank(g):
+    fan = O.T2(g["fan"], int(g["fan_c"][0]), int(g["fan_c"][1]))
+    q = None
+    if "lowpass" in g.files:
+        h = O.T1(g["lowpass"], int(g["lowpass_c"]))
+        q = O.Qmf(h, O.mirror_highpass(h))
+    return fan, q
+
+
+@pytest.mark.parametrize("name", ["bank_2d_32_fan2_legall", "bank_2d_48x40_fan3"])
+def test_oracle_custom_bank_2d_golden(name):
+    # build_system_2d with an explicit FanFilter / QmfPair (system2d.cpp:75-116)
+    g = golden(name)
+    fan, q = _bank(g)
+    f = g["f"]
+    s = O.build_system_2d(f.shape[0], f.shape[1], list(g["levels"]), 0, False, fan, q)
+    np.testing.assert_array_equal(np.array(s.index), g["index"])
+    np.testing.assert_allclose(s.filter_norms, g["filter_norms"], rtol=1e-12)
+    assert rel_l2(O.forward_2d(f, s), g["bands"]) < 1e-12
+    assert rel_l2(O.inverse_2d(g["bands"], s), g["rec"]) < 1e-12
+
+
+def test_oracle_custom_bank_3d_golden():
+    g = golden("bank_3d_16_fan2_legall")
+    fan, q = _bank(g)
+    f = g["f"]
+    s = O.build_system_3d(f.shape, list(g["levels"]), 0, False, fan, q)
+    np.testing.assert_allclose(s.filter_norms, g["filter_norms"], rtol=1e-12)
+    b = O.forward_3d(f, s)
+    np.testing.assert_allclose(np.sqrt((b.reshape(b.shape[0], -1) ** 2).sum(1)), g["band_l2"], rtol=1e-10)
+    assert rel_l2(O.inverse_3d(b, s), g["rec"]) < 1e-12
+
+
+def test_python_bank_helpers():
+    # host-side mirrors of filters.hpp helpers; maxflat_fan computed by the library (host code, no GPU)
+    import paper_1402_5670_b200 as P
+    g = golden("maxflat_fans")
+    for o in range(1, 7):
+        np.testing.assert_array_equal(P.FanFilter.maxflat(o).taps, g[f"order{o}"])
+    assert P.fan_checksum(P.FanFilter.default()) == P.DEFAULT_FAN_CHECKSUM
+    q = P.QmfPair.from_lowpass([-0.125, 0.25, 0.75, 0.25, -0.125])
+    np.testing.assert_array_equal(q.highpass, O.mirror_highpass(O.T1(q.lowpass, 2)).v)
+    assert P.alpha_to_shear_levels([1.0, 1.0, 1.0], 1) == [1, 1, 2]
+    with pytest.raises(P.DomainError):
+        P.alpha_to_shear_levels([2.0], 0)
+    with pytest.raises(P.DomainError):
+        P.FanFilter.maxflat(0)
+
+
+def test_fan_asset_round_trip(tmp_path):
+    # load_fan_filter / save_fan_filter text format (filters.cpp:124-156)
+    import paper_1402_5670_b200 as P
+    f = P.FanFilter.maxflat(3)
+    p = str(tmp_path / "fan.txt")
+    f.save(p)
+    back = P.FanFilter.load(p)
+    np.testing.assert_array_equal(back.taps, f.taps)
+    assert (back.center0, back.center1) == (f.center0, f.center1)
+    (tmp_path / "bad.txt").write_text("3 3 1\n")
+    with pytest.raises(P.AssetError):
+        P.FanFilter.load(str(tmp_path / "bad.txt"))
+    (tmp_path / "short.txt").write_text("2 2 0 0\n1 2\n3\n")
+    with pytest.raises(P.AssetError):
+        P.FanFilter.load(str(tmp_path / "short.txt"))
+    with pytest.raises(P.AssetError):
+        P.FanFilter.load(str(tmp_path / "missing.txt"))

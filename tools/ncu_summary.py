@@ -1,0 +1,66 @@
+"""Summarise ncu output into the tracked profiles/ files.
+
+    python tools/ncu_summary.py full   <report.ncu-rep> <out.csv>
+        one row per captured kernel: duration, grid/block/regs, occupancy,
+        FP64/L1/L2/DRAM utilisation, DRAM bytes, top-4 stall reasons.
+    python tools/ncu_summary.py launches <launches.csv> <out.md>
+        per-kernel launch count, mean duration and share of the captured
+        launches (the `--metrics gpu__time_duration.sum` launch list).
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+COLS = [
+    "gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+]
+STALL = "smsp__average_warps_issue_stalled_"
+
+
+def full(rep, out):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    stall_cols = [i for i, n in enumerate(h) if n.startswith(STALL) and n.endswith("_per_issue_active.ratio")]
+    with open(out, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["kernel"] + [c for c in COLS if c in h] + ["top_stalls"])
+        for r in rows[2:]:
+            vals = [f"{r[h.index(c)]} {units[h.index(c)]}".strip() for c in COLS if c in h]
+            st = sorted(((float(r[i] or 0), h[i][len(STALL):].replace("_per_issue_active.ratio", "")) for i in stall_cols),
+                        reverse=True)[:4]
+            w.writerow([r[h.index("Kernel Name")][:40]] + vals + [str([(round(v, 3), n) for v, n in st])])
+    print(f"wrote {out}")
+
+
+def launches(path, out):
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    t, n = collections.defaultdict(float), collections.Counter()
+    for r in rows[1:]:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
+        scale = {"ns": 1e-3, "us": 1.0, "ms": 1e3}.get(r[ui], 1.0)
+        k = r[ki].split(">(")[0].replace("void ", "").replace("(int)", "") + ">"
+        t[k] += float(r[vi].replace(",", "")) * scale
+        n[k] += 1
+    tot = sum(t.values())
+    with open(out, "w") as fh:
+        fh.write(f"# launch list summary: {path.split('/')[-1]}\n\n")
+        fh.write("cold-cache, serialised ncu launches (`--metrics gpu__time_duration.sum --clock-control none`);\n")
+        fh.write("compare SHARES with bench.py's live per-pass timing, not absolute times.\n\n")
+        fh.write("| kernel | launches | mean us | share |\n|---|---|---|---|\n")
+        for k in sorted(t, key=lambda k: -t[k]):
+            fh.write(f"| `{k}` | {n[k]} | {t[k] / n[k]:.1f} | {100 * t[k] / tot:.1f} % |\n")
+        fh.write(f"\ntotal captured: {tot:.0f} us over {sum(n.values())} launches\n")
+    print(f"wrote {out}")
+
+
+if __name__ == "__main__":
+    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
