@@ -238,7 +238,7 @@ def main():
         scaling = "strong" if world > 1 else "weak"
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
-        sysg.set_streams(int(os.environ.get("SLB_STREAMS", "4")))
+        sysg.set_streams(int(os.environ.get("SLB_STREAMS", "8")))
         if args.config == "2d1024x64":
             frames = cfg["batch"] // world  # fixed total batch sharded by image
             scaling = "strong"

@@ -168,6 +168,16 @@ int sl_shcf_size(const sl_system* sys, int nbands, size_t* bytes);
 int sl_shcf_serialize(const sl_system* sys, const double* coeffs, int nbands, unsigned char* out, size_t cap);
 int sl_shcf_deserialize(const sl_system* sys, const unsigned char* in, size_t len, double* coeffs, int nbands);
 
+/* ---- signal files (image_io.hpp:9-24, image_io.cpp:43-159), host ---------
+ * PGM: binary P5, 8-bit (maxval <= 255) or 16-bit big-endian samples; rows =
+ * image height = axis 0. Load with pixels == NULL to query rows/cols/maxval.
+ * Save rounds, clamps to [0, maxval]. SVOL: "SVOL", u16 1, 3 x u32 dims, f64
+ * samples, little-endian. Errors: SL_ERR_FORMAT as the reference's FormatError. */
+int sl_load_pgm(const char* path, double* pixels, int64_t cap, int* rows, int* cols, int* maxval);
+int sl_save_pgm(const double* pixels, int rows, int cols, const char* path, int maxval);
+int sl_load_svol(const char* path, double* volume, int64_t cap, int64_t dims[3]);
+int sl_save_svol(const double* volume, const int64_t dims[3], const char* path);
+
 /* ---- instrumentation ---------------------------------------------------
  * sl_profile(enable) clears the per-pass statistics and turns CUDA-event timing
  * of every kernel launch on/off; sl_pass_stats returns, per pass name (32-byte

@@ -138,6 +138,24 @@ def gen_banks():
     save("maxflat_fans", **{f"order{o}": ref.maxflat_fan(o)[0] for o in range(1, 7)})
 
 
+def gen_io():
+    """PGM (8/16-bit) and SVOL bytes written by the reference (image_io.cpp:77-159)."""
+    import tempfile
+    d = tempfile.mkdtemp()
+    img = ref.add_noise(ref.cartoon(48), 40.0, 5)[:40, :]  # 40 x 48, values outside [0, 255] too
+    vol = np.random.default_rng(4).uniform(-2, 2, (5, 6, 7))
+    out = {"img": img, "vol": vol}
+    for name, mv in (("pgm8", 255), ("pgm16", 4095)):
+        p = os.path.join(d, name + ".pgm")
+        ref.save_pgm(img * (mv / 255.0), p, mv)
+        out[name] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
+        out[name + "_loaded"] = ref.load_pgm(p)[0]
+    p = os.path.join(d, "v.svol")
+    ref.save_svol(vol, p)
+    out["svol"] = np.frombuffer(open(p, "rb").read(), dtype=np.uint8)
+    save("io_pgm_svol", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
@@ -193,6 +211,7 @@ def main():
     save("shcf_3d_8x12x10_0", levels=np.array([0]), bands=b3,
          shcf=np.frombuffer(ref.serialize(s3, b3), dtype=np.uint8))
     gen_banks()
+    gen_io()
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

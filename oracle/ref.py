@@ -66,6 +66,9 @@ def lib():
         L.ref_build_2d_bank.argtypes = [C.c_int] * 2 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
         L.ref_build_3d_bank.argtypes = [C.c_int] * 3 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
         L.ref_maxflat_fan.argtypes = [C.c_int, dp, C.c_longlong, ip]
+        L.ref_save_pgm.argtypes = [dp, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.ref_load_pgm.argtypes = [C.c_char_p, dp, C.c_longlong, ip]
+        L.ref_save_svol.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
         for d in ("2d", "3d"):
             getattr(L, f"ref_serialize_{d}").argtypes = [P, dp, C.c_int, C.c_char_p, C.c_longlong]
             getattr(L, f"ref_serialize_{d}").restype = C.c_longlong
@@ -325,6 +328,24 @@ def deserialize(data: bytes):
     out = np.zeros((nb,) + shape)
     lib().ref_deserialize(data, len(data), C.byref(nd), _ip(dims), _dp(out), out.size)
     return out
+
+
+def save_pgm(px, path, maxval=255):
+    px = np.ascontiguousarray(px, dtype=np.float64)
+    _check(lib().ref_save_pgm(_dp(px), px.shape[0], px.shape[1], path.encode(), maxval))
+
+
+def load_pgm(path):
+    info = np.zeros(3, dtype=np.int32)
+    _check(lib().ref_load_pgm(path.encode(), None, 0, _ip(info)))
+    out = np.zeros((info[0], info[1]))
+    _check(lib().ref_load_pgm(path.encode(), _dp(out), out.size, _ip(info)))
+    return out, int(info[2])
+
+
+def save_svol(v, path):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    _check(lib().ref_save_svol(_dp(v), *v.shape, path.encode()))
 
 
 def random_mask(rows, cols, keep, seed):

@@ -17,6 +17,7 @@
 
 #include "shearlet/apps.hpp"
 #include "shearlet/fft.hpp"
+#include "shearlet/image_io.hpp"
 #include "shearlet/phantoms.hpp"
 #include "shearlet/system2d.hpp"
 #include "shearlet/system3d.hpp"
@@ -427,6 +428,32 @@ int ref_deserialize(const unsigned char* in, long long len, int* ndim, int* dims
         }
     });
     return rc ? -rc : nb;
+}
+
+// ---------------------------------------------------------------- PGM / SVOL (image_io.hpp:9-24)
+int ref_save_pgm(const double* px, int rows, int cols, const char* path, int maxval) {
+    return guard([&] {
+        Signal2D s(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols));
+        std::memcpy(s.data(), px, sizeof(double) * s.size());
+        save_pgm(s, path, maxval);
+    });
+}
+int ref_load_pgm(const char* path, double* out, long long cap, int* info) {
+    return guard([&] {
+        const PgmImage im = load_pgm(path);
+        info[0] = static_cast<int>(im.pixels.size0());
+        info[1] = static_cast<int>(im.pixels.size1());
+        info[2] = im.maxval;
+        if (out && cap >= static_cast<long long>(im.pixels.size()))
+            std::memcpy(out, im.pixels.data(), sizeof(double) * im.pixels.size());
+    });
+}
+int ref_save_svol(const double* v, int n0, int n1, int n2, const char* path) {
+    return guard([&] {
+        Signal3D s(static_cast<std::size_t>(n0), static_cast<std::size_t>(n1), static_cast<std::size_t>(n2));
+        std::memcpy(s.data(), v, sizeof(double) * s.size());
+        save_svol(s, path);
+    });
 }
 
 void ref_random_mask(int rows, int cols, double keep, std::uint64_t seed, double* out) {

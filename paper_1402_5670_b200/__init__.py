@@ -139,6 +139,10 @@ def lib():
     L.sl_shcf_size.argtypes = [P, i, C.POINTER(C.c_size_t)]
     L.sl_shcf_serialize.argtypes = [P, dp, i, C.c_char_p, C.c_size_t]
     L.sl_shcf_deserialize.argtypes = [P, C.c_char_p, C.c_size_t, dp, i]
+    L.sl_load_pgm.argtypes = [C.c_char_p, dp, C.c_int64, ip, ip, ip]
+    L.sl_save_pgm.argtypes = [dp, i, i, C.c_char_p, i]
+    L.sl_load_svol.argtypes = [C.c_char_p, dp, C.c_int64, C.POINTER(C.c_int64)]
+    L.sl_save_svol.argtypes = [dp, C.POINTER(C.c_int64), C.c_char_p]
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
@@ -159,6 +163,7 @@ EXPORTED_SYMBOLS = [
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
+    "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
 ]
@@ -698,6 +703,50 @@ def deserialize(data: bytes, sys: _System) -> np.ndarray:
     out = np.empty((sys.n_bands,) + tuple(sys.shape))
     _check(lib().sl_shcf_deserialize(sys.handle, data, len(data), _dp(out), sys.n_bands))
     return out
+
+
+# ------------------------------------------------------------------ signal files
+@dataclass
+class PgmImage:
+    """image_io.hpp:9-15: pixels [rows][cols] (axis 0 = image rows), maxval."""
+    pixels: np.ndarray
+    maxval: int = 255
+
+
+def load_pgm(path: str) -> PgmImage:
+    """load_pgm (image_io.cpp:43-75): binary P5, 8- or 16-bit."""
+    r, c, m = C.c_int(), C.c_int(), C.c_int()
+    b = os.fsencode(path)
+    _check(lib().sl_load_pgm(b, None, 0, C.byref(r), C.byref(c), C.byref(m)))
+    px = np.empty((r.value, c.value))
+    _check(lib().sl_load_pgm(b, _dp(px), px.size, None, None, None))
+    return PgmImage(px, m.value)
+
+
+def save_pgm(pixels, path: str, maxval: int = 255):
+    """save_pgm (image_io.cpp:77-100): rounds and clamps to [0, maxval]."""
+    px = np.ascontiguousarray(pixels, dtype=np.float64)
+    if px.ndim != 2:
+        raise ShapeError("save_pgm: pixels must be 2D")
+    _check(lib().sl_save_pgm(_dp(px), px.shape[0], px.shape[1], os.fsencode(path), int(maxval)))
+
+
+def load_svol(path: str) -> np.ndarray:
+    """load_svol (image_io.cpp:125-143)."""
+    d = (C.c_int64 * 3)()
+    b = os.fsencode(path)
+    _check(lib().sl_load_svol(b, None, 0, d))
+    v = np.empty(tuple(d))
+    _check(lib().sl_load_svol(b, _dp(v), v.size, d))
+    return v
+
+
+def save_svol(volume, path: str):
+    """save_svol (image_io.cpp:145-159)."""
+    v = np.ascontiguousarray(volume, dtype=np.float64)
+    if v.ndim != 3:
+        raise ShapeError("save_svol: volume must be 3D")
+    _check(lib().sl_save_svol(_dp(v), (C.c_int64 * 3)(*v.shape), os.fsencode(path)))
 
 
 # ------------------------------------------------------------------ iterative pipelines

@@ -13,6 +13,7 @@
 #include "phantoms.cuh"
 #include "iterative.cuh"
 #include "shcf.cuh"
+#include "image_io.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
@@ -416,6 +417,7 @@ void fan_out(System& s, int nframes, cudaStream_t user, Fn&& per_frame) {
         SL_CUDA(cudaEventRecord(s.fork_ev, user));
         for (int k = 1; k < K; ++k) SL_CUDA(cudaStreamWaitEvent(s.ws[static_cast<size_t>(k)]->st, s.fork_ev, 0));
     }
+    s.concurrency = K;
     try {
         for (int f = 0; f < nframes; ++f) {
             const int k = f % K;
@@ -424,9 +426,11 @@ void fan_out(System& s, int nframes, cudaStream_t user, Fn&& per_frame) {
         }
     } catch (...) {
         s.w = s.ws[0].get();
+        s.concurrency = 1;
         throw;
     }
     s.w = s.ws[0].get();
+    s.concurrency = 1;
     for (int k = 1; k < K; ++k) {
         System::Workspace& wk = *s.ws[static_cast<size_t>(k)];
         SL_CUDA(cudaEventRecord(wk.ev, wk.st));
@@ -691,6 +695,45 @@ int sl_shcf_deserialize(const sl_system* h, const unsigned char* in, size_t len,
         const System& s = sys_of(h);
         if (!in || !coeffs) throw SlError(SL_ERR_INVALID, "null pointer");
         shcf_deserialize(s, in, len, coeffs, nbands);
+    });
+}
+
+int sl_load_pgm(const char* path, double* pixels, int64_t cap, int* rows, int* cols, int* maxval) {
+    return guard([&] {
+        if (!path) throw SlError(SL_ERR_INVALID, "null path");
+        const PgmHeader hd = pgm_load(path, pixels, cap);
+        if (rows) *rows = static_cast<int>(hd.rows);
+        if (cols) *cols = static_cast<int>(hd.cols);
+        if (maxval) *maxval = hd.maxval;
+    });
+}
+
+int sl_save_pgm(const double* pixels, int rows, int cols, const char* path, int maxval) {
+    return guard([&] {
+        if (!path || !pixels) throw SlError(SL_ERR_INVALID, "null argument");
+        if (rows < 0 || cols < 0) throw SlError(SL_ERR_SHAPE, "PGM: negative dims");
+        pgm_save(pixels, static_cast<size_t>(rows), static_cast<size_t>(cols), path, maxval);
+    });
+}
+
+int sl_load_svol(const char* path, double* volume, int64_t cap, int64_t dims[3]) {
+    return guard([&] {
+        if (!path || !dims) throw SlError(SL_ERR_INVALID, "null argument");
+        long long d[3];
+        svol_load(path, volume, cap, d);
+        for (int a = 0; a < 3; ++a) dims[a] = d[a];
+    });
+}
+
+int sl_save_svol(const double* volume, const int64_t dims[3], const char* path) {
+    return guard([&] {
+        if (!path || !volume || !dims) throw SlError(SL_ERR_INVALID, "null argument");
+        long long d[3];
+        for (int a = 0; a < 3; ++a) {
+            if (dims[a] < 0 || dims[a] > 0xFFFFFFFFll) throw SlError(SL_ERR_SHAPE, "SVOL: dims out of range");
+            d[a] = dims[a];
+        }
+        svol_save(volume, d, path);
     });
 }
 

@@ -189,7 +189,8 @@ struct System {
     };
     std::vector<std::unique_ptr<Workspace>> ws;
     Workspace* w = nullptr;
-    int nstreams = 4;               // workspaces used by batched calls
+    int nstreams = 8;               // workspaces used by batched calls
+    int concurrency = 1;            // frames in flight on other streams (set by batched calls)
     cudaEvent_t fork_ev = nullptr;
     DBuf<double> delta, stack, io_in, io_out;
     std::shared_ptr<void> mega;  // MegaState of the 2D megakernel (mega2d_host.cuh)

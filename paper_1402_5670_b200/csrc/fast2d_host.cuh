@@ -26,10 +26,15 @@ static int env_int(const char* name, int dflt) {
 struct Fast2DCfg {
     int G, C;
 };
+// A lone frame needs many CTAs per launch (small G); with >= 4 frames in flight
+// on other streams the SMs stay busy, and a large G cuts the slot traffic of the
+// rec sum (16 Nh per G bands) and the F re-reads (bench sweep, profiles/).
 static Fast2DCfg fast2d_cfg(const System& s) {
-    const int G = env_int("SLB_GROUP", 2);
+    const bool conc = s.concurrency >= 4;
+    const int G = env_int(conc ? "SLB_GROUP" : "SLB_GROUP1", conc ? 14 : 4);
     const double per = static_cast<double>(s.H) * s.n[0] * sizeof(double2);
-    int C = env_int("SLB_CHUNK", std::max(1, static_cast<int>((32.0 * 1024 * 1024) / per)));
+    int C = env_int(conc ? "SLB_CHUNK" : "SLB_CHUNK1",
+                    std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
     C = std::max(G, (C / G) * G);
     return {G, C};
 }
