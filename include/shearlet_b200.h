@@ -74,19 +74,31 @@ int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales,
  * (fan_c0, fan_c1); load_fan_filter / maxflat_fan(order), filters.hpp:54-67,
  * fan_design.cpp:70-108) and QmfPair (1D taps + centre index; filters.hpp:14-21).
  * lowpass NULL = maximally_flat_9tap(); highpass NULL = mirror_highpass(lowpass)
- * (QmfPair::from_lowpass); fan NULL = default_fan_filter(). The filter spectra
- * must come out real (centrally symmetric taps), else SL_ERR_DOMAIN. */
+ * (QmfPair::from_lowpass); fan NULL = default_fan_filter(). fan_provenance is
+ * FanFilter::provenance ("dmaxflat4", "impulse", anything else = "custom" in
+ * descriptors; NULL = "custom"). The filter spectra must come out real
+ * (centrally symmetric taps), else SL_ERR_DOMAIN. */
 int sl_system_create_2d_ex(int rows, int cols, const int* levels, int n_scales, int j0, int full_system,
                            const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
                            int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
-                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out);
+                           int fan_c0, int fan_c1, const char* fan_provenance, int device, int shard_lo,
+                           int shard_hi, sl_system** out);
 int sl_system_create_3d_ex(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
                            const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
                            int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
-                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out);
+                           int fan_c0, int fan_c1, const char* fan_provenance, int device, int shard_lo,
+                           int shard_hi, sl_system** out);
 /* fan_design::maxflat_fan(order) (fan_design.cpp:70-108), host: dims/centre
  * always written; taps written when non-NULL (cap doubles). */
 int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1);
+/* System descriptors (descriptor.hpp:12-39): sl_describe writes the text
+ * write_descriptor() would write (describe(sys)); len = its length without the
+ * NUL; text may be NULL to size. sl_system_create_from_descriptor parses that
+ * text (read_descriptor) and rebuilds (build_from_descriptor_2d/3d; ndim 2 or
+ * 3 asserts the kind, 0 accepts both). FormatError cases as the reference. */
+int sl_describe(const sl_system* sys, char* text, size_t cap, size_t* len);
+int sl_system_create_from_descriptor(const char* text, int ndim, int device, int shard_lo, int shard_hi,
+                                     sl_system** out);
 int sl_system_destroy(sl_system* sys);
 
 /* ---- system queries (ShearletSystem2D/3D members) ------------------------ */

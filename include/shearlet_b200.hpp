@@ -150,13 +150,15 @@ struct QmfPair {
 struct FanFilter {
     std::vector<double> taps;  // row-major rows x cols
     int rows = 0, cols = 0, center0 = 0, center1 = 0;
-    static FanFilter impulse() { return FanFilter{{1.0}, 1, 1, 0, 0}; }
+    std::string provenance = "custom";
+    static FanFilter impulse() { return FanFilter{{1.0}, 1, 1, 0, 0, "impulse"}; }
     static FanFilter maxflat(int order) {  // fan_design::maxflat_fan
         FanFilter f;
         check(sl_maxflat_fan(order, nullptr, 0, &f.rows, &f.cols, &f.center0, &f.center1));
         f.taps.resize(static_cast<std::size_t>(f.rows) * f.cols);
         check(sl_maxflat_fan(order, f.taps.data(), static_cast<int64_t>(f.taps.size()), nullptr, nullptr, nullptr,
                              nullptr));
+        f.provenance = order == 4 ? "dmaxflat4" : "dmaxflat" + std::to_string(order);
         return f;
     }
 };
@@ -168,7 +170,8 @@ inline ShearletSystem build_system_2d(std::size_t rows, std::size_t cols, const 
         static_cast<int>(rows), static_cast<int>(cols), p.shear_levels.data(), p.n_scales(), p.coarsest_scale_offset,
         full_system, qmf.lowpass.v.empty() ? nullptr : qmf.lowpass.v.data(), static_cast<int>(qmf.lowpass.v.size()), qmf.lowpass.center,
         hp ? qmf.highpass.v.data() : nullptr, static_cast<int>(qmf.highpass.v.size()), qmf.highpass.center,
-        fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1, device, 0, -1, &h));
+        fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1,
+        fan.provenance.c_str(), device, 0, -1, &h));
     return ShearletSystem(h);
 }
 inline ShearletSystem build_system_3d(std::array<std::size_t, 3> d, const ScaleProfile& p, const FanFilter& fan,
@@ -179,7 +182,8 @@ inline ShearletSystem build_system_3d(std::array<std::size_t, 3> d, const ScaleP
         static_cast<int>(d[0]), static_cast<int>(d[1]), static_cast<int>(d[2]), p.shear_levels.data(), p.n_scales(),
         p.coarsest_scale_offset, full_system, qmf.lowpass.v.empty() ? nullptr : qmf.lowpass.v.data(), static_cast<int>(qmf.lowpass.v.size()),
         qmf.lowpass.center, hp ? qmf.highpass.v.data() : nullptr, static_cast<int>(qmf.highpass.v.size()),
-        qmf.highpass.center, fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1, device, 0, -1, &h));
+        qmf.highpass.center, fan.taps.empty() ? nullptr : fan.taps.data(), fan.rows, fan.cols, fan.center0, fan.center1,
+        fan.provenance.c_str(), device, 0, -1, &h));
     return ShearletSystem(h);
 }
 

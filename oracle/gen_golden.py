@@ -156,6 +156,23 @@ def gen_io():
     save("io_pgm_svol", **out)
 
 
+def gen_descriptors():
+    """describe() + write_descriptor() texts of the reference (descriptor.cpp:30-67), and the
+    RMS of systems rebuilt from them (build_from_descriptor_2d/3d)."""
+    systems = {
+        "d2_512_1122": ref.RefSystem2D(512, 512, [1, 1, 2, 2]),
+        "d2_48x40_full_j1": ref.RefSystem2D(48, 40, [0, 1], j0=1, full=True),
+        "d2_32_legall": ref.RefSystem2D(32, 32, [0, 1], qmf=(LEGALL_LOWPASS, 2), fan=ref.maxflat_fan(2)),
+        "d3_16_impulse": ref.RefSystem3D((16, 16, 16), [0, 1], impulse_fan=True),
+        "d3_16x20x24_legall": ref.RefSystem3D((16, 20, 24), [0, 1], qmf=(LEGALL_LOWPASS, 2)),
+    }
+    out = {}
+    for k, sy in systems.items():
+        out[k + "_text"] = np.array(ref.descriptor_text(sy))
+        out[k + "_rms"] = sy.filter_norms()
+    save("descriptors", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
@@ -212,6 +229,7 @@ def main():
          shcf=np.frombuffer(ref.serialize(s3, b3), dtype=np.uint8))
     gen_banks()
     gen_io()
+    gen_descriptors()
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

@@ -66,6 +66,9 @@ def lib():
         L.ref_build_2d_bank.argtypes = [C.c_int] * 2 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
         L.ref_build_3d_bank.argtypes = [C.c_int] * 3 + [ip] + [C.c_int] * 3 + bank + [C.c_int, C.POINTER(P)]
         L.ref_maxflat_fan.argtypes = [C.c_int, dp, C.c_longlong, ip]
+        L.ref_write_descriptor_2d.argtypes = [P, C.c_char_p]
+        L.ref_write_descriptor_3d.argtypes = [P, C.c_char_p]
+        L.ref_build_from_descriptor.argtypes = [C.c_char_p, ip, C.POINTER(P)]
         L.ref_save_pgm.argtypes = [dp, C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.ref_load_pgm.argtypes = [C.c_char_p, dp, C.c_longlong, ip]
         L.ref_save_svol.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
@@ -328,6 +331,16 @@ def deserialize(data: bytes):
     out = np.zeros((nb,) + shape)
     lib().ref_deserialize(data, len(data), C.byref(nd), _ip(dims), _dp(out), out.size)
     return out
+
+
+def descriptor_text(system) -> str:
+    """write_descriptor(describe(system)) (descriptor.cpp:30-67) -> text."""
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "sys.txt")
+        fn = lib().ref_write_descriptor_2d if isinstance(system, RefSystem2D) else lib().ref_write_descriptor_3d
+        _check(fn(system.h, p.encode()))
+        return open(p).read()
 
 
 def save_pgm(px, path, maxval=255):

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "shearlet/apps.hpp"
+#include "shearlet/descriptor.hpp"
 #include "shearlet/fft.hpp"
 #include "shearlet/image_io.hpp"
 #include "shearlet/phantoms.hpp"
@@ -453,6 +454,25 @@ int ref_save_svol(const double* v, int n0, int n1, int n2, const char* path) {
         Signal3D s(static_cast<std::size_t>(n0), static_cast<std::size_t>(n1), static_cast<std::size_t>(n2));
         std::memcpy(s.data(), v, sizeof(double) * s.size());
         save_svol(s, path);
+    });
+}
+
+// ---------------------------------------------------------------- descriptors (descriptor.hpp:25-39)
+int ref_write_descriptor_2d(void* h, const char* path) {
+    return guard([&] { write_descriptor(describe(*static_cast<ShearletSystem2D*>(h)), path); });
+}
+int ref_write_descriptor_3d(void* h, const char* path) {
+    return guard([&] { write_descriptor(describe(*static_cast<ShearletSystem3D*>(h)), path); });
+}
+// read_descriptor + build_from_descriptor_2d/3d; *is3d tells which handle kind came back
+int ref_build_from_descriptor(const char* path, int* is3d, void** out) {
+    return guard([&] {
+        const SystemDescriptor d = read_descriptor(path);
+        *is3d = d.is_3d ? 1 : 0;
+        if (d.is_3d)
+            *out = new ShearletSystem3D(build_from_descriptor_3d(d));
+        else
+            *out = new ShearletSystem2D(build_from_descriptor_2d(d));
     });
 }
 

@@ -105,10 +105,12 @@ def lib():
     L.sl_device_count.argtypes = [ip]
     L.sl_system_create_2d.argtypes = [i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
     L.sl_system_create_3d.argtypes = [i, i, i, ip, i, i, i, i, i, i, i, C.POINTER(P)]
-    bank = [dp, i, i, dp, i, i, dp, i, i, i, i]
+    bank = [dp, i, i, dp, i, i, dp, i, i, i, i, C.c_char_p]
     L.sl_system_create_2d_ex.argtypes = [i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
     L.sl_system_create_3d_ex.argtypes = [i, i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
     L.sl_maxflat_fan.argtypes = [i, dp, C.c_int64, ip, ip, ip, ip]
+    L.sl_describe.argtypes = [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
+    L.sl_system_create_from_descriptor.argtypes = [C.c_char_p, i, i, i, i, C.POINTER(P)]
     L.sl_system_destroy.argtypes = [P]
     L.sl_ndim.argtypes = [P, ip, C.POINTER(C.c_int64)]
     L.sl_redundancy.argtypes = [P, ip]
@@ -163,6 +165,7 @@ EXPORTED_SYMBOLS = [
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
+    "sl_describe", "sl_system_create_from_descriptor",
     "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
@@ -478,11 +481,11 @@ def _bank_args(fan, qmf):
             raise ConfigError(f"unknown fan filter {fan!r}")
         fan = FanFilter.impulse() if fan == "impulse" else None
     if fan is None:
-        f = [None, 0, 0, 0, 0]
+        f = [None, 0, 0, 0, 0, None]
     else:
         t = np.ascontiguousarray(fan.taps, dtype=np.float64)
         keep.append(t)
-        f = [_dp(t), t.shape[0], t.shape[1], int(fan.center0), int(fan.center1)]
+        f = [_dp(t), t.shape[0], t.shape[1], int(fan.center0), int(fan.center1), fan.provenance.encode()]
     return q + f, keep
 
 
@@ -530,6 +533,119 @@ def redundancy_3d(profile: ScaleProfile, full_system: bool = False) -> int:  # s
         q = 2 * (1 << d) + 1
         r += 3 * q * q if full_system else 3 * q * q - 6 * q + 4
     return r
+
+
+# ------------------------------------------------------------------ descriptors
+@dataclass
+class SystemDescriptor:
+    """descriptor.hpp:14-23: enough to rebuild a system bit-identically."""
+    is_3d: bool = False
+    dims: tuple = (0, 0)
+    j0: int = 0
+    shear_levels: List[int] = field(default_factory=list)
+    full_system: bool = False
+    qmf_lowpass: Optional[np.ndarray] = None
+    qmf_center: int = 0
+    fan_name: str = ""
+    fan_checksum: int = 0
+
+    def text(self) -> str:
+        """write_descriptor's text (descriptor.cpp:48-67)."""
+        lines = ["shearlet-system 1", "dims " + " ".join(str(int(d)) for d in self.dims), f"j0 {self.j0}",
+                 "shear_levels" + "".join(f" {v}" for v in self.shear_levels),
+                 f"full_system {1 if self.full_system else 0}", f"qmf_center {self.qmf_center}",
+                 "qmf" + "".join(" %.17g" % v for v in self.qmf_lowpass),
+                 f"fan {self.fan_name} {self.fan_checksum:x}"]
+        return "\n".join(lines) + "\n"
+
+    @staticmethod
+    def parse(text: str) -> "SystemDescriptor":
+        """read_descriptor's grammar (descriptor.cpp:69-126)."""
+        d = SystemDescriptor()
+        seen = set()
+        for line in text.splitlines():
+            w = line.split()
+            if not w or w[0].startswith("#"):
+                continue
+            key, rest = w[0], w[1:]
+            try:
+                if key == "shearlet-system":
+                    if not rest or int(rest[0]) != 1:
+                        raise FormatError("descriptor: unsupported version")
+                elif key == "dims":
+                    if len(rest) not in (2, 3):
+                        raise FormatError("descriptor: dims must have 2 or 3 entries")
+                    d.dims, d.is_3d = tuple(int(x) for x in rest), len(rest) == 3
+                elif key == "j0":
+                    d.j0 = int(rest[0])
+                elif key == "shear_levels":
+                    d.shear_levels = [int(x) for x in rest]
+                elif key == "full_system":
+                    d.full_system = int(rest[0]) != 0
+                elif key == "qmf_center":
+                    d.qmf_center = int(rest[0])
+                elif key == "qmf":
+                    if not rest:
+                        raise FormatError("descriptor: empty qmf taps")
+                    d.qmf_lowpass = np.array([float(x) for x in rest])
+                elif key == "fan":
+                    d.fan_name, d.fan_checksum = rest[0], int(rest[1], 16)
+                else:
+                    raise FormatError(f"descriptor: unknown key '{key}'")
+            except (IndexError, ValueError):
+                raise FormatError(f"descriptor: bad {key} line")
+            seen.add(key)
+        if not {"shearlet-system", "dims", "shear_levels", "qmf", "fan"} <= seen:
+            raise FormatError("descriptor: missing required fields")
+        return d
+
+
+def describe(sys: "_System") -> SystemDescriptor:
+    """describe(sys) (descriptor.cpp:30-46), from the library's record of the build."""
+    n = C.c_size_t()
+    _check(lib().sl_describe(sys.handle, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().sl_describe(sys.handle, buf, n.value + 1, C.byref(n)))
+    return SystemDescriptor.parse(buf.value.decode())
+
+
+def write_descriptor(d: SystemDescriptor, path: str):
+    try:
+        with open(path, "w") as fh:
+            fh.write(d.text())
+    except OSError:
+        raise FormatError("cannot write system descriptor: " + path)
+
+
+def read_descriptor(path: str) -> SystemDescriptor:
+    try:
+        with open(path) as fh:
+            text = fh.read()
+    except OSError:
+        raise FormatError("cannot open system descriptor: " + path)
+    return SystemDescriptor.parse(text)
+
+
+def _from_descriptor(d: SystemDescriptor, ndim: int, device: int, shard):
+    h = C.c_void_p()
+    lo, hi = (0, -1) if shard is None else shard
+    _check(lib().sl_system_create_from_descriptor(d.text().encode(), ndim, int(device), int(lo), int(hi),
+                                                  C.byref(h)))
+    return h
+
+
+def build_from_descriptor_2d(d: SystemDescriptor, device: int = 0, shard=None) -> "ShearletSystem2D":
+    """build_from_descriptor_2d (descriptor.cpp:142-147)."""
+    h = _from_descriptor(d, 2, device, shard)
+    prof = ScaleProfile(list(d.shear_levels), d.j0)
+    return ShearletSystem2D(h, d.dims[0], d.dims[1], prof, d.full_system, device)
+
+
+def build_from_descriptor_3d(d: SystemDescriptor, device: int = 0, shard=None) -> "ShearletSystem3D":
+    """build_from_descriptor_3d (descriptor.cpp:149-154)."""
+    h = _from_descriptor(d, 3, device, shard)
+    prof = ScaleProfile(list(d.shear_levels), d.j0)
+    return ShearletSystem3D(h, tuple(d.dims), prof, d.full_system, device)
 
 
 # ------------------------------------------------------------------ transforms

@@ -242,8 +242,11 @@ static Taps2 fan_of(int impulse_fan) {
 struct Bank {
     Taps2 fan;
     Qmf qmf;
+    std::string fan_name;  // descriptor name: "dmaxflat4", "impulse" or "custom" (descriptor.cpp:12-15)
 };
-static Bank default_bank(int impulse_fan) { return Bank{fan_of(impulse_fan), qmf_from_lowpass(maxflat9_lowpass())}; }
+static Bank default_bank(int impulse_fan) {
+    return Bank{fan_of(impulse_fan), qmf_from_lowpass(maxflat9_lowpass()), impulse_fan ? "impulse" : "dmaxflat4"};
+}
 
 static void set_shard(System& s, int lo, int hi) {
     if (hi < 0) hi = s.R;

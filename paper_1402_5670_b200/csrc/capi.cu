@@ -14,6 +14,7 @@
 #include "iterative.cuh"
 #include "shcf.cuh"
 #include "image_io.cuh"
+#include "descriptor.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
@@ -74,7 +75,7 @@ void require_dev_ptr(const void* p, const char* what) {
 // highpass = mirror_highpass(lowpass) (QmfPair::from_lowpass), NULL fan =
 // default_fan_filter() (filters.cpp:32-38, 114-122).
 Bank bank_of(const double* lp, int lp_len, int lp_c, const double* hp, int hp_len, int hp_c, const double* fan, int fr,
-             int fc, int fc0, int fc1) {
+             int fc, int fc0, int fc1, const char* provenance) {
     Bank b = default_bank(0);
     if (lp) {
         if (lp_len < 1) throw SlError(SL_ERR_INVALID, "QmfPair: empty lowpass");
@@ -90,6 +91,8 @@ Bank bank_of(const double* lp, int lp_len, int lp_c, const double* hp, int hp_le
         Taps2 t = Taps2::zeros(static_cast<size_t>(fr), static_cast<size_t>(fc), fc0, fc1);
         std::memcpy(t.v.data(), fan, sizeof(double) * t.v.size());
         b.fan = std::move(t);
+        const std::string pv = provenance ? provenance : "";
+        b.fan_name = (pv == "dmaxflat4" || pv == "impulse") ? pv : "custom";
     }
     return b;
 }
@@ -115,6 +118,10 @@ int create(int ndim, const int* n, const int* levels, int n_scales, int j0, int 
         s.full = full != 0;
         s.device = device;
         init_geometry(s);
+        s.qmf_lowpass = bank_in->qmf.lowpass.v;
+        s.qmf_center = bank_in->qmf.lowpass.c;
+        s.fan_name = bank_in->fan_name;
+        s.fan_ck = fan_checksum(bank_in->fan);
         cudaStream_t st;
         SL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         try {
@@ -167,12 +174,13 @@ int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales,
 int sl_system_create_2d_ex(int rows, int cols, const int* levels, int n_scales, int j0, int full_system,
                            const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
                            int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
-                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out) {
+                           int fan_c0, int fan_c1, const char* fan_provenance, int device, int shard_lo,
+                           int shard_hi, sl_system** out) {
     const int n[2] = {rows, cols};
     Bank bank;
     const int rc = guard([&] {
         bank = bank_of(lowpass, lowpass_len, lowpass_center, highpass, highpass_len, highpass_center, fan, fan_rows,
-                       fan_cols, fan_c0, fan_c1);
+                       fan_cols, fan_c0, fan_c1, fan_provenance);
     });
     if (rc) return rc;
     return create(2, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
@@ -181,15 +189,61 @@ int sl_system_create_2d_ex(int rows, int cols, const int* levels, int n_scales, 
 int sl_system_create_3d_ex(int n0, int n1, int n2, const int* levels, int n_scales, int j0, int full_system,
                            const double* lowpass, int lowpass_len, int lowpass_center, const double* highpass,
                            int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
-                           int fan_c0, int fan_c1, int device, int shard_lo, int shard_hi, sl_system** out) {
+                           int fan_c0, int fan_c1, const char* fan_provenance, int device, int shard_lo,
+                           int shard_hi, sl_system** out) {
     const int n[3] = {n0, n1, n2};
     Bank bank;
     const int rc = guard([&] {
         bank = bank_of(lowpass, lowpass_len, lowpass_center, highpass, highpass_len, highpass_center, fan, fan_rows,
-                       fan_cols, fan_c0, fan_c1);
+                       fan_cols, fan_c0, fan_c1, fan_provenance);
     });
     if (rc) return rc;
     return create(3, n, levels, n_scales, j0, full_system, &bank, device, shard_lo, shard_hi, out);
+}
+
+int sl_describe(const sl_system* h, char* text, size_t cap, size_t* len) {
+    return guard([&] {
+        const System& s = sys_of(h);
+        Descriptor d;
+        d.ndim = s.ndim;
+        for (int a = 0; a < s.ndim; ++a) d.dims[a] = s.n[a];
+        d.j0 = s.prof.j0;
+        d.levels = s.prof.levels;
+        d.full = s.full;
+        d.qmf = s.qmf_lowpass;
+        d.qmf_center = s.qmf_center;
+        d.fan_name = s.fan_name;
+        d.fan_ck = s.fan_ck;
+        const std::string t = descriptor_text(d);
+        if (len) *len = t.size();
+        if (text) {
+            if (cap < t.size() + 1) throw SlError(SL_ERR_INVALID, "describe: buffer too small");
+            std::memcpy(text, t.c_str(), t.size() + 1);
+        }
+    });
+}
+
+int sl_system_create_from_descriptor(const char* text, int ndim, int device, int shard_lo, int shard_hi,
+                                     sl_system** out) {
+    Bank bank;
+    Descriptor d;
+    const int rc = guard([&] {
+        if (!text) throw SlError(SL_ERR_INVALID, "null descriptor text");
+        d = descriptor_parse(text);
+        if (ndim == 2 && d.ndim != 2) throw SlError(SL_ERR_FORMAT, "descriptor: expected a 2D system");
+        if (ndim == 3 && d.ndim != 3) throw SlError(SL_ERR_FORMAT, "descriptor: expected a 3D system");
+        for (int v : d.levels)
+            if (v < 0) throw SlError(SL_ERR_CONFIG, "ScaleProfile: shear levels must be >= 0");
+        bank.fan = descriptor_fan(d);
+        bank.fan_name = d.fan_name;
+        bank.qmf = qmf_from_lowpass(Taps1{d.qmf, d.qmf_center});
+        for (int a = 0; a < d.ndim; ++a)
+            if (d.dims[a] < 0 || d.dims[a] > (1 << 20)) throw SlError(SL_ERR_FORMAT, "descriptor: bad dims");
+    });
+    if (rc) return rc;
+    const int n[3] = {static_cast<int>(d.dims[0]), static_cast<int>(d.dims[1]), static_cast<int>(d.dims[2])};
+    return create(d.ndim, n, d.levels.data(), static_cast<int>(d.levels.size()), d.j0, d.full, &bank, device, shard_lo,
+                  shard_hi, out);
 }
 
 int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1) {

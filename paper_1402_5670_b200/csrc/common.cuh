@@ -161,6 +161,11 @@ struct System {
     int lo = 0, hi = 0;  // shard
     std::vector<double> rms;
     double Wmin = 0, Wmax = 0;
+    // what describe() reports (descriptor.hpp:14-23)
+    std::vector<double> qmf_lowpass;
+    long qmf_center = 0;
+    std::string fan_name;
+    uint64_t fan_ck = 0;
 
     std::map<int, std::unique_ptr<PlanHolder>> plans;
     DBuf<double> psi;   // 2D: [R][nhalf] real

@@ -66,3 +66,27 @@ def test_svol_errors(tmp_path):
         (tmp_path / name).write_bytes(data)
         with pytest.raises(P.FormatError):
             P.load_svol(str(tmp_path / name))
+
+
+DESC = ["d2_512_1122", "d2_48x40_full_j1", "d2_32_legall", "d3_16_impulse", "d3_16x20x24_legall"]
+
+
+@pytest.mark.parametrize("name", DESC)
+def test_descriptor_text_round_trip(name):
+    # read_descriptor / write_descriptor grammar (descriptor.cpp:48-126) on the reference's own texts
+    text = str(golden("descriptors")[name + "_text"])
+    d = P.SystemDescriptor.parse(text)
+    assert d.text() == text
+
+
+def test_descriptor_parse_errors(tmp_path):
+    good = str(golden("descriptors")["d2_32_legall_text"])
+    for bad in (good.replace("shearlet-system 1", "shearlet-system 2"), good.replace("dims 32 32", "dims 32"),
+                good + "colour blue\n", good.replace("qmf -0.125", "qmf x"), "\n".join(good.splitlines()[:-1])):
+        with pytest.raises(P.FormatError):
+            P.SystemDescriptor.parse(bad)
+    with pytest.raises(P.FormatError):
+        P.read_descriptor(str(tmp_path / "missing.txt"))
+    p = str(tmp_path / "d.txt")
+    P.write_descriptor(P.SystemDescriptor.parse(good), p)
+    assert open(p).read() == good
