@@ -68,99 +68,130 @@ enum Ax0Mode : int {
 template <int L, int DIR, int MODE>
 __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
     k3_ax0_to_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int H,
-                  FiltSynth3D filt, int band0, const double* __restrict__ WN, const double2* __restrict__ tw) {
+                  FiltSynth3D filt, int band0, int G, int nb, const double* __restrict__ WN,
+                  const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
     constexpr int n = L;
     extern __shared__ double2 tile[];  // [L][V] tile + V line buffers
     const int lines_per_k2 = n / V;
     const int k2 = blockIdx.x / lines_per_k2;
     const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
-    const int band = band0 + blockIdx.y;
-    src += blockIdx.y * sbs;
-    dst += blockIdx.y * dbs;
+    // DecMul: CTA y handles bands [g0, g0 + gn) of the chunk, re-reading the same
+    // F lines (L1/L2 hits after the first band); other modes: one spectrum per y.
+    const int g0 = MODE == kAx0DecMul ? blockIdx.y * G : 0;
+    const int gn = MODE == kAx0DecMul ? min(G, nb - g0) : 1;
+    if (MODE != kAx0DecMul) {
+        src += blockIdx.y * sbs;
+        dst += blockIdx.y * dbs;
+    }
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
     const double2* s = src + ((long long)k2 * n + k1) * n;
-    BandDesc3D bd{};
-    if (MODE == kAx0DecMul) bd = filt.bands[band];
-    double2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k0 = t + T * m;
-        double2 z = __ldcg(s + k0);
-        if (MODE == kAx0DecMul) {
-            const double p = filt.get_d(bd, k0, k1, k2);
-            z = make_double2(z.x * p, z.y * p);
-        } else if (MODE == kAx0DivW) {
-            const double w = __ldg(WN + ((long long)k2 * n + k1) * n + k0);
-            z = make_double2(z.x / w, z.y / w);
-        }
-        x[m] = z;
-    }
     double2* lb = tile + li * L;  // line exchange buffers alias the output tile
-    reg_fft<L, DIR>(x, lb, t, tw);
-    __syncthreads();              // every line's FFT is done with the aliased buffers
-    // publish into the [i0][v] tile, then write 128-byte rotated runs
+    for (int bb = 0; bb < gn; ++bb) {
+        BandDesc3D bd{};
+        if (MODE == kAx0DecMul) bd = filt.bands[band0 + g0 + bb];
+        double2 x[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) tile[aslot<V>(t + T * m, li)] = x[m];
-    __syncthreads();
-    double2* o = dst + (long long)k2 * n * n + k1_0;
-    for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
-        const int i0 = idx / V, v = idx - i0 * V;
-        __stcg(o + (long long)i0 * n + v, tile[aslot<V>(i0, v)]);
+        for (int m = 0; m < E; ++m) {
+            const int k0 = t + T * m;
+            double2 z = MODE == kAx0DecMul ? __ldg(s + k0) : __ldcg(s + k0);
+            if (MODE == kAx0DecMul) {
+                const double p = filt.get_d(bd, k0, k1, k2);
+                z = make_double2(z.x * p, z.y * p);
+            } else if (MODE == kAx0DivW) {
+                const double w = __ldg(WN + ((long long)k2 * n + k1) * n + k0);
+                z = make_double2(z.x / w, z.y / w);
+            }
+            x[m] = z;
+        }
+        if (bb > 0) __syncthreads();  // previous band's tile fully written out
+        reg_fft<L, DIR>(x, lb, t, tw);
+        __syncthreads();              // every line's FFT is done with the aliased buffers
+        // publish into the [i0][v] tile, then write 128-byte rotated runs
+#pragma unroll
+        for (int m = 0; m < E; ++m) tile[aslot<V>(t + T * m, li)] = x[m];
+        __syncthreads();
+        double2* o = dst + (long long)(g0 + bb) * dbs + (long long)k2 * n * n + k1_0;
+        for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+            const int i0 = idx / V, v = idx - i0 * V;
+            __stcg(o + (long long)i0 * n + v, tile[aslot<V>(i0, v)]);
+        }
     }
     (void)H;
 }
 
 // ---------------------------------------------------------------- axis 0: R -> N
-// One spectrum per blockIdx.y. kAx0RecAcc: blockIdx.y walks nothing -- the
-// host launches one band at a time and the epilogue read-modify-writes the
-// accumulator (acc (+)= FFT_0(x) psi_b, band order = launch order, deterministic).
+// kAx0RecAcc: one CTA walks the chunk's bands [0, nbands) in order, summing
+// FFT_0(x_b) psi_b in registers, then read-modify-writes the accumulator once
+// (acc (+)= sum; deterministic, independent of the stream count). Other modes:
+// one spectrum per blockIdx.y.
 template <int L, int DIR, int MODE>
 __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
     k3_ax0_from_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int nbands,
                     FiltSynth3D filt, int band0, int accumulate, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
     constexpr int n = L;
-    extern __shared__ double2 tile[];  // [L][V] tile + V line buffers
+    extern __shared__ double2 tile[];  // [L][V] tile (line buffers alias it) [+ V accumulator lines]
     const int lines_per_k2 = n / V;
     const int k2 = blockIdx.x / lines_per_k2;
     const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
     double2* lb = tile + li * L;  // line exchange buffers alias the input tile (after the gather)
-    src += blockIdx.y * sbs;
-    if (MODE != kAx0RecAcc) dst += blockIdx.y * dbs;
-    const double2* si = src + (long long)k2 * n * n + k1_0;
-    for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
-        const int i0 = idx / V, v = idx - i0 * V;
-        cp_async16(tile + aslot<V>(i0, v), si + (long long)i0 * n + v);
+    if (MODE != kAx0RecAcc) {
+        src += blockIdx.y * sbs;
+        dst += blockIdx.y * dbs;
     }
-    cp_async_wait_all();
-    __syncthreads();
-    double2 x[E];
+    const int nb = MODE == kAx0RecAcc ? nbands : 1;
+    // RecAcc: per-thread accumulator slots after the tile (acc[li][t + T m]),
+    // registers stay free for the FFT line
+    double2* acc = tile + V * L + li * L;
+    if (MODE == kAx0RecAcc) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
-    __syncthreads();  // all lines gathered: the tile becomes the line buffers
-    reg_fft<L, DIR>(x, lb, t, tw);
+        for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
+    }
+    double2 x[E];
+    for (int b = 0; b < nb; ++b) {
+        const double2* si = src + (long long)b * sbs + (long long)k2 * n * n + k1_0;
+        if (b > 0) __syncthreads();  // previous band's line buffers are free again
+        for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+            const int i0 = idx / V, v = idx - i0 * V;
+            cp_async16(tile + aslot<V>(i0, v), si + (long long)i0 * n + v);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
+        __syncthreads();  // all lines gathered: the tile becomes the line buffers
+        reg_fft<L, DIR>(x, lb, t, tw);
+        if (MODE == kAx0RecAcc) {
+            const BandDesc3D bd = filt.bands[band0 + b];
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const double p = filt.get_d(bd, t + T * m, k1, k2);
+                double2 a = acc[t + T * m];
+                a.x = fma(x[m].x, p, a.x);
+                a.y = fma(x[m].y, p, a.y);
+                acc[t + T * m] = a;
+            }
+        }
+    }
     double2* d = dst + ((long long)k2 * n + k1) * n;
     if (MODE == kAx0RecAcc) {
-        const BandDesc3D bd = filt.bands[band0 + blockIdx.y];
-        double2 a[E];
-#pragma unroll
-        for (int m = 0; m < E; ++m) a[m] = accumulate ? __ldcg(d + t + T * m) : make_double2(0.0, 0.0);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double p = filt.get_d(bd, t + T * m, k1, k2);
-            a[m].x = fma(x[m].x, p, a[m].x);
-            a[m].y = fma(x[m].y, p, a[m].y);
-            __stcg(d + t + T * m, a[m]);
+            double2 v = acc[t + T * m];
+            if (accumulate) {
+                const double2 o = __ldcg(d + t + T * m);
+                v = make_double2(o.x + v.x, o.y + v.y);
+            }
+            __stcg(d + t + T * m, v);
         }
     } else {
 #pragma unroll
         for (int m = 0; m < E; ++m) __stcg(d + t + T * m, x[m]);
     }
-    (void)nbands;
 }
 
 // [i0][i1][ldh] row-major half (build layout) -> natural N[k2][k1][k0]

@@ -15,10 +15,13 @@ static bool fast3d_supported(const int* n) {
     }
 }
 
-// bands per chunk: the rotated intermediate of a chunk stays around 64 MiB
+// bands per chunk: the rotated intermediate of a chunk stays around 64 MiB,
+// but at least SLB_G3 bands so the axis-0 passes can share F / the accumulator
+// RMW across a band group.
+static int fast3d_group(const System&) { return env_int("SLB_G3", 16); }
 static int fast3d_chunk(const System& s) {
     const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
-    return env_int("SLB_CHUNK3", std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
+    return env_int("SLB_CHUNK3", std::max(fast3d_group(s), static_cast<int>((64.0 * 1024 * 1024) / per)));
 }
 
 template <int n>
@@ -77,21 +80,22 @@ struct Fast3DLaunch {
     void to_rot(const double2* src, long long sbs, double2* dst, int nb, int band0, const double* WN, const char* nm) {
         set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
         LaunchScope ls(s, nm, st, nb);
-        k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, nb), AC::THREADS, ax_smem, st>>>(src, sbs, dst, nT, H, s.synth,
-                                                                                        band0, WN, tw);
+        const int G = MODE == kAx0DecMul ? std::min(fast3d_group(s), nb) : 1;
+        const int groups = (nb + G - 1) / G;
+        k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, groups), AC::THREADS, ax_smem, st>>>(
+            src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw);
         check_launch("k3_ax0_to_rot");
     }
     template <int DIR, int MODE>
     void from_rot(const double2* src, double2* dst, int nb, int band0, int accumulate, const char* nm) {
-        set_smem(k3_ax0_from_rot<n, DIR, MODE>, ax_smem);
+        const size_t smem = MODE == kAx0RecAcc ? 2 * ax_smem : ax_smem;
+        set_smem(k3_ax0_from_rot<n, DIR, MODE>, smem);
         LaunchScope ls(s, nm, st, nb);
         if (MODE == kAx0RecAcc) {
-            // bands one launch at a time: the accumulator RMW stays in band order
-            for (int b = 0; b < nb; ++b) {
-                k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, 1), AC::THREADS, ax_smem, st>>>(
-                    src + b * nT, nT, dst, nT, 1, s.synth, band0 + b, accumulate || b > 0, tw);
-                check_launch("k3_ax0_from_rot");
-            }
+            // one launch per chunk; every CTA walks the chunk's bands in order
+            k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, 1), AC::THREADS, smem, st>>>(
+                src, nT, dst, nT, nb, s.synth, band0, accumulate, tw);
+            check_launch("k3_ax0_from_rot");
             return;
         }
         k3_ax0_from_rot<n, DIR, MODE><<<dim3(ax_blocks, nb), AC::THREADS, ax_smem, st>>>(
