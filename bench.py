@@ -367,7 +367,9 @@ def main():
         dom_bytes = per_unit * dom_units / max(dom_n, 1) if per_unit else None
         dom_avg_s = dom_ms / max(dom_n, 1) / 1000.0
         achieved = (dom_bytes / dom_avg_s / 1e9) if dom_avg_s > 0 and dom_bytes else None
-        path_gbs = nbytes * (total_units / world if is3d else frames) / (ms_step / 1000.0) / 1e9
+        traffic = measured_traffic(args.config, dom_name, dom_units / max(dom_n, 1))
+        # per-rank compulsory bytes per step: `frames` frames (2D) or 1/world of a volume's bands (3D)
+        path_gbs = nbytes * (1.0 / world if is3d else frames) / (ms_step / 1000.0) / 1e9
         line = {
             "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
@@ -378,7 +380,7 @@ def main():
                        "l2": "flushed between timed steps (256 MB write); stack per frame > L2",
                        "parallelism": (f"shearlet-shard{world}" if is3d else f"dp{world}")},
             "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_avg_s * 1000.0,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "path_roofline": {"bytes_per_unit": nbytes, "achieved": path_gbs, "frac": path_gbs / peak,
@@ -400,11 +402,25 @@ def main():
         dist.destroy_process_group()
 
 
+def measured_traffic(config, pass_name, bands_per_launch):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    pass, from the committed ncu --set full summary (profiles/traffic.json,
+    written by tools/ncu_summary.py traffic; cold-cache per-band bytes scaled to
+    this run's bands per launch), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            e = json.load(fh)[config][pass_name]
+        return e["dram_bytes_per_band"] * bands_per_launch
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def pass_bytes(name, dims):
     """Bytes at the boundary of each pass per band (or spectrum) processed, for
     the current multi-pass design."""
     N = int(np.prod(dims))
     Nh = N // dims[-1] * (dims[-1] // 2 + 1)
+    G3 = int(os.environ.get("SLB_G3", "16"))  # 3D band group (csrc/fast3d_host.cuh)
     return None if name == "none" else {
         # generic path
         "rows_c2r_thr": 16 * Nh + 8 * N,          # intermediate read + band write, per band
@@ -430,8 +446,8 @@ def pass_bytes(name, dims):
         "f3_rows_c2r_thr": 16 * Nh + 8 * N,
         "f3_rows_c2r": 16 * Nh + 8 * N,
         "f3_axis1": 32 * Nh,
-        "f3_ax0_dec": 32 * Nh,                    # F read + rotated write
-        "f3_ax0_rec": 48 * Nh,                    # rotated read + accumulator read-modify-write
+        "f3_ax0_dec": 16 * Nh + 16 * Nh / G3,     # rotated write + F read once per band group
+        "f3_ax0_rec": 16 * Nh + 32 * Nh / G3,     # rotated read + accumulator RMW once per group
         "f3_ax0_fwd": 32 * Nh,
         "f3_ax0_final": 40 * Nh,
     }.get(name, None)

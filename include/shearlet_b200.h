@@ -45,6 +45,7 @@ enum sl_status {
     SL_ERR_ASSET = 7,            /* shearlet::AssetError                         */
     SL_ERR_FORMAT = 8,           /* shearlet::FormatError                        */
     SL_ERR_DEGENERATE_MASK = 9,  /* shearlet::DegenerateMaskError                */
+    SL_ERR_DEGENERATE_TRUTH = 10, /* shearlet::DegenerateTruthError              */
     SL_ERR_CUDA = 20,            /* CUDA runtime failure                         */
     SL_ERR_INVALID = 22,         /* null handle / bad argument at the ABI        */
 };
@@ -189,6 +190,21 @@ int sl_load_pgm(const char* path, double* pixels, int64_t cap, int* rows, int* c
 int sl_save_pgm(const double* pixels, int rows, int cols, const char* path, int maxval);
 int sl_load_svol(const char* path, double* volume, int64_t cap, int64_t dims[3]);
 int sl_save_svol(const double* volume, const int64_t dims[3], const char* path);
+
+/* ---- separation-quality metrics (apps.hpp:92-101, apps.cpp:282-362) -----
+ * Host buffers, rows x cols row-major. The periodic Gaussian blur runs on the
+ * GPU through the hot path's single-band decomposition; the kernel taps must
+ * be centrally symmetric (gaussian_kernel's are). Errors as the reference:
+ * DomainError (truth not binary, delta < 0, sigma <= 0), DegenerateTruthError. */
+int sl_gaussian_kernel(double sigma_pixels, double* taps, int64_t cap, int* size, int* center);
+int sl_binarize(const double* in, double* out, int64_t count, double delta);
+int sl_quality_q(int rows, int cols, const double* recovered, const double* truth, double delta,
+                 const double* kernel, int k_rows, int k_cols, int k_c0, int k_c1, int device, double* q);
+/* quality_q_opt: minimum over integer delta = 0..255 (ties: smallest delta);
+ * q_all (optional, 256 doubles) receives every Q(delta). */
+int sl_quality_q_opt(int rows, int cols, const double* recovered, const double* truth, const double* kernel,
+                     int k_rows, int k_cols, int k_c0, int k_c1, int device, double* q, int* best_delta,
+                     double* q_all);
 
 /* ---- instrumentation ---------------------------------------------------
  * sl_profile(enable) clears the per-pass statistics and turns CUDA-event timing

@@ -173,6 +173,21 @@ def gen_descriptors():
     save("descriptors", **out)
 
 
+def gen_quality():
+    """quality_q / quality_q_opt (apps.cpp:289-362) on the separation fixture's curves."""
+    g = np.load(os.path.join(OUT, "it_separate128.npz"))
+    truth = (np.abs(ref.curves_plus_dots(128)) > 100.0).astype(np.float64)
+    rec = np.abs(g["curves"])
+    out = {"rec": rec, "truth": truth, "gauss2": ref.gaussian_kernel(2.0)[0], "gauss07": ref.gaussian_kernel(0.7)[0]}
+    for name, sigma in (("s2", 2.0), ("s07", 0.7)):
+        q, d = ref.quality_q_opt(rec, truth, sigma)
+        out[f"qopt_{name}"], out[f"dopt_{name}"] = q, d
+        out[f"q40_{name}"] = ref.quality_q(rec, truth, 40.0, sigma)
+    # non-power-of-two grid (generic FFT path): 96 x 80 crop
+    out["qopt_crop"], out["dopt_crop"] = ref.quality_q_opt(rec[:96, :80], truth[:96, :80], 1.5)
+    save("quality_q", **out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
@@ -212,6 +227,12 @@ def main():
     rec = s.inpaint(masked, mask, 12)
     save("it_inpaint128", masked=masked, mask=mask, levels=np.array([0, 1, 1]), iterations=12, delta_min=0.01,
          out=rec)
+    # 3D inpainting (apps.hpp:70-72): 32^3 [0,1], 30 % of the voxels observed
+    s3 = ref.RefSystem3D((32, 32, 32), [0, 1])
+    mask3 = (np.random.default_rng(6).uniform(size=(32, 32, 32)) < 0.3).astype(np.float64)
+    masked3 = ref.cartoon_volume(32) * mask3
+    save("it_inpaint3d32", masked=masked3, mask=mask3, levels=np.array([0, 1]), iterations=6, delta_min=0.01,
+         out=s3.inpaint(masked3, mask3, 6))
     sd = ref.RefSystem2D(128, 128, [0, 1])
     si = ref.RefSystem2D(128, 128, [0, 0], impulse_fan=True)
     sig = ref.curves_plus_dots(128)
@@ -230,6 +251,7 @@ def main():
     gen_banks()
     gen_io()
     gen_descriptors()
+    gen_quality()
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))

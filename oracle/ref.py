@@ -52,6 +52,7 @@ def lib():
             getattr(L, f"ref_denoise_{d}").argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.c_int]
         L.ref_denoise_3d_stats.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.POINTER(C.c_longlong), dp, dp, C.POINTER(C.c_longlong), C.c_int, C.c_int]
         L.ref_inpaint_2d.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, C.c_int]
+        L.ref_inpaint_3d.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, C.c_int]
         L.ref_separate_2d.argtypes = [P, P, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, dp, C.c_int]
         L.ref_random_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint64, dp]
         L.ref_curves_plus_dots.argtypes = [C.c_int, dp]
@@ -69,6 +70,9 @@ def lib():
         L.ref_write_descriptor_2d.argtypes = [P, C.c_char_p]
         L.ref_write_descriptor_3d.argtypes = [P, C.c_char_p]
         L.ref_build_from_descriptor.argtypes = [C.c_char_p, ip, C.POINTER(P)]
+        L.ref_gaussian_kernel.argtypes = [C.c_double, dp, C.c_longlong, ip]
+        L.ref_quality_q_opt.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, dp, ip]
+        L.ref_quality_q.argtypes = [C.c_int, C.c_int, dp, dp, C.c_double, C.c_double, dp]
         L.ref_save_pgm.argtypes = [dp, C.c_int, C.c_int, C.c_char_p, C.c_int]
         L.ref_load_pgm.argtypes = [C.c_char_p, dp, C.c_longlong, ip]
         L.ref_save_svol.argtypes = [dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
@@ -290,6 +294,14 @@ class RefSystem3D:
         _check(lib().ref_denoise_3d(self.h, _dp(f), _dp(K), len(K), sigma, int(scaled), _dp(out), threads))
         return out
 
+    def inpaint(self, masked, mask, iterations, delta_init=-1.0, delta_min=0.01, scaled=True, threads=0):
+        masked = np.ascontiguousarray(masked, dtype=np.float64)
+        mask = np.ascontiguousarray(mask, dtype=np.float64)
+        out = np.zeros(self.shape)
+        _check(lib().ref_inpaint_3d(self.h, _dp(masked), _dp(mask), iterations, delta_init, delta_min, int(scaled),
+                                    _dp(out), threads))
+        return out
+
     def denoise_stats(self, f, K, sigma, sample_idx, scaled=True, threads=0):
         f = np.ascontiguousarray(f, dtype=np.float64)
         K = np.ascontiguousarray(K, dtype=np.float64)
@@ -341,6 +353,30 @@ def descriptor_text(system) -> str:
         fn = lib().ref_write_descriptor_2d if isinstance(system, RefSystem2D) else lib().ref_write_descriptor_3d
         _check(fn(system.h, p.encode()))
         return open(p).read()
+
+
+def gaussian_kernel(sigma):
+    info = np.zeros(2, dtype=np.int32)
+    _check(lib().ref_gaussian_kernel(sigma, None, 0, _ip(info)))
+    t = np.zeros((info[0], info[0]))
+    _check(lib().ref_gaussian_kernel(sigma, _dp(t), t.size, _ip(info)))
+    return t, int(info[1])
+
+
+def quality_q_opt(rec, truth, sigma):
+    rec = np.ascontiguousarray(rec, dtype=np.float64)
+    truth = np.ascontiguousarray(truth, dtype=np.float64)
+    q, d = C.c_double(), C.c_int()
+    _check(lib().ref_quality_q_opt(rec.shape[0], rec.shape[1], _dp(rec), _dp(truth), sigma, C.byref(q), C.byref(d)))
+    return q.value, d.value
+
+
+def quality_q(rec, truth, delta, sigma):
+    rec = np.ascontiguousarray(rec, dtype=np.float64)
+    truth = np.ascontiguousarray(truth, dtype=np.float64)
+    q = C.c_double()
+    _check(lib().ref_quality_q(rec.shape[0], rec.shape[1], _dp(rec), _dp(truth), delta, sigma, C.byref(q)))
+    return q.value
 
 
 def save_pgm(px, path, maxval=255):

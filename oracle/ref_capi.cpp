@@ -42,6 +42,7 @@ int guard(F&& f) {
     catch (const AssetError& e) { g_err = e.what(); return 7; }
     catch (const FormatError& e) { g_err = e.what(); return 8; }
     catch (const DegenerateMaskError& e) { g_err = e.what(); return 9; }
+    catch (const DegenerateTruthError& e) { g_err = e.what(); return 10; }
     catch (const Error& e) { g_err = e.what(); return 1; }
     catch (const std::exception& e) { g_err = e.what(); return 99; }
 }
@@ -358,6 +359,22 @@ int ref_inpaint_2d(void* h, const double* masked, const double* mask, int iterat
         std::memcpy(out, r.data(), sizeof(double) * r.size());
     });
 }
+int ref_inpaint_3d(void* h, const double* masked, const double* mask, int iterations, double delta_init,
+                   double delta_min, int scaled, double* out, int threads) {
+    return guard([&] {
+        const auto& s = *static_cast<ShearletSystem3D*>(h);
+        Signal3D x(s.dims[0], s.dims[1], s.dims[2]), m(s.dims[0], s.dims[1], s.dims[2]);
+        std::memcpy(x.data(), masked, sizeof(double) * x.size());
+        std::memcpy(m.data(), mask, sizeof(double) * m.size());
+        InpaintConfig cfg;
+        cfg.iterations = iterations;
+        cfg.delta_init = delta_init;
+        cfg.delta_min = delta_min;
+        cfg.scale_by_filter_norm = scaled != 0;
+        const auto r = inpaint(x, m, s, cfg, threads);
+        std::memcpy(out, r.data(), sizeof(double) * r.size());
+    });
+}
 int ref_separate_2d(void* hd, void* hi, const double* signal, int iterations, double delta_init, double delta_min,
                     int scaled, double* curves, double* blobs, int threads) {
     return guard([&] {
@@ -473,6 +490,35 @@ int ref_build_from_descriptor(const char* path, int* is3d, void** out) {
             *out = new ShearletSystem3D(build_from_descriptor_3d(d));
         else
             *out = new ShearletSystem2D(build_from_descriptor_2d(d));
+    });
+}
+
+// ---------------------------------------------------------------- Q metrics (apps.hpp:92-101)
+int ref_gaussian_kernel(double sigma, double* out, long long cap, int* info) {
+    return guard([&] {
+        const Taps2d t = gaussian_kernel(sigma);
+        info[0] = static_cast<int>(t.size0());
+        info[1] = static_cast<int>(t.center0);
+        if (out && cap >= static_cast<long long>(t.size0() * t.size1()))
+            std::memcpy(out, t.v.data(), sizeof(double) * t.size0() * t.size1());
+    });
+}
+int ref_quality_q_opt(int rows, int cols, const double* rec, const double* truth, double sigma, double* q, int* delta) {
+    return guard([&] {
+        Signal2D r(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols)), t(r.size0(), r.size1());
+        std::memcpy(r.data(), rec, sizeof(double) * r.size());
+        std::memcpy(t.data(), truth, sizeof(double) * t.size());
+        const auto res = quality_q_opt(r, t, gaussian_kernel(sigma));
+        *q = res.first;
+        *delta = res.second;
+    });
+}
+int ref_quality_q(int rows, int cols, const double* rec, const double* truth, double d, double sigma, double* q) {
+    return guard([&] {
+        Signal2D r(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols)), t(r.size0(), r.size1());
+        std::memcpy(r.data(), rec, sizeof(double) * r.size());
+        std::memcpy(t.data(), truth, sizeof(double) * t.size());
+        *q = quality_q(r, t, d, gaussian_kernel(sigma));
     });
 }
 

@@ -71,6 +71,10 @@ class DegenerateMaskError(Error):
     pass
 
 
+class DegenerateTruthError(Error):
+    pass
+
+
 class CudaError(Error):
     pass
 
@@ -80,7 +84,7 @@ class InvalidArgument(Error):
 
 
 _CODES = {1: Error, 2: ShapeError, 3: ConfigError, 4: DomainError, 5: SingularFrameError,
-          6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 9: DegenerateMaskError, 20: CudaError,
+          6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 9: DegenerateMaskError, 10: DegenerateTruthError, 20: CudaError,
           22: InvalidArgument}
 
 # ------------------------------------------------------------------ library
@@ -145,6 +149,11 @@ def lib():
     L.sl_save_pgm.argtypes = [dp, i, i, C.c_char_p, i]
     L.sl_load_svol.argtypes = [C.c_char_p, dp, C.c_int64, C.POINTER(C.c_int64)]
     L.sl_save_svol.argtypes = [dp, C.POINTER(C.c_int64), C.c_char_p]
+    L.sl_gaussian_kernel.argtypes = [C.c_double, dp, C.c_int64, ip, ip]
+    L.sl_binarize.argtypes = [dp, dp, C.c_int64, C.c_double]
+    kern = [dp, i, i, i, i, i]
+    L.sl_quality_q.argtypes = [i, i, dp, dp, C.c_double] + kern + [dp]
+    L.sl_quality_q_opt.argtypes = [i, i, dp, dp] + kern + [dp, ip, dp]
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
@@ -166,6 +175,7 @@ EXPORTED_SYMBOLS = [
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
     "sl_describe", "sl_system_create_from_descriptor",
+    "sl_gaussian_kernel", "sl_binarize", "sl_quality_q", "sl_quality_q_opt",
     "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
@@ -863,6 +873,54 @@ def save_svol(volume, path: str):
     if v.ndim != 3:
         raise ShapeError("save_svol: volume must be 3D")
     _check(lib().sl_save_svol(_dp(v), (C.c_int64 * 3)(*v.shape), os.fsencode(path)))
+
+
+# ------------------------------------------------------------------ quality metrics
+def gaussian_kernel(sigma_pixels: float = 2.0) -> "FanFilter":
+    """gaussian_kernel (apps.cpp:289-306): L1-normalised taps, radius ceil(4 sigma); returned as
+    Taps2d-like (taps, center0, center1)."""
+    n, c = C.c_int(), C.c_int()
+    _check(lib().sl_gaussian_kernel(float(sigma_pixels), None, 0, C.byref(n), C.byref(c)))
+    t = np.empty((n.value, n.value))
+    _check(lib().sl_gaussian_kernel(float(sigma_pixels), _dp(t), t.size, None, None))
+    return FanFilter(t, c.value, c.value, f"gaussian{sigma_pixels}")
+
+
+def binarize(signal, delta: float) -> np.ndarray:
+    """binarize (apps.cpp:282-287): 1 where |g| >= delta, else 0."""
+    x = np.ascontiguousarray(signal, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(lib().sl_binarize(_dp(x), _dp(out), x.size, float(delta)))
+    return out
+
+
+def _quality_args(recovered, truth, gaussian):
+    r = np.ascontiguousarray(recovered, dtype=np.float64)
+    t = np.ascontiguousarray(truth, dtype=np.float64)
+    if r.shape != t.shape or r.ndim != 2:
+        raise ShapeError("quality_q: dimension mismatch")
+    g = gaussian_kernel(2.0) if gaussian is None else gaussian
+    k = np.ascontiguousarray(g.taps, dtype=np.float64)
+    return r, t, k, g
+
+
+def quality_q(recovered, truth, delta: float, gaussian=None, device: int = 0) -> float:
+    """quality_q (apps.cpp:309-326); the blurs run on the GPU."""
+    r, t, k, g = _quality_args(recovered, truth, gaussian)
+    q = C.c_double()
+    _check(lib().sl_quality_q(r.shape[0], r.shape[1], _dp(r), _dp(t), float(delta), _dp(k), k.shape[0], k.shape[1],
+                              int(g.center0), int(g.center1), int(device), C.byref(q)))
+    return q.value
+
+
+def quality_q_opt(recovered, truth, gaussian=None, device: int = 0, return_all: bool = False):
+    """quality_q_opt (apps.cpp:328-360): (min Q over delta = 0..255, argmin); 256 blurs batched on the GPU."""
+    r, t, k, g = _quality_args(recovered, truth, gaussian)
+    q, d = C.c_double(), C.c_int()
+    allq = np.empty(256)
+    _check(lib().sl_quality_q_opt(r.shape[0], r.shape[1], _dp(r), _dp(t), _dp(k), k.shape[0], k.shape[1],
+                                  int(g.center0), int(g.center1), int(device), C.byref(q), C.byref(d), _dp(allq)))
+    return (q.value, d.value, allq) if return_all else (q.value, d.value)
 
 
 # ------------------------------------------------------------------ iterative pipelines

@@ -15,6 +15,7 @@
 #include "shcf.cuh"
 #include "image_io.cuh"
 #include "descriptor.cuh"
+#include "quality.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
@@ -788,6 +789,82 @@ int sl_save_svol(const double* volume, const int64_t dims[3], const char* path) 
             d[a] = dims[a];
         }
         svol_save(volume, d, path);
+    });
+}
+
+int sl_gaussian_kernel(double sigma, double* taps, int64_t cap, int* size, int* center) {
+    return guard([&] {
+        const Taps2 t = gaussian_taps(sigma);
+        if (size) *size = static_cast<int>(t.n0);
+        if (center) *center = static_cast<int>(t.c0);
+        if (taps) {
+            if (cap < static_cast<int64_t>(t.v.size())) throw SlError(SL_ERR_INVALID, "gaussian_kernel: buffer too small");
+            std::memcpy(taps, t.v.data(), sizeof(double) * t.v.size());
+        }
+    });
+}
+
+int sl_binarize(const double* in, double* out, int64_t count, double delta) {
+    return guard([&] {
+        if (delta < 0.0) throw SlError(SL_ERR_DOMAIN, "binarize: delta must be >= 0");
+        if (!in || !out || count < 0) throw SlError(SL_ERR_INVALID, "null argument");
+        for (int64_t i = 0; i < count; ++i) out[i] = std::fabs(in[i]) >= delta ? 1.0 : 0.0;
+    });
+}
+
+namespace {
+// one-band blur system for the quality metrics, on `device`, with its own stream
+struct BlurRun {
+    sl_system h;
+    cudaStream_t st = nullptr;
+    BlurRun(int rows, int cols, const double* kernel, int kr, int kc, int kc0, int kc1, int device) {
+        if (rows < 1 || cols < 1) throw SlError(SL_ERR_SHAPE, "quality_q: empty grid");
+        if (!kernel || kr < 1 || kc < 1) throw SlError(SL_ERR_INVALID, "quality_q: empty blur kernel");
+        System& s = h.s;
+        s.ndim = 2;
+        s.n[0] = rows;
+        s.n[1] = cols;
+        s.device = device;
+        init_geometry(s);
+        Taps2 t = Taps2::zeros(static_cast<size_t>(kr), static_cast<size_t>(kc), kc0, kc1);
+        std::memcpy(t.v.data(), kernel, sizeof(double) * t.v.size());
+        SL_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        build_blur_2d(s, t, st);
+    }
+    ~BlurRun() {
+        if (st) cudaStreamDestroy(st);
+    }
+    QualityResult run(const double* rec, const double* truth, double d0, int nd, std::vector<double>* all) {
+        System& s = h.s;
+        return quality_run(
+            s, rec, truth, d0, nd,
+            [&](int n, auto&& fn) { fan_out(s, n, st, [&](int f, cudaStream_t fst) { fn(f, fst); }); }, st, all);
+    }
+};
+}  // namespace
+
+int sl_quality_q(int rows, int cols, const double* recovered, const double* truth, double delta, const double* kernel,
+                 int kr, int kc, int kc0, int kc1, int device, double* q) {
+    return guard([&] {
+        if (!recovered || !truth || !q) throw SlError(SL_ERR_INVALID, "null argument");
+        if (delta < 0.0) throw SlError(SL_ERR_DOMAIN, "binarize: delta must be >= 0");
+        DeviceGuard dg(device);
+        BlurRun b(rows, cols, kernel, kr, kc, kc0, kc1, device);
+        *q = b.run(recovered, truth, delta, 1, nullptr).q;
+    });
+}
+
+int sl_quality_q_opt(int rows, int cols, const double* recovered, const double* truth, const double* kernel, int kr,
+                     int kc, int kc0, int kc1, int device, double* q, int* best_delta, double* q_all) {
+    return guard([&] {
+        if (!recovered || !truth || !q || !best_delta) throw SlError(SL_ERR_INVALID, "null argument");
+        DeviceGuard dg(device);
+        BlurRun b(rows, cols, kernel, kr, kc, kc0, kc1, device);
+        std::vector<double> all;
+        const QualityResult r = b.run(recovered, truth, 0.0, 256, &all);
+        *q = r.q;
+        *best_delta = r.delta;
+        if (q_all) std::memcpy(q_all, all.data(), sizeof(double) * all.size());
     });
 }
 

@@ -42,3 +42,12 @@ def test_separate_matches_reference(cuda):
     r = P.separate(g["signal"], sd, si, cfg)
     assert rel_l2(r.curvilinear, g["curves"]) <= 1e-10
     assert rel_l2(r.blobs, g["blobs"]) <= 1e-10
+
+
+def test_inpaint_3d_matches_reference(cuda):
+    # Signal3D inpaint (apps.hpp:70-72) through the same device-resident loop
+    g = golden("it_inpaint3d32")
+    s = P.build_system_3d((32, 32, 32), P.ScaleProfile.from_levels(list(g["levels"])))
+    cfg = P.InpaintConfig(iterations=int(g["iterations"]), delta_min=float(g["delta_min"]))
+    out = P.inpaint(g["masked"], g["mask"], s, cfg)
+    assert rel_l2(out, g["out"]) <= 1e-10

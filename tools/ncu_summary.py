@@ -62,5 +62,43 @@ def launches(path, out):
     print(f"wrote {out}")
 
 
+# pass names bench.py reports -> kernel whose grid y counts the bands of a launch
+PASS_KERNEL = {"f2_rows_fused": "k2_rows_fused", "f3_rows_fused": "k2_rows_fused",
+               "f2_rows_c2r_thr": "k2_rows_c2r", "f3_axis1": "k3_lines_contig"}
+
+
+def traffic(rep, out, config):
+    """DRAM bytes per band of each pass's kernel from one `ncu --set full`
+    capture (cold caches: ncu flushes between replays), merged into the
+    JSON bench.py reads for roofline.traffic (profiles/traffic.json)."""
+    import json
+    import os
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    col = lambda r, name: float(r[h.index(name)].replace(",", "")) * scale.get(units[h.index(name)], 1)
+    per_kernel = {}
+    for r in rows[2:]:
+        k = r[h.index("Kernel Name")].split("<")[0].replace("void ", "")
+        gy = int(r[h.index("launch__grid_dim_y")])
+        b = col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum")
+        per_kernel.setdefault(k, []).append(b / max(gy, 1))
+    doc = json.load(open(out)) if os.path.exists(out) else {}
+    entry = {}
+    for pname, k in PASS_KERNEL.items():
+        if k in per_kernel and pname.startswith("f3" if config.startswith("3d") else "f2"):
+            v = per_kernel[k]
+            entry[pname] = {"dram_bytes_per_band": sum(v) / len(v), "launches_captured": len(v)}
+    entry["source"] = os.path.basename(rep)
+    doc[config] = entry
+    with open(out, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    print(f"wrote {out}: {config} {entry}")
+
+
 if __name__ == "__main__":
-    {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4])
+    else:
+        {"full": full, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])

@@ -8,7 +8,7 @@ dev = torch.device("cuda:0")
 s = P.build_system_3d((n, n, n), P.ScaleProfile.from_levels([1, 1, 2]), shard=(100, 112))
 f = torch.from_numpy(P.add_gaussian_noise(P.cartoon_volume(n), 40.0, 3)).to(dev)
 sch = P.ThresholdSchedule.defaults_3d(40.0)
-for _ in range(2):
+for _ in range(3):
     r = P.denoise(f, s, sch)
 torch.cuda.synchronize()
 print("ok", float(r.abs().sum()))
