@@ -230,6 +230,7 @@ def main():
     R_full = P.redundancy_3d(prof) if is3d else P.redundancy_2d(prof)
 
     # ---- work partition
+    nstreams = int(os.environ.get("SLB_STREAMS", "8"))
     if is3d:
         # shearlet-index sharding: contiguous balanced band ranges
         lo, hi = R_full * rank // world, R_full * (rank + 1) // world
@@ -238,7 +239,7 @@ def main():
         scaling = "strong" if world > 1 else "weak"
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
-        sysg.set_streams(int(os.environ.get("SLB_STREAMS", "8")))
+        sysg.set_streams(nstreams)
         if args.config == "2d1024x64":
             frames = cfg["batch"] // world  # fixed total batch sharded by image
             scaling = "strong"
@@ -251,7 +252,6 @@ def main():
     d_in = [torch.from_numpy(x).to(dev) for x in host_in]
     d_out = [torch.empty_like(x) for x in d_in]
     N = int(np.prod(dims))
-    stack = torch.empty((sysg.n_bands,) + tuple(dims), dtype=torch.float64, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
     stream_ptr = lambda: P._stream_ptr(local)  # noqa: E731
     K = np.ascontiguousarray(sch.per_scale_factors, dtype=np.float64)
@@ -272,16 +272,12 @@ def main():
             return
         for i in range(frames):
             x = d_in[i]
-            if world == 1:
-                # fused denoise (dec rows + threshold + rec rows in one pass), stack materialised
-                P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(d_out[i].data_ptr()),
-                                          Kp, len(K), float(sch.sigma), 1, stream_ptr()))
-                continue
-            dist.broadcast(x, src=0)
-            P._check(L.sl_sheardec_threshold_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(stack.data_ptr()),
-                                                 Kp, len(K), float(sch.sigma), 1, stream_ptr()))
-            P._check(L.sl_shearrec_dev(sysg.handle, C.c_void_p(stack.data_ptr()), sysg.n_bands,
-                                       C.c_void_p(d_out[i].data_ptr()), stream_ptr()))
+            if world > 1:
+                dist.broadcast(x, src=0)
+            # fused denoise of this rank's bands (dec rows + threshold + rec rows in one
+            # pass, stack materialised); on a shard the output is the partial reconstruction
+            P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(d_out[i].data_ptr()),
+                                      Kp, len(K), float(sch.sigma), 1, stream_ptr()))
             if world > 1:
                 dist.reduce(d_out[i], dst=0, op=dist.ReduceOp.SUM)
 
@@ -326,7 +322,7 @@ def main():
     torch.cuda.synchronize()
     stats = sysg.pass_stats()
     sysg.set_profiling(False)
-    sysg.set_streams(4)
+    sysg.set_streams(nstreams)
 
     # ---- end to end through the public API with host buffers (pinned)
     pinned_in = torch.from_numpy(np.stack(host_in)).pin_memory()
@@ -344,7 +340,7 @@ def main():
                 xd = pinned_in[i].to(dev, non_blocking=True)
                 if world > 1:
                     dist.broadcast(xd, src=0)
-                od = P.inverse(P.forward_thresholded(xd, sysg, sch), sysg)
+                od = P.denoise(xd, sysg, sch)
                 if world > 1:
                     dist.reduce(od, dst=0, op=dist.ReduceOp.SUM)
                 pinned_out[i].copy_(od)
@@ -389,7 +385,7 @@ def main():
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
                     "d2h_bytes_per_step": frames * N * 8,
-                    "api": ("sl_denoise_batch_host (pinned host in/out; H2D + batched dec/thr/rec + D2H)" if not is3d else "forward_thresholded + inverse with pinned H2D/D2H")},
+                    "api": ("sl_denoise_batch_host (pinned host in/out; per-frame H2D + fused dec/thr/rec + D2H over the handle's streams)" if not is3d else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:

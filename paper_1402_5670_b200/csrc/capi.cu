@@ -573,16 +573,24 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         s.io_in.alloc(n);
         s.io_out.alloc(n);
         cudaStream_t st = 0;
-        SL_CUDA(cudaMemcpyAsync(s.io_in.p, in, n * sizeof(double), cudaMemcpyHostToDevice, st));
         deltas(s, K, nK, sigma, scaled, st);
-        s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
-        if (!denoise_batch_mega(s, s.io_in.p, nframes, s.stack.p, s.io_out.p, s.delta.p, st))
+        if (mega2d_enabled(s)) {  // opt-in megakernel: whole batch in one launch
+            SL_CUDA(cudaMemcpyAsync(s.io_in.p, in, n * sizeof(double), cudaMemcpyHostToDevice, st));
+            s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
+            denoise_batch_mega(s, s.io_in.p, nframes, s.stack.p, s.io_out.p, s.delta.p, st);
+            SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        } else {
+            // per frame on its workspace stream: H2D -> fused denoise -> D2H, so one
+            // frame's copies overlap the other frames' kernels (both copy engines busy)
+            const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);
             fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+                const size_t off = static_cast<size_t>(fr) * s.nreal;
+                SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, fb, cudaMemcpyHostToDevice, fst));
                 s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-                denoise(s, s.io_in.p + static_cast<size_t>(fr) * s.nreal, s.w->stack.p,
-                        s.io_out.p + static_cast<size_t>(fr) * s.nreal, s.delta.p, fst);
+                denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, fst);
+                SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, fb, cudaMemcpyDeviceToHost, fst));
             });
-        SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+        }
         SL_CUDA(cudaStreamSynchronize(st));
     });
 }

@@ -168,3 +168,19 @@ def test_gpu_tap_construction_matches_host_taps(cuda, monkeypatch):
     np.testing.assert_allclose(dev.filter_norms, host.filter_norms, rtol=1e-14)
     for i in (0, 1, 20, 40, 75):
         assert np.abs(dev.filter_freq(i) - host.filter_freq(i)).max() <= 1e-14
+
+
+def test_sharded_denoise_partials_sum_to_full(cuda):
+    # denoise on a shard handle returns that shard's partial reconstruction
+    # (linear after the per-band threshold), so shards sum to the full denoise
+    import torch
+    prof = P.ScaleProfile.from_levels([0, 1])
+    full = P.build_system_3d((32, 32, 32), prof)
+    R = full.redundancy()
+    sch = P.ThresholdSchedule.defaults_3d(0.3, 2)
+    x = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, (32, 32, 32))).to(cuda)
+    want = P.denoise(x, full, sch).cpu().numpy()
+    got = np.zeros_like(want)
+    for lo, hi in ((0, R // 3), (R // 3, R - 5), (R - 5, R)):
+        got += P.denoise(x, P.build_system_3d((32, 32, 32), prof, shard=(lo, hi)), sch).cpu().numpy()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
