@@ -43,6 +43,12 @@ struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
     static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
     static constexpr int THREADS = V * T;
+#ifndef SLB_FUSED_MINB
+    // 192 (3D rows pass) would take ~124 registers -> 2 CTAs/SM; cap for 3
+    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 3 : 1;
+#else
+    static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
+#endif
 };
 template <int L>
 struct ColCfg {

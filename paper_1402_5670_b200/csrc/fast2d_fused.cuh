@@ -14,7 +14,7 @@
 namespace slb {
 
 template <int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS)
+__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
     k2_rows_fused(double2* __restrict__ inter, long long ibs, double* __restrict__ band, long long bbs, int n0, int H,
                   double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
