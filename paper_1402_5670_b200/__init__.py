@@ -338,9 +338,26 @@ class _System:
         return c.value
 
     def filter_freq(self, i: int) -> np.ndarray:
+        """psi_hat_i on the full grid (filters[i], system2d.hpp:38; filter_freq, system3d.cpp:144-186)."""
         out = np.zeros(self.shape + (2,))
         _check(lib().sl_filter_spectrum(self._h, int(i), _dp(out)))
         return out[..., 0] + 1j * out[..., 1]
+
+    def dual_freq(self, i: int) -> np.ndarray:
+        """psi_hat_i / W (dual_freq, system3d.cpp:188-195; duals()[i], system2d.cpp:128-148)."""
+        W = self.frame_weight
+        if W.min() < 1e-12:
+            raise SingularFrameError("duals: frame weight below 1e-12")
+        return self.filter_freq(i) / W
+
+    def duals(self):
+        """All dual spectra (system2d.hpp:45); materialised on request, R full complex grids."""
+        return [self.dual_freq(i) for i in range(self._R)]
+
+    @property
+    def filters(self):
+        """All filter spectra as full complex grids (system2d.hpp:38), materialised on request."""
+        return [self.filter_freq(i) for i in range(self._R)]
 
 
 class ShearletSystem2D(_System):

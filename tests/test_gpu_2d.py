@@ -292,3 +292,15 @@ def test_gpu_tap_construction_matches_host_taps(cuda, shape, levels, monkeypatch
     np.testing.assert_allclose(dev.filter_norms, host.filter_norms, rtol=1e-14)
     for i in range(dev.redundancy()):
         assert np.abs(dev.filter_freq(i) - host.filter_freq(i)).max() <= 1e-14
+
+
+def test_duals_match_oracle(cuda):
+    # duals() / dual_freq (system2d.cpp:128-148): psi_hat_i / W
+    g = golden("t2d_16_01_seed21")
+    s = P.build_system_2d(16, 16, P.ScaleProfile.from_levels([0, 1]))
+    o = O.build_system_2d(16, 16, [0, 1])
+    d = s.duals()
+    assert len(d) == s.redundancy() == len(s.filters)
+    for i in range(s.redundancy()):
+        assert np.abs(d[i] - o.filters[i] / o.frame_weight).max() < 1e-12
+    np.testing.assert_allclose(s.frame_weight, g["frame_weight"], rtol=1e-12)
