@@ -549,8 +549,6 @@ int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* ou
         DeviceGuard dg(s.device);
         cudaStream_t st = stream_of(stream);
         deltas(s, K, nK, sigma, scaled, st);
-        s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
-        if (denoise_batch_mega(s, in, nframes, s.stack.p, out, s.delta.p, st)) return;
         fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
             s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
             denoise(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal,
@@ -574,12 +572,7 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         s.io_out.alloc(n);
         cudaStream_t st = 0;
         deltas(s, K, nK, sigma, scaled, st);
-        if (mega2d_enabled(s)) {  // opt-in megakernel: whole batch in one launch
-            SL_CUDA(cudaMemcpyAsync(s.io_in.p, in, n * sizeof(double), cudaMemcpyHostToDevice, st));
-            s.stack.alloc(static_cast<size_t>(nframes) * s.nb() * s.nreal);
-            denoise_batch_mega(s, s.io_in.p, nframes, s.stack.p, s.io_out.p, s.delta.p, st);
-            SL_CUDA(cudaMemcpyAsync(out, s.io_out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
-        } else {
+        {
             // per frame on its workspace stream: H2D -> fused denoise -> D2H, so one
             // frame's copies overlap the other frames' kernels (both copy engines busy)
             const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);

@@ -198,7 +198,6 @@ struct System {
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
     cudaEvent_t fork_ev = nullptr;
     DBuf<double> delta, stack, io_in, io_out;
-    std::shared_ptr<void> mega;  // MegaState of the 2D megakernel (mega2d_host.cuh)
     int chunk = 1;
     std::mutex mu;
 

@@ -3,18 +3,9 @@
 #include "launch.cuh"
 #include "fast2d_host.cuh"
 #include "fast3d_host.cuh"
-#include "fast2d_p_host.cuh"
 #include "fast2d_fused.cuh"
-#include "mega2d_host.cuh"
 
 namespace slb {
-
-// one-tile-per-CTA 2D kernels by default (same speed as the persistent
-// pipelined variants in our measurements); SLB_FAST2D_V=2 selects fast2d_p.cuh
-static bool fast2d_persistent() {
-    const char* e = std::getenv("SLB_FAST2D_V");
-    return e && std::atoi(e) == 2;
-}
 
 // ------------------------------------------------------------------ thresholds
 // delta_i = K[scale - j0] * sigma (* RMS_i) for this handle's bands; -1 for the
@@ -100,10 +91,7 @@ static void rec_bands(System& s, const Filt& filt, const double* coeffs, double*
 
 static void dec(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
     if (s.fast2d) {
-        if (fast2d_persistent())
-            dec2d_fastp(s, f, out, delta, st);
-        else
-            dec2d_fast(s, f, out, delta, st);
+        dec2d_fast(s, f, out, delta, st);
         return;
     }
     if (s.fast3d) {
@@ -120,10 +108,7 @@ static void dec(System& s, const double* f, double* out, const double* delta, cu
 static void rec(System& s, const double* coeffs, double* out, cudaStream_t st) {
     if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
     if (s.fast2d) {
-        if (fast2d_persistent())
-            rec2d_fastp(s, coeffs, out, st);
-        else
-            rec2d_fast(s, coeffs, out, st);
+        rec2d_fast(s, coeffs, out, st);
         return;
     }
     if (s.fast3d) {
@@ -161,16 +146,5 @@ static void denoise(System& s, const double* f, double* stack, double* out, cons
     rec(s, stack, out, st);
 }
 
-// Batched denoise of nframes contiguous frames with per-frame stacks in
-// `stacks` ([nframes][nb][dims]). The 2D fast path runs one persistent
-// megakernel for the whole batch; otherwise frames go through denoise().
-static bool denoise_batch_mega(System& s, const double* in, int nframes, double* stacks, double* out,
-                               const double* delta, cudaStream_t st) {
-    if (!mega2d_enabled(s) || nframes < 1) return false;
-    if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-    if (!s.mega) s.mega = std::make_shared<MegaState>();
-    mega_denoise(s, *static_cast<MegaState*>(s.mega.get()), in, nframes, stacks, out, delta, st);
-    return true;
-}
 
 }  // namespace slb

@@ -271,7 +271,7 @@ def test_batched_api_matches_per_frame(cuda):
     torch.cuda.synchronize()
     for i in range(5):
         one = P.denoise(ft[i], s, sch)
-        # the batched path may sum bands in a different association (megakernel)
+        # batched frames use the concurrent band grouping (G), a different summation association
         assert (torch.linalg.norm(den_b[i] - one) / torch.linalg.norm(one)).item() <= 1e-12
         assert torch.equal(rec_b[i], one)
         assert torch.equal(dec_b[i], P.forward_thresholded(ft[i], s, sch))
