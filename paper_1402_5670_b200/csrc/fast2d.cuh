@@ -44,8 +44,10 @@ struct RowCfg {
     static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
     static constexpr int THREADS = V * T;
 #ifndef SLB_FUSED_MINB
-    // 192 (3D rows pass) would take ~124 registers -> 2 CTAs/SM; cap for 3
-    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 3 : 1;
+    // explicit occupancy targets: without them ptxas takes 124-154 registers for
+    // 192/512 (3 CTAs/SM fit in <= 85); the smaller plans fit 4 CTAs (<= 64);
+    // 2048 needs more registers (2 CTAs)
+    static constexpr int FUSED_MIN_BLOCKS = (L == 192 || L == 512) ? 3 : (L == 2048 ? 2 : 4);
 #else
     static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
 #endif
@@ -57,6 +59,21 @@ struct ColCfg {
     static constexpr int THREADS = LINES * T;
     static constexpr int MIN_BLOCKS = 65536 / (THREADS * 88) > 0 ? 65536 / (THREADS * 88) : 1;  // <= ~88 regs
 };
+
+// dynamic shared memory of the kernels (line buffers padded, LineBuf<L>)
+template <int L>
+static size_t row_smem_bytes(int H) {  // [H][2V] tile; V padded line buffers alias it
+    using RC = RowCfg<L>;
+    return std::max(static_cast<size_t>(2 * RC::V) * H, static_cast<size_t>(RC::V) * LineBuf<L, false>::N) * sizeof(double2);
+}
+template <int L>
+static size_t col1_smem_bytes() {  // one padded exchange buffer per line
+    return static_cast<size_t>(ColCfg<L>::LINES) * LineBuf<L>::N * sizeof(double2);
+}
+template <int L>
+static size_t col2_smem_bytes() {  // exchange buffer + a second L-line (F column / accumulator)
+    return static_cast<size_t>(ColCfg<L>::LINES) * (LineBuf<L>::N + L) * sizeof(double2);
+}
 
 // ---------------------------------------------------------------- rows c2r
 // In : src[k1 * n0 + r] (column-major half spectrum), bands strided by sbs.
@@ -105,8 +122,8 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     // the tile is dead once every line has gathered its inputs: the line
     // exchange buffers alias it (H*2V >= V*L), halving shared memory per CTA
     __syncthreads();
-    double2* lb = tile + q * L;
-    reg_fft<L, +1>(x, lb, t, tw);
+    double2* lb = tile + q * LineBuf<L, false>::N;
+    reg_fft<L, +1, false>(x, lb, t, tw);
     const double dl = delta ? delta[band0 + blockIdx.y] : -1.0;
     const int ra = r0 + 2 * q;
 #pragma unroll
@@ -144,19 +161,19 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
         const double b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : 0.0;
         x[m] = make_double2(a, b);
     }
-    double2* lb = tile + q * L;  // line buffers alias the (not yet used) output tile
-    reg_fft<L, -1>(x, lb, t, tw);
+    double2* lb = tile + q * LineBuf<L, false>::N;  // line buffers alias the (not yet used) output tile
+    reg_fft<L, -1, false>(x, lb, t, tw);
     // Z in registers (element t + T m); publish to the line buffer, then split
 #pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz(t + T * m)] = x[m];
+    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
     line_sync<T>();
     double2 zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            zk[u] = lb[swz(k)];
-            zm[u] = lb[swz(k == 0 ? 0 : L - k)];
+            zk[u] = lb[swz<false>(k)];
+            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
         }
     }
     __syncthreads();  // all line buffers read before the tile is written
@@ -190,8 +207,8 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * 2 * L;
-    double2* fs = sm + L;
+    double2* sm = lbuf + li * (LineBuf<L>::N + L);
+    double2* fs = sm + LineBuf<L>::N;
 #ifndef SLB_NO_CPASYNC
 #pragma unroll
     for (int m = 0; m < E; ++m) {
@@ -238,8 +255,8 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * 2 * L;
-    double2* acc = sm + L;  // thread t owns acc[t + T m]
+    double2* sm = lbuf + li * (LineBuf<L>::N + L);
+    double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
 #pragma unroll
     for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
     const int g0 = blockIdx.y * G;
@@ -280,7 +297,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * L;
+    double2* sm = lbuf + li * LineBuf<L>::N;
     double2 x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) x[m] = make_double2(0.0, 0.0);

@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         }
     }
     __syncthreads();              // every line has gathered: the tile is dead
-    double2* lb = tile + q * L;   // line buffers alias it (H*2V >= V*L)
-    reg_fft<L, +1>(x, lb, t, tw);
+    double2* lb = tile + q * LineBuf<L, false>::N;   // line buffers alias it (smem sized for both)
+    reg_fft<L, +1, false>(x, lb, t, tw);
     const double dl = delta[band0 + blockIdx.y];
     const int ra = r0 + 2 * q;
 #pragma unroll
@@ -70,17 +70,17 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
         x[m] = make_double2(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : 0.0);  // rec input: the thresholded rows
     }
-    reg_fft<L, -1>(x, lb, t, tw);
+    reg_fft<L, -1, false>(x, lb, t, tw);
 #pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz(t + T * m)] = x[m];
+    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
     line_sync<T>();
     double2 zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            zk[u] = lb[swz(k)];
-            zm[u] = lb[swz(k == 0 ? 0 : L - k)];
+            zk[u] = lb[swz<false>(k)];
+            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
         }
     }
     __syncthreads();  // all line buffers read before the tile is rewritten
@@ -117,15 +117,16 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     const double2* tw1 = s.plan(L1, st).tw;
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
-    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    const size_t row_smem = row_smem_bytes<L1>(H);
+    const size_t col_smem = col1_smem_bytes<L0>();
+    const size_t col2_smem = col2_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_rows_fused<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);
     set_smem(k2_cols_sum<L0, +1>, col_smem);
-    set_smem(k2_cols_dec<L0>, 2 * col_smem);
-    set_smem(k2_cols_rec<L0>, 2 * col_smem);
+    set_smem(k2_cols_dec<L0>, col2_smem);
+    set_smem(k2_cols_rec<L0>, col2_smem);
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     {
@@ -145,7 +146,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
         const int groups = (cb + cfg.G - 1) / cfg.G;
         {
             LaunchScope ls(s, "f2_cols_dec", st, cb);
-            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
                 s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0);
             check_launch("k2_cols_dec");
         }
@@ -158,7 +159,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, cb);
-            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
                 s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0);
             check_launch("k2_cols_rec");
         }

@@ -52,12 +52,13 @@ static void dec2d_fast_t(System& s, const double* f, double* out, const double* 
     const double2* tw1 = s.plan(L1, st).tw;
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
-    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    const size_t row_smem = row_smem_bytes<L1>(H);
+    const size_t col_smem = col1_smem_bytes<L0>();
+    const size_t col2_smem = col2_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);
-    set_smem(k2_cols_dec<L0>, 2 * col_smem);
+    set_smem(k2_cols_dec<L0>, col2_smem);
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     {  // F^T = FFT_0(FFT_1(f))
@@ -76,7 +77,7 @@ static void dec2d_fast_t(System& s, const double* f, double* out, const double* 
         const int groups = (cb + cfg.G - 1) / cfg.G;
         {
             LaunchScope ls(s, "f2_cols_dec", st, cb);
-            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
                 s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0);
             check_launch("k2_cols_dec");
         }
@@ -104,11 +105,12 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
     const double2* tw1 = s.plan(L1, st).tw;
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
-    const size_t col_smem = static_cast<size_t>(CC::LINES) * L0 * sizeof(double2);
+    const size_t row_smem = row_smem_bytes<L1>(H);
+    const size_t col_smem = col1_smem_bytes<L0>();
+    const size_t col2_smem = col2_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
-    set_smem(k2_cols_rec<L0>, 2 * col_smem);
+    set_smem(k2_cols_rec<L0>, col2_smem);
     set_smem(k2_cols_sum<L0, +1>, col_smem);
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
@@ -124,7 +126,7 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, cb);
-            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, 2 * col_smem, st>>>(
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
                 s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0);
             check_launch("k2_cols_rec");
         }

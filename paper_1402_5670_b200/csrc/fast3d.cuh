@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS)
     double2 x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(d + t + T * m) : make_double2(0.0, 0.0);
-    reg_fft<L, DIR>(x, lbuf + li * L, t, tw);
+    reg_fft<L, DIR, false>(x, lbuf + li * LineBuf<L, false>::N, t, tw);
     if (valid) {
 #pragma unroll
         for (int m = 0; m < E; ++m) __stcg(d + t + T * m, x[m]);
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
     const double2* s = src + ((long long)k2 * n + k1) * n;
-    double2* lb = tile + li * L;  // line exchange buffers alias the output tile
+    double2* lb = tile + li * LineBuf<L, false>::N;  // line exchange buffers alias the output tile
     for (int bb = 0; bb < gn; ++bb) {
         BandDesc3D bd{};
         if (MODE == kAx0DecMul) bd = filt.bands[band0 + g0 + bb];
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
             x[m] = z;
         }
         if (bb > 0) __syncthreads();  // previous band's tile fully written out
-        reg_fft<L, DIR>(x, lb, t, tw);
+        reg_fft<L, DIR, false>(x, lb, t, tw);
         __syncthreads();              // every line's FFT is done with the aliased buffers
         // publish into the [i0][v] tile, then write 128-byte rotated runs
 #pragma unroll
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
     const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = k1_0 + li;
-    double2* lb = tile + li * L;  // line exchange buffers alias the input tile (after the gather)
+    double2* lb = tile + li * LineBuf<L, false>::N;  // line exchange buffers alias the input tile (after the gather)
     if (MODE != kAx0RecAcc) {
         src += blockIdx.y * sbs;
         dst += blockIdx.y * dbs;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
     const int nb = MODE == kAx0RecAcc ? nbands : 1;
     // RecAcc: per-thread accumulator slots after the tile (acc[li][t + T m]),
     // registers stay free for the FFT line
-    double2* acc = tile + V * L + li * L;
+    double2* acc = tile + V * LineBuf<L, false>::N + li * L;
     if (MODE == kAx0RecAcc) {
 #pragma unroll
         for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
 #pragma unroll
         for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
-        reg_fft<L, DIR>(x, lb, t, tw);
+        reg_fft<L, DIR, false>(x, lb, t, tw);
         if (MODE == kAx0RecAcc) {
             const BandDesc3D bd = filt.bands[band0 + b];
 #pragma unroll

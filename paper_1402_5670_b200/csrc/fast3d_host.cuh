@@ -40,9 +40,9 @@ struct Fast3DLaunch {
         H = s.H;
         nT = static_cast<long long>(H) * n * n;
         tw = s.plan(n, st).tw;
-        row_smem = static_cast<size_t>(2 * RC::V) * H * sizeof(double2);  // line buffers alias the tile
-        col_smem = static_cast<size_t>(CC::LINES) * n * sizeof(double2);
-        ax_smem = static_cast<size_t>(AC::V) * n * sizeof(double2);  // tile; line buffers alias it
+        row_smem = row_smem_bytes<n>(H);
+        col_smem = static_cast<size_t>(CC::LINES) * LineBuf<n, false>::N * sizeof(double2);
+        ax_smem = static_cast<size_t>(AC::V) * LineBuf<n, false>::N * sizeof(double2);  // [n][V] tile; line buffers alias it
         row_blocks = (n * n + 2 * RC::V - 1) / (2 * RC::V);
         line_blocks = static_cast<int>((static_cast<long long>(H) * n + CC::LINES - 1) / CC::LINES);
         ax_blocks = H * (n / AC::V);
@@ -88,7 +88,7 @@ struct Fast3DLaunch {
     }
     template <int DIR, int MODE>
     void from_rot(const double2* src, double2* dst, int nb, int band0, int accumulate, const char* nm) {
-        const size_t smem = MODE == kAx0RecAcc ? 2 * ax_smem : ax_smem;
+        const size_t smem = MODE == kAx0RecAcc ? ax_smem + static_cast<size_t>(AC::V) * n * sizeof(double2) : ax_smem;
         set_smem(k3_ax0_from_rot<n, DIR, MODE>, smem);
         LaunchScope ls(s, nm, st, nb);
         if (MODE == kAx0RecAcc) {

@@ -61,7 +61,23 @@ constexpr int plan_ns(int s) {
     return ns;
 }
 
-__device__ __forceinline__ int swz(int e) { return e ^ ((e >> 3) & 7); }
+// Line exchange buffers are padded by one slot per 8 elements: e -> e + e/8.
+// Stockham stores (stride NS, or 8 consecutive elements per thread) and loads
+// (stride L/R) are then bank-conflict free for 16-byte accesses, and every
+// address is a per-thread base plus a compile-time offset (no per-access XOR).
+// The rows kernels keep the unpadded XOR swizzle (PAD = false): their line
+// buffers alias a staging tile sized for L-element lines, and measured faster.
+template <bool PAD = true>
+__device__ __forceinline__ int swz(int e) {
+    if constexpr (PAD)
+        return e + (e >> 3);
+    else
+        return e ^ ((e >> 3) & 7);
+}
+template <int L, bool PAD = true>
+struct LineBuf {
+    static constexpr int N = PAD ? L + L / 8 : L;  // double2 slots per line buffer
+};
 
 template <int T>
 __device__ __forceinline__ void line_sync() {
@@ -170,7 +186,7 @@ __device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
     for (int r = 0; r < R; ++r) x[q + B * r] = v[r];
 }
 
-template <int L, int DIR, int S>
+template <int L, int DIR, int S, bool PAD>
 struct RegStage {
     using P = RegPlan<L>;
     static constexpr int R = P::R[S];
@@ -206,7 +222,7 @@ struct RegStage {
                 const int jm = j % NS;
                 const int base = (j - jm) * R + jm;
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[swz(base + r * NS)] = x[q + B * r];
+                for (int r = 0; r < R; ++r) sm[swz<PAD>(base + r * NS)] = x[q + B * r];
             }
             line_sync<T>();
             constexpr int R2 = P::R[S + 1];
@@ -215,19 +231,19 @@ struct RegStage {
             for (int q = 0; q < B2; ++q) {
                 const int j = t + T * q;
 #pragma unroll
-                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz(j + r * (L / R2))];
+                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD>(j + r * (L / R2))];
             }
             line_sync<T>();
-            RegStage<L, DIR, S + 1>::run(x, sm, t, tw);
+            RegStage<L, DIR, S + 1, PAD>::run(x, sm, t, tw);
         }
     }
 };
 
 // In/out: x[m] = element t + T*m of the line. sm: the line's L-element buffer.
-template <int L, int DIR>
+template <int L, int DIR, bool PAD = true>
 __device__ __forceinline__ void reg_fft(double2 (&x)[RegPlan<L>::E], double2* sm, int t,
                                         const double2* __restrict__ tw) {
-    RegStage<L, DIR, 0>::run(x, sm, t, tw);
+    RegStage<L, DIR, 0, PAD>::run(x, sm, t, tw);
 }
 
 }  // namespace slb
