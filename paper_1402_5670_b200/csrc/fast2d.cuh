@@ -44,10 +44,10 @@ struct RowCfg {
     static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
     static constexpr int THREADS = V * T;
 #ifndef SLB_FUSED_MINB
-    // explicit occupancy targets: without them ptxas takes 124-154 registers for
-    // 192/512 (3 CTAs/SM fit in <= 85); the smaller plans fit 4 CTAs (<= 64);
-    // 2048 needs more registers (2 CTAs)
-    static constexpr int FUSED_MIN_BLOCKS = (L == 192 || L == 512) ? 3 : (L == 2048 ? 2 : 4);
+    // explicit occupancy targets (measured): without them ptxas takes 124-154
+    // registers; 4 CTAs/SM (<= 64 registers) except 192 (3: E = 12 needs more)
+    // and 2048 (2)
+    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 3 : (L == 2048 ? 2 : 4);
 #else
     static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
 #endif
@@ -57,7 +57,11 @@ struct ColCfg {
     static constexpr int T = RegPlan<L>::T;
     static constexpr int LINES = (128 / T) > 0 ? 128 / T : 1;
     static constexpr int THREADS = LINES * T;
+#ifndef SLB_COL_MINB
     static constexpr int MIN_BLOCKS = 65536 / (THREADS * 88) > 0 ? 65536 / (THREADS * 88) : 1;  // <= ~88 regs
+#else
+    static constexpr int MIN_BLOCKS = SLB_COL_MINB;
+#endif
 };
 
 // dynamic shared memory of the kernels (line buffers padded, LineBuf<L>)
