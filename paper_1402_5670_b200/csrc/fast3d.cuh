@@ -32,11 +32,24 @@ struct Ax0Cfg {
     static constexpr int V = SLB_AX0_V;
 #endif
     static constexpr int THREADS = V * T;
+    // occupancy targets (CTAs/SM, measured at 128^3 / 192^3; overridable for A/B builds)
+#ifndef SLB_AX0_MINB
+    static constexpr int TO_MIN_BLOCKS = 6;                 // N -> R (<= 85 registers)
+    static constexpr int FROM_MIN_BLOCKS = L <= 128 ? 4 : 5;  // R -> N
+#else
+    static constexpr int TO_MIN_BLOCKS = SLB_AX0_MINB;
+    static constexpr int FROM_MIN_BLOCKS = SLB_AX0_MINB;
+#endif
+#ifndef SLB_LINES_MINB
+    static constexpr int LINES_MIN_BLOCKS = 5;
+#else
+    static constexpr int LINES_MIN_BLOCKS = SLB_LINES_MINB;
+#endif
 };
 
 // ---------------------------------------------------------------- axis 1 (contiguous lines, in place)
 template <int L, int DIR>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCKS)
     k3_lines_contig(double2* __restrict__ data, long long bstride, long long nlines, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
     extern __shared__ double2 lbuf[];
@@ -66,7 +79,7 @@ enum Ax0Mode : int {
 // goes to R[(k2*n + i0)*n + k1], staged through the tile so each i0 writes V
 // consecutive k1 (a 128-byte run).
 template <int L, int DIR, int MODE>
-__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     k3_ax0_to_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int H,
                   FiltSynth3D filt, int band0, int G, int nb, const double* __restrict__ WN,
                   const double2* __restrict__ tw) {
@@ -127,7 +140,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREAD
 // (acc (+)= sum; deterministic, independent of the stream count). Other modes:
 // one spectrum per blockIdx.y.
 template <int L, int DIR, int MODE>
-__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, 65536 / (Ax0Cfg<L>::THREADS * 96))
+__global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS)
     k3_ax0_from_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int nbands,
                     FiltSynth3D filt, int band0, int accumulate, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
