@@ -3,6 +3,7 @@
 #include "fast2d_host.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
+#include "fast3d_plane.cuh"
 
 namespace slb {
 
@@ -67,6 +68,22 @@ struct Fast3DLaunch {
         k2_rows_fused<n><<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(
             inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
         check_launch("k2_rows_fused");
+    }
+    // axis1<+1> + rows_fused + axis1<-1> as one plane pass on 2-CTA clusters
+    // (fast3d_plane.cuh); n = 128 / 192 (a 256 plane needs > 2 SMs of smem)
+    static constexpr bool kPlane = n == 128 || n == 192;
+    static bool plane_enabled() {
+        const char* e = std::getenv("SLB_PLANE3");
+        return kPlane && e && std::atoi(e) == 1;
+    }
+    void plane_fused(double2* inter, double* band, long long bbs, int nb, const double* delta, int band0) {
+        if constexpr (kPlane) {
+            set_smem(k3_plane_fused<n>, PlaneCfg<n>::SMEM);
+            LaunchScope ls(s, "f3_plane_fused", st, nb);
+            k3_plane_fused<n><<<dim3(2 * n, nb), PlaneCfg<n>::THREADS, PlaneCfg<n>::SMEM, st>>>(
+                inter, nT, band, bbs, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
+            check_launch("k3_plane_fused");
+        }
     }
     template <int DIR>
     void axis1(double2* data, int nb) {
@@ -158,9 +175,13 @@ static void denoise3d_fast_t(System& s, const double* f, double* stack, double* 
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         K.template to_rot<+1, kAx0DecMul>(s.w->F.p, 0, s.w->inter.p, cb, s.lo + b0, nullptr, "f3_ax0_dec");
-        K.template axis1<+1>(s.w->inter.p, cb);
-        K.rows_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
-        K.template axis1<-1>(s.w->inter.p, cb);
+        if (Fast3DLaunch<n>::plane_enabled()) {
+            K.plane_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+        } else {
+            K.template axis1<+1>(s.w->inter.p, cb);
+            K.rows_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+            K.template axis1<-1>(s.w->inter.p, cb);
+        }
         K.template from_rot<-1, kAx0RecAcc>(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, "f3_ax0_rec");
     }
     K.template to_rot<+1, kAx0DivW>(s.w->acc.p, 0, s.w->inter.p, 1, 0, s.WN.p, "f3_ax0_final");

@@ -184,3 +184,17 @@ def test_sharded_denoise_partials_sum_to_full(cuda):
     for lo, hi in ((0, R // 3), (R // 3, R - 5), (R - 5, R)):
         got += P.denoise(x, P.build_system_3d((32, 32, 32), prof, shard=(lo, hi)), sch).cpu().numpy()
     assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [128, 192])
+def test_plane_fused_matches_pass_by_pass(cuda, n, monkeypatch):
+    # k3_plane_fused (2-CTA cluster, plane on chip) == axis1 + rows_fused + axis1
+    import torch
+    s = P.build_system_3d((n, n, n), P.ScaleProfile.from_levels([0, 1]))
+    sch = P.ThresholdSchedule.defaults_3d(0.3, 2)
+    x = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, (n, n, n))).to(cuda)
+    monkeypatch.setenv("SLB_PLANE3", "0")
+    want = P.denoise(x, s, sch).cpu().numpy()
+    monkeypatch.setenv("SLB_PLANE3", "1")
+    got = P.denoise(x, s, sch).cpu().numpy()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-13
