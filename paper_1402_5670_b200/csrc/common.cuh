@@ -198,6 +198,7 @@ struct System {
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
     cudaEvent_t fork_ev = nullptr;
     DBuf<double> delta, stack, io_in, io_out;
+    std::vector<double> delta_host;  // host copy of `delta` (deltas() skips unchanged uploads)
     int chunk = 1;
     std::mutex mu;
 
