@@ -58,7 +58,8 @@ struct ColCfg {
     static constexpr int LINES = (128 / T) > 0 ? 128 / T : 1;
     static constexpr int THREADS = LINES * T;
 #ifndef SLB_COL_MINB
-    static constexpr int MIN_BLOCKS = 65536 / (THREADS * 88) > 0 ? 65536 / (THREADS * 88) : 1;  // <= ~88 regs
+    // measured: 4 CTAs/SM (<= 128 registers) beats 5 (<= 102) for the column passes
+    static constexpr int MIN_BLOCKS = 65536 / (THREADS * 128) > 0 ? 65536 / (THREADS * 128) : 1;
 #else
     static constexpr int MIN_BLOCKS = SLB_COL_MINB;
 #endif
@@ -228,15 +229,25 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
 #endif
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
+    // psi of band b+1 is loaded while band b is in the FFT
+    double p[E];
+    {
+        const double* ps = psiT + (long long)(band0 + g0) * pbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) p[m] = (valid && gn > 0) ? __ldg(ps + t + T * m) : 0.0;
+    }
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
-        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
         double2 x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double p = valid ? __ldg(ps + t + T * m) : 0.0;
             const double2 fv = fs[t + T * m];
-            x[m] = make_double2(fv.x * p, fv.y * p);  // conj(psi) * F, psi real
+            x[m] = make_double2(fv.x * p[m], fv.y * p[m]);  // conj(psi) * F, psi real
+        }
+        if (bb + 1 < gn) {
+            const double* ps = psiT + (long long)(band0 + b + 1) * pbs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
         }
         reg_fft<L, +1>(x, sm, t, tw);
         if (valid) {
@@ -267,18 +278,21 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     const int gn = min(G, nb - g0);
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
-        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
         double2 x[E];
+        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
 #pragma unroll
         for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : make_double2(0.0, 0.0);
-        reg_fft<L, -1>(x, sm, t, tw);
+        // the band's psi is loaded before the FFT so its latency overlaps it
+        double p[E];
         const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
 #pragma unroll
+        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
+        reg_fft<L, -1>(x, sm, t, tw);
+#pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double p = valid ? __ldg(ps + t + T * m) : 0.0;
             double2 a = acc[t + T * m];
-            a.x = fma(x[m].x, p, a.x);
-            a.y = fma(x[m].y, p, a.y);
+            a.x = fma(x[m].x, p[m], a.x);
+            a.y = fma(x[m].y, p[m], a.y);
             acc[t + T * m] = a;
         }
         line_sync<T>();
