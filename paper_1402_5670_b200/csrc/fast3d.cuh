@@ -34,7 +34,7 @@ struct Ax0Cfg {
     static constexpr int THREADS = V * T;
     // occupancy targets (CTAs/SM, measured at 128^3 / 192^3; overridable for A/B builds)
 #ifndef SLB_AX0_MINB
-    static constexpr int TO_MIN_BLOCKS = 6;                 // N -> R (<= 85 registers)
+    static constexpr int TO_MIN_BLOCKS = L <= 128 ? 4 : 6;    // N -> R (192: <= 85 registers)
     static constexpr int FROM_MIN_BLOCKS = L <= 128 ? 4 : 5;  // R -> N
 #else
     static constexpr int TO_MIN_BLOCKS = SLB_AX0_MINB;
@@ -101,6 +101,16 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     const int k1 = k1_0 + li;
     const double2* s = src + ((long long)k2 * n + k1) * n;
     double2* lb = tile + li * LineBuf<L, false>::N;  // line exchange buffers alias the output tile
+    // L <= 128 (measured): the next band's filter values are synthesised while
+    // this band is in the FFT (DecMul) / before the FFT (RecAcc); at 192 the
+    // extra registers cost more than the latency they hide
+    constexpr bool PF = L <= 128;
+    double pn[E];
+    if (PF && MODE == kAx0DecMul) {
+        const BandDesc3D bd = filt.bands[band0 + g0];
+#pragma unroll
+        for (int m = 0; m < E; ++m) pn[m] = filt.get_d(bd, t + T * m, k1, k2);
+    }
     for (int bb = 0; bb < gn; ++bb) {
         BandDesc3D bd{};
         if (MODE == kAx0DecMul) bd = filt.bands[band0 + g0 + bb];
@@ -110,13 +120,18 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
             const int k0 = t + T * m;
             double2 z = MODE == kAx0DecMul ? __ldg(s + k0) : __ldcg(s + k0);
             if (MODE == kAx0DecMul) {
-                const double p = filt.get_d(bd, k0, k1, k2);
+                const double p = PF ? pn[m] : filt.get_d(bd, k0, k1, k2);
                 z = make_double2(z.x * p, z.y * p);
             } else if (MODE == kAx0DivW) {
                 const double w = __ldg(WN + ((long long)k2 * n + k1) * n + k0);
                 z = make_double2(z.x / w, z.y / w);
             }
             x[m] = z;
+        }
+        if (PF && MODE == kAx0DecMul && bb + 1 < gn) {
+            const BandDesc3D bn = filt.bands[band0 + g0 + bb + 1];
+#pragma unroll
+            for (int m = 0; m < E; ++m) pn[m] = filt.get_d(bn, t + T * m, k1, k2);
         }
         if (bb > 0) __syncthreads();  // previous band's tile fully written out
         reg_fft<L, DIR, false>(x, lb, t, tw);
@@ -177,17 +192,25 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
 #pragma unroll
         for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
+        constexpr bool PF = L <= 128;  // see k3_ax0_to_rot
+        double p[E];  // this band's filter values, synthesised before the FFT
+        if (PF && MODE == kAx0RecAcc) {
+            const BandDesc3D bd = filt.bands[band0 + b];
+#pragma unroll
+            for (int m = 0; m < E; ++m) p[m] = filt.get_d(bd, t + T * m, k1, k2);
+        }
         reg_fft<L, DIR, false>(x, lb, t, tw);
         if (MODE == kAx0RecAcc) {
             const BandDesc3D bd = filt.bands[band0 + b];
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const double p = filt.get_d(bd, t + T * m, k1, k2);
+                const double p_ = PF ? p[m] : filt.get_d(bd, t + T * m, k1, k2);
                 double2 a = acc[t + T * m];
-                a.x = fma(x[m].x, p, a.x);
-                a.y = fma(x[m].y, p, a.y);
+                a.x = fma(x[m].x, p_, a.x);
+                a.y = fma(x[m].y, p_, a.y);
                 acc[t + T * m] = a;
             }
+            (void)bd;
         }
     }
     double2* d = dst + ((long long)k2 * n + k1) * n;
