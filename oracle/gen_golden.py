@@ -188,6 +188,18 @@ def gen_quality():
     save("quality_q", **out)
 
 
+def gen_acceptance():
+    """acceptance.cpp criterion 7 (173-191): 256^2 cartoon, sigma 30, seed 11;
+    SL2D_2 vs the separable system ([0,0,0,0], impulse fan), PSNRs from the reference."""
+    img = ref.cartoon(256)
+    noisy = ref.add_noise(img, 30.0, 11)
+    K = [2.5, 2.5, 2.5, 3.8]
+    sl2 = ref.RefSystem2D(256, 256, [1, 1, 2, 2])
+    swt = ref.RefSystem2D(256, 256, [0, 0, 0, 0], impulse_fan=True)
+    save("acceptance_c7", p_noisy=ref.psnr(img, noisy), p_sl2=ref.psnr(img, sl2.denoise(noisy, K, 30.0)),
+         p_swt=ref.psnr(img, swt.denoise(noisy, K, 30.0)))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
@@ -252,6 +264,7 @@ def main():
     gen_io()
     gen_descriptors()
     gen_quality()
+    gen_acceptance()
     if a.big:
         # cfg4: cartoon_volume(128), [1,1]
         gen_3d("cfg4_cartoonvol128_11", (128, 128, 128), [1, 1], ref.cartoon_volume(128))
