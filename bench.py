@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
+FP64_PEAK_TFLOPS = 34.0  # measured: tools/fp64_peak.cu (DFMA loop, 64 FMA/clk/SM at 1965 MHz)
 
 CONFIGS = {
     # name: (dims, levels, schedule kind, sigma, frames per step per rank, seed base)
@@ -83,6 +84,15 @@ def algorithmic_bytes(cfg, R, frames):
     if len(dims) == 2:
         return frames * (16 * N + 16 * R * N + 16 * R * Nh)
     return frames * (16 * N + 16 * R * N + 8 * Nh)
+
+
+def algorithmic_flops(cfg, R):
+    """(2R+2) real-input FFTs at 2.5 N log2 N plus 14 flops per
+    half-spectrum point per band (conj-multiply + multiply-add), per frame."""
+    dims = cfg["dims"]
+    N = int(np.prod(dims))
+    Nh = N // dims[-1] * (dims[-1] // 2 + 1)
+    return (2 * R + 2) * 2.5 * N * np.log2(N) + R * Nh * 14
 
 
 # ------------------------------------------------------------------ clocks
@@ -385,6 +395,13 @@ def main():
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "path_roofline": {"bytes_per_unit": nbytes, "achieved": path_gbs, "frac": path_gbs / peak,
                               "note": "whole dec+thr+rec step: compulsory HBM bytes / device time"},
+            "fp64": {"flops_per_unit": algorithmic_flops(cfg, R),
+                     "achieved_tflops": algorithmic_flops(cfg, R) * (1.0 / world if is3d else frames)
+                     / (ms_step / 1000.0) / 1e12,
+                     "peak_tflops": FP64_PEAK_TFLOPS,
+                     "frac": algorithmic_flops(cfg, R) * (1.0 / world if is3d else frames) / (ms_step / 1000.0)
+                     / 1e12 / FP64_PEAK_TFLOPS,
+                     "note": "per GPU; SURVEY 8(d) flop count; peak measured by tools/fp64_peak.cu"},
             "kernels": {k: {"ms_total": v[0], "launches": v[1], "bands": v[2]} for k, v in sorted(stats.items())},
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
