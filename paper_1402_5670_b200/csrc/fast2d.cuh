@@ -259,63 +259,14 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     }
 }
 
-// rec: slot[g] = sum_{b in group g} FFT_0(inter[b]) * psi_b.
-template <int L>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
-    k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
-                double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
-                const double2* __restrict__ tw) {
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
-    extern __shared__ double2 lbuf[];  // per line: [exchange L][accumulator L]
-    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
-    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
-    const bool valid = k1 < H;
-    double2* sm = lbuf + li * (LineBuf<L>::N + L);
-    double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
-#pragma unroll
-    for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
-    const int g0 = blockIdx.y * G;
-    const int gn = min(G, nb - g0);
-    for (int bb = 0; bb < gn; ++bb) {
-        const int b = g0 + bb;
-        double2 x[E];
-        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
-#pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : make_double2(0.0, 0.0);
-        // the band's psi is loaded before the FFT so its latency overlaps it
-        double p[E];
-        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
-#pragma unroll
-        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
-        reg_fft<L, -1>(x, sm, t, tw);
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            double2 a = acc[t + T * m];
-            a.x = fma(x[m].x, p[m], a.x);
-            a.y = fma(x[m].y, p[m], a.y);
-            acc[t + T * m] = a;
-        }
-        line_sync<T>();
-    }
-    if (valid) {
-        double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
-#pragma unroll
-        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, acc[t + T * m]);
-    }
-}
-
-// final rec column pass: IFFT_0((sum_s slot[s]) / W) -> out; also the plain
-// forward column FFT (F = FFT_0 of the rows pass) when W == nullptr && DIR < 0.
+// final rec column pass for one line: IFFT_0((sum_s slot[s]) / W) -> out; also
+// the plain forward column FFT (F = FFT_0 of the rows pass) when W == nullptr &&
+// DIR < 0. Slots are summed in index order (deterministic).
 template <int L, int DIR>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS)
-    k2_cols_sum(const double2* __restrict__ slots, long long sbs, int nslots, const double* __restrict__ WT,
-                double2* __restrict__ out, int H, const double2* __restrict__ tw) {
+__device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots, long long sbs, int nslots,
+                                              const double* __restrict__ WT, double2* __restrict__ out, int k1,
+                                              bool valid, double2* sm, int t, const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
-    extern __shared__ double2 lbuf[];
-    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
-    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
-    const bool valid = k1 < H;
-    double2* sm = lbuf + li * LineBuf<L>::N;
     double2 x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) x[m] = make_double2(0.0, 0.0);
@@ -353,6 +304,79 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS)
 #pragma unroll
         for (int m = 0; m < E; ++m) __stcg(o + t + T * m, x[m]);
     }
+}
+
+// rec: slot[g] = sum_{b in group g} FFT_0(inter[b]) * psi_b.
+template <int L>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
+    k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
+                double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
+                const double2* __restrict__ tw, int* __restrict__ done, int nslots, const double* __restrict__ WT,
+                double2* __restrict__ fout) {
+    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    extern __shared__ double2 lbuf[];  // per line: [exchange L][accumulator L]
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
+    const bool valid = k1 < H;
+    double2* sm = lbuf + li * (LineBuf<L>::N + L);
+    double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
+#pragma unroll
+    for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
+    const int g0 = blockIdx.y * G;
+    const int gn = min(G, nb - g0);
+    for (int bb = 0; bb < gn; ++bb) {
+        const int b = g0 + bb;
+        double2 x[E];
+        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : make_double2(0.0, 0.0);
+        // the band's psi is loaded before the FFT so its latency overlaps it
+        double p[E];
+        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
+        reg_fft<L, -1>(x, sm, t, tw);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            double2 a = acc[t + T * m];
+            a.x = fma(x[m].x, p[m], a.x);
+            a.y = fma(x[m].y, p[m], a.y);
+            acc[t + T * m] = a;
+        }
+        line_sync<T>();
+    }
+    if (valid) {
+        double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, acc[t + T * m]);
+    }
+    if (done == nullptr) return;
+    // last chunk: the CTA that finishes its column block last sums every slot
+    // (in slot order, as k2_cols_sum), divides by W and runs the final IFFT_0,
+    // so the reconstruction needs no separate sum launch
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int prev = atomicAdd(done + blockIdx.x, 1);
+        last = prev == static_cast<int>(gridDim.y) - 1;
+        if (last) done[blockIdx.x] = 0;  // reset for the next call on this workspace
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    cols_sum_line<L, +1>(slots, sbs, nslots, WT, fout, k1, valid, sm, t, tw);
+}
+
+template <int L, int DIR>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS)
+    k2_cols_sum(const double2* __restrict__ slots, long long sbs, int nslots, const double* __restrict__ WT,
+                double2* __restrict__ out, int H, const double2* __restrict__ tw) {
+    constexpr int T = RegPlan<L>::T;
+    extern __shared__ double2 lbuf[];
+    const int li = threadIdx.x / T, t = threadIdx.x - li * T;
+    const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
+    cols_sum_line<L, DIR>(slots, sbs, nslots, WT, out, k1, k1 < H, lbuf + li * LineBuf<L>::N, t, tw);
 }
 
 }  // namespace slb

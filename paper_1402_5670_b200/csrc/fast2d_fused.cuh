@@ -129,6 +129,10 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     set_smem(k2_cols_rec<L0>, col2_smem);
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
+    if (s.w->done.n < static_cast<size_t>(col_blocks)) {  // zeroed once; the kernel resets its counters
+        s.w->done.alloc(static_cast<size_t>(col_blocks));
+        SL_CUDA(cudaMemsetAsync(s.w->done.p, 0, static_cast<size_t>(col_blocks) * sizeof(int), st));
+    }
     {
         LaunchScope ls(s, "f2_rows_r2c", st, 1);
         k2_rows_r2c<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(f, 0, s.w->inter.p, 0, n0, H, tw1);
@@ -159,17 +163,14 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, cb);
+            // the last chunk's CTAs also finish the reconstruction (k2_cols_rec)
+            const bool fin = b0 + cb >= nb;
             k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
-                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0);
+                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
+                fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p);
             check_launch("k2_cols_rec");
         }
         slot0 += groups;
-    }
-    {
-        LaunchScope ls(s, "f2_cols_final", st, 1);
-        k2_cols_sum<L0, +1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->slots.p, nhT, nslots, s.WT.p,
-                                                                        s.w->inter.p, H, tw0);
-        check_launch("k2_cols_sum");
     }
     {
         LaunchScope ls(s, "f2_rows_c2r", st, 1);
