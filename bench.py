@@ -455,7 +455,7 @@ def pass_bytes(name, dims):
         "f2_rows_fused": 16 * Nh + 8 * N + 16 * Nh,  # half read, thresholded band write, rec half write
         "f3_rows_fused": 16 * Nh + 8 * N + 16 * Nh,
         "f2_cols_dec": 8 * Nh + 16 * Nh,          # real psi + half write (F re-reads hit L2)
-        "f2_cols_rec": 16 * Nh + 8 * Nh,          # half read + real psi (slot writes amortised)
+        "f2_cols_rec": 16 * Nh + 8 * Nh,          # half read + real psi (slot writes / final sum amortised)
         "f2_cols_fwd": 32 * Nh,
         "f2_cols_final": 32 * Nh + 8 * Nh,
         # fast 3D path (fast3d.cuh); psi synthesised from L2-resident tables
