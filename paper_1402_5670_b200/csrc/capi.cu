@@ -492,6 +492,29 @@ void fan_out(System& s, int nframes, cudaStream_t user, Fn&& per_frame) {
         SL_CUDA(cudaStreamWaitEvent(user, wk.ev, 0));
     }
 }
+// Lock-step 2D batches (fast2d_fused.cuh denoise2d_fast_batch): all frames of
+// a group pass through each kernel together on one stream. SLB_LOCKSTEP=0
+// restores the per-frame fan-out over the workspace streams.
+bool lockstep_batch(const System& s, int nframes) {
+    const char* e = std::getenv("SLB_LOCKSTEP");
+    return s.fast2d && nframes > 1 && (e ? std::atoi(e) != 0 : true) && !std::getenv("SLB_DENOISE_UNFUSED");
+}
+void denoise_lockstep(System& s, const double* in, int nframes, double* out, cudaStream_t st) {
+    if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+    const int group = std::max(1, std::min(nframes, env_int("SLB_LOCKSTEP_FRAMES", 2)));
+    const int ngroups = (nframes + group - 1) / group;
+    const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
+    // groups spread over the workspace streams like single frames
+    fan_out(s, ngroups, st, [&](int g, cudaStream_t fst) {
+        const int f0 = g * group, nf = std::min(group, nframes - f0);
+        const size_t off = static_cast<size_t>(f0) * s.nreal;
+        s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+        const int conc = s.concurrency;
+        s.concurrency = std::max(conc, 4);  // full-machine band grouping (fast2d_cfg)
+        denoise2d_fast_batch(s, in + off, s.nreal, nf, s.w->stack.p, sfs, out + off, s.nreal, s.delta.p, fst);
+        s.concurrency = conc;
+    });
+}
 }  // namespace
 extern "C" {
 
@@ -549,6 +572,10 @@ int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* ou
         DeviceGuard dg(s.device);
         cudaStream_t st = stream_of(stream);
         deltas(s, K, nK, sigma, scaled, st);
+        if (lockstep_batch(s, nframes)) {
+            denoise_lockstep(s, in, nframes, out, st);
+            return;
+        }
         fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
             s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
             denoise(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal,

@@ -206,7 +206,9 @@ template <int L>
 __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     k2_cols_dec(const double2* __restrict__ FT, const double* __restrict__ psiT, long long pbs,
                 double2* __restrict__ inter, long long ibs, int H, int band0, int G, int nb,
-                const double2* __restrict__ tw) {
+                const double2* __restrict__ tw, long long fzs = 0, long long izs = 0) {
+    FT += blockIdx.z * fzs;  // blockIdx.z: frame of a lock-step batch
+    inter += blockIdx.z * izs;
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
     extern __shared__ double2 lbuf[];  // per line: [exchange L][F column L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
@@ -312,7 +314,11 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
                 double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
                 const double2* __restrict__ tw, int* __restrict__ done, int nslots, const double* __restrict__ WT,
-                double2* __restrict__ fout) {
+                double2* __restrict__ fout, long long izs = 0, long long szs = 0, long long fozs = 0) {
+    inter += blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
+    slots += blockIdx.z * szs;
+    fout += blockIdx.z * fozs;
+    if (done) done += blockIdx.z * gridDim.x;
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
     extern __shared__ double2 lbuf[];  // per line: [exchange L][accumulator L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
@@ -371,7 +377,10 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
 template <int L, int DIR>
 __global__ void __launch_bounds__(ColCfg<L>::THREADS)
     k2_cols_sum(const double2* __restrict__ slots, long long sbs, int nslots, const double* __restrict__ WT,
-                double2* __restrict__ out, int H, const double2* __restrict__ tw) {
+                double2* __restrict__ out, int H, const double2* __restrict__ tw, long long szs = 0,
+                long long ozs = 0) {
+    slots += blockIdx.z * szs;  // blockIdx.z: frame of a lock-step batch
+    out += blockIdx.z * ozs;
     constexpr int T = RegPlan<L>::T;
     extern __shared__ double2 lbuf[];
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;

@@ -16,13 +16,14 @@ namespace slb {
 template <int L>
 __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
     k2_rows_fused(double2* __restrict__ inter, long long ibs, double* __restrict__ band, long long bbs, int n0, int H,
-                  double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
+                  double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw,
+                  long long izs = 0, long long bzs = 0) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;
     extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
-    inter += blockIdx.y * ibs;
-    band += blockIdx.y * bbs;
+    inter += blockIdx.y * ibs + blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
+    band += blockIdx.y * bbs + blockIdx.z * bzs;
     const int nrows = min(2 * V, n0 - r0);
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
@@ -178,6 +179,97 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
                                                                             nullptr, 0, tw1);
         check_launch("k2_rows_c2r");
     }
+}
+
+// Lock-step batch: nf frames advance through the same passes together, one
+// launch per pass covering every frame (blockIdx.z), so each band's psi is read
+// once from HBM for all frames (L2 hits for the rest) and launches/tails are
+// amortised over the batch. Per-frame stacks at stack + f * sfs.
+template <int L0, int L1>
+static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, int nf, double* stack, long long sfs,
+                                   double* out, long long ofs, const double* delta, cudaStream_t st) {
+    const int n0 = s.n[0], H = s.H;
+    const long long nhT = static_cast<long long>(H) * n0;
+    const Fast2DCfg cfg = fast2d_cfg(s);
+    const int nb = s.nb();
+    const int C = std::min(cfg.C, nb);
+    const long long izs = static_cast<long long>(C) * nhT;
+    s.w->inter.alloc(static_cast<size_t>(nf) * izs);
+    s.w->F.alloc(static_cast<size_t>(nf) * nhT);
+    int nslots = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) nslots += (std::min(C, nb - b0) + cfg.G - 1) / cfg.G;
+    const long long szs = static_cast<long long>(nslots) * nhT;
+    s.w->slots.alloc(static_cast<size_t>(nf) * szs);
+    const double2* tw0 = s.plan(L0, st).tw;
+    const double2* tw1 = s.plan(L1, st).tw;
+    using RC = RowCfg<L1>;
+    using CC = ColCfg<L0>;
+    const size_t row_smem = row_smem_bytes<L1>(H);
+    const size_t col_smem = col1_smem_bytes<L0>();
+    const size_t col2_smem = col2_smem_bytes<L0>();
+    set_smem(k2_rows_r2c<L1>, row_smem);
+    set_smem(k2_rows_c2r<L1>, row_smem);
+    set_smem(k2_rows_fused<L1>, row_smem);
+    set_smem(k2_cols_sum<L0, -1>, col_smem);
+    set_smem(k2_cols_dec<L0>, col2_smem);
+    set_smem(k2_cols_rec<L0>, col2_smem);
+    const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
+    const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
+    const size_t ndone = static_cast<size_t>(col_blocks) * nf;
+    if (s.w->done.n < ndone) {  // zeroed once; the kernel resets its counters
+        s.w->done.alloc(ndone);
+        SL_CUDA(cudaMemsetAsync(s.w->done.p, 0, ndone * sizeof(int), st));
+    }
+    {  // F^T of every frame
+        LaunchScope ls(s, "f2_rows_r2c", st, nf);
+        k2_rows_r2c<L1><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(f, ffs, s.w->inter.p, izs, n0, H, tw1);
+        check_launch("k2_rows_r2c");
+    }
+    {
+        LaunchScope ls(s, "f2_cols_fwd", st, nf);
+        k2_cols_sum<L0, -1><<<dim3(col_blocks, 1, nf), CC::THREADS, col_smem, st>>>(s.w->inter.p, 0, 1, nullptr,
+                                                                                  s.w->F.p, H, tw0, izs, nhT);
+        check_launch("k2_cols_sum");
+    }
+    const double scale = 1.0 / static_cast<double>(s.nreal);
+    int slot0 = 0;
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        const int groups = (cb + cfg.G - 1) / cfg.G;
+        {
+            LaunchScope ls(s, "f2_cols_dec", st, static_cast<long long>(cb) * nf);
+            k2_cols_dec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, col2_smem, st>>>(
+                s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0, nhT, izs);
+            check_launch("k2_cols_dec");
+        }
+        {
+            LaunchScope ls(s, "f2_rows_fused", st, static_cast<long long>(cb) * nf);
+            k2_rows_fused<L1><<<dim3(row_blocks, cb, nf), RC::THREADS, row_smem, st>>>(
+                s.w->inter.p, nhT, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, n0, H, scale, delta,
+                s.lo + b0, tw1, izs, sfs);
+            check_launch("k2_rows_fused");
+        }
+        {
+            LaunchScope ls(s, "f2_cols_rec", st, static_cast<long long>(cb) * nf);
+            const bool fin = b0 + cb >= nb;
+            k2_cols_rec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, col2_smem, st>>>(
+                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
+                fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p, izs, szs, izs);
+            check_launch("k2_cols_rec");
+        }
+        slot0 += groups;
+    }
+    {
+        LaunchScope ls(s, "f2_rows_c2r", st, nf);
+        k2_rows_c2r<L1><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(s.w->inter.p, izs, out, ofs, n0, H,
+                                                                             scale, nullptr, 0, tw1);
+        check_launch("k2_rows_c2r");
+    }
+}
+
+static void denoise2d_fast_batch(System& s, const double* f, long long ffs, int nf, double* stack, long long sfs,
+                                 double* out, long long ofs, const double* delta, cudaStream_t st) {
+    SLB_FAST2D_DISPATCH(denoise2d_fast_batch_t, s, f, ffs, nf, stack, sfs, out, ofs, delta, st)
 }
 
 static void denoise2d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
