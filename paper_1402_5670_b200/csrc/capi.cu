@@ -499,9 +499,10 @@ bool lockstep_batch(const System& s, int nframes) {
     const char* e = std::getenv("SLB_LOCKSTEP");
     return s.fast2d && nframes > 1 && (e ? std::atoi(e) != 0 : true) && !std::getenv("SLB_DENOISE_UNFUSED");
 }
+int lockstep_group(int nframes) { return std::max(1, std::min(nframes, env_int("SLB_LOCKSTEP_FRAMES", 2))); }
 void denoise_lockstep(System& s, const double* in, int nframes, double* out, cudaStream_t st) {
     if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-    const int group = std::max(1, std::min(nframes, env_int("SLB_LOCKSTEP_FRAMES", 2)));
+    const int group = lockstep_group(nframes);
     const int ngroups = (nframes + group - 1) / group;
     const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
     // groups spread over the workspace streams like single frames
@@ -600,15 +601,30 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         cudaStream_t st = 0;
         deltas(s, K, nK, sigma, scaled, st);
         {
-            // per frame on its workspace stream: H2D -> fused denoise -> D2H, so one
-            // frame's copies overlap the other frames' kernels (both copy engines busy)
-            const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);
-            fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
-                const size_t off = static_cast<size_t>(fr) * s.nreal;
-                SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, fb, cudaMemcpyHostToDevice, fst));
-                s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-                denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, fst);
-                SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, fb, cudaMemcpyDeviceToHost, fst));
+            // per frame (or lock-step frame group) on its workspace stream: H2D ->
+            // fused denoise -> D2H, so one group's copies overlap the other groups'
+            // kernels (both copy engines busy)
+            const int group = lockstep_batch(s, nframes) ? lockstep_group(nframes) : 1;
+            if (group > 1 && s.Wmin < 1e-12)
+                throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+            const int ngroups = (nframes + group - 1) / group;
+            const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
+            fan_out(s, ngroups, st, [&](int g, cudaStream_t fst) {
+                const int f0 = g * group, nf = std::min(group, nframes - f0);
+                const size_t off = static_cast<size_t>(f0) * s.nreal;
+                const size_t bytes = static_cast<size_t>(nf) * s.nreal * sizeof(double);
+                SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, bytes, cudaMemcpyHostToDevice, fst));
+                s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+                if (group > 1) {
+                    const int conc = s.concurrency;
+                    s.concurrency = std::max(conc, 4);
+                    denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.w->stack.p, sfs, s.io_out.p + off,
+                                         s.nreal, s.delta.p, fst);
+                    s.concurrency = conc;
+                } else {
+                    denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, fst);
+                }
+                SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, bytes, cudaMemcpyDeviceToHost, fst));
             });
         }
         SL_CUDA(cudaStreamSynchronize(st));
