@@ -41,7 +41,11 @@ __device__ __forceinline__ int tslot(int k, int rr) {
 template <int L>
 struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
+#ifndef SLB_ROW_THREADS
     static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
+#else
+    static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
+#endif
     static constexpr int THREADS = V * T;
 #ifndef SLB_FUSED_MINB
     // explicit occupancy targets (measured): without them ptxas takes 124-154
