@@ -42,16 +42,17 @@ template <int L>
 struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
 #ifndef SLB_ROW_THREADS
-    static constexpr int V = (256 / T) > 0 ? 256 / T : 1;
+    // 256 threads; 192 (the 3D rows pass) measured faster with 128 at 6 CTAs/SM
+    static constexpr int V = ((L == 192 ? 128 : 256) / T) > 0 ? (L == 192 ? 128 : 256) / T : 1;
 #else
     static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
 #endif
     static constexpr int THREADS = V * T;
 #ifndef SLB_FUSED_MINB
     // explicit occupancy targets (measured): without them ptxas takes 124-154
-    // registers; 4 CTAs/SM (<= 64 registers) except 192 (3: E = 12 needs more)
-    // and 2048 (2)
-    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 3 : (L == 2048 ? 2 : 4);
+    // registers; 4 CTAs/SM (<= 64 registers) except 192 (6 CTAs of 128 threads,
+    // <= 85 registers) and 2048 (2)
+    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 6 : (L == 2048 ? 2 : 4);
 #else
     static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
 #endif
