@@ -437,7 +437,8 @@ def pass_bytes(name, dims):
     the current multi-pass design."""
     N = int(np.prod(dims))
     Nh = N // dims[-1] * (dims[-1] // 2 + 1)
-    G3 = int(os.environ.get("SLB_G3", "16"))  # 3D band group (csrc/fast3d_host.cuh)
+    # 3D band group (csrc/fast3d_host.cuh fast3d_group): ~6 GB of rotated intermediate, >= 16
+    G3 = int(os.environ.get("SLB_G3", "0")) or max(16, int(6 * 2 ** 30 / (16 * Nh)))
     return None if name == "none" else {
         # generic path
         "rows_c2r_thr": 16 * Nh + 8 * N,          # intermediate read + band write, per band

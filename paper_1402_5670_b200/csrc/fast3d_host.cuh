@@ -19,7 +19,17 @@ static bool fast3d_supported(const int* n) {
 // bands per chunk: the rotated intermediate of a chunk stays around 64 MiB,
 // but at least SLB_G3 bands so the axis-0 passes can share F / the accumulator
 // RMW across a band group.
-static int fast3d_group(const System&) { return env_int("SLB_G3", 16); }
+// Larger groups measured faster all the way up (fewer, larger launches; F and
+// the accumulator touched once per group): take as many bands as ~6 GB of
+// rotated intermediate allows (192^3: ~100 bands, 128^3: all 99), split across
+// the frames in flight, at least 16.
+static int fast3d_group(const System& s) {
+    const char* e = std::getenv("SLB_G3");
+    if (e) return std::max(1, std::atoi(e));
+    const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
+    const double budget = 6.0 * 1024 * 1024 * 1024 / std::max(1, s.concurrency);
+    return std::max(1, std::min(s.nb(), std::max(16, static_cast<int>(budget / per))));
+}
 static int fast3d_chunk(const System& s) {
     const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
     return env_int("SLB_CHUNK3", std::max(fast3d_group(s), static_cast<int>((64.0 * 1024 * 1024) / per)));
