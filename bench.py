@@ -250,7 +250,7 @@ def main():
         lo, hi = R_full * rank // world, R_full * (rank + 1) // world
         sysg = P.build_system_3d(dims, prof, device=local, shard=(lo, hi) if world > 1 else None)
         frames = 1
-        scaling = "strong" if world > 1 else "weak"
+        scaling = "strong"  # one volume per step whatever the rank count
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
         sysg.set_streams(nstreams)
