@@ -604,7 +604,11 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             // per frame (or lock-step frame group) on its workspace stream: H2D ->
             // fused denoise -> D2H, so one group's copies overlap the other groups'
             // kernels (both copy engines busy)
-            const int group = lockstep_batch(s, nframes) ? lockstep_group(nframes) : 1;
+            // single frames measured better here than lock-step pairs: the first
+            // H2D and the last D2H are one frame each (SLB_LOCKSTEP_HOST=1: pairs)
+            const char* lh = std::getenv("SLB_LOCKSTEP_HOST");
+            const bool lock = lh && std::atoi(lh) != 0;
+            const int group = (lock && lockstep_batch(s, nframes)) ? lockstep_group(nframes) : 1;
             if (group > 1 && s.Wmin < 1e-12)
                 throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
             const int ngroups = (nframes + group - 1) / group;
