@@ -1,5 +1,6 @@
-# A/B of the host batch path with / without lock-step frame pairs (e2e probe, 3 rounds)
+# A/B of a host batch path switch (env VAR in {0,1}) with the e2e probe, 3 rounds
+VAR=${VAR:-SLB_HOST_PRIO}
 for r in 1 2 3; do for v in 0 1; do
-  SLB_LOCKSTEP_HOST=$v timeout 120 python tools/e2e_probe.py 8 > /tmp/e2e_$v.txt 2>&1
-  echo "host_lockstep=$v $(head -1 /tmp/e2e_$v.txt)"
+  env $VAR=$v timeout 120 python tools/e2e_probe.py 8 > /tmp/e2e_$v.txt 2>&1
+  echo "$VAR=$v $(head -2 /tmp/e2e_$v.txt | tr '\n' ' ')"
 done; done
