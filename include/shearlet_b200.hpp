@@ -12,6 +12,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "shearlet_b200.h"
@@ -28,6 +29,7 @@ struct FormatError : Error { using Error::Error; };
 struct SingularFrameError : Error { using Error::Error; };
 struct UnsupportedSizeError : Error { using Error::Error; };
 struct DegenerateMaskError : Error { using Error::Error; };
+struct DegenerateTruthError : Error { using Error::Error; };
 struct CudaError : Error { using Error::Error; };
 
 inline void check(int rc) {
@@ -42,6 +44,7 @@ inline void check(int rc) {
         case SL_ERR_ASSET: throw AssetError(m);
         case SL_ERR_FORMAT: throw FormatError(m);
         case SL_ERR_DEGENERATE_MASK: throw DegenerateMaskError(m);
+        case SL_ERR_DEGENERATE_TRUTH: throw DegenerateTruthError(m);
         case SL_ERR_CUDA: throw CudaError(m);
         default: throw Error(m);
     }
@@ -233,6 +236,85 @@ inline std::vector<double> deserialize(const std::vector<unsigned char>& bytes, 
     std::vector<double> c(s.n_bands() * s.size());
     check(sl_shcf_deserialize(s.handle(), bytes.data(), bytes.size(), c.data(), static_cast<int>(s.n_bands())));
     return c;
+}
+
+// System descriptors (descriptor.hpp:12-39): write_descriptor(describe(s)) text, rebuild from text
+inline std::string describe(const ShearletSystem& s) {
+    std::size_t n = 0;
+    check(sl_describe(s.handle(), nullptr, 0, &n));
+    std::string t(n + 1, '\0');
+    check(sl_describe(s.handle(), t.data(), t.size(), &n));
+    t.resize(n);
+    return t;
+}
+inline ShearletSystem build_from_descriptor(const std::string& text, int device = 0) {
+    sl_system* h = nullptr;
+    check(sl_system_create_from_descriptor(text.c_str(), 0, device, 0, -1, &h));
+    return ShearletSystem(h);
+}
+
+// Signal files (image_io.hpp:9-24)
+struct PgmImage {
+    std::vector<double> pixels;  // rows x cols, axis 0 = image rows
+    int rows = 0, cols = 0, maxval = 255;
+};
+inline PgmImage load_pgm(const std::string& path) {
+    PgmImage im;
+    check(sl_load_pgm(path.c_str(), nullptr, 0, &im.rows, &im.cols, &im.maxval));
+    im.pixels.resize(static_cast<std::size_t>(im.rows) * im.cols);
+    check(sl_load_pgm(path.c_str(), im.pixels.data(), static_cast<int64_t>(im.pixels.size()), nullptr, nullptr,
+                      nullptr));
+    return im;
+}
+inline void save_pgm(const std::vector<double>& pixels, int rows, int cols, const std::string& path,
+                     int maxval = 255) {
+    if (pixels.size() != static_cast<std::size_t>(rows) * cols) throw ShapeError("save_pgm: pixel count");
+    check(sl_save_pgm(pixels.data(), rows, cols, path.c_str(), maxval));
+}
+inline std::vector<double> load_svol(const std::string& path, std::array<std::size_t, 3>* dims) {
+    int64_t d[3] = {0, 0, 0};
+    check(sl_load_svol(path.c_str(), nullptr, 0, d));
+    std::vector<double> v(static_cast<std::size_t>(d[0] * d[1] * d[2]));
+    check(sl_load_svol(path.c_str(), v.data(), static_cast<int64_t>(v.size()), d));
+    if (dims) *dims = {static_cast<std::size_t>(d[0]), static_cast<std::size_t>(d[1]), static_cast<std::size_t>(d[2])};
+    return v;
+}
+inline void save_svol(const std::vector<double>& v, std::array<std::size_t, 3> dims, const std::string& path) {
+    if (v.size() != dims[0] * dims[1] * dims[2]) throw ShapeError("save_svol: sample count");
+    const int64_t d[3] = {static_cast<int64_t>(dims[0]), static_cast<int64_t>(dims[1]), static_cast<int64_t>(dims[2])};
+    check(sl_save_svol(v.data(), d, path.c_str()));
+}
+
+// Separation quality (apps.hpp:86-101): Gaussian taps (size x size, centre) and Q / Q_opt
+struct GaussianKernel {
+    std::vector<double> taps;
+    int size = 0, center = 0;
+};
+inline GaussianKernel gaussian_kernel(double sigma_pixels = 2.0) {
+    GaussianKernel g;
+    check(sl_gaussian_kernel(sigma_pixels, nullptr, 0, &g.size, &g.center));
+    g.taps.resize(static_cast<std::size_t>(g.size) * g.size);
+    check(sl_gaussian_kernel(sigma_pixels, g.taps.data(), static_cast<int64_t>(g.taps.size()), nullptr, nullptr));
+    return g;
+}
+inline double quality_q(const std::vector<double>& recovered, const std::vector<double>& truth, int rows, int cols,
+                        double delta, const GaussianKernel& g, int device = 0) {
+    if (recovered.size() != truth.size() || recovered.size() != static_cast<std::size_t>(rows) * cols)
+        throw ShapeError("quality_q: dimension mismatch");
+    double q = 0.0;
+    check(sl_quality_q(rows, cols, recovered.data(), truth.data(), delta, g.taps.data(), g.size, g.size, g.center,
+                       g.center, device, &q));
+    return q;
+}
+inline std::pair<double, int> quality_q_opt(const std::vector<double>& recovered, const std::vector<double>& truth,
+                                            int rows, int cols, const GaussianKernel& g, int device = 0) {
+    if (recovered.size() != truth.size() || recovered.size() != static_cast<std::size_t>(rows) * cols)
+        throw ShapeError("quality_q_opt: dimension mismatch");
+    double q = 0.0;
+    int d = 0;
+    check(sl_quality_q_opt(rows, cols, recovered.data(), truth.data(), g.taps.data(), g.size, g.size, g.center,
+                           g.center, device, &q, &d, nullptr));
+    return {q, d};
 }
 
 }  // namespace shearlet_b200

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <string>
 
 #include "shearlet_b200.hpp"
 
@@ -59,6 +60,21 @@ int main() {
         d2 += g[i] * g[i];
     }
     if (!(std::sqrt(n2 / d2) <= 1e-10)) { std::printf("custom bank round trip %g\n", std::sqrt(n2 / d2)); ++fails; }
+    // descriptor round trip, SVOL round trip, Q_opt of an exact recovery
+    const std::string text = describe(sys);
+    auto sys3 = build_from_descriptor(text);
+    if (describe(sys3) != text || sys3.redundancy() != sys.redundancy()) { std::printf("descriptor\n"); ++fails; }
+    std::vector<double> vol(8 * 9 * 10);
+    for (double& x : vol) x = static_cast<double>(rng() % 1000) / 7.0;
+    save_svol(vol, {8, 9, 10}, "/tmp/api_smoke.svol");
+    std::array<std::size_t, 3> vd{};
+    if (load_svol("/tmp/api_smoke.svol", &vd) != vol || vd[2] != 10) { std::printf("svol\n"); ++fails; }
+    std::vector<double> truth(64 * 64, 0.0);
+    for (int i = 20; i < 30; ++i) truth[static_cast<std::size_t>(i) * 64 + 32] = 1.0;
+    std::vector<double> recovered(truth.size());
+    for (std::size_t i = 0; i < truth.size(); ++i) recovered[i] = 200.0 * truth[i];
+    const auto [qmin, dbest] = quality_q_opt(recovered, truth, 64, 64, gaussian_kernel(2.0));
+    if (!(qmin < 1e-12) || dbest != 1) { std::printf("q_opt %g %d\n", qmin, dbest); ++fails; }
     std::printf("cpp api: err %.2e R %zu A %.6f B %.6f fails %d\n", err, sys.redundancy(), A, B, fails);
     return fails;
 }
