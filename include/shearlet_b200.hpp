@@ -223,6 +223,33 @@ inline std::vector<double> denoise(const std::vector<double>& noisy, const Shear
     return out;
 }
 
+// Iterative thresholding (apps.hpp:46-90): the whole loop runs on the device
+struct InpaintConfig {
+    int iterations = 100;
+    double delta_init = -1.0;  // < 0: the largest (RMS-scaled) coefficient of the input
+    double delta_min = 0.01;
+    bool scale_by_filter_norm = true;
+};
+inline std::vector<double> inpaint(const std::vector<double>& masked, const std::vector<double>& mask,
+                                   const ShearletSystem& s, const InpaintConfig& c = InpaintConfig()) {
+    if (masked.size() != s.size() || mask.size() != s.size()) throw ShapeError("inpaint: dims do not match the system");
+    std::vector<double> out(s.size());
+    check(sl_inpaint_host(s.handle(), masked.data(), mask.data(), out.data(), c.iterations, c.delta_init, c.delta_min,
+                          c.scale_by_filter_norm));
+    return out;
+}
+struct SeparationResult {
+    std::vector<double> curvilinear, blobs;
+};
+inline SeparationResult separate(const std::vector<double>& signal, const ShearletSystem& directional,
+                                 const ShearletSystem& isotropic, const InpaintConfig& c = InpaintConfig()) {
+    if (signal.size() != directional.size()) throw ShapeError("separate: dims do not match the system");
+    SeparationResult r{std::vector<double>(signal.size()), std::vector<double>(signal.size())};
+    check(sl_separate_host(directional.handle(), isotropic.handle(), signal.data(), r.curvilinear.data(),
+                           r.blobs.data(), c.iterations, c.delta_init, c.delta_min, c.scale_by_filter_norm));
+    return r;
+}
+
 // SHCF coefficient files (transform.hpp:39-52): bytes of serialize() / deserialize_2d/3d
 inline std::vector<unsigned char> serialize(const std::vector<double>& coeffs, const ShearletSystem& s) {
     if (coeffs.size() != s.n_bands() * s.size()) throw ShapeError("serialize: stack does not match the system");

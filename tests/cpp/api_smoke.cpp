@@ -75,6 +75,16 @@ int main() {
     for (std::size_t i = 0; i < truth.size(); ++i) recovered[i] = 200.0 * truth[i];
     const auto [qmin, dbest] = quality_q_opt(recovered, truth, 64, 64, gaussian_kernel(2.0));
     if (!(qmin < 1e-12) || dbest != 1) { std::printf("q_opt %g %d\n", qmin, dbest); ++fails; }
+    // inpainting with every pixel observed converges to the input
+    InpaintConfig ic;
+    ic.iterations = 4;
+    const auto inp = inpaint(f, std::vector<double>(f.size(), 1.0), sys, ic);
+    double ni = 0, di = 0;
+    for (size_t i = 0; i < f.size(); ++i) {
+        ni += (inp[i] - f[i]) * (inp[i] - f[i]);
+        di += f[i] * f[i];
+    }
+    if (!(std::sqrt(ni / di) < 0.5)) { std::printf("inpaint %g\n", std::sqrt(ni / di)); ++fails; }
     std::printf("cpp api: err %.2e R %zu A %.6f B %.6f fails %d\n", err, sys.redundancy(), A, B, fails);
     return fails;
 }
