@@ -244,7 +244,7 @@ def main():
     R_full = P.redundancy_3d(prof) if is3d else P.redundancy_2d(prof)
 
     # ---- work partition
-    nstreams = int(os.environ.get("SLB_STREAMS", "8"))
+    nstreams = int(os.environ.get("SLB_STREAMS", "6"))
     if is3d:
         # shearlet-index sharding: contiguous balanced band ranges
         lo, hi = R_full * rank // world, R_full * (rank + 1) // world

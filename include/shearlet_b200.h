@@ -136,7 +136,7 @@ int sl_denoise_dev(sl_system* sys, const double* in, double* out, const double* 
 /* ---- batched hot path (device pointers) ----------------------------------
  * nframes independent signals, contiguous [nframes][dims]; stacks
  * [nframes][nbands][dims]. Frames are spread over up to sl_set_streams()
- * internal streams (default 4) that fork from and join back into `stream`,
+ * internal streams (default 6) that fork from and join back into `stream`,
  * so concurrent frames overlap on the GPU; results are identical to
  * per-frame calls. sl_sheardec_batch_dev thresholds when K != NULL. */
 int sl_set_streams(sl_system* sys, int nstreams);
