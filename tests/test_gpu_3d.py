@@ -216,3 +216,19 @@ def test_batched_api_3d(cuda):
         assert (torch.linalg.norm(den[i] - one) / torch.linalg.norm(one)).item() <= 1e-12
         assert (torch.linalg.norm(rec[i] - one) / torch.linalg.norm(one)).item() <= 1e-12
         assert np.linalg.norm(host[i] - one.cpu().numpy()) <= 1e-12 * np.linalg.norm(host[i])
+
+
+def test_largest_specialised_sizes_round_trip(cuda):
+    # the largest fast-path grids: 2048^2 (2D) and 256^3 (3D); sigma 0 denoise == identity
+    import torch
+    for shape, lv in (((2048, 2048), [0, 1, 1]), ((256, 256, 256), [0, 1])):
+        prof = P.ScaleProfile.from_levels(lv)
+        s = P.build_system_2d(*shape, prof) if len(shape) == 2 else P.build_system_3d(shape, prof)
+        f = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, shape)).to(cuda)
+        r = P.inverse(P.forward(f, s), s)
+        sch = (P.ThresholdSchedule.defaults_2d if len(shape) == 2 else P.ThresholdSchedule.defaults_3d)(0.0, len(lv))
+        d = P.denoise(f, s, sch)
+        assert (torch.linalg.norm(r - f) / torch.linalg.norm(f)).item() <= 1e-10
+        assert (torch.linalg.norm(d - f) / torch.linalg.norm(f)).item() <= 1e-10
+        del s, r, d
+        torch.cuda.empty_cache()
