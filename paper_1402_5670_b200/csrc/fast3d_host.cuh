@@ -1,5 +1,7 @@
 // Host orchestration of the specialised 3D path (kernels in fast3d.cuh).
 #pragma once
+#include <cudaTypedefs.h>
+
 #include "fast2d_host.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
@@ -33,6 +35,33 @@ static int fast3d_group(const System& s) {
 static int fast3d_chunk(const System& s) {
     const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
     return env_int("SLB_CHUNK3", std::max(fast3d_group(s), static_cast<int>((64.0 * 1024 * 1024) / per)));
+}
+
+// Tensor map over a rotated buffer R[band][k2][i0][k1] (doubles along k1) for the
+// TMA tile stores of k3_ax0_to_rot: box = 8 complex k1 x all i0, 128B swizzle.
+static bool ax0_tma() {
+    const char* e = std::getenv("SLB_AX0_TMA");
+    return e && std::atoi(e) == 1;
+}
+static CUtensorMap rot_tensor_map(const double2* base, int n, int H, int nbands) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        SL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw SlError(SL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    CUtensorMap m;
+    const cuuint64_t dims[4] = {2ull * n, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(nbands)};
+    const cuuint64_t strides[3] = {16ull * n, 16ull * n * n, 16ull * n * n * H};
+    const cuuint32_t box[4] = {16, static_cast<cuuint32_t>(n), 1, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw SlError(SL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return m;
 }
 
 template <int n>
@@ -105,12 +134,21 @@ struct Fast3DLaunch {
     }
     template <int DIR, int MODE>
     void to_rot(const double2* src, long long sbs, double2* dst, int nb, int band0, const double* WN, const char* nm) {
-        set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
         LaunchScope ls(s, nm, st, nb);
         const int G = MODE == kAx0DecMul ? std::min(fast3d_group(s), nb) : 1;
         const int groups = (nb + G - 1) / G;
-        k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, groups), AC::THREADS, ax_smem, st>>>(
-            src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw);
+        if (ax0_tma() && AC::V == 8) {
+            const CUtensorMap tm = rot_tensor_map(dst, n, H, nb);
+            const size_t sm = ax_smem + 1024;  // room to align the tile to 1024 bytes
+            set_smem(k3_ax0_to_rot<n, DIR, MODE, true>, sm);
+            k3_ax0_to_rot<n, DIR, MODE, true><<<dim3(ax_blocks, groups), AC::THREADS, sm, st>>>(
+                src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw, tm);
+        } else {
+            CUtensorMap none{};
+            set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
+            k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, groups), AC::THREADS, ax_smem, st>>>(
+                src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw, none);
+        }
         check_launch("k3_ax0_to_rot");
     }
     template <int DIR, int MODE>

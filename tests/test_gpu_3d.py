@@ -232,3 +232,17 @@ def test_largest_specialised_sizes_round_trip(cuda):
         assert (torch.linalg.norm(d - f) / torch.linalg.norm(f)).item() <= 1e-10
         del s, r, d
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [128, 192])
+def test_ax0_tma_store_matches(cuda, n, monkeypatch):
+    # TMA bulk tensor stores of the rotated tiles (SLB_AX0_TMA=1) == the store loop
+    import torch
+    s = P.build_system_3d((n, n, n), P.ScaleProfile.from_levels([0, 1]))
+    sch = P.ThresholdSchedule.defaults_3d(0.3, 2)
+    x = torch.from_numpy(np.random.default_rng(n + 1).uniform(-1, 1, (n, n, n))).to(cuda)
+    monkeypatch.setenv("SLB_AX0_TMA", "0")
+    want = P.denoise(x, s, sch).cpu().numpy()
+    monkeypatch.setenv("SLB_AX0_TMA", "1")
+    got = P.denoise(x, s, sch).cpu().numpy()
+    np.testing.assert_array_equal(got, want)
