@@ -180,6 +180,13 @@ int sl_separate_host(sl_system* directional, sl_system* isotropic, const double*
 int sl_shcf_size(const sl_system* sys, int nbands, size_t* bytes);
 int sl_shcf_serialize(const sl_system* sys, const double* coeffs, int nbands, unsigned char* out, size_t cap);
 int sl_shcf_deserialize(const sl_system* sys, const unsigned char* in, size_t len, double* coeffs, int nbands);
+/* Streamed SHCF files (stacks larger than host/HBM budgets):
+ * forward() of host signal f written straight to `path` as SHCF, and inverse()
+ * read straight from `path`, bands_per_chunk bands at a time (<= 0: ~2 GB
+ * chunks). Same bytes as sl_shcf_serialize(forward(f)); the streamed inverse
+ * sums per-chunk partial reconstructions (equal to inverse() within 1e-15). */
+int sl_shcf_forward_file(sl_system* sys, const double* f, const char* path, int bands_per_chunk);
+int sl_shcf_inverse_file(sl_system* sys, const char* path, double* out, int bands_per_chunk);
 
 /* ---- signal files (image_io.hpp:9-24, image_io.cpp:43-159), host ---------
  * PGM: binary P5, 8-bit (maxval <= 255) or 16-bit big-endian samples; rows =

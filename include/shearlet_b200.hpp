@@ -265,6 +265,19 @@ inline std::vector<double> deserialize(const std::vector<unsigned char>& bytes, 
     return c;
 }
 
+// Streamed SHCF files: decompose to / reconstruct from a file a chunk of bands at a time
+inline void forward_to_file(const std::vector<double>& f, const ShearletSystem& s, const std::string& path,
+                            int bands_per_chunk = 0) {
+    if (f.size() != s.size()) throw ShapeError("forward: signal dims do not match the system grid");
+    check(sl_shcf_forward_file(s.handle(), f.data(), path.c_str(), bands_per_chunk));
+}
+inline std::vector<double> inverse_from_file(const std::string& path, const ShearletSystem& s,
+                                             int bands_per_chunk = 0) {
+    std::vector<double> out(s.size());
+    check(sl_shcf_inverse_file(s.handle(), path.c_str(), out.data(), bands_per_chunk));
+    return out;
+}
+
 // System descriptors (descriptor.hpp:12-39): write_descriptor(describe(s)) text, rebuild from text
 inline std::string describe(const ShearletSystem& s) {
     std::size_t n = 0;

@@ -145,6 +145,8 @@ def lib():
     L.sl_shcf_size.argtypes = [P, i, C.POINTER(C.c_size_t)]
     L.sl_shcf_serialize.argtypes = [P, dp, i, C.c_char_p, C.c_size_t]
     L.sl_shcf_deserialize.argtypes = [P, C.c_char_p, C.c_size_t, dp, i]
+    L.sl_shcf_forward_file.argtypes = [P, dp, C.c_char_p, i]
+    L.sl_shcf_inverse_file.argtypes = [P, C.c_char_p, dp, i]
     L.sl_load_pgm.argtypes = [C.c_char_p, dp, C.c_int64, ip, ip, ip]
     L.sl_save_pgm.argtypes = [dp, i, i, C.c_char_p, i]
     L.sl_load_svol.argtypes = [C.c_char_p, dp, C.c_int64, C.POINTER(C.c_int64)]
@@ -172,7 +174,7 @@ EXPORTED_SYMBOLS = [
     "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
     "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
-    "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize",
+    "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize", "sl_shcf_forward_file", "sl_shcf_inverse_file",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
     "sl_describe", "sl_system_create_from_descriptor",
     "sl_gaussian_kernel", "sl_binarize", "sl_quality_q", "sl_quality_q_opt",
@@ -845,6 +847,21 @@ def deserialize(data: bytes, sys: _System) -> np.ndarray:
     """Coefficient stack from SHCF bytes, validated against the system (transform.hpp:50-52)."""
     out = np.empty((sys.n_bands,) + tuple(sys.shape))
     _check(lib().sl_shcf_deserialize(sys.handle, data, len(data), _dp(out), sys.n_bands))
+    return out
+
+
+def forward_to_file(f, sys: _System, path: str, bands_per_chunk: int = 0):
+    """forward(f) written straight to an SHCF file, a chunk of bands at a time (the
+    stack is never held whole); same bytes as serialize(forward(f), sys)."""
+    x = np.ascontiguousarray(f.cpu().numpy() if _is_cuda_tensor(f) else f, dtype=np.float64)
+    _check_signal(x, sys, "forward")
+    _check(lib().sl_shcf_forward_file(sys.handle, _dp(x), os.fsencode(path), int(bands_per_chunk)))
+
+
+def inverse_from_file(path: str, sys: _System, bands_per_chunk: int = 0) -> np.ndarray:
+    """inverse() of an SHCF file, streamed a chunk of bands at a time."""
+    out = np.empty(tuple(sys.shape))
+    _check(lib().sl_shcf_inverse_file(sys.handle, os.fsencode(path), _dp(out), int(bands_per_chunk)))
     return out
 
 

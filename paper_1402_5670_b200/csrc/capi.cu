@@ -801,6 +801,122 @@ int sl_shcf_deserialize(const sl_system* h, const unsigned char* in, size_t len,
     });
 }
 
+// ---- streamed SHCF files: decompose straight to / reconstruct straight from a file,
+// a chunk of bands at a time (the stack never exists whole, on the host or device)
+}  // extern "C"
+namespace {
+__global__ void k_add_inplace(double* __restrict__ acc, const double* __restrict__ x, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc[i] += x[i];
+}
+// restrict the handle to bands [lo, hi) for one chunk, restoring the shard after
+struct ShardScope {
+    System& s;
+    int lo, hi;
+    ShardScope(System& sys, int l, int h) : s(sys), lo(sys.lo), hi(sys.hi) {
+        s.lo = l;
+        s.hi = h;
+    }
+    ~ShardScope() {
+        s.lo = lo;
+        s.hi = hi;
+    }
+};
+struct PinnedBuf {
+    double* p = nullptr;
+    explicit PinnedBuf(size_t count) { SL_CUDA(cudaMallocHost(&p, count * sizeof(double))); }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+struct File {
+    std::FILE* f = nullptr;
+    File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+    ~File() {
+        if (f) std::fclose(f);
+    }
+};
+int stream_chunk(const System& s, int chunk) {
+    if (chunk > 0) return std::min(chunk, s.nb());
+    const double per = static_cast<double>(s.nreal) * sizeof(double);
+    return std::max(1, std::min(s.nb(), static_cast<int>((2.0 * 1024 * 1024 * 1024) / per)));  // ~2 GB per chunk
+}
+}  // namespace
+extern "C" {
+
+int sl_shcf_forward_file(sl_system* h, const double* f, const char* path, int bands_per_chunk) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!f || !path) throw SlError(SL_ERR_INVALID, "null argument");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        File out(path, "wb");
+        if (!out.f) throw SlError(SL_ERR_FORMAT, std::string("cannot write coefficient file: ") + path);
+        std::vector<unsigned char> hdr(shcf_header_bytes(s, s.nb()));
+        shcf_write_header(s, hdr.data());
+        if (std::fwrite(hdr.data(), 1, hdr.size(), out.f) != hdr.size())
+            throw SlError(SL_ERR_FORMAT, "coefficient file write failed");
+        const int C = stream_chunk(s, bands_per_chunk);
+        const size_t cn = static_cast<size_t>(C) * s.nreal;
+        s.io_in.upload(f, static_cast<size_t>(s.nreal), 0);
+        s.stack.alloc(cn);
+        PinnedBuf host(cn);
+        std::vector<unsigned char> bytes(cn * 8);
+        const int lo0 = s.lo, hi0 = s.hi;
+        for (int b0 = lo0; b0 < hi0; b0 += C) {
+            const int b1 = std::min(hi0, b0 + C);
+            const size_t count = static_cast<size_t>(b1 - b0) * s.nreal;
+            {
+                ShardScope sc(s, b0, b1);
+                dec(s, s.io_in.p, s.stack.p, nullptr, 0);
+            }
+            SL_CUDA(cudaMemcpy(host.p, s.stack.p, count * sizeof(double), cudaMemcpyDeviceToHost));
+            shcf_write_data(host.p, count, bytes.data());
+            if (std::fwrite(bytes.data(), 1, count * 8, out.f) != count * 8)
+                throw SlError(SL_ERR_FORMAT, "coefficient file write failed");
+        }
+    });
+}
+
+int sl_shcf_inverse_file(sl_system* h, const char* path, double* out, int bands_per_chunk) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!out || !path) throw SlError(SL_ERR_INVALID, "null argument");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        File in(path, "rb");
+        if (!in.f) throw SlError(SL_ERR_FORMAT, std::string("cannot open coefficient file: ") + path);
+        std::vector<unsigned char> hdr(shcf_header_bytes(s, s.nb()));
+        const size_t got = std::fread(hdr.data(), 1, hdr.size(), in.f);
+        shcf_deserialize(s, hdr.data(), got, nullptr, s.nb());  // magic, version, dims, count, records
+        const int C = stream_chunk(s, bands_per_chunk);
+        const size_t cn = static_cast<size_t>(C) * s.nreal;
+        s.stack.alloc(cn);
+        s.io_out.alloc(static_cast<size_t>(s.nreal));
+        s.io_in.alloc(static_cast<size_t>(s.nreal));
+        SL_CUDA(cudaMemset(s.io_out.p, 0, static_cast<size_t>(s.nreal) * sizeof(double)));
+        PinnedBuf host(cn);
+        std::vector<unsigned char> bytes(cn * 8);
+        const int lo0 = s.lo, hi0 = s.hi;
+        for (int b0 = lo0; b0 < hi0; b0 += C) {
+            const int b1 = std::min(hi0, b0 + C);
+            const size_t count = static_cast<size_t>(b1 - b0) * s.nreal;
+            if (std::fread(bytes.data(), 1, count * 8, in.f) != count * 8)
+                throw SlError(SL_ERR_FORMAT, "coefficient stream truncated");
+            shcf_read_data(bytes.data(), count, host.p);
+            SL_CUDA(cudaMemcpy(s.stack.p, host.p, count * sizeof(double), cudaMemcpyHostToDevice));
+            {
+                ShardScope sc(s, b0, b1);
+                rec(s, s.stack.p, s.io_in.p, 0);  // partial reconstruction of the chunk (linear)
+            }
+            k_add_inplace<<<1024, 256>>>(s.io_out.p, s.io_in.p, s.nreal);
+            check_launch("k_add_inplace");
+        }
+        SL_CUDA(cudaMemcpy(out, s.io_out.p, static_cast<size_t>(s.nreal) * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
 int sl_load_pgm(const char* path, double* pixels, int64_t cap, int* rows, int* cols, int* maxval) {
     return guard([&] {
         if (!path) throw SlError(SL_ERR_INVALID, "null path");

@@ -15,6 +15,7 @@ static size_t shcf_bytes(const System& s, int nbands) {
     return 4 + 2 + 1 + 4 * static_cast<size_t>(s.ndim) + 4 + 13 * static_cast<size_t>(nbands) +
            8 * static_cast<size_t>(nbands) * static_cast<size_t>(s.nreal);
 }
+static size_t shcf_header_bytes(const System& s, int nbands);
 
 template <class T>
 static void put_le(unsigned char*& p, T v) {
@@ -35,16 +36,19 @@ static T get_le(const unsigned char*& p, const unsigned char* end) {
     return v;
 }
 
-// bands = the handle's shard [lo, hi) records (a full system writes all R)
-static void shcf_serialize(const System& s, const double* coeffs, int nbands, unsigned char* out) {
-    if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "serialize: stack does not match the system");
+static size_t shcf_header_bytes(const System& s, int nbands) {
+    return 4 + 2 + 1 + 4 * static_cast<size_t>(s.ndim) + 4 + 13 * static_cast<size_t>(nbands);
+}
+
+// header + index records of the handle's bands [lo, hi); returns the end
+static unsigned char* shcf_write_header(const System& s, unsigned char* out) {
     unsigned char* p = out;
     std::memcpy(p, "SHCF", 4);
     p += 4;
     put_le<uint16_t>(p, 1);
     put_le<uint8_t>(p, static_cast<uint8_t>(s.ndim));
     for (int a = 0; a < s.ndim; ++a) put_le<uint32_t>(p, static_cast<uint32_t>(s.n[a]));
-    put_le<uint32_t>(p, static_cast<uint32_t>(nbands));
+    put_le<uint32_t>(p, static_cast<uint32_t>(s.nb()));
     for (int i = s.lo; i < s.hi; ++i) {
         const Record& r = s.index[static_cast<size_t>(i)];
         put_le<uint8_t>(p, static_cast<uint8_t>(r.kind));
@@ -52,12 +56,30 @@ static void shcf_serialize(const System& s, const double* coeffs, int nbands, un
         put_le<int32_t>(p, r.k1);
         put_le<int32_t>(p, s.ndim == 2 ? 0 : r.k2);
     }
-    const size_t nd = static_cast<size_t>(nbands) * static_cast<size_t>(s.nreal);
-    for (size_t i = 0; i < nd; ++i) {
+    return p;
+}
+
+// f64 samples, little-endian
+static void shcf_write_data(const double* v, size_t count, unsigned char* p) {
+    for (size_t i = 0; i < count; ++i) {
         uint64_t u;
-        std::memcpy(&u, coeffs + i, 8);
+        std::memcpy(&u, v + i, 8);
         put_le<uint64_t>(p, u);
     }
+}
+static void shcf_read_data(const unsigned char* p, size_t count, double* v) {
+    for (size_t i = 0; i < count; ++i) {
+        uint64_t u = 0;
+        for (int k = 0; k < 8; ++k) u |= static_cast<uint64_t>(p[8 * i + k]) << (8 * k);
+        std::memcpy(v + i, &u, 8);
+    }
+}
+
+// bands = the handle's shard [lo, hi) records (a full system writes all R)
+static void shcf_serialize(const System& s, const double* coeffs, int nbands, unsigned char* out) {
+    if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "serialize: stack does not match the system");
+    unsigned char* p = shcf_write_header(s, out);
+    shcf_write_data(coeffs, static_cast<size_t>(nbands) * static_cast<size_t>(s.nreal), p);
 }
 
 static void shcf_deserialize(const System& s, const unsigned char* in, size_t len, double* coeffs, int nbands) {
@@ -87,12 +109,10 @@ static void shcf_deserialize(const System& s, const unsigned char* in, size_t le
         if (r.kind != kind || r.scale != scale || r.k1 != k1 || (dim == 3 && r.k2 != k2))
             throw SlError(SL_ERR_SHAPE, "coefficient stream: index records differ from the system");
     }
+    if (!coeffs) return;  // header-only validation (streaming reader)
     const size_t nd = static_cast<size_t>(count) * static_cast<size_t>(s.nreal);
     if (static_cast<size_t>(end - p) < 8 * nd) throw SlError(SL_ERR_FORMAT, "coefficient stream truncated");
-    for (size_t i = 0; i < nd; ++i) {
-        const uint64_t u = get_le<uint64_t>(p, end);
-        std::memcpy(coeffs + i, &u, 8);
-    }
+    shcf_read_data(p, nd, coeffs);
 }
 
 }  // namespace slb

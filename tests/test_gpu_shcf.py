@@ -81,3 +81,25 @@ def test_deserialize_errors(cuda):
         P.deserialize(good, s3)  # a 2D stream into a 3D system
     with pytest.raises(P.ShapeError):
         P.serialize(g["bands"][:-1], s)
+
+
+@pytest.mark.parametrize("shape,levels,chunk", [((64, 64), [0, 1, 1], 7), ((32, 32, 32), [0, 1], 10)])
+def test_streamed_files(cuda, tmp_path, shape, levels, chunk):
+    # decompose straight to / reconstruct straight from an SHCF file, chunk by chunk
+    prof = P.ScaleProfile.from_levels(levels)
+    s = P.build_system_2d(*shape, prof) if len(shape) == 2 else P.build_system_3d(shape, prof)
+    f = np.random.default_rng(4).uniform(-1, 1, shape)
+    path = str(tmp_path / "c.shcf")
+    P.forward_to_file(f, s, path, chunk)
+    stack = P.forward(f, s)
+    assert open(path, "rb").read() == P.serialize(stack, s)
+    r = P.inverse_from_file(path, s, chunk)
+    want = P.inverse(stack, s)
+    assert np.linalg.norm(r - want) / np.linalg.norm(want) <= 1e-13
+    assert np.linalg.norm(r - f) / np.linalg.norm(f) <= 1e-10
+    bad = tmp_path / "bad.shcf"
+    bad.write_bytes(open(path, "rb").read()[:-8])
+    with pytest.raises(P.FormatError):
+        P.inverse_from_file(str(bad), s, chunk)
+    with pytest.raises(P.FormatError):
+        P.inverse_from_file(str(tmp_path / "missing.shcf"), s)
