@@ -60,7 +60,11 @@ struct RowCfg {
 template <int L>
 struct ColCfg {
     static constexpr int T = RegPlan<L>::T;
+#ifndef SLB_COL_THREADS
     static constexpr int LINES = (128 / T) > 0 ? 128 / T : 1;
+#else
+    static constexpr int LINES = (SLB_COL_THREADS / T) > 0 ? SLB_COL_THREADS / T : 1;
+#endif
     static constexpr int THREADS = LINES * T;
 #ifndef SLB_COL_MINB
     // measured: 4 CTAs/SM (<= 128 registers) beats 5 (<= 102) for the column passes
