@@ -22,19 +22,25 @@ static int env_int(const char* name, int dflt) {
 }
 
 // Band grouping: G bands per column-pass CTA (F / accumulator reuse), C bands
-// per chunk (intermediate kept around 32 MiB so it stays L2-resident).
+// per chunk (one launch per pass and chunk).
 struct Fast2DCfg {
     int G, C;
 };
-// A lone frame needs many CTAs per launch (small G); with >= 4 frames in flight
-// on other streams the SMs stay busy, and a large G cuts the slot traffic of the
-// rec sum (16 Nh per G bands) and the F re-reads (bench sweep, profiles/).
+// Measured (tools/sweep2d.sh, tools/single2d.py): with >= 4 frames in flight on
+// other streams the SMs stay busy, and G = 14 cuts the slot traffic of the rec
+// sum (16 Nh per G bands) and the F re-reads, chunks of ~64 MiB; a lone frame
+// takes every band in one chunk (up to 256 MiB) so each pass is one
+// full-machine launch, G = 7 from 512^2 up.
 static Fast2DCfg fast2d_cfg(const System& s) {
     const bool conc = s.concurrency >= 4;
-    const int G = env_int(conc ? "SLB_GROUP" : "SLB_GROUP1", conc ? 14 : 4);
     const double per = static_cast<double>(s.H) * s.n[0] * sizeof(double2);
-    int C = env_int(conc ? "SLB_CHUNK" : "SLB_CHUNK1",
-                    std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
+    if (!conc) {
+        const int G = env_int("SLB_GROUP1", s.n[0] >= 512 ? 7 : 4);
+        const int C = env_int("SLB_CHUNK1", std::max(G, static_cast<int>((256.0 * 1024 * 1024) / per)));
+        return {G, std::max(1, C)};
+    }
+    const int G = env_int("SLB_GROUP", 14);
+    int C = env_int("SLB_CHUNK", std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
     C = std::max(G, (C / G) * G);
     return {G, C};
 }
