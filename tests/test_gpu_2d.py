@@ -304,3 +304,22 @@ def test_duals_match_oracle(cuda):
     for i in range(s.redundancy()):
         assert np.abs(d[i] - o.filters[i] / o.frame_weight).max() < 1e-12
     np.testing.assert_allclose(s.frame_weight, g["frame_weight"], rtol=1e-12)
+
+
+def test_run_to_run_bit_identical(cuda):
+    # DESIGN 6: band-order sums, deterministic slot / accumulator order -> repeated
+    # calls (batched over streams, lone frames, 3D groups) are bitwise identical
+    import torch
+    s = P.build_system_2d(512, 512, P.ScaleProfile.from_levels([1, 1, 2, 2]))
+    sch = P.ThresholdSchedule.defaults_2d(40.0)
+    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(512), 40.0, i) for i in range(8)])).to(cuda)
+    a = P.denoise_batch(x, s, sch)
+    for _ in range(3):
+        assert torch.equal(P.denoise_batch(x, s, sch), a)
+    one = P.denoise(x[0], s, sch)
+    assert torch.equal(P.denoise(x[0], s, sch), one)
+    s3 = P.build_system_3d((64, 64, 64), P.ScaleProfile.from_levels([0, 1]))
+    v = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, (64, 64, 64))).to(cuda)
+    sch3 = P.ThresholdSchedule.defaults_3d(0.2, 2)
+    d3 = P.denoise(v, s3, sch3)
+    assert torch.equal(P.denoise(v, s3, sch3), d3)
