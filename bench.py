@@ -41,6 +41,9 @@ CONFIGS = {
     # name: (dims, levels, schedule kind, sigma, frames per step per rank, seed base)
     "2d512": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s",
                   metric="2D 512^2 dec+thr+rec frames/s (nScales=4, R=49)", baseline_cfg=1),
+    "2d512_nostack": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s", nostack=True,
+                          metric="2D 512^2 denoise frames/s, coefficient stack not materialised (nScales=4, R=49)",
+                          baseline_cfg=1),
     "2d256": dict(dims=(256, 256), levels=[1, 1], sigma=40.0, batch=32, unit="frames/s",
                   metric="2D 256^2 dec+rec frames/s (nScales=2, R=17)", baseline_cfg=0),
     "2d1024x64": dict(dims=(1024, 1024), levels=[1, 1, 2, 2], sigma=40.0, batch=64, unit="frames/s",
@@ -84,6 +87,8 @@ def algorithmic_bytes(cfg, R, frames):
     N = int(np.prod(dims))
     Nh = N // dims[-1] * (dims[-1] // 2 + 1)
     if len(dims) == 2:
+        if cfg.get("nostack"):  # stack never written: f/f_rec + real psi halves read twice
+            return frames * (16 * N + 16 * R * Nh)
         return frames * (16 * N + 16 * R * N + 16 * R * Nh)
     return frames * (16 * N + 16 * R * N + 8 * Nh)
 
@@ -256,6 +261,8 @@ def main():
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
         sysg.set_streams(nstreams)
+        if cfg.get("nostack"):
+            sysg.set_stack_output(False)  # reported separately from the materialised-stack metric
         if args.config == "2d1024x64":
             frames = cfg["batch"] // world  # fixed total batch sharded by image
             scaling = "strong"

@@ -140,6 +140,11 @@ int sl_denoise_dev(sl_system* sys, const double* in, double* out, const double* 
  * so concurrent frames overlap on the GPU; results are identical to
  * per-frame calls. sl_sheardec_batch_dev thresholds when K != NULL. */
 int sl_set_streams(sl_system* sys, int nstreams);
+/* Whether the fused denoise (sl_denoise_*) writes the thresholded coefficient
+ * stack to HBM (default 1, as the reference's denoise materialises it). With 0
+ * the stack is never written: the same reconstruction, ~1/6 less HBM traffic
+ * (reported separately from the stack-materialised numbers). */
+int sl_set_stack_output(sl_system* sys, int materialize);
 int sl_sheardec_batch_dev(sl_system* sys, const double* f, int nframes, double* coeffs, const double* K, int nK,
                           double sigma, int scale_by_rms, void* stream);
 int sl_shearrec_batch_dev(sl_system* sys, const double* coeffs, int nframes, double* f, void* stream);

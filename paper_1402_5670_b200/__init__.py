@@ -133,6 +133,7 @@ def lib():
     L.sl_shearrec_host.argtypes = [P, dp, i, dp]
     L.sl_hard_threshold_host.argtypes = [P, dp, dp, i, dp, i, C.c_double, i]
     L.sl_denoise_host.argtypes = [P, dp, dp, dp, i, C.c_double, i]
+    L.sl_set_stack_output.argtypes = [P, i]
     L.sl_set_streams.argtypes = [P, i]
     L.sl_sheardec_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
     L.sl_shearrec_batch_dev.argtypes = [P, P, i, P, P]
@@ -172,7 +173,7 @@ EXPORTED_SYMBOLS = [
     "sl_frame_weight", "sl_frame_bounds", "sl_filter_spectrum", "sl_sheardec_dev", "sl_sheardec_threshold_dev",
     "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_sheardec_host", "sl_shearrec_host",
     "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
-    "sl_set_streams", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
+    "sl_set_streams", "sl_set_stack_output", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
     "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize", "sl_shcf_forward_file", "sl_shcf_inverse_file",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
@@ -329,6 +330,10 @@ class _System:
         raw = names.raw
         return {raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i]), int(units[i]))
                 for i in range(n.value)}
+
+    def set_stack_output(self, materialize: bool = True):
+        """Fused denoise writes the thresholded stack (default, as the reference) or not."""
+        _check(lib().sl_set_stack_output(self._h, int(materialize)))
 
     def set_streams(self, n: int):
         """Concurrent internal streams used by the batched entry points."""

@@ -512,12 +512,21 @@ void denoise_lockstep(System& s, const double* in, int nframes, double* out, cud
         s.w->stack.alloc(static_cast<size_t>(group) * sfs);
         const int conc = s.concurrency;
         s.concurrency = std::max(conc, 4);  // full-machine band grouping (fast2d_cfg)
-        denoise2d_fast_batch(s, in + off, s.nreal, nf, s.w->stack.p, sfs, out + off, s.nreal, s.delta.p, fst);
+        denoise2d_fast_batch(s, in + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs, out + off, s.nreal,
+                             s.delta.p, fst);
         s.concurrency = conc;
     });
 }
 }  // namespace
 extern "C" {
+
+int sl_set_stack_output(sl_system* h, int materialize) {
+    return guard([&] {
+        System& s = sys_of(h);
+        std::lock_guard<std::mutex> lk(s.mu);
+        s.materialize = materialize != 0;
+    });
+}
 
 int sl_set_streams(sl_system* h, int nstreams) {
     return guard([&] {
@@ -622,7 +631,8 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
                 if (group > 1) {
                     const int conc = s.concurrency;
                     s.concurrency = std::max(conc, 4);
-                    denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.w->stack.p, sfs, s.io_out.p + off,
+                    denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs,
+                                         s.io_out.p + off,
                                          s.nreal, s.delta.p, fst);
                     s.concurrency = conc;
                 } else {

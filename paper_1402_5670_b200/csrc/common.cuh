@@ -197,6 +197,7 @@ struct System {
     Workspace* w = nullptr;
     int nstreams = 6;               // workspaces used by batched calls (measured: 6 best for 8-frame host batches)
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
+    bool materialize = true;        // fused denoise writes the thresholded stack (sl_set_stack_output)
     cudaEvent_t fork_ev = nullptr;
     DBuf<double> delta, stack, io_in, io_out;
     std::vector<double> delta_host;  // host copy of `delta` (deltas() skips unchanged uploads)

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
     inter += blockIdx.y * ibs + blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
-    band += blockIdx.y * bbs + blockIdx.z * bzs;
+    if (band) band += blockIdx.y * bbs + blockIdx.z * bzs;  // null: stack not materialised
     const int nrows = min(2 * V, n0 - r0);
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
@@ -67,8 +67,10 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
             if (fabs(c) < dl) c = 0.0;
         }
         const int i = t + T * m;
-        if (ra < n0) band[(long long)ra * L + i] = a;
-        if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
+        if (band) {
+            if (ra < n0) band[(long long)ra * L + i] = a;
+            if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
+        }
         x[m] = make_double2(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : 0.0);  // rec input: the thresholded rows
     }
     reg_fft<L, -1, false>(x, lb, t, tw);
@@ -158,7 +160,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
         {
             LaunchScope ls(s, "f2_rows_fused", st, cb);
             k2_rows_fused<L1><<<dim3(row_blocks, cb), RC::THREADS, row_smem, st>>>(
-                s.w->inter.p, nhT, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, n0, H, scale, delta,
+                s.w->inter.p, nhT, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale, delta,
                 s.lo + b0, tw1);
             check_launch("k2_rows_fused");
         }
@@ -245,7 +247,7 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
         {
             LaunchScope ls(s, "f2_rows_fused", st, static_cast<long long>(cb) * nf);
             k2_rows_fused<L1><<<dim3(row_blocks, cb, nf), RC::THREADS, row_smem, st>>>(
-                s.w->inter.p, nhT, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, n0, H, scale, delta,
+                s.w->inter.p, nhT, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale, delta,
                 s.lo + b0, tw1, izs, sfs);
             check_launch("k2_rows_fused");
         }

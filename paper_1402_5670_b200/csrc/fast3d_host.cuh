@@ -224,10 +224,10 @@ static void denoise3d_fast_t(System& s, const double* f, double* stack, double* 
         const int cb = std::min(C, nb - b0);
         K.template to_rot<+1, kAx0DecMul>(s.w->F.p, 0, s.w->inter.p, cb, s.lo + b0, nullptr, "f3_ax0_dec");
         if (Fast3DLaunch<n>::plane_enabled()) {
-            K.plane_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+            K.plane_fused(s.w->inter.p, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, cb, delta, s.lo + b0);
         } else {
             K.template axis1<+1>(s.w->inter.p, cb);
-            K.rows_fused(s.w->inter.p, stack + static_cast<size_t>(b0) * s.nreal, s.nreal, cb, delta, s.lo + b0);
+            K.rows_fused(s.w->inter.p, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, cb, delta, s.lo + b0);
             K.template axis1<-1>(s.w->inter.p, cb);
         }
         K.template from_rot<-1, kAx0RecAcc>(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, "f3_ax0_rec");

@@ -51,7 +51,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PlaneCfg<L>::THREADS
     const int i0 = blockIdx.x >> 1;
     const int b = blockIdx.y;
     rot += b * rbs;
-    band += b * bbs;
+    if (band) band += b * bbs;
     const int k2lo = rank * H0;
     const int nrows = rank == 0 ? H0 : H - H0;
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
@@ -119,8 +119,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PlaneCfg<L>::THREADS
                 if (fabs(c) < dl) c = 0.0;
             }
             const int i = t + T * m;
-            ba[i] = a;
-            ba[n + i] = c;
+            if (band) {
+                ba[i] = a;
+                ba[n + i] = c;
+            }
             x[m] = make_double2(a, c);  // rec input: the thresholded rows
         }
         line_sync<T>();

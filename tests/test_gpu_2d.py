@@ -323,3 +323,19 @@ def test_run_to_run_bit_identical(cuda):
     sch3 = P.ThresholdSchedule.defaults_3d(0.2, 2)
     d3 = P.denoise(v, s3, sch3)
     assert torch.equal(P.denoise(v, s3, sch3), d3)
+
+
+def test_stack_free_denoise_same_result(cuda):
+    # sl_set_stack_output(0): the fused denoise never writes the stack; same reconstruction
+    import torch
+    for shape, lv, mk in (((512, 512), [1, 1, 2, 2], P.build_system_2d), ((64, 64, 64), [0, 1], P.build_system_3d)):
+        prof = P.ScaleProfile.from_levels(lv)
+        s = mk(*shape, prof) if len(shape) == 2 else mk(shape, prof)
+        sch = (P.ThresholdSchedule.defaults_2d if len(shape) == 2 else P.ThresholdSchedule.defaults_3d)(0.2, len(lv))
+        x = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, (3,) + shape)).to(cuda)
+        want = P.denoise_batch(x, s, sch)
+        one = P.denoise(x[0], s, sch)
+        s.set_stack_output(False)
+        assert torch.equal(P.denoise_batch(x, s, sch), want)
+        assert torch.equal(P.denoise(x[0], s, sch), one)
+        s.set_stack_output(True)
