@@ -1,8 +1,7 @@
 // Host orchestration of the specialised 3D path (kernels in fast3d.cuh).
 #pragma once
-#include <cudaTypedefs.h>
-
 #include "fast2d_host.cuh"
+#include "tma.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
 #include "fast3d_plane.cuh"
@@ -44,24 +43,11 @@ static bool ax0_tma() {
     return e && std::atoi(e) == 1;
 }
 static CUtensorMap rot_tensor_map(const double2* base, int n, int H, int nbands) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        SL_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-        if (!fn || q != cudaDriverEntryPointSuccess) throw SlError(SL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
-    CUtensorMap m;
     const cuuint64_t dims[4] = {2ull * n, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(H),
                                 static_cast<cuuint64_t>(nbands)};
     const cuuint64_t strides[3] = {16ull * n, 16ull * n * n, 16ull * n * n * H};
     const cuuint32_t box[4] = {16, static_cast<cuuint32_t>(n), 1, 1};
-    const cuuint32_t es[4] = {1, 1, 1, 1};
-    const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double2*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw SlError(SL_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    return m;
+    return tma_map_f64(base, 4, dims, strides, box);
 }
 
 template <int n>

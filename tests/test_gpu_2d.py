@@ -339,3 +339,17 @@ def test_stack_free_denoise_same_result(cuda):
         assert torch.equal(P.denoise_batch(x, s, sch), want)
         assert torch.equal(P.denoise(x[0], s, sch), one)
         s.set_stack_output(True)
+
+
+def test_rows_tma_matches(cuda, monkeypatch):
+    # TMA staging of the fused rows pass (SLB_ROWS_TMA=1) == the cp.async kernel, bitwise
+    import torch
+    s = P.build_system_2d(512, 512, P.ScaleProfile.from_levels([1, 1, 2, 2]))
+    sch = P.ThresholdSchedule.defaults_2d(40.0)
+    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(512), 40.0, i) for i in range(4)])).to(cuda)
+    monkeypatch.setenv("SLB_ROWS_TMA", "0")
+    want_b = P.denoise_batch(x, s, sch)
+    want_1 = P.denoise(x[0], s, sch)
+    monkeypatch.setenv("SLB_ROWS_TMA", "1")
+    assert torch.equal(P.denoise_batch(x, s, sch), want_b)
+    assert torch.equal(P.denoise(x[0], s, sch), want_1)
