@@ -54,6 +54,8 @@ CONFIGS = {
                   metric="3D 192^3 dec+thr+rec vols/s (nScales=3 SL3D_2, R=292)", baseline_cfg=4),
     "3d192sl1": dict(dims=(192, 192, 192), levels=[0, 0, 1], sigma=40.0, batch=1, unit="vols/s",
                      metric="3D 192^3 dec+thr+rec vols/s (nScales=3 SL3D_1, R=76)", baseline_cfg=4),
+    "3d256": dict(dims=(256, 256, 256), levels=[1, 1], sigma=40.0, batch=1, unit="vols/s",
+                  metric="3D 256^3 dec+thr+rec vols/s (nScales=2, R=99)", baseline_cfg=None),
 }
 
 

@@ -91,6 +91,27 @@ _CODES = {1: Error, 2: ShapeError, 3: ConfigError, 4: DomainError, 5: SingularFr
 _lib = None
 
 
+class _DevLib:
+    """SLB_LIB variant wrapper: symbols the variant does not export bind to a stub."""
+
+    class _Missing:
+        argtypes = restype = None
+
+        def __call__(self, *a):
+            raise AttributeError("entry point missing from this SLB_LIB variant")
+
+    def __init__(self, lib):
+        object.__setattr__(self, "_l", lib)
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._l, name)
+        except AttributeError:
+            m = _DevLib._Missing()
+            object.__setattr__(self, name, m)
+            return m
+
+
 def lib():
     """Load libshearlet_b200.so; raises loudly if it has not been built."""
     global _lib
@@ -100,6 +121,8 @@ def lib():
         raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                           "(there is no CPU fallback for the shearlet hot path)")
     L = C.CDLL(LIB_PATH)
+    if "SLB_LIB" in os.environ:
+        L = _DevLib(L)  # A/B variants built from older commits may lack newer entry points
     P = C.c_void_p
     i = C.c_int
     dp = C.POINTER(C.c_double)

@@ -14,7 +14,10 @@
 
 namespace slb {
 
-template <int L>
+// STORE = false: the stack is not materialised (sl_set_stack_output, band
+// null); a separate instantiation so the stack-writing variant keeps its
+// register allocation (a runtime null test spilled 136 B/thread at L = 128)
+template <int L, bool STORE = true>
 __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
     k2_rows_fused(double2* __restrict__ inter, long long ibs, double* __restrict__ band, long long bbs, int n0, int H,
                   double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw,
@@ -24,7 +27,12 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
     inter += blockIdx.y * ibs + blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
-    if (band) band += blockIdx.y * bbs + blockIdx.z * bzs;  // null: stack not materialised
+    // STORE = false keeps a (never taken) runtime test on the stores: ptxas
+    // allocates that body without spills, while deleting the stores outright
+    // spills 24-296 B/thread; L = 2048 also spills less with the test
+    // (measured -Xptxas -v for every L)
+    constexpr bool kTest = !STORE || L == 2048;
+    if (!kTest || band) band += blockIdx.y * bbs + blockIdx.z * bzs;
     const int nrows = min(2 * V, n0 - r0);
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
@@ -68,7 +76,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
             if (fabs(c) < dl) c = 0.0;
         }
         const int i = t + T * m;
-        if (band) {
+        if (!kTest || band) {
             if (ra < n0) band[(long long)ra * L + i] = a;
             if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
         }
@@ -262,9 +270,9 @@ static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, doub
             return;
         }
     }
-    set_smem(k2_rows_fused<L>, tile_smem);
-    k2_rows_fused<L><<<grid, RC::THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw,
-                                                             izs, bzs);
+    auto* k = band ? k2_rows_fused<L, true> : k2_rows_fused<L, false>;
+    set_smem(k, tile_smem);
+    k<<<grid, RC::THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
     check_launch("k2_rows_fused");
 }
 

@@ -88,10 +88,11 @@ struct Fast3DLaunch {
     }
     // dec rows pass + threshold + rec rows pass (fast2d_fused.cuh) over n*n rows
     void rows_fused(double2* inter, double* band, long long bbs, int nb, const double* delta, int band0) {
-        set_smem(k2_rows_fused<n>, row_smem);
+        auto* k = band ? k2_rows_fused<n, true> : k2_rows_fused<n, false>;
+        set_smem(k, row_smem);
         LaunchScope ls(s, "f3_rows_fused", st, nb);
-        k2_rows_fused<n><<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(
-            inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
+        k<<<dim3(row_blocks, nb), RC::THREADS, row_smem, st>>>(
+            inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw, 0, 0);
         check_launch("k2_rows_fused");
     }
     // axis1<+1> + rows_fused + axis1<-1> as one plane pass on 2-CTA clusters

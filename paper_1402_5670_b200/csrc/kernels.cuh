@@ -60,16 +60,20 @@ struct FiltSynth3D {
             return __ldg(tab1d + lp_off[0] + i0) * __ldg(tab1d + lp_off[1] + i1) * __ldg(tab1d + lp_off[2] + i2);
         auto pick = [=](int ax) { return ax == 0 ? i0 : (ax == 1 ? i1 : i2); };  // no local-memory array
         const int p = pick(d.pa), a = pick(d.s1), b = pick(d.s2);
+        // selects, not n[d.s1]: a dynamic index into the by-value parameter
+        // copies it to a local-memory frame (48 B/thread, L1 traffic per element)
+        auto len = [&](int ax) { return ax == 0 ? n[0] : (ax == 1 ? n[1] : n[2]); };
+        const int ns1 = len(d.s1), ns2 = len(d.s2);
         if (d.pa == 0) {
             // pyramid 1: the principal index runs along axis 0, the line direction
             // of the axis-0 passes -> read the transposed copy of each plane
             // (stored right after it) so consecutive threads hit consecutive entries
             const int np = n[0];
-            return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + np * n[d.s1] + a * np + p) *
-                   __ldg(tab2d + d.p2_off + np * n[d.s2] + b * np + p);
+            return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + np * ns1 + a * np + p) *
+                   __ldg(tab2d + d.p2_off + np * ns2 + b * np + p);
         }
-        return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + p * n[d.s1] + a) *
-               __ldg(tab2d + d.p2_off + p * n[d.s2] + b);
+        return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + p * ns1 + a) *
+               __ldg(tab2d + d.p2_off + p * ns2 + b);
     }
 };
 
