@@ -11,6 +11,7 @@ python bench.py --config 3d192 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench
 python bench.py --config 3d128 --steps 10 --warmup 3 --no-cpu-baseline > $O/bench3d128_$R.json 2> $O/bench3d128_$R.err
 python bench.py --config 2d1024x64 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench1024_$R.json 2> $O/bench1024_$R.err
 python bench.py --config 3d192sl1 --steps 10 --warmup 3 --no-cpu-baseline > $O/bench3dsl1_$R.json 2> $O/bench3dsl1_$R.err
+python bench.py --config 3d256 --steps 5 --warmup 3 --no-cpu-baseline > $O/bench3d256_$R.json 2> $O/bench3d256_$R.err
 python bench.py --config 2d512_nostack --steps 100 --warmup 3 --no-cpu-baseline > $O/benchnostack_$R.json 2> $O/benchnostack_$R.err
 python bench.py --impl reference --steps 10 --warmup 1 > $O/bench_ref_$R.json 2> $O/bench_ref_$R.err
 # launch lists (the bench command that just exited 0, under ncu)
