@@ -33,16 +33,28 @@ struct RegPlan;  // T, E, NST, R[]
 // E = 8 complex per thread (16 doubles) keeps kernels near 64-80 registers.
 #ifndef SLB_WIDE_E
 SLB_REG_PLAN(64, 8, 8, 8)
+#ifndef SLB_PLAN128
 SLB_REG_PLAN(128, 16, 8, 4, 4)
+#else
+SLB_PLAN128
+#endif
 SLB_REG_PLAN(256, 32, 8, 8, 4)
 #ifndef SLB_PLAN512
 SLB_REG_PLAN(512, 64, 8, 8, 8)
 #else
 SLB_PLAN512
 #endif
+#ifndef SLB_PLAN1024
 SLB_REG_PLAN(1024, 128, 8, 8, 4, 4)
+#else
+SLB_PLAN1024
+#endif
 SLB_REG_PLAN(2048, 256, 8, 8, 8, 4)
-SLB_REG_PLAN(192, 16, 4, 4, 4, 3)
+#ifndef SLB_PLAN192
+SLB_REG_PLAN(192, 16, 12, 4, 4)  // radix 12 in registers: 2 exchanges instead of 3 (4,4,4,3)
+#else
+SLB_PLAN192
+#endif
 #else
 SLB_REG_PLAN(64, 8, 8, 8)
 SLB_REG_PLAN(128, 16, 8, 4, 4)
@@ -124,6 +136,35 @@ __device__ __forceinline__ void bfly16(double2* a) {
     for (int i = 0; i < 16; ++i) a[i] = o[i];
 }
 
+// radix-12 = 4 x 3: n = n1 + 3 n2, radix-4 over n2, twiddle w12^{n1 k1},
+// radix-3 over n1; output index k1 + 4 k2
+template <int DIR>
+__device__ __forceinline__ void bfly12(double2* a) {
+    constexpr double h = 0.86602540378443864676;  // sqrt(3)/2
+#pragma unroll
+    for (int n1 = 0; n1 < 3; ++n1) bfly4<DIR>(a[n1], a[n1 + 3], a[n1 + 6], a[n1 + 9]);
+    auto tw = [](double2 v, double c, double s) {  // v * (c + DIR i s)
+        return make_double2(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
+    };
+    a[4] = tw(a[4], h, 0.5);      // n1=1,k1=1: w^1
+    a[7] = tw(a[7], 0.5, h);      // n1=1,k1=2: w^2
+    a[10] = mul_di<DIR>(a[10]);   // n1=1,k1=3: w^3
+    a[5] = tw(a[5], 0.5, h);      // n1=2,k1=1: w^2
+    a[8] = tw(a[8], -0.5, h);     // n1=2,k1=2: w^4
+    a[11] = make_double2(-a[11].x, -a[11].y);  // n1=2,k1=3: w^6
+    double2 o[12];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+        double2 b0 = a[3 * k1], b1 = a[3 * k1 + 1], b2 = a[3 * k1 + 2];
+        bfly3<DIR>(b0, b1, b2);
+        o[k1] = b0;
+        o[k1 + 4] = b1;
+        o[k1 + 8] = b2;
+    }
+#pragma unroll
+    for (int i = 0; i < 12; ++i) a[i] = o[i];
+}
+
 // radix-32 = radix-2 over two radix-16 halves (decimation in time):
 // X[k] = E[k] + w32^k O[k], X[k+16] = E[k] - w32^k O[k].
 template <int DIR>
@@ -177,6 +218,8 @@ __device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
         bfly4<DIR>(v[0], v[1], v[2], v[3]);
     } else if constexpr (R == 8) {
         bfly8<DIR>(v);
+    } else if constexpr (R == 12) {
+        bfly12<DIR>(v);
     } else if constexpr (R == 16) {
         bfly16<DIR>(v);
     } else if constexpr (R == 32) {
