@@ -43,7 +43,7 @@ struct Ax0Cfg {
     static constexpr int TO_MIN_BLOCKS = SLB_AX0_TO_MINB;
 #endif
 #ifndef SLB_AX0_FROM_MINB
-    static constexpr int FROM_MIN_BLOCKS = L <= 128 ? 4 : (L <= 192 ? 5 : 4);  // R -> N
+    static constexpr int FROM_MIN_BLOCKS = 4;  // R -> N (192 with the filter prefetch: 4 beats 5)
 #else
     static constexpr int FROM_MIN_BLOCKS = SLB_AX0_FROM_MINB;
 #endif
@@ -73,6 +73,15 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCK
         for (int m = 0; m < E; ++m) __stcg(d + t + T * m, x[m]);
     }
 }
+
+// filter prefetch up to this line length (measured at 192: N -> R loses 7 %
+// with it, R -> N gains 3.5 % with it at 4 CTAs/SM)
+#ifndef SLB_AX0_PF_TO_MAXL
+#define SLB_AX0_PF_TO_MAXL 128
+#endif
+#ifndef SLB_AX0_PF_FROM_MAXL
+#define SLB_AX0_PF_FROM_MAXL 192
+#endif
 
 enum Ax0Mode : int {
     kAx0Plain = 0,   // no filter
@@ -118,10 +127,9 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     const int k1 = k1_0 + li;
     const double2* s = src + ((long long)k2 * n + k1) * n;
     double2* lb = tile + li * LineBuf<L, false>::N;  // line exchange buffers alias the output tile
-    // L <= 128 (measured): the next band's filter values are synthesised while
-    // this band is in the FFT (DecMul) / before the FFT (RecAcc); at 192 the
-    // extra registers cost more than the latency they hide
-    constexpr bool PF = L <= 128;
+    // PF: the next band's filter values are synthesised while this band is in
+    // the FFT (DecMul) / before the FFT (RecAcc); measured per direction
+    constexpr bool PF = L <= SLB_AX0_PF_TO_MAXL;
     double pn[E];
     if (PF && MODE == kAx0DecMul) {
         const BandDesc3D bd = filt.bands[band0 + g0];
@@ -228,7 +236,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
 #pragma unroll
         for (int m = 0; m < E; ++m) x[m] = tile[aslot<V>(t + T * m, li)];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
-        constexpr bool PF = L <= 128;  // see k3_ax0_to_rot
+        constexpr bool PF = L <= SLB_AX0_PF_FROM_MAXL;  // see k3_ax0_to_rot
         double p[E];  // this band's filter values, synthesised before the FFT
         if (PF && MODE == kAx0RecAcc) {
             const BandDesc3D bd = filt.bands[band0 + b];
