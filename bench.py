@@ -417,7 +417,7 @@ def main():
             "gpu_launches": int(launches),
             "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
                     "d2h_bytes_per_step": frames * N * 8,
-                    "api": ("sl_denoise_batch_host (pinned host in/out; per-frame H2D + fused dec/thr/rec + D2H over the handle's streams)" if not is3d else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
+                    "api": ("sl_denoise_batch_host (pinned host in/out; H2D in frame order on a copy stream, fused dec/thr/rec on 3 compute streams, D2H in frame order on a second copy stream)" if not is3d else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -199,6 +199,7 @@ struct System {
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
     bool materialize = true;        // fused denoise writes the thresholded stack (sl_set_stack_output)
     cudaEvent_t fork_ev = nullptr;
+    std::vector<cudaEvent_t> pipe_ev;  // per-frame H2D / compute-done events of pipelined host batches
     DBuf<double> delta, stack, io_in, io_out;
     std::vector<double> delta_host;  // host copy of `delta` (deltas() skips unchanged uploads)
     int chunk = 1;
@@ -229,8 +230,16 @@ struct System {
     }
     ~System() {
         if (fork_ev) cudaEventDestroy(fork_ev);
+        for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
     }
     // Ensure n workspaces exist (1..n-1 with their own non-blocking streams).
+    void ensure_pipe_events(size_t n) {
+        while (pipe_ev.size() < n) {
+            cudaEvent_t e;
+            SL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            pipe_ev.push_back(e);
+        }
+    }
     void ensure_workspaces(int n) {
         if (!fork_ev) SL_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
         while (static_cast<int>(ws.size()) < n) {

@@ -14,7 +14,7 @@ import paper_1402_5670_b200 as P  # noqa: E402
 
 n, frames = 512, int(sys.argv[1]) if len(sys.argv) > 1 else 8
 s = P.build_system_2d(n, n, P.ScaleProfile.from_levels([1, 1, 2, 2]))
-s.set_streams(int(os.environ.get("SLB_STREAMS", "8")))
+s.set_streams(int(os.environ.get("SLB_STREAMS", "6")))
 sch = P.ThresholdSchedule.defaults_2d(40.0)
 K = np.ascontiguousarray(sch.per_scale_factors, dtype=np.float64)
 Kp = K.ctypes.data_as(C.POINTER(C.c_double))
