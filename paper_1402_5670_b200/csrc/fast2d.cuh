@@ -318,8 +318,14 @@ __device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots,
 }
 
 // rec: slot[g] = sum_{b in group g} FFT_0(inter[b]) * psi_b.
+#ifndef SLB_COLREC_REGACC
+#define SLB_COLREC_REGACC 0  // 1: accumulator in registers instead of shared memory (A/B)
+#endif
+#ifndef SLB_COLREC_MINB
+#define SLB_COLREC_MINB ColCfg<L>::MIN_BLOCKS
+#endif
 template <int L>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
                 double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
                 const double2* __restrict__ tw, int* __restrict__ done, int nslots, const double* __restrict__ WT,
@@ -335,8 +341,12 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     const bool valid = k1 < H;
     double2* sm = lbuf + li * (LineBuf<L>::N + L);
     double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
+    double2 ar[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
+    for (int m = 0; m < E; ++m) {
+        ar[m] = make_double2(0.0, 0.0);
+        if (!SLB_COLREC_REGACC) acc[t + T * m] = ar[m];
+    }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
     for (int bb = 0; bb < gn; ++bb) {
@@ -353,17 +363,20 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
         reg_fft<L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            double2 a = acc[t + T * m];
+            double2 a = SLB_COLREC_REGACC ? ar[m] : acc[t + T * m];
             a.x = fma(x[m].x, p[m], a.x);
             a.y = fma(x[m].y, p[m], a.y);
-            acc[t + T * m] = a;
+            if (SLB_COLREC_REGACC)
+                ar[m] = a;
+            else
+                acc[t + T * m] = a;
         }
         line_sync<T>();
     }
     if (valid) {
         double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
 #pragma unroll
-        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, acc[t + T * m]);
+        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, SLB_COLREC_REGACC ? ar[m] : acc[t + T * m]);
     }
     if (done == nullptr) return;
     // last chunk: the CTA that finishes its column block last sums every slot

@@ -280,6 +280,20 @@ def test_batched_api_matches_per_frame(cuda):
         P.denoise_batch(ft[:, :128], s, sch)
 
 
+@pytest.mark.parametrize("pipe", ["0", "1", "3", "6"])
+def test_host_batch_pipelines_agree(cuda, monkeypatch, pipe):
+    # the pipelined host batch (copy streams + SLB_HOST_PIPE compute streams)
+    # and the per-frame fan-out return the per-frame result for every frame
+    s = system(128, 128, [1, 2])
+    sch = P.ThresholdSchedule.defaults_2d(25.0, 2)
+    frames = np.stack([P.add_gaussian_noise(P.cartoon(128), 25.0, 40 + i) for i in range(7)])
+    monkeypatch.setenv("SLB_HOST_PIPE", pipe)
+    got = P.denoise_batch(frames, s, sch)
+    for i in range(7):
+        one = P.denoise(frames[i], s, sch)
+        assert np.linalg.norm(got[i] - one) <= 1e-12 * np.linalg.norm(one)
+
+
 @pytest.mark.parametrize("shape,levels", [((64, 64), [0, 0, 1, 1]), ((128, 128), [1, 1, 2]), ((48, 80), [0, 1])])
 def test_gpu_tap_construction_matches_host_taps(cuda, shape, levels, monkeypatch):
     # upsampling, separable convolutions and the digital shear run on the GPU
