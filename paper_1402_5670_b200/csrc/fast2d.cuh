@@ -89,6 +89,22 @@ static size_t col2_smem_bytes() {  // exchange buffer + a second L-line (F colum
     return static_cast<size_t>(ColCfg<L>::LINES) * (LineBuf<L>::N + L) * sizeof(double2);
 }
 
+// accumulator in registers (measured: cols_rec<512> -6 %, <1024> -10 %); at
+// 192 it spills under the 128-register cap, so that length keeps the
+// shared-memory accumulator
+template <int L>
+struct ColRec {
+#ifndef SLB_COLREC_REGACC
+    static constexpr bool REGACC = L != 192;
+#else
+    static constexpr bool REGACC = SLB_COLREC_REGACC;
+#endif
+};
+template <int L>
+static size_t colrec_smem_bytes() {  // register accumulator: exchange buffers only
+    return ColRec<L>::REGACC ? col1_smem_bytes<L>() : col2_smem_bytes<L>();
+}
+
 // ---------------------------------------------------------------- rows c2r
 // In : src[k1 * n0 + r] (column-major half spectrum), bands strided by sbs.
 // Out: dst[r * L + i] real rows, scaled, optionally thresholded (delta >= 0).
@@ -318,9 +334,6 @@ __device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots,
 }
 
 // rec: slot[g] = sum_{b in group g} FFT_0(inter[b]) * psi_b.
-#ifndef SLB_COLREC_REGACC
-#define SLB_COLREC_REGACC 0  // 1: accumulator in registers instead of shared memory (A/B)
-#endif
 #ifndef SLB_COLREC_MINB
 #define SLB_COLREC_MINB ColCfg<L>::MIN_BLOCKS
 #endif
@@ -339,13 +352,14 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * (LineBuf<L>::N + L);
+    // per line: [exchange L] (+ [accumulator L] unless it lives in registers)
+    double2* sm = lbuf + li * (LineBuf<L>::N + (ColRec<L>::REGACC ? 0 : L));
     double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
     double2 ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         ar[m] = make_double2(0.0, 0.0);
-        if (!SLB_COLREC_REGACC) acc[t + T * m] = ar[m];
+        if (!ColRec<L>::REGACC) acc[t + T * m] = ar[m];
     }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
@@ -363,10 +377,10 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
         reg_fft<L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            double2 a = SLB_COLREC_REGACC ? ar[m] : acc[t + T * m];
+            double2 a = ColRec<L>::REGACC ? ar[m] : acc[t + T * m];
             a.x = fma(x[m].x, p[m], a.x);
             a.y = fma(x[m].y, p[m], a.y);
-            if (SLB_COLREC_REGACC)
+            if (ColRec<L>::REGACC)
                 ar[m] = a;
             else
                 acc[t + T * m] = a;
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     if (valid) {
         double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
 #pragma unroll
-        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, SLB_COLREC_REGACC ? ar[m] : acc[t + T * m]);
+        for (int m = 0; m < E; ++m) __stcg(o + t + T * m, ColRec<L>::REGACC ? ar[m] : acc[t + T * m]);
     }
     if (done == nullptr) return;
     // last chunk: the CTA that finishes its column block last sums every slot

@@ -302,7 +302,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     set_smem(k2_cols_sum<L0, -1>, col_smem);
     set_smem(k2_cols_sum<L0, +1>, col_smem);
     set_smem(k2_cols_dec<L0>, col2_smem);
-    set_smem(k2_cols_rec<L0>, col2_smem);
+    set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     if (s.w->done.n < static_cast<size_t>(col_blocks)) {  // zeroed once; the kernel resets its counters
@@ -340,7 +340,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
             LaunchScope ls(s, "f2_cols_rec", st, cb);
             // the last chunk's CTAs also finish the reconstruction (k2_cols_rec)
             const bool fin = b0 + cb >= nb;
-            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, colrec_smem_bytes<L0>(), st>>>(
                 s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
                 fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p);
             check_launch("k2_cols_rec");
@@ -385,7 +385,7 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);
     set_smem(k2_cols_dec<L0>, col2_smem);
-    set_smem(k2_cols_rec<L0>, col2_smem);
+    set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     const size_t ndone = static_cast<size_t>(col_blocks) * nf;
@@ -424,7 +424,7 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
         {
             LaunchScope ls(s, "f2_cols_rec", st, static_cast<long long>(cb) * nf);
             const bool fin = b0 + cb >= nb;
-            k2_cols_rec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, col2_smem, st>>>(
+            k2_cols_rec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, colrec_smem_bytes<L0>(), st>>>(
                 s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
                 fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p, izs, szs, izs);
             check_launch("k2_cols_rec");

@@ -116,7 +116,7 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
     const size_t col2_smem = col2_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
-    set_smem(k2_cols_rec<L0>, col2_smem);
+    set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
     set_smem(k2_cols_sum<L0, +1>, col_smem);
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
@@ -138,7 +138,7 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
             LaunchScope ls(s, "f2_cols_rec", st, cb);
             // the last chunk's CTAs also finish the reconstruction (k2_cols_rec)
             const bool fin = b0 + cb >= nb;
-            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
+            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, colrec_smem_bytes<L0>(), st>>>(
                 s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
                 fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p);
             check_launch("k2_cols_rec");
