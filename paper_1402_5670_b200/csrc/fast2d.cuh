@@ -227,8 +227,27 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
 // Column k1 of a column-major half spectrum is the contiguous line src[k1 * L ...].
 
 // dec: inter[b] = IFFT_0(F * psi_b) for the G bands of this CTA's group.
+// F column in registers instead of shared memory at 3 CTAs/SM (measured per
+// length: cols_dec<512> -4 %, <256> -8 %; <1024> +7 %, kept in shared memory)
 template <int L>
-__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
+struct ColDec {
+#ifndef SLB_COLDEC_REGF
+    static constexpr bool REGF = L == 256 || L == 512;
+#else
+    static constexpr bool REGF = SLB_COLDEC_REGF;
+#endif
+#ifndef SLB_COLDEC_MINB
+    static constexpr int MIN_BLOCKS = REGF ? 3 : ColCfg<L>::MIN_BLOCKS;
+#else
+    static constexpr int MIN_BLOCKS = SLB_COLDEC_MINB;
+#endif
+};
+template <int L>
+static size_t coldec_smem_bytes() {
+    return ColDec<L>::REGF ? col1_smem_bytes<L>() : col2_smem_bytes<L>();
+}
+template <int L>
+__global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
     k2_cols_dec(const double2* __restrict__ FT, const double* __restrict__ psiT, long long pbs,
                 double2* __restrict__ inter, long long ibs, int H, int band0, int G, int nb,
                 const double2* __restrict__ tw, long long fzs = 0, long long izs = 0) {
@@ -239,21 +258,22 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * (LineBuf<L>::N + L);
+    double2* sm = lbuf + li * (LineBuf<L>::N + (ColDec<L>::REGF ? 0 : L));
     double2* fs = sm + LineBuf<L>::N;
-#ifndef SLB_NO_CPASYNC
+    double2 fr[E];
+    if (ColDec<L>::REGF) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-        if (valid)
-            cp_async16(fs + t + T * m, FT + (long long)k1 * L + t + T * m);
-        else
-            fs[t + T * m] = make_double2(0.0, 0.0);
+        for (int m = 0; m < E; ++m) fr[m] = valid ? __ldg(FT + (long long)k1 * L + t + T * m) : make_double2(0.0, 0.0);
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            if (valid)
+                cp_async16(fs + t + T * m, FT + (long long)k1 * L + t + T * m);
+            else
+                fs[t + T * m] = make_double2(0.0, 0.0);
+        }
+        cp_async_wait_all();
     }
-    cp_async_wait_all();
-#else
-#pragma unroll
-    for (int m = 0; m < E; ++m) fs[t + T * m] = valid ? __ldg(FT + (long long)k1 * L + t + T * m) : make_double2(0.0, 0.0);
-#endif
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
     // psi of band b+1 is loaded while band b is in the FFT
@@ -268,7 +288,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColCfg<L>::MIN_BLOCKS)
         double2 x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double2 fv = fs[t + T * m];
+            const double2 fv = ColDec<L>::REGF ? fr[m] : fs[t + T * m];
             x[m] = make_double2(fv.x * p[m], fv.y * p[m]);  // conj(psi) * F, psi real
         }
         if (bb + 1 < gn) {

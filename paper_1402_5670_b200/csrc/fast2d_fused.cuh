@@ -296,7 +296,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     using CC = ColCfg<L0>;
     const size_t row_smem = row_smem_bytes<L1>(H);
     const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = col2_smem_bytes<L0>();
+    const size_t col2_smem = coldec_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);
@@ -380,7 +380,7 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
     using CC = ColCfg<L0>;
     const size_t row_smem = row_smem_bytes<L1>(H);
     const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = col2_smem_bytes<L0>();
+    const size_t col2_smem = coldec_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);

@@ -60,7 +60,7 @@ static void dec2d_fast_t(System& s, const double* f, double* out, const double* 
     using CC = ColCfg<L0>;
     const size_t row_smem = row_smem_bytes<L1>(H);
     const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = col2_smem_bytes<L0>();
+    const size_t col2_smem = coldec_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_sum<L0, -1>, col_smem);
@@ -113,7 +113,7 @@ static void rec2d_fast_t(System& s, const double* coeffs, double* out, cudaStrea
     using CC = ColCfg<L0>;
     const size_t row_smem = row_smem_bytes<L1>(H);
     const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = col2_smem_bytes<L0>();
+    const size_t col2_smem = coldec_smem_bytes<L0>();
     set_smem(k2_rows_r2c<L1>, row_smem);
     set_smem(k2_rows_c2r<L1>, row_smem);
     set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
