@@ -36,9 +36,10 @@ struct Ax0Cfg {
     static constexpr int THREADS = V * T;
     // occupancy targets (CTAs/SM, measured at 128^3 / 192^3; overridable for A/B builds)
 #ifndef SLB_AX0_TO_MINB
-    // N -> R (192: <= 85 registers; 256: 4 CTAs of 256 threads, 64 registers:
-    // 36.2 vols/s at 256^3 vs 35.1 with 3 and 32.3 with 2)
-    static constexpr int TO_MIN_BLOCKS = L <= 128 ? 4 : (L <= 192 ? 6 : 4);
+    // N -> R (192: 4 CTAs, 128 registers with the F line held in registers --
+    // 6 CTAs at <= 85 registers without it; 256: 4 CTAs of 256 threads, 64
+    // registers: 36.2 vols/s at 256^3 vs 35.1 with 3 and 32.3 with 2)
+    static constexpr int TO_MIN_BLOCKS = 4;
 #else
     static constexpr int TO_MIN_BLOCKS = SLB_AX0_TO_MINB;
 #endif
@@ -74,6 +75,14 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCK
     }
 }
 
+// N -> R keeps the F line in registers across the band group at 192 (with
+// 4 CTAs/SM: ax0 dec -4 %); at 128 it measured slower
+#ifndef SLB_AX0_TO_REGF
+#define SLB_AX0_TO_REGF(L) ((L) == 192)
+#endif
+#ifndef SLB_AX0_FROM_REGACC
+#define SLB_AX0_FROM_REGACC 0  // A/B: R -> N band sum in registers
+#endif
 // filter prefetch up to this line length (measured at 192: N -> R loses 7 %
 // with it, R -> N gains 3.5 % with it at 4 CTAs/SM)
 #ifndef SLB_AX0_PF_TO_MAXL
@@ -130,6 +139,13 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     // PF: the next band's filter values are synthesised while this band is in
     // the FFT (DecMul) / before the FFT (RecAcc); measured per direction
     constexpr bool PF = L <= SLB_AX0_PF_TO_MAXL;
+    // REGF: DecMul's F line loaded once into registers for the whole band group
+    constexpr bool REGF = MODE == kAx0DecMul && SLB_AX0_TO_REGF(L);
+    double2 fr[E];
+    if (REGF) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) fr[m] = __ldg(s + t + T * m);
+    }
     double pn[E];
     if (PF && MODE == kAx0DecMul) {
         const BandDesc3D bd = filt.bands[band0 + g0];
@@ -143,7 +159,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k0 = t + T * m;
-            double2 z = MODE == kAx0DecMul ? __ldg(s + k0) : __ldcg(s + k0);
+            double2 z = REGF ? fr[m] : (MODE == kAx0DecMul ? __ldg(s + k0) : __ldcg(s + k0));
             if (MODE == kAx0DecMul) {
                 const double p = PF ? pn[m] : filt.get_d(bd, k0, k1, k2);
                 z = make_double2(z.x * p, z.y * p);
@@ -219,9 +235,14 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
     // RecAcc: per-thread accumulator slots after the tile (acc[li][t + T m]),
     // registers stay free for the FFT line
     double2* acc = tile + V * LineBuf<L, false>::N + li * L;
+    constexpr bool REGACC = MODE == kAx0RecAcc && SLB_AX0_FROM_REGACC;
+    double2 ar[E];
     if (MODE == kAx0RecAcc) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) acc[t + T * m] = make_double2(0.0, 0.0);
+        for (int m = 0; m < E; ++m) {
+            ar[m] = make_double2(0.0, 0.0);
+            if (!REGACC) acc[t + T * m] = ar[m];
+        }
     }
     double2 x[E];
     for (int b = 0; b < nb; ++b) {
@@ -249,10 +270,13 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const double p_ = PF ? p[m] : filt.get_d(bd, t + T * m, k1, k2);
-                double2 a = acc[t + T * m];
+                double2 a = REGACC ? ar[m] : acc[t + T * m];
                 a.x = fma(x[m].x, p_, a.x);
                 a.y = fma(x[m].y, p_, a.y);
-                acc[t + T * m] = a;
+                if (REGACC)
+                    ar[m] = a;
+                else
+                    acc[t + T * m] = a;
             }
             (void)bd;
         }
@@ -261,7 +285,7 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
     if (MODE == kAx0RecAcc) {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            double2 v = acc[t + T * m];
+            double2 v = REGACC ? ar[m] : acc[t + T * m];
             if (accumulate) {
                 const double2 o = __ldcg(d + t + T * m);
                 v = make_double2(o.x + v.x, o.y + v.y);
