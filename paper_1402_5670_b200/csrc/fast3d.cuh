@@ -83,13 +83,16 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCK
 #ifndef SLB_AX0_FROM_REGACC
 #define SLB_AX0_FROM_REGACC 0  // A/B: R -> N band sum in registers
 #endif
+#ifndef SLB_AX0_LINEFILT
+#define SLB_AX0_LINEFILT 1  // per-line filter setup (FiltSynth3D::ax0_line); 0: get_d per element (A/B)
+#endif
 // filter prefetch up to this line length (measured at 192: N -> R loses 7 %
 // with it, R -> N gains 3.5 % with it at 4 CTAs/SM)
 #ifndef SLB_AX0_PF_TO_MAXL
 #define SLB_AX0_PF_TO_MAXL 128
 #endif
 #ifndef SLB_AX0_PF_FROM_MAXL
-#define SLB_AX0_PF_FROM_MAXL 192
+#define SLB_AX0_PF_FROM_MAXL 128
 #endif
 
 enum Ax0Mode : int {
@@ -149,19 +152,22 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     double pn[E];
     if (PF && MODE == kAx0DecMul) {
         const BandDesc3D bd = filt.bands[band0 + g0];
+        const FiltSynth3D::Ax0Line fl = filt.ax0_line(bd, k1, k2);
 #pragma unroll
-        for (int m = 0; m < E; ++m) pn[m] = filt.get_d(bd, t + T * m, k1, k2);
+        for (int m = 0; m < E; ++m) pn[m] = SLB_AX0_LINEFILT ? fl.at(t + T * m) : filt.get_d(bd, t + T * m, k1, k2);
     }
     for (int bb = 0; bb < gn; ++bb) {
         BandDesc3D bd{};
         if (MODE == kAx0DecMul) bd = filt.bands[band0 + g0 + bb];
+        FiltSynth3D::Ax0Line fl{};
+        if (MODE == kAx0DecMul && !PF) fl = filt.ax0_line(bd, k1, k2);
         double2 x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k0 = t + T * m;
             double2 z = REGF ? fr[m] : (MODE == kAx0DecMul ? __ldg(s + k0) : __ldcg(s + k0));
             if (MODE == kAx0DecMul) {
-                const double p = PF ? pn[m] : filt.get_d(bd, k0, k1, k2);
+                const double p = PF ? pn[m] : (SLB_AX0_LINEFILT ? fl.at(k0) : filt.get_d(bd, k0, k1, k2));
                 z = make_double2(z.x * p, z.y * p);
             } else if (MODE == kAx0DivW) {
                 const double w = __ldg(WN + ((long long)k2 * n + k1) * n + k0);
@@ -171,8 +177,9 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
         }
         if (PF && MODE == kAx0DecMul && bb + 1 < gn) {
             const BandDesc3D bn = filt.bands[band0 + g0 + bb + 1];
+            const FiltSynth3D::Ax0Line fn = filt.ax0_line(bn, k1, k2);
 #pragma unroll
-            for (int m = 0; m < E; ++m) pn[m] = filt.get_d(bn, t + T * m, k1, k2);
+            for (int m = 0; m < E; ++m) pn[m] = SLB_AX0_LINEFILT ? fn.at(t + T * m) : filt.get_d(bn, t + T * m, k1, k2);
         }
         if (bb > 0) {
             if (TMA && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -261,15 +268,18 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::FROM_MIN_BLOCKS
         double p[E];  // this band's filter values, synthesised before the FFT
         if (PF && MODE == kAx0RecAcc) {
             const BandDesc3D bd = filt.bands[band0 + b];
+            const FiltSynth3D::Ax0Line fl = filt.ax0_line(bd, k1, k2);
 #pragma unroll
-            for (int m = 0; m < E; ++m) p[m] = filt.get_d(bd, t + T * m, k1, k2);
+            for (int m = 0; m < E; ++m) p[m] = SLB_AX0_LINEFILT ? fl.at(t + T * m) : filt.get_d(bd, t + T * m, k1, k2);
         }
         reg_fft<L, DIR, false>(x, lb, t, tw);
         if (MODE == kAx0RecAcc) {
             const BandDesc3D bd = filt.bands[band0 + b];
+            FiltSynth3D::Ax0Line fl{};
+            if (!PF) fl = filt.ax0_line(bd, k1, k2);
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const double p_ = PF ? p[m] : filt.get_d(bd, t + T * m, k1, k2);
+                const double p_ = PF ? p[m] : (SLB_AX0_LINEFILT ? fl.at(t + T * m) : filt.get_d(bd, t + T * m, k1, k2));
                 double2 a = REGACC ? ar[m] : acc[t + T * m];
                 a.x = fma(x[m].x, p_, a.x);
                 a.y = fma(x[m].y, p_, a.y);

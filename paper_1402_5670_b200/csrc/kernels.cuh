@@ -75,6 +75,54 @@ struct FiltSynth3D {
         return __ldg(tab1d + d.g_off + p) * __ldg(tab2d + d.p1_off + p * ns1 + a) *
                __ldg(tab2d + d.p2_off + p * ns2 + b);
     }
+    // An axis-0 line (k1, k2 fixed, k0 varying) of one band: only the factors
+    // indexed by k0 are loaded per element, the others once per line. Value
+    // = three ? (A[k0] B[k0]) C[k0] : (c1 A[k0]) c2 -- the same products in
+    // the same order as get_d (IEEE multiplication commutes), so bit-identical.
+    struct Ax0Line {
+        const double *A, *B, *C;
+        double c1, c2;
+        bool three;
+        __device__ __forceinline__ double at(int k0) const {
+            return three ? (__ldg(A + k0) * __ldg(B + k0)) * __ldg(C + k0) : (c1 * __ldg(A + k0)) * c2;
+        }
+    };
+    __device__ __forceinline__ Ax0Line ax0_line(const BandDesc3D& d, int k1, int k2) const {
+        Ax0Line l{};
+        if (d.kind == 0) {  // (hJ0[k0] hJ1[k1]) hJ2[k2]
+            l.three = false;
+            l.A = tab1d + lp_off[0];
+            l.c1 = __ldg(tab1d + lp_off[1] + k1);
+            l.c2 = __ldg(tab1d + lp_off[2] + k2);
+            return l;
+        }
+        auto len = [&](int ax) { return ax == 0 ? n[0] : (ax == 1 ? n[1] : n[2]); };
+        const int ns1 = len(d.s1), ns2 = len(d.s2);
+        if (d.pa == 0) {  // every factor runs along k0 (transposed planes)
+            const int np = n[0];
+            const int a = d.s1 == 1 ? k1 : k2, b = d.s2 == 1 ? k1 : k2;
+            l.three = true;
+            l.A = tab1d + d.g_off;
+            l.B = tab2d + d.p1_off + np * ns1 + a * np;
+            l.C = tab2d + d.p2_off + np * ns2 + b * np;
+            return l;
+        }
+        const int p = d.pa == 1 ? k1 : k2;
+        const double g = __ldg(tab1d + d.g_off + p);
+        l.three = false;
+        if (d.s1 == 0) {  // (g Phi1[p][k0]) Phi2[p][b]
+            const int b = d.s2 == 1 ? k1 : k2;
+            l.A = tab2d + d.p1_off + p * ns1;
+            l.c1 = g;
+            l.c2 = __ldg(tab2d + d.p2_off + p * ns2 + b);
+        } else {  // (g Phi1[p][a]) Phi2[p][k0]
+            const int a = d.s1 == 1 ? k1 : k2;
+            l.A = tab2d + d.p2_off + p * ns2;
+            l.c1 = g * __ldg(tab2d + d.p1_off + p * ns1 + a);
+            l.c2 = 1.0;
+        }
+        return l;
+    }
 };
 
 // ------------------------------------------------------------------ rows pass
