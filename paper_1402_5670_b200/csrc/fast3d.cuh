@@ -75,10 +75,11 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCK
     }
 }
 
-// N -> R keeps the F line in registers across the band group at 192 (with
-// 4 CTAs/SM: ax0 dec -4 %); at 128 it measured slower
+// N -> R keeps the F line in registers across the band group at 128 / 192
+// (4 CTAs/SM; with the per-line filter setup: ax0 dec -12 % at 192 vs 6 CTAs
+// without it, -1.5 % at 128 together with no filter prefetch there)
 #ifndef SLB_AX0_TO_REGF
-#define SLB_AX0_TO_REGF(L) ((L) == 192)
+#define SLB_AX0_TO_REGF(L) ((L) == 128 || (L) == 192)
 #endif
 #ifndef SLB_AX0_FROM_REGACC
 #define SLB_AX0_FROM_REGACC 0  // A/B: R -> N band sum in registers
@@ -86,10 +87,10 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, Ax0Cfg<L>::LINES_MIN_BLOCK
 #ifndef SLB_AX0_LINEFILT
 #define SLB_AX0_LINEFILT 1  // per-line filter setup (FiltSynth3D::ax0_line); 0: get_d per element (A/B)
 #endif
-// filter prefetch up to this line length (measured at 192: N -> R loses 7 %
-// with it, R -> N gains 3.5 % with it at 4 CTAs/SM)
+// filter prefetch up to this line length (measured with the per-line filter
+// setup: it pays only at 64 for N -> R and up to 128 for R -> N)
 #ifndef SLB_AX0_PF_TO_MAXL
-#define SLB_AX0_PF_TO_MAXL 128
+#define SLB_AX0_PF_TO_MAXL 64
 #endif
 #ifndef SLB_AX0_PF_FROM_MAXL
 #define SLB_AX0_PF_FROM_MAXL 128
