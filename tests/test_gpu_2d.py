@@ -342,7 +342,8 @@ def test_run_to_run_bit_identical(cuda):
 def test_stack_free_denoise_same_result(cuda):
     # sl_set_stack_output(0): the fused denoise never writes the stack; same reconstruction
     import torch
-    for shape, lv, mk in (((512, 512), [1, 1, 2, 2], P.build_system_2d), ((64, 64, 64), [0, 1], P.build_system_3d)):
+    for shape, lv, mk in (((512, 512), [1, 1, 2, 2], P.build_system_2d), ((64, 64, 64), [0, 1], P.build_system_3d),
+                          ((128, 128, 128), [0, 1], P.build_system_3d), ((192, 192, 192), [0], P.build_system_3d)):
         prof = P.ScaleProfile.from_levels(lv)
         s = mk(*shape, prof) if len(shape) == 2 else mk(shape, prof)
         sch = (P.ThresholdSchedule.defaults_2d if len(shape) == 2 else P.ThresholdSchedule.defaults_3d)(0.2, len(lv))
