@@ -42,17 +42,18 @@ template <int L>
 struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
 #ifndef SLB_ROW_THREADS
-    // 256 threads; 192 (the 3D rows pass) measured faster with 128 at 6 CTAs/SM
-    static constexpr int V = ((L == 192 ? 128 : 256) / T) > 0 ? (L == 192 ? 128 : 256) / T : 1;
+    // 256 threads; 192 (the 3D rows pass) measured faster with 64 at 12 CTAs/SM
+    // (fused rows -3 % vs 128 threads at 6, +18 % slower with 32 threads)
+    static constexpr int V = ((L == 192 ? 64 : 256) / T) > 0 ? (L == 192 ? 64 : 256) / T : 1;
 #else
     static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
 #endif
     static constexpr int THREADS = V * T;
 #ifndef SLB_FUSED_MINB
     // explicit occupancy targets (measured): without them ptxas takes 124-154
-    // registers; 4 CTAs/SM (<= 64 registers) except 192 (6 CTAs of 128 threads,
+    // registers; 4 CTAs/SM (<= 64 registers) except 192 (12 CTAs of 64 threads,
     // <= 85 registers) and 2048 (2)
-    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 6 : (L == 2048 ? 2 : 4);
+    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 12 : (L == 2048 ? 2 : 4);
 #else
     static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
 #endif
