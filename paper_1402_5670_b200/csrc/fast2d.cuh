@@ -43,8 +43,10 @@ struct RowCfg {
     static constexpr int T = RegPlan<L>::T;
 #ifndef SLB_ROW_THREADS
     // 256 threads; 192 (the 3D rows pass) measured faster with 64 at 12 CTAs/SM
-    // (fused rows -3 % vs 128 threads at 6, +18 % slower with 32 threads)
-    static constexpr int V = ((L == 192 ? 64 : 256) / T) > 0 ? (L == 192 ? 64 : 256) / T : 1;
+    // (fused rows -3 % vs 128 threads at 6, +18 % slower with 32 threads) and
+    // 1024 with 512 at 2 CTAs/SM (2D 1024^2 +2.4 %)
+    static constexpr int NT = L == 192 ? 64 : (L == 1024 ? 512 : 256);
+    static constexpr int V = (NT / T) > 0 ? NT / T : 1;
 #else
     static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
 #endif
@@ -52,8 +54,8 @@ struct RowCfg {
 #ifndef SLB_FUSED_MINB
     // explicit occupancy targets (measured): without them ptxas takes 124-154
     // registers; 4 CTAs/SM (<= 64 registers) except 192 (12 CTAs of 64 threads,
-    // <= 85 registers) and 2048 (2)
-    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 12 : (L == 2048 ? 2 : 4);
+    // <= 85 registers), 1024 (2 of 512 threads) and 2048 (2)
+    static constexpr int FUSED_MIN_BLOCKS = L == 192 ? 12 : ((L == 2048 || L == 1024) ? 2 : 4);
 #else
     static constexpr int FUSED_MIN_BLOCKS = SLB_FUSED_MINB;
 #endif
