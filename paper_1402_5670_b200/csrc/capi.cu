@@ -625,20 +625,31 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             SL_CUDA(cudaEventRecord(s.fork_ev, st));
             for (int k = 1; k <= P + 2; ++k) SL_CUDA(cudaStreamWaitEvent(s.ws[static_cast<size_t>(k)]->st, s.fork_ev, 0));
             const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);
-            s.concurrency = P;
+            s.concurrency = env_int("SLB_PIPE_CONC", P);  // band grouping of fast2d_cfg
+            // SLB_PIPE_GROUP = 2: lock-step frame pairs per compute stream (one
+            // launch per pass covers both frames, as in the device batch)
+            const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, env_int("SLB_PIPE_GROUP", 1))) : 1;
+            if (grp > 1 && s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+            const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
+            const int ngroups = (nframes + grp - 1) / grp;
             try {
-                for (int f = 0; f < nframes; ++f) {
-                    const size_t off = static_cast<size_t>(f) * s.nreal;
-                    cudaEvent_t ein = s.pipe_ev[2 * static_cast<size_t>(f)], ec = s.pipe_ev[2 * static_cast<size_t>(f) + 1];
-                    SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, fb, cudaMemcpyHostToDevice, cin));
+                for (int g = 0; g < ngroups; ++g) {
+                    const int f0 = g * grp, nf = std::min(grp, nframes - f0);
+                    const size_t off = static_cast<size_t>(f0) * s.nreal;
+                    cudaEvent_t ein = s.pipe_ev[2 * static_cast<size_t>(g)], ec = s.pipe_ev[2 * static_cast<size_t>(g) + 1];
+                    SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, nf * fb, cudaMemcpyHostToDevice, cin));
                     SL_CUDA(cudaEventRecord(ein, cin));
-                    s.w = s.ws[static_cast<size_t>(1 + f % P)].get();
+                    s.w = s.ws[static_cast<size_t>(1 + g % P)].get();
                     SL_CUDA(cudaStreamWaitEvent(s.w->st, ein, 0));
-                    s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-                    denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, s.w->st);
+                    s.w->stack.alloc(static_cast<size_t>(grp) * sfs);
+                    if (grp > 1)
+                        denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs,
+                                             s.io_out.p + off, s.nreal, s.delta.p, s.w->st);
+                    else
+                        denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, s.w->st);
                     SL_CUDA(cudaEventRecord(ec, s.w->st));
                     SL_CUDA(cudaStreamWaitEvent(cout, ec, 0));
-                    SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, fb, cudaMemcpyDeviceToHost, cout));
+                    SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, nf * fb, cudaMemcpyDeviceToHost, cout));
                 }
             } catch (...) {
                 s.w = s.ws[0].get();

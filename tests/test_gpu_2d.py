@@ -280,14 +280,16 @@ def test_batched_api_matches_per_frame(cuda):
         P.denoise_batch(ft[:, :128], s, sch)
 
 
-@pytest.mark.parametrize("pipe", ["0", "1", "3", "6"])
-def test_host_batch_pipelines_agree(cuda, monkeypatch, pipe):
-    # the pipelined host batch (copy streams + SLB_HOST_PIPE compute streams)
-    # and the per-frame fan-out return the per-frame result for every frame
+@pytest.mark.parametrize("pipe,group", [("0", "1"), ("1", "1"), ("3", "1"), ("6", "1"), ("3", "2"), ("2", "3")])
+def test_host_batch_pipelines_agree(cuda, monkeypatch, pipe, group):
+    # the pipelined host batch (copy streams + SLB_HOST_PIPE compute streams,
+    # SLB_PIPE_GROUP lock-step frames per stream, ragged last group) and the
+    # per-frame fan-out return the per-frame result for every frame
     s = system(128, 128, [1, 2])
     sch = P.ThresholdSchedule.defaults_2d(25.0, 2)
     frames = np.stack([P.add_gaussian_noise(P.cartoon(128), 25.0, 40 + i) for i in range(7)])
     monkeypatch.setenv("SLB_HOST_PIPE", pipe)
+    monkeypatch.setenv("SLB_PIPE_GROUP", group)
     got = P.denoise_batch(frames, s, sch)
     for i in range(7):
         one = P.denoise(frames[i], s, sch)
