@@ -12,6 +12,10 @@
 #include "fast2d_host.cuh"
 #include "tma.cuh"
 
+#ifndef SLB_ROWS_DIRECT_STORE
+#define SLB_ROWS_DIRECT_STORE 0
+#endif
+
 namespace slb {
 
 // STORE = false: the stack is not materialised (sl_set_stack_output, band
@@ -95,6 +99,22 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
             zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
         }
     }
+#if SLB_ROWS_DIRECT_STORE
+    // rows 2q and 2q+1 of spectrum column k are one aligned 32-byte sector of
+    // the column-major intermediate: store straight from registers (no tile
+    // round trip through shared memory, no barriers)
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            double2* dst = inter + (long long)k * n0 + r0 + 2 * q;
+            if (2 * q < nrows)
+                __stcg(dst, make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y)));
+            if (2 * q + 1 < nrows)
+                __stcg(dst + 1, make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x)));
+        }
+    }
+#else
     __syncthreads();  // all line buffers read before the tile is rewritten
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
@@ -109,6 +129,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
         if (rr < nrows) __stcg(inter + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
     }
+#endif
 }
 
 // TMA variant of k2_rows_fused (2V = 8 rows, 128-byte tile rows): the
