@@ -27,7 +27,7 @@ struct Fast2DCfg {
     int G, C;
 };
 // Measured (tools/sweep2d.sh, tools/single2d.py): with >= 4 frames in flight on
-// other streams the SMs stay busy, and G = 14 cuts the slot traffic of the rec
+// other streams the SMs stay busy, and G = 14-28 cuts the slot traffic of the rec
 // sum (16 Nh per G bands) and the F re-reads, chunks of ~64 MiB; a lone frame
 // takes every band in one chunk (up to 256 MiB) so each pass is one
 // full-machine launch, G = 7 from 512^2 up.
@@ -39,8 +39,12 @@ static Fast2DCfg fast2d_cfg(const System& s) {
         const int C = env_int("SLB_CHUNK1", std::max(G, static_cast<int>((256.0 * 1024 * 1024) / per)));
         return {G, std::max(1, C)};
     }
-    const int G = env_int("SLB_GROUP", 14);
-    int C = env_int("SLB_CHUNK", std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per)));
+    // G = 28 where 28 bands fit the 64 MiB chunk (512^2: one group per chunk,
+    // +1.2 % over G = 14 after the register-resident column state, r1o sweep),
+    // else 14 (1024^2: chunks of 14)
+    const int cfit = std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per));
+    const int G = env_int("SLB_GROUP", cfit >= 28 ? 28 : 14);
+    int C = env_int("SLB_CHUNK", cfit);
     C = std::max(G, (C / G) * G);
     return {G, C};
 }
