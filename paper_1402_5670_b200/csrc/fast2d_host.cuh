@@ -35,7 +35,10 @@ static Fast2DCfg fast2d_cfg(const System& s) {
     const bool conc = s.concurrency >= 4;
     const double per = static_cast<double>(s.H) * s.n[0] * sizeof(double2);
     if (!conc) {
-        const int G = env_int("SLB_GROUP1", s.n[0] >= 512 ? 7 : 4);
+        // 2-3 frames in flight (the pipelined host batch's 3 compute streams):
+        // G = 14 at 512^2 (e2e +2 % over 7, r1p tools/ab_group1.sh)
+        const int G = s.concurrency > 1 ? env_int("SLB_GROUP2", s.n[0] >= 512 ? 14 : 4)
+                                        : env_int("SLB_GROUP1", s.n[0] >= 512 ? 7 : 4);
         const int C = env_int("SLB_CHUNK1", std::max(G, static_cast<int>((256.0 * 1024 * 1024) / per)));
         return {G, std::max(1, C)};
     }
