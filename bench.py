@@ -1,23 +1,38 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the shearlet dec -> hard-threshold -> rec hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2d512|3d192|2d1024x64|3d128|2d256]
-                    [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2d512|3d192|...]
+                    [--impl ours|reference] [--no-3d] [--no-cpu-baseline]
 
-Default workload (BASELINE.json configs[1], the metric's 2D config): 512^2
-frames, nScales=4 shear levels [1,1,2,2] (R=49 shearlets), one step =
-decompose -> hard_threshold(defaults_2d(40), RMS-scaled) -> reconstruct of a
-batch of 8 distinct noisy cartoon frames (each frame's 103 MB coefficient
-stack is materialised in HBM, so a step moves ~2.5 GB > L2; L2 is also flushed
-between timed steps). Metric: frames/s (whole job, summed over ranks).
+BASELINE.json's metric has two halves; the default run measures both:
+  * the headline line: 2D 512^2 (configs[1]), nScales=4 shear levels
+    [1,1,2,2] (R=49); one step = decompose -> hard_threshold(defaults_2d(40),
+    RMS-scaled) -> reconstruct of 8 distinct noisy cartoon frames through the
+    fused device batch (sl_denoise_batch_dev: lock-step frame pairs, each
+    frame's 103 MB thresholded stack materialised in HBM);
+  * "workloads": {"3d192": ...}: 3D 192^3 SL3D_2 [1,1,2] (R=292, configs[4]),
+    one step = the fused denoise of one noisy cartoon volume (sl_denoise_dev,
+    16.5 GB stack materialised), timed the same way.
+Each entry also reports the lone-frame (b = 1) fused denoise, the unfused
+operators the reference's callers hit (sl_sheardec_threshold_dev +
+sl_shearrec_dev = hard_threshold(forward) then inverse), the system build
+time, the dominant kernel's roofline (live CUDA events) and the whole path's
+HBM / FP64 fractions by SURVEY 8(d)'s byte and flop counts.
 
-Multi-GPU (torchrun, one rank per GPU, NCCL): 2D frames are replicas/shards by
-image (no collective); 3D shards the filter bank by shearlet index, broadcasts
-the input volume and NCCL-reduces the reconstruction partial sums.
+Timing: CUDA events on the launch stream around each step, L2 flushed
+(256 MB write) between steps outside the timed interval, W >= 3 warm-up
+steps, barrier + synchronize on both sides, max over ranks; nvidia-smi clocks
+sampled during the timed region. e2e = the same metric through the host
+entry points with pinned host in/out, copies inside the timed region.
+
+Multi-GPU (torchrun, one rank per GPU): 2D frames are replicas (weak scaling,
+no collective); 3D shards the filter bank by shearlet index inside one
+process per GPU, broadcasts the volume and reduces the partial
+reconstructions (NCCL through torch.distributed).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 the unmodified reference library compiled with our FFTW-API shim, all host
-threads) on the same config, rank 0 only.
+threads) on the same configs, rank 0 only, same JSON keys.
 """
 from __future__ import annotations
 
@@ -34,11 +49,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-FALLBACK_HBM_GBS = 6650.0
-FP64_PEAK_TFLOPS = 34.0  # measured: tools/fp64_peak.cu (DFMA loop, 64 FMA/clk/SM at 1965 MHz)
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+SMS = 148
+FP64_FLOP_PER_CLK_SM = 128  # 64 DFMA / clk / SM (tools/fp64_peak.cu measured 34 TF at 1965 MHz under load)
 
 CONFIGS = {
-    # name: (dims, levels, schedule kind, sigma, frames per step per rank, seed base)
+    # name: dims, shear levels, sigma, frames per step per rank, unit, metric
     "2d512": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s",
                   metric="2D 512^2 dec+thr+rec frames/s (nScales=4, R=49)", baseline_cfg=1),
     "2d512_nostack": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s", nostack=True,
@@ -62,9 +78,22 @@ CONFIGS = {
 def hbm_peak():
     try:
         with open(MEASURED_PEAKS) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return FALLBACK_HBM_GBS, "fallback"
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def fp64_peak_tflops(sm_mhz):
+    """Theoretical DFMA peak at the sampled max SM clock: 148 SMs x 64 FMA x 2."""
+    return SMS * FP64_FLOP_PER_CLK_SM * (sm_mhz or 1965.0) * 1e6 / 1e12
+
+
+def config_dict(name, cfg, frames, world):
+    """The `config` object both arms print (same keys and values)."""
+    return {"workload": name, "dims": list(cfg["dims"]), "shear_levels": cfg["levels"],
+            "frames_per_step_per_rank": frames, "threshold": "defaults_2d/3d(40), RMS-scaled",
+            "l2": "flushed between timed steps (256 MB write); per-frame stack > L2",
+            "parallelism": (f"shearlet-shard{world}" if len(cfg["dims"]) == 3 else f"dp{world}")}
 
 
 def schedule_for(P, cfg):
@@ -73,35 +102,95 @@ def schedule_for(P, cfg):
         P.ThresholdSchedule.defaults_3d(cfg["sigma"], n)
 
 
-def make_inputs(gen_cartoon, add_noise, cfg, count, seed0):
-    dims = cfg["dims"]
-    clean = gen_cartoon(dims[0])
-    return [add_noise(clean, cfg["sigma"], seed0 + i) for i in range(count)]
-
-
-def algorithmic_bytes(cfg, R, frames):
-    """Compulsory HBM bytes of one dec+thr+rec per frame with the stack
-    materialised (SURVEY.md 8(d) with our real-valued filter representation):
-    16 N (f read + f_rec write) + 16 R N (band write in dec + read in rec)
-    + 16 R Nh (real psi half-spectrum read in dec and in rec; 2D) or the
-    3D factor tables (L2-resident, counted once) + 8 N (W half read)."""
-    dims = cfg["dims"]
+# ------------------------------------------------------------------ accounting
+def _sizes(dims):
     N = int(np.prod(dims))
-    Nh = N // dims[-1] * (dims[-1] // 2 + 1)
+    return N, N // dims[-1] * (dims[-1] // 2 + 1)
+
+
+def table_bytes(cfg, R):
+    """3D factor tables (ĝ + Φ̂ planes, L2-resident): counted once per call."""
+    dims = cfg["dims"]
     if len(dims) == 2:
-        if cfg.get("nostack"):  # stack never written: f/f_rec + real psi halves read twice
-            return frames * (16 * N + 16 * R * Nh)
+        return 0
+    n = dims[0]
+    K = [2 ** (lv) for lv in cfg["levels"]]
+    return sum((2 * k + 1) * n * n * 16 for k in K)
+
+
+def path_bytes(cfg, R, frames, kind, group=1):
+    """Compulsory HBM bytes of one call of `frames` frames.
+    kind "fused": the fused denoise as timed -- f read + f_rec write (16 N),
+    thresholded stack written once (8 R N, 0 when not materialised), real ψ̂
+    halves read in dec and in rec once per lock-step group (2D: 16 R Nh per
+    group of `group` frames) or the 3D factor tables + W half (8 Nh).
+    kind "decrec": forward -> hard_threshold -> inverse through the
+    materialised stack (the reference's operators): the stack is written and
+    read back (16 R N), ψ̂ read per frame."""
+    dims = cfg["dims"]
+    N, Nh = _sizes(dims)
+    stack_w = 0 if cfg.get("nostack") else 8 * R * N
+    if len(dims) == 2:
+        if kind == "fused":
+            ngroups = -(-frames // group)
+            return frames * (16 * N + stack_w) + ngroups * 16 * R * Nh
         return frames * (16 * N + 16 * R * N + 16 * R * Nh)
-    return frames * (16 * N + 16 * R * N + 8 * Nh)
+    T = table_bytes(cfg, R)
+    if kind == "fused":
+        return frames * (16 * N + stack_w + 8 * Nh) + T
+    return frames * (16 * N + 16 * R * N + 8 * Nh) + T
 
 
 def algorithmic_flops(cfg, R):
     """(2R+2) real-input FFTs at 2.5 N log2 N plus 14 flops per
     half-spectrum point per band (conj-multiply + multiply-add), per frame."""
-    dims = cfg["dims"]
-    N = int(np.prod(dims))
-    Nh = N // dims[-1] * (dims[-1] // 2 + 1)
+    N, Nh = _sizes(cfg["dims"])
     return (2 * R + 2) * 2.5 * N * np.log2(N) + R * Nh * 14
+
+
+def pass_bytes(name, dims, G3=None):
+    """I/O bytes at the boundary of each pass per band (or spectrum) processed,
+    for the kernel design in DESIGN.md section 4."""
+    N, Nh = _sizes(dims)
+    if G3 is None:
+        G3 = max(16, int(6 * 2 ** 30 / (16 * Nh)))
+    return None if name == "none" else {
+        # generic path
+        "rows_c2r_thr": 16 * Nh + 8 * N, "rows_c2r": 16 * Nh + 8 * N, "rows_r2c": 8 * N + 16 * Nh,
+        "lines_decmul": 16 * Nh + 8 * Nh + 16 * Nh, "lines_recmul": 16 * Nh + 8 * Nh + 16 * Nh,
+        "lines_plain": 32 * Nh, "lines_divw": 32 * Nh + 8 * Nh, "reduce_bands": 16 * Nh,
+        # fast 2D path (fast2d.cuh, fast2d_fused.cuh)
+        "f2_rows_r2c": 8 * N + 16 * Nh,             # band rows read + column-major half write
+        "f2_rows_c2r_thr": 16 * Nh + 8 * N,         # half read + thresholded band write
+        "f2_rows_c2r": 16 * Nh + 8 * N,
+        "f2_rows_fused": 16 * Nh + 8 * N + 16 * Nh,  # half read, thresholded band write, rec half write
+        "f2_cols_dec": 8 * Nh + 16 * Nh,            # real psi + half write (F re-reads hit L2)
+        "f2_cols_rec": 16 * Nh + 8 * Nh,            # half read + real psi (slot writes / final sum amortised)
+        "f2_cols_fwd": 32 * Nh, "f2_cols_final": 32 * Nh + 8 * Nh,
+        # fast 3D path (fast3d.cuh); psi synthesised from L2-resident tables
+        "f3_rows_fused": 16 * Nh + 8 * N + 16 * Nh,
+        "f3_rows_r2c": 8 * N + 16 * Nh, "f3_rows_c2r_thr": 16 * Nh + 8 * N, "f3_rows_c2r": 16 * Nh + 8 * N,
+        "f3_axis1": 32 * Nh,
+        "f3_ax0_dec": 16 * Nh + 16 * Nh / G3,       # rotated write + F read once per band group
+        "f3_ax0_rec": 16 * Nh + 32 * Nh / G3,       # rotated read + accumulator RMW once per group
+        "f3_ax0_fwd": 32 * Nh, "f3_ax0_final": 40 * Nh,
+        # three-pass 3D path (fast3d_split.cuh)
+        "f3s_dec": 16 * Nh + 16 * Nh / G3,          # Z write (+ F once per group)
+        "f3s_mid": 16 * Nh + 8 * N + 16 * Nh,       # Z read, thresholded band write, Z' write
+        "f3s_rec": 16 * Nh + 32 * Nh / G3,          # Z' read (+ accumulator RMW once per group)
+    }.get(name, None)
+
+
+def measured_traffic(config, pass_name, bands_per_launch):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    pass, from the committed ncu --set full summary (profiles/traffic.json,
+    cold-cache per-band bytes scaled to this run's bands per launch), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            e = json.load(fh)[config][pass_name]
+        return e["dram_bytes_per_band"] * bands_per_launch
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 # ------------------------------------------------------------------ clocks
@@ -119,8 +208,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            # wait for the first sample so the timed region is covered from its start
-            t0 = time.time()
+            t0 = time.time()  # wait for the first sample so the timed region is covered from its start
             self.first = self.proc.stdout.readline() if self.proc.stdout else ""
             while not self.first and time.time() - t0 < 5:
                 time.sleep(0.05)
@@ -161,17 +249,20 @@ class ClockSampler:
 def cpu_reference(cfg, seconds=12.0, steps=5, warmup=1):
     """The reference's own CPU path (oracle/_ref, all host threads): `warmup`
     untimed then up to `steps` timed single-frame (or single-volume)
-    dec+thr+rec runs, stopping early once `seconds` of timed work is done (a
-    bounded sample; at least one timed run). Falls back to the numpy oracle
-    port when oracle/_ref is not built."""
+    dec+thr+rec runs, stopping once `seconds` of timed work is done (a
+    bounded sample; at least one timed run), plus its system build time.
+    Falls back to the numpy oracle port when oracle/_ref is not built."""
     from oracle import ref
     dims, levels = cfg["dims"], cfg["levels"]
     cores = os.cpu_count() or 1
     n = len(levels)
     K = ([2.5] * (n - 1) + [3.8]) if len(dims) == 2 else ([3.0] * (n - 1) + [4.0])
+    build_s = None
     if ref.available():
         kind = "reference"
+        t0 = time.perf_counter()
         sysr = ref.RefSystem2D(*dims, levels) if len(dims) == 2 else ref.RefSystem3D(dims, levels)
+        build_s = time.perf_counter() - t0
         clean = ref.cartoon(dims[0]) if len(dims) == 2 else ref.cartoon_volume(dims[0])
         x = ref.add_noise(clean, cfg["sigma"], 7)
         run = lambda: sysr.denoise(x, K, cfg["sigma"], threads=0)  # noqa: E731
@@ -202,109 +293,97 @@ def cpu_reference(cfg, seconds=12.0, steps=5, warmup=1):
     total = sum(times)
     unit1 = "frame" if len(dims) == 2 else "volume"
     return {"value": len(times) / total, "unit": cfg["unit"], "cores": cores, "kind": kind,
+            "build_s": build_s,
             "sample": f"{len(times)} timed x 1 {unit1} dec+thr+rec (of {steps} requested, capped at ~{seconds:.0f} s) "
                       f"after {nwarm} warm-up, threads=0 (all {os.cpu_count()} host cores)"
                       + ("" if kind == "reference" else " [numpy port: oracle/_ref not built]")
                       + "; FFT = our FFTW-API shim (no libfftw3 in the image)"}
 
 
-# ------------------------------------------------------------------ main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="2d512", choices=sorted(CONFIGS))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
-    cfg = CONFIGS[args.config]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+# ------------------------------------------------------------------ GPU workload
+class Ctx:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
 
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        res = cpu_reference(cfg, seconds=60.0, steps=args.steps, warmup=args.warmup)
-        line = {"metric": cfg["metric"], "value": res["value"], "unit": cfg["unit"], "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / res["value"],
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (reference phantoms + seeded Gaussian noise)", "impl": "reference",
-                "config": {"workload": args.config, "dims": list(cfg["dims"]), "shear_levels": cfg["levels"]},
-                "cpu_baseline": res,
-                "e2e": {"value": res["value"], "unit": cfg["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
 
+def run_workload(name, steps, warmup, ctx, want_cpu):
+    import ctypes as C
     import torch
     import torch.distributed as dist
     import paper_1402_5670_b200 as P
 
-    torch.cuda.set_device(local)
+    cfg = CONFIGS[name]
+    world, rank, local = ctx.world, ctx.rank, ctx.local
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
     dims = cfg["dims"]
     is3d = len(dims) == 3
     prof = P.ScaleProfile.from_levels(cfg["levels"])
     sch = schedule_for(P, cfg)
     R_full = P.redundancy_3d(prof) if is3d else P.redundancy_2d(prof)
 
-    # ---- work partition
-    nstreams = int(os.environ.get("SLB_STREAMS", "6"))
+    # ---- system build (timed: the reference times build_system_* separately)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     if is3d:
-        # shearlet-index sharding: contiguous balanced band ranges
-        lo, hi = R_full * rank // world, R_full * (rank + 1) // world
+        lo, hi = R_full * rank // world, R_full * (rank + 1) // world  # contiguous balanced band ranges
         sysg = P.build_system_3d(dims, prof, device=local, shard=(lo, hi) if world > 1 else None)
-        frames = 1
-        scaling = "strong"  # one volume per step whatever the rank count
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    nstreams = int(os.environ.get("SLB_STREAMS", "6"))
+    if is3d:
+        frames, scaling = 1, "strong"  # one volume per step whatever the rank count
+    else:
         sysg.set_streams(nstreams)
-        if cfg.get("nostack"):
-            sysg.set_stack_output(False)  # reported separately from the materialised-stack metric
-        if args.config == "2d1024x64":
-            frames = cfg["batch"] // world  # fixed total batch sharded by image
-            scaling = "strong"
+        if name == "2d1024x64":
+            frames, scaling = cfg["batch"] // world, "strong"  # fixed total batch sharded by image
         else:
-            frames = cfg["batch"]  # per-rank batch fixed (replicas)
-            scaling = "weak"
+            frames, scaling = cfg["batch"], "weak"  # per-rank batch fixed (replicas)
+    if cfg.get("nostack"):
+        sysg.set_stack_output(False)  # reported separately from the materialised-stack metric
 
     gen = P.cartoon_volume if is3d else P.cartoon
-    host_in = make_inputs(gen, P.add_gaussian_noise, cfg, frames, 1000 * rank)
-    d_in = [torch.from_numpy(x).to(dev) for x in host_in]
-    d_out = [torch.empty_like(x) for x in d_in]
+    clean = gen(dims[0])
+    host_in = [P.add_gaussian_noise(clean, cfg["sigma"], 1000 * rank + i) for i in range(frames)]
+    d_in_b = torch.from_numpy(np.stack(host_in)).to(dev)
+    d_out_b = torch.empty_like(d_in_b)
     N = int(np.prod(dims))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
-    stream_ptr = lambda: P._stream_ptr(local)  # noqa: E731
     K = np.ascontiguousarray(sch.per_scale_factors, dtype=np.float64)
-    import ctypes as C
     Kp = K.ctypes.data_as(C.POINTER(C.c_double))
     L = P.lib()
+    sg = float(sch.sigma)
 
-    d_in_b = torch.stack(d_in)
-    d_out_b = torch.empty_like(d_in_b)
+    def sp():
+        return P._stream_ptr(local)
 
-    def step():
+    def step_fused():
         if not is3d:
-            # batched denoise: frames spread over the handle's internal streams,
-            # each frame's stack materialised in that stream's workspace
+            # batched fused denoise: lock-step frame pairs spread over the handle's streams
             P._check(L.sl_denoise_batch_dev(sysg.handle, C.c_void_p(d_in_b.data_ptr()), frames,
-                                            C.c_void_p(d_out_b.data_ptr()), Kp, len(K), float(sch.sigma), 1,
-                                            stream_ptr()))
+                                            C.c_void_p(d_out_b.data_ptr()), Kp, len(K), sg, 1, sp()))
             return
         for i in range(frames):
-            x = d_in[i]
+            x, o = d_in_b[i], d_out_b[i]
             if world > 1:
                 dist.broadcast(x, src=0)
-            # fused denoise of this rank's bands (dec rows + threshold + rec rows in one
-            # pass, stack materialised); on a shard the output is the partial reconstruction
-            P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(d_out[i].data_ptr()),
-                                      Kp, len(K), float(sch.sigma), 1, stream_ptr()))
+            P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
+                                      Kp, len(K), sg, 1, sp()))
             if world > 1:
-                dist.reduce(d_out[i], dst=0, op=dist.ReduceOp.SUM)
+                dist.reduce(o, dst=0, op=dist.ReduceOp.SUM)
+
+    def step_lone():  # b = 1: one frame through sl_denoise_dev
+        P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(d_in_b[0].data_ptr()), C.c_void_p(d_out_b[0].data_ptr()),
+                                  Kp, len(K), sg, 1, sp()))
+
+    stack = torch.empty((sysg.n_bands,) + tuple(dims), dtype=torch.float64, device=dev)
+
+    def step_unfused():  # forward + fused hard_threshold, then inverse, through the stack
+        P._check(L.sl_sheardec_threshold_dev(sysg.handle, C.c_void_p(d_in_b[0].data_ptr()),
+                                             C.c_void_p(stack.data_ptr()), Kp, len(K), sg, 1, sp()))
+        P._check(L.sl_shearrec_dev(sysg.handle, C.c_void_p(stack.data_ptr()), sysg.n_bands,
+                                   C.c_void_p(d_out_b[0].data_ptr()), sp()))
 
     def barrier():
         torch.cuda.synchronize()
@@ -312,38 +391,48 @@ def main():
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        step()
-    barrier()
-
-    launches0 = sysg.launch_count()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
+    def timed(fn, k, w, clk=None):
+        for _ in range(w):
+            fn()
         barrier()
-        for k in range(args.steps):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        l0 = sysg.launch_count()
+        if clk:
+            clk.__enter__()
+        barrier()
+        for j in range(k):
             flush.zero_()  # evict L2 between timed steps (outside the timed interval)
-            starts[k].record()
-            step()
-            ends[k].record()
+            starts[j].record()
+            fn()
+            ends[j].record()
         barrier()
-    launches = sysg.launch_count() - launches0
-    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
-    ms_step = ms_total / args.steps
-    total_units = (frames * world if not is3d else 1) * args.steps
-    value = total_units / (ms_total / 1000.0)
+        if clk:
+            clk.__exit__()
+        launches = sysg.launch_count() - l0
+        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / k, launches
+
+    clk = ClockSampler(local)
+    ms_step, launches = timed(step_fused, steps, warmup, clk)
+    units_step = frames * world if not is3d else 1
+    value = units_step / (ms_step / 1000.0)
+    k_side = max(3, min(steps, 20 if is3d else 50))
+    ms_lone, _ = timed(step_lone, k_side, 2) if not is3d else (ms_step, None)
+    ms_unf, _ = timed(step_unfused, k_side, 2) if world == 1 else (None, None)
+    del stack
+    torch.cuda.empty_cache()
 
     # ---- instrumented pass: per-kernel device time (CUDA events on the launch
     # stream), frames serialised on one stream so kernel durations do not overlap
     sysg.set_streams(1)
     sysg.set_profiling(True)
-    for k in range(max(2, args.steps // 2)):
+    for _ in range(max(2, min(steps, 10) // 2)):
         flush.zero_()
-        step()
+        step_fused()
     torch.cuda.synchronize()
     stats = sysg.pass_stats()
     sysg.set_profiling(False)
@@ -354,12 +443,12 @@ def main():
     pinned_out = torch.empty_like(pinned_in).pin_memory()
     barrier()
     e2e_times = []
-    for k in range(max(3, args.steps // 2) + 1):
+    for k in range(max(3, min(steps, 20 if is3d else 100) // 2) + 1):
         barrier()
         t0 = time.perf_counter()
         if not is3d:
             P._check(L.sl_denoise_batch_host(sysg.handle, P._dp(pinned_in.numpy()), frames, P._dp(pinned_out.numpy()),
-                                             Kp, len(K), float(sch.sigma), 1))
+                                             Kp, len(K), sg, 1))
         else:
             for i in range(frames):
                 xd = pinned_in[i].to(dev, non_blocking=True)
@@ -375,111 +464,139 @@ def main():
     te = torch.tensor([float(np.median(e2e_times))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = (frames * world if not is3d else 1) / float(te.item())
+    e2e_value = units_step / float(te.item())
+    if rank != 0:
+        return None
 
+    peak, peak_src = hbm_peak()
+    clocks = clk.summary()
+    fp64_peak = fp64_peak_tflops(clocks.get("sm_max_mhz"))
+    R = R_full
+    share = (1.0 / world) if is3d else 1.0  # per-GPU share of a volume's bands
+    group = 2 if (not is3d and frames > 1) else 1  # lock-step frame pairs in the device batch
+    fused_b = path_bytes(cfg, R, frames, "fused", group) * share
+    lone_b = path_bytes(cfg, R, 1, "fused") * share
+    unf_b = path_bytes(cfg, R, 1, "decrec") * share
+    flops = algorithmic_flops(cfg, R) * share
+
+    def frac(nbytes, ms):
+        gbs = nbytes / (ms / 1000.0) / 1e9
+        return {"bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak}
+
+    # dominant kernel by device time (serialised instrumented pass)
+    dom_name, (dom_ms, dom_n, dom_units) = max(stats.items(), key=lambda kv: kv[1][0]) if stats else \
+        ("none", (0.0, 0, 0))
+    per_unit = pass_bytes(dom_name, dims)
+    dom_bytes = per_unit * dom_units / max(dom_n, 1) if per_unit else None
+    dom_avg_s = dom_ms / max(dom_n, 1) / 1000.0
+    achieved = (dom_bytes / dom_avg_s / 1e9) if dom_avg_s > 0 and dom_bytes else None
+    step_ms_serial = sum(v[0] for v in stats.values()) / max(1, max(2, min(steps, 10) // 2))
+    out = {
+        "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": world, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference cartoon phantom + seeded Gaussian noise (sigma 40)",
+        "config": config_dict(name, cfg, frames, world),
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": measured_traffic(name, dom_name, dom_units / max(dom_n, 1)),
+                     "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_avg_s * 1000.0,
+                     "share_of_serial_step": (dom_ms / max(1, max(2, min(steps, 10) // 2))) / step_ms_serial
+                     if step_ms_serial > 0 else None,
+                     "peak_source": peak_src,
+                     "note": "achieved = the pass's I/O bytes per launch (DESIGN.md 4) / its live CUDA-event "
+                             "launch time; traffic = ncu dram bytes of the same kernel (profiles/traffic.json)"},
+        "path_roofline": {
+            "fused_denoise": dict(frac(fused_b, ms_step), frames_per_call=frames, lockstep_group=group,
+                                  note="timed path: f + f_rec, stack written once (never read back), "
+                                       "psi halves per lock-step group (2D) / factor tables + W (3D)"),
+            "lone_frame": dict(frac(lone_b, ms_lone), ms=ms_lone, units_per_s=(1 if is3d else 1) / (ms_lone / 1e3),
+                               note="b = 1 through sl_denoise_dev"),
+            "dec_rec_unfused": (dict(frac(unf_b, ms_unf), ms=ms_unf, units_per_s=1.0 / (ms_unf / 1e3),
+                                     note="sl_sheardec_threshold_dev + sl_shearrec_dev: stack written and read back")
+                                if ms_unf else None),
+        },
+        "fp64": {"flops_per_unit": algorithmic_flops(cfg, R), "achieved_tflops": flops * frames / (ms_step / 1e3) / 1e12
+                 if not is3d else flops / (ms_step / 1e3) / 1e12,
+                 "peak_tflops": fp64_peak,
+                 "note": "per GPU; SURVEY 8(d) flop count; peak = 148 SMs x 128 flop/clk x max SM clock"},
+        "build_s": build_s,
+        "kernels": {k: {"ms_total": v[0], "launches": v[1], "bands": v[2]} for k, v in sorted(stats.items())},
+        "gpu_launches": int(launches),
+        "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
+                "d2h_bytes_per_step": frames * N * 8,
+                "api": ("sl_denoise_batch_host (pinned host in/out; H2D in frame order on a copy stream, fused "
+                        "dec/thr/rec on 3 compute streams, D2H in frame order on a second copy stream)" if not is3d
+                        else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
+        "clocks": clocks,
+    }
+    out["fp64"]["frac"] = out["fp64"]["achieved_tflops"] / fp64_peak
+    if world == 1 and want_cpu:
+        try:
+            out["cpu_baseline"] = cpu_reference(cfg, seconds=12.0, steps=10 if not is3d else 1, warmup=1)
+        except Exception as e:  # reported, never fatal
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    del sysg
+    torch.cuda.empty_cache()
+    return out
+
+
+# ------------------------------------------------------------------ main
+def reference_line(name, steps, warmup, ngpus):
+    cfg = CONFIGS[name]
+    res = cpu_reference(cfg, seconds=60.0 if len(cfg["dims"]) == 2 else 240.0,
+                        steps=steps if len(cfg["dims"]) == 2 else 1, warmup=warmup)
+    frames = cfg["batch"] if name != "2d1024x64" else cfg["batch"] // max(1, ngpus)
+    return {"metric": cfg["metric"], "value": res["value"], "unit": cfg["unit"], "n_gpus": ngpus,
+            "ms_per_step": 1000.0 / res["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: reference cartoon phantom + seeded Gaussian "
+            "noise (sigma 40)", "impl": "reference", "config": config_dict(name, cfg, frames, ngpus),
+            "build_s": res.get("build_s"), "cpu_baseline": res,
+            "e2e": {"value": res["value"], "unit": cfg["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="2d512", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-3d", action="store_true", help="skip the nested 3d192 workload of the default run")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    nested = args.config == "2d512" and not args.no_3d
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        line = reference_line(args.config, args.steps, args.warmup, args.gpus)
+        line.update(steps=args.steps, warmup=args.warmup)
+        if nested:
+            line["workloads"] = {"3d192": reference_line("3d192", args.steps, args.warmup, args.gpus)}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = Ctx(world, rank, local)
+    line = run_workload(args.config, args.steps, args.warmup, ctx, not args.no_cpu_baseline)
+    if nested:
+        k3 = max(3, min(args.steps, 20))
+        w3 = run_workload("3d192", k3, max(3, args.warmup), ctx, not args.no_cpu_baseline)
+        if rank == 0:
+            w3["steps"], w3["warmup"] = k3, max(3, args.warmup)
+            line["workloads"] = {"3d192": w3}
     if rank == 0:
-        peak, peak_kind = hbm_peak()
-        R = R_full
-        nbytes = algorithmic_bytes(cfg, R, 1)
-        # dominant kernel by device time
-        dom = max(stats.items(), key=lambda kv: kv[1][0]) if stats else ("none", (0.0, 0))
-        dom_name, (dom_ms, dom_n, dom_units) = dom
-        per_unit = pass_bytes(dom_name, dims)
-        dom_bytes = per_unit * dom_units / max(dom_n, 1) if per_unit else None
-        dom_avg_s = dom_ms / max(dom_n, 1) / 1000.0
-        achieved = (dom_bytes / dom_avg_s / 1e9) if dom_avg_s > 0 and dom_bytes else None
-        traffic = measured_traffic(args.config, dom_name, dom_units / max(dom_n, 1))
-        # per-rank compulsory bytes per step: `frames` frames (2D) or 1/world of a volume's bands (3D)
-        path_gbs = nbytes * (1.0 / world if is3d else frames) / (ms_step / 1000.0) / 1e9
-        line = {
-            "metric": cfg["metric"], "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: reference cartoon phantom + seeded Gaussian noise (sigma 40)",
-            "config": {"workload": args.config, "dims": list(dims), "shear_levels": cfg["levels"], "R": R_full,
-                       "frames_per_step_per_rank": frames, "threshold": "defaults (RMS-scaled)",
-                       "l2": "flushed between timed steps (256 MB write); stack per frame > L2",
-                       "parallelism": (f"shearlet-shard{world}" if is3d else f"dp{world}")},
-            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "bytes_per_launch": dom_bytes, "avg_launch_ms": dom_avg_s * 1000.0,
-                         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"},
-            "path_roofline": {"bytes_per_unit": nbytes, "achieved": path_gbs, "frac": path_gbs / peak,
-                              "note": "whole dec+thr+rec step: compulsory HBM bytes / device time"},
-            "fp64": {"flops_per_unit": algorithmic_flops(cfg, R),
-                     "achieved_tflops": algorithmic_flops(cfg, R) * (1.0 / world if is3d else frames)
-                     / (ms_step / 1000.0) / 1e12,
-                     "peak_tflops": FP64_PEAK_TFLOPS,
-                     "frac": algorithmic_flops(cfg, R) * (1.0 / world if is3d else frames) / (ms_step / 1000.0)
-                     / 1e12 / FP64_PEAK_TFLOPS,
-                     "note": "per GPU; SURVEY 8(d) flop count; peak measured by tools/fp64_peak.cu"},
-            "kernels": {k: {"ms_total": v[0], "launches": v[1], "bands": v[2]} for k, v in sorted(stats.items())},
-            "gpu_launches": int(launches),
-            "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
-                    "d2h_bytes_per_step": frames * N * 8,
-                    "api": ("sl_denoise_batch_host (pinned host in/out; H2D in frame order on a copy stream, fused dec/thr/rec on 3 compute streams, D2H in frame order on a second copy stream)" if not is3d else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
-            "clocks": clk.summary(),
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                line["cpu_baseline"] = cpu_reference(cfg, seconds=12.0, steps=10, warmup=1)
-            except Exception as e:  # reported, never fatal
-                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        line.update(steps=args.steps, warmup=args.warmup)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-def measured_traffic(config, pass_name, bands_per_launch):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    pass, from the committed ncu --set full summary (profiles/traffic.json,
-    written by tools/ncu_summary.py traffic; cold-cache per-band bytes scaled to
-    this run's bands per launch), else None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            e = json.load(fh)[config][pass_name]
-        return e["dram_bytes_per_band"] * bands_per_launch
-    except (OSError, KeyError, ValueError):
-        return None
-
-
-def pass_bytes(name, dims):
-    """Bytes at the boundary of each pass per band (or spectrum) processed, for
-    the current multi-pass design."""
-    N = int(np.prod(dims))
-    Nh = N // dims[-1] * (dims[-1] // 2 + 1)
-    # 3D band group (csrc/fast3d_host.cuh fast3d_group): ~6 GB of rotated intermediate, >= 16
-    G3 = int(os.environ.get("SLB_G3", "0")) or max(16, int(6 * 2 ** 30 / (16 * Nh)))
-    return None if name == "none" else {
-        # generic path
-        "rows_c2r_thr": 16 * Nh + 8 * N,          # intermediate read + band write, per band
-        "rows_c2r": 16 * Nh + 8 * N,
-        "rows_r2c": 8 * N + 16 * Nh,
-        "lines_decmul": 16 * Nh + 8 * Nh + 16 * Nh,  # F + psi (real) + intermediate write
-        "lines_recmul": 16 * Nh + 8 * Nh + 16 * Nh,
-        "lines_plain": 32 * Nh,
-        "lines_divw": 32 * Nh + 8 * Nh,
-        "reduce_bands": 16 * Nh,
-        # fast 2D path (fast2d.cuh)
-        "f2_rows_r2c": 8 * N + 16 * Nh,           # band rows read + column-major half write
-        "f2_rows_c2r_thr": 16 * Nh + 8 * N,       # half read + thresholded band write
-        "f2_rows_c2r": 16 * Nh + 8 * N,
-        "f2_rows_fused": 16 * Nh + 8 * N + 16 * Nh,  # half read, thresholded band write, rec half write
-        "f3_rows_fused": 16 * Nh + 8 * N + 16 * Nh,
-        "f2_cols_dec": 8 * Nh + 16 * Nh,          # real psi + half write (F re-reads hit L2)
-        "f2_cols_rec": 16 * Nh + 8 * Nh,          # half read + real psi (slot writes / final sum amortised)
-        "f2_cols_fwd": 32 * Nh,
-        "f2_cols_final": 32 * Nh + 8 * Nh,
-        # fast 3D path (fast3d.cuh); psi synthesised from L2-resident tables
-        "f3_rows_r2c": 8 * N + 16 * Nh,
-        "f3_rows_c2r_thr": 16 * Nh + 8 * N,
-        "f3_rows_c2r": 16 * Nh + 8 * N,
-        "f3_axis1": 32 * Nh,
-        "f3_ax0_dec": 16 * Nh + 16 * Nh / G3,     # rotated write + F read once per band group
-        "f3_ax0_rec": 16 * Nh + 32 * Nh / G3,     # rotated read + accumulator RMW once per group
-        "f3_ax0_fwd": 32 * Nh,
-        "f3_ax0_final": 40 * Nh,
-    }.get(name, None)
 
 
 if __name__ == "__main__":

@@ -22,7 +22,10 @@
  * "_dev" entry points take device pointers on the handle's device and run on
  * the given CUDA stream (NULL = legacy default stream); "_host" entry points
  * take host pointers and include the H2D/D2H copies (synchronous).
- * A handle owns its device memory; calls on one handle are serialised.
+ * A handle owns its device memory. Calls on one handle are serialised on the
+ * GPU too: every call waits (cudaStreamWaitEvent) for the previous call on the
+ * handle to finish, whatever streams the two were issued on, because they
+ * share the handle's scratch.
  */
 #ifndef SHEARLET_B200_H
 #define SHEARLET_B200_H
@@ -128,10 +131,16 @@ int sl_shearrec_dev(sl_system* sys, const double* coeffs, int nbands, double* f,
 /* hard_threshold(): in -> out (may alias), nK must equal n_scales. */
 int sl_hard_threshold_dev(sl_system* sys, const double* in, double* out, int nbands, const double* K, int nK,
                           double sigma, int scale_by_rms, void* stream);
-/* denoise(): inverse(hard_threshold(forward(in))) with the stack kept in the
- * handle's device scratch. */
+/* denoise(): inverse(hard_threshold(forward(in))) (apps.cpp:114-121), fused:
+ * the threshold runs in the dec epilogue and the rec reads the thresholded
+ * rows in the same pass. The stack goes to the handle's device scratch while
+ * sl_set_stack_output is on (default). */
 int sl_denoise_dev(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
                    int scale_by_rms, void* stream);
+/* The same fused denoise, also writing the thresholded stack
+ * hard_threshold(forward(in)) [nbands][dims] into `stack` (device). */
+int sl_denoise_stack_dev(sl_system* sys, const double* in, double* stack, double* out, const double* K, int nK,
+                         double sigma, int scale_by_rms, void* stream);
 
 /* ---- batched hot path (device pointers) ----------------------------------
  * nframes independent signals, contiguous [nframes][dims]; stacks
@@ -150,7 +159,13 @@ int sl_sheardec_batch_dev(sl_system* sys, const double* f, int nframes, double* 
 int sl_shearrec_batch_dev(sl_system* sys, const double* coeffs, int nframes, double* f, void* stream);
 int sl_denoise_batch_dev(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
                          double sigma, int scale_by_rms, void* stream);
-/* host in/out: H2D of all frames + batched denoise + D2H, synchronous */
+/* batched fused denoise that also returns every frame's thresholded stack,
+ * stacks [nframes][nbands][dims] (device) -- the timed path's own output */
+int sl_denoise_batch_stack_dev(sl_system* sys, const double* in, int nframes, double* stacks, double* out,
+                               const double* K, int nK, double sigma, int scale_by_rms, void* stream);
+/* host in/out: H2D of all frames + batched denoise + D2H, synchronous.
+ * Pinned buffers are used as they are; pageable ones are page-locked
+ * (cudaHostRegister) for the duration of the call. */
 int sl_denoise_batch_host(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
                           double sigma, int scale_by_rms);
 

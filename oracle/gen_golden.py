@@ -33,6 +33,19 @@ def sample_idx(n, k=257):
     return (np.arange(k, dtype=np.int64) * 7919) % n
 
 
+def kept_fingerprint(bands):
+    """Per band (count, sum of kept flat indices, sum of (index mod 1000003)^2):
+    a position fingerprint of the thresholded support (same as
+    oracle/ref_capi.cpp ref_denoise_3d_stats and tests/conftest.py)."""
+    flat = bands.reshape(bands.shape[0], -1)
+    out = np.zeros((flat.shape[0], 3), dtype=np.int64)
+    for i in range(flat.shape[0]):
+        idx = np.flatnonzero(flat[i]).astype(np.int64)
+        r = idx % 1000003
+        out[i] = (idx.size, idx.sum(), (r * r).sum())
+    return out
+
+
 def band_stats(bands):
     flat = bands.reshape(bands.shape[0], -1)
     return {
@@ -71,7 +84,7 @@ def gen_2d_stats(name, n, levels, f, K=None, sigma=None, j0=0):
         thr = s.hard_threshold(bands, K, sigma)
         kept = np.count_nonzero(thr.reshape(thr.shape[0], -1), axis=1)
         den = s.inverse(thr)
-        kw.update(K=np.array(K), sigma=sigma, kept=kept,
+        kw.update(K=np.array(K), sigma=sigma, kept=kept, kept_fp=kept_fingerprint(thr),
                   den_sample=den.reshape(-1)[sample_idx(den.size)], den_sum=den.sum(),
                   den_l2=np.sqrt((den * den).sum()))
     save(name, **kw)
@@ -93,7 +106,8 @@ def gen_3d(name, dims, levels, f, K=None, sigma=None, full=False, threads=0):
     if K is not None and not full:
         si = sample_idx(W.size)
         den, kept, l2, smp = s.denoise_stats(f, K, sigma, si, threads=threads)
-        kw.update(K=np.array(K), sigma=sigma, kept=kept, band_l2=l2, band_sample=smp,
+        fp = np.concatenate([kept[:, None], s.last_kept_fp], axis=1)
+        kw.update(K=np.array(K), sigma=sigma, kept=kept, kept_fp=fp, band_l2=l2, band_sample=smp,
                   den_sample=den.reshape(-1)[si], den_sum=den.sum(), den_l2=np.sqrt((den * den).sum()))
     elif full:
         bands = s.forward(f, threads=threads)
@@ -203,9 +217,18 @@ def gen_acceptance():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
+    ap.add_argument("--only", choices=["cfg2", "cfg5"], help="regenerate one timed-config fixture")
     a = ap.parse_args()
     if not ref.available():
         sys.exit("build the reference first: make -C oracle ref")
+    if a.only == "cfg2":
+        noisy = ref.add_noise(ref.cartoon(512), 40.0, 7)
+        gen_2d_stats("cfg2_denoise512_1122", 512, [1, 1, 2, 2], noisy, K=[2.5, 2.5, 2.5, 3.8], sigma=40.0)
+        return
+    if a.only == "cfg5":
+        noisy3 = ref.add_noise(ref.cartoon_volume(192), 40.0, 3)
+        gen_3d("cfg5_denoise192_112", (192, 192, 192), [1, 1, 2], noisy3, K=[3.0, 3.0, 4.0], sigma=40.0)
+        return
 
     # test_transform.cpp:55-64 (naive-correlation pin): 16^2 [0,1] seed 21
     gen_2d_full("t2d_16_01_seed21", 16, [0, 1], O.random_grid((16, 16), 21))

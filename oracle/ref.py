@@ -50,7 +50,7 @@ def lib():
             getattr(L, f"ref_inverse_{d}").argtypes = [P, dp, C.c_int, dp, C.c_int]
             getattr(L, f"ref_hard_threshold_{d}").argtypes = [P, dp, C.c_int, dp, C.c_int, C.c_double, C.c_int, dp]
             getattr(L, f"ref_denoise_{d}").argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.c_int]
-        L.ref_denoise_3d_stats.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.POINTER(C.c_longlong), dp, dp, C.POINTER(C.c_longlong), C.c_int, C.c_int]
+        L.ref_denoise_3d_stats.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_int, dp, C.POINTER(C.c_longlong), dp, dp, C.POINTER(C.c_longlong), C.c_int, C.c_int, C.POINTER(C.c_longlong)]
         L.ref_inpaint_2d.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, C.c_int]
         L.ref_inpaint_3d.argtypes = [P, dp, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, C.c_int]
         L.ref_separate_2d.argtypes = [P, P, dp, C.c_int, C.c_double, C.c_double, C.c_int, dp, dp, C.c_int]
@@ -310,10 +310,12 @@ class RefSystem3D:
         kept = np.zeros(self.R, dtype=np.int64)
         l2 = np.zeros(self.R)
         smp = np.zeros((self.R, len(si)))
+        fp = np.zeros((self.R, 2), dtype=np.int64)
         LL = C.POINTER(C.c_longlong)
         _check(lib().ref_denoise_3d_stats(self.h, _dp(f), _dp(K), len(K), sigma, int(scaled), _dp(out),
                                           kept.ctypes.data_as(LL), _dp(l2), _dp(smp), si.ctypes.data_as(LL),
-                                          len(si), threads))
+                                          len(si), threads, fp.ctypes.data_as(LL)))
+        self.last_kept_fp = fp
         return out, kept, l2, smp
 
 

@@ -315,7 +315,7 @@ int ref_denoise_3d(void* h, const double* in, const double* K, int nK, double si
 int ref_denoise_3d_stats(void* h, const double* in, const double* K, int nK, double sigma,
                          int scaled, double* out, long long* kept, double* band_l2,
                          double* band_sample, const long long* sample_idx, int n_sample,
-                         int threads) {
+                         int threads, long long* kept_fp) {
     return guard([&] {
         const auto& s = *static_cast<ShearletSystem3D*>(h);
         Signal3D f(s.dims[0], s.dims[1], s.dims[2]);
@@ -333,9 +333,20 @@ int ref_denoise_3d_stats(void* h, const double* in, const double* K, int nK, dou
         CoefficientStack3D t = hard_threshold(c, sch, s);
         c = CoefficientStack3D{};
         for (std::size_t i = 0; i < t.bands.size(); ++i) {
-            long long k = 0;
-            for (double x : t.bands[i].raw()) k += (x != 0.0);
+            long long k = 0, s1 = 0, s2 = 0;
+            const auto& raw = t.bands[i].raw();
+            for (std::size_t e = 0; e < raw.size(); ++e) {
+                if (raw[e] == 0.0) continue;
+                ++k;
+                const long long id = static_cast<long long>(e), r = id % 1000003;
+                s1 += id;  // kept-position fingerprint (tests/conftest.py kept_fingerprint)
+                s2 += r * r;
+            }
             kept[i] = k;
+            if (kept_fp) {
+                kept_fp[2 * i] = s1;
+                kept_fp[2 * i + 1] = s2;
+            }
         }
         const auto r = inverse(t, s, threads);
         std::memcpy(out, r.data(), sizeof(double) * r.size());

@@ -152,6 +152,7 @@ def lib():
     L.sl_shearrec_dev.argtypes = [P, P, i, P, P]
     L.sl_hard_threshold_dev.argtypes = [P, P, P, i, dp, i, C.c_double, i, P]
     L.sl_denoise_dev.argtypes = [P, P, P, dp, i, C.c_double, i, P]
+    L.sl_denoise_stack_dev.argtypes = [P, P, P, P, dp, i, C.c_double, i, P]
     L.sl_sheardec_host.argtypes = [P, dp, dp]
     L.sl_shearrec_host.argtypes = [P, dp, i, dp]
     L.sl_hard_threshold_host.argtypes = [P, dp, dp, i, dp, i, C.c_double, i]
@@ -161,6 +162,7 @@ def lib():
     L.sl_sheardec_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
     L.sl_shearrec_batch_dev.argtypes = [P, P, i, P, P]
     L.sl_denoise_batch_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
+    L.sl_denoise_batch_stack_dev.argtypes = [P, P, i, P, P, dp, i, C.c_double, i, P]
     L.sl_denoise_batch_host.argtypes = [P, dp, i, dp, dp, i, C.c_double, i]
     L.sl_inpaint_dev.argtypes = [P, P, P, P, i, C.c_double, C.c_double, i, P]
     L.sl_inpaint_host.argtypes = [P, dp, dp, dp, i, C.c_double, C.c_double, i]
@@ -194,10 +196,10 @@ EXPORTED_SYMBOLS = [
     "sl_version", "sl_last_error", "sl_device_count", "sl_system_create_2d", "sl_system_create_3d",
     "sl_system_destroy", "sl_ndim", "sl_redundancy", "sl_shard", "sl_index", "sl_filter_norms",
     "sl_frame_weight", "sl_frame_bounds", "sl_filter_spectrum", "sl_sheardec_dev", "sl_sheardec_threshold_dev",
-    "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_sheardec_host", "sl_shearrec_host",
+    "sl_shearrec_dev", "sl_hard_threshold_dev", "sl_denoise_dev", "sl_denoise_stack_dev", "sl_sheardec_host", "sl_shearrec_host",
     "sl_hard_threshold_host", "sl_denoise_host", "sl_profile", "sl_pass_stats", "sl_launch_count",
     "sl_set_streams", "sl_set_stack_output", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
-    "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
+    "sl_denoise_batch_stack_dev", "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize", "sl_shcf_forward_file", "sl_shcf_inverse_file",
     "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
     "sl_describe", "sl_system_create_from_descriptor",
@@ -786,8 +788,10 @@ def forward_thresholded(f, sys: _System, schedule: ThresholdSchedule):
     return out
 
 
-def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0):
-    """inverse(hard_threshold(forward(noisy))) (apps.hpp:40-43, apps.cpp:114-121)."""
+def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0, return_stack: bool = False):
+    """inverse(hard_threshold(forward(noisy))) (apps.hpp:40-43, apps.cpp:114-121),
+    fused on the device. return_stack=True (CUDA tensors) also returns the
+    thresholded stack the fused pass wrote: (denoised, stack)."""
     _check_signal(noisy, sys, "forward")
     K, Kp = _k_arg(schedule)
     L = lib()
@@ -795,10 +799,16 @@ def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0):
         import torch
         noisy = noisy.contiguous().to(torch.float64)
         out = torch.empty_like(noisy)
-        _check(L.sl_denoise_dev(sys.handle, C.c_void_p(noisy.data_ptr()), C.c_void_p(out.data_ptr()), Kp, len(K),
-                                float(schedule.sigma), int(schedule.scale_by_filter_norm),
-                                _stream_ptr(noisy.device.index)))
+        args = (Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm), _stream_ptr(noisy.device.index))
+        if return_stack:
+            stack = torch.empty((sys.n_bands,) + tuple(sys.shape), dtype=torch.float64, device=noisy.device)
+            _check(L.sl_denoise_stack_dev(sys.handle, C.c_void_p(noisy.data_ptr()), C.c_void_p(stack.data_ptr()),
+                                          C.c_void_p(out.data_ptr()), *args))
+            return out, stack
+        _check(L.sl_denoise_dev(sys.handle, C.c_void_p(noisy.data_ptr()), C.c_void_p(out.data_ptr()), *args))
         return out
+    if return_stack:
+        raise InvalidArgument("return_stack needs a CUDA tensor input")
     noisy = np.ascontiguousarray(noisy, dtype=np.float64)
     out = np.empty_like(noisy)
     _check(L.sl_denoise_host(sys.handle, _dp(noisy), _dp(out), Kp, len(K), float(schedule.sigma),
@@ -839,9 +849,10 @@ def inverse_batch(coeffs, sys: _System):
     return out
 
 
-def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule):
+def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule, return_stacks: bool = False):
     """denoise() of [nframes, *dims] frames; CUDA tensors stay on the device, numpy
-    arrays go through the host entry point (H2D + dec/thr/rec + D2H)."""
+    arrays go through the host entry point (H2D + dec/thr/rec + D2H).
+    return_stacks=True (CUDA) also returns the [nframes, nb, *dims] thresholded stacks."""
     _check_batch(frames, sys)
     K, Kp = _k_arg(schedule)
     args = (Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm))
@@ -849,9 +860,18 @@ def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule):
         import torch
         frames = frames.contiguous().to(torch.float64)
         out = torch.empty_like(frames)
+        if return_stacks:
+            st = torch.empty((frames.shape[0], sys.n_bands) + tuple(sys.shape), dtype=torch.float64,
+                             device=frames.device)
+            _check(lib().sl_denoise_batch_stack_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
+                                                    C.c_void_p(st.data_ptr()), C.c_void_p(out.data_ptr()), *args,
+                                                    _stream_ptr(frames.device.index)))
+            return out, st
         _check(lib().sl_denoise_batch_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
                                           C.c_void_p(out.data_ptr()), *args, _stream_ptr(frames.device.index)))
         return out
+    if return_stacks:
+        raise InvalidArgument("return_stacks needs CUDA tensor frames")
     frames = np.ascontiguousarray(frames, dtype=np.float64)
     out = np.empty_like(frames)
     _check(lib().sl_denoise_batch_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))

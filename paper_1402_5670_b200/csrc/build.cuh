@@ -179,11 +179,6 @@ static std::vector<double> real_spectrum_full(System& s, const DTaps2& t, int n0
     return full;
 }
 
-// Filters must be real to this relative level (override: SLB_REAL_TOL, debugging only).
-static double real_tol() {
-    const char* e = std::getenv("SLB_REAL_TOL");
-    return e ? std::atof(e) : 1e-9;
-}
 
 static void finish_rms(System& s, const double* partial, int nblocks, int R) {
     s.rms.assign(static_cast<size_t>(R), 0.0);
@@ -304,7 +299,7 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
             worst_i = i;
         }
     }
-    if (worst > real_tol())
+    if (worst > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan; filter " + std::to_string(worst_i) +
                                          " has |im|/|re| = " + std::to_string(worst) + "); unsupported by this build");
     s.W.alloc(static_cast<size_t>(s.nhalf));
@@ -322,7 +317,7 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     finish_rms(s, hp.data(), nblk, s.R);
     // pad entries of W are never read as divisors; set them to 1 for safety
     finish_W(s, st);
-    if (fast2d_supported(s.n[0], s.n[1])) {
+    if (fast2d_supported(s.knobs, s.n[0], s.n[1])) {
         s.fast2d = true;
         s.psiT.alloc(static_cast<size_t>(s.R) * s.H * s.n[0]);
         s.WT.alloc(static_cast<size_t>(s.H) * s.n[0]);
@@ -429,7 +424,7 @@ static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
         b.p2_off = add_2d(S.phi[static_cast<size_t>(r.k2 + K)], phi_id[static_cast<size_t>(si)][static_cast<size_t>(r.k2 + K)],
                           np, s.n[b.s2]);
     }
-    if (worst > real_tol())
+    if (worst > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan); unsupported by this build");
     s.tab1.upload(tab1.data(), tab1.size(), st);
     s.tab2.upload(tab2.data(), tab2.size(), st);
@@ -452,7 +447,7 @@ static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
     SL_CUDA(cudaStreamSynchronize(st));
     finish_rms(s, hp.data(), nblk, s.R);
     finish_W(s, st);
-    if (fast3d_supported(s.n)) {
+    if (fast3d_supported(s.knobs, s.n)) {
         s.fast3d = true;
         const int n = s.n[0];
         const long long tot = static_cast<long long>(s.H) * n * n;

@@ -356,6 +356,7 @@ int sl_filter_spectrum(sl_system* h, int i, double* out) {
         if (i < 0 || i >= s.R) throw SlError(SL_ERR_DOMAIN, "filter index out of range");
         if (!out) throw SlError(SL_ERR_INVALID, "null output");
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         std::vector<double> half(static_cast<size_t>(s.nhalf));
         if (s.ndim == 2) {
             SL_CUDA(cudaMemcpy(half.data(), s.psi.p + static_cast<size_t>(i) * s.nhalf, half.size() * sizeof(double),
@@ -395,6 +396,7 @@ int sl_sheardec_dev(sl_system* h, const double* f, double* coeffs, void* stream)
         require_dev_ptr(coeffs, "sheardec output");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         dec(s, f, coeffs, nullptr, stream_of(stream));
     });
 }
@@ -408,6 +410,7 @@ int sl_sheardec_threshold_dev(sl_system* h, const double* f, double* coeffs, con
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         deltas(s, K, nK, sigma, scaled, stream_of(stream));
         dec(s, f, coeffs, s.delta.p, stream_of(stream));
     });
@@ -421,6 +424,7 @@ int sl_shearrec_dev(sl_system* h, const double* coeffs, int nbands, double* f, v
         require_dev_ptr(f, "shearrec output");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         rec(s, coeffs, f, stream_of(stream));
     });
 }
@@ -432,6 +436,7 @@ int sl_hard_threshold_dev(sl_system* h, const double* in, double* out, int nband
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         deltas(s, K, nK, sigma, scaled, stream_of(stream));
         if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "hard_threshold: stack does not match the system");
         require_dev_ptr(in, "hard_threshold input");
@@ -443,6 +448,20 @@ int sl_hard_threshold_dev(sl_system* h, const double* in, double* out, int nband
     });
 }
 
+// Fused dec -> threshold -> rec. `stack` (device, [nbands][dims]) receives the
+// thresholded coefficient stack -- what hard_threshold(forward(in)) returns in
+// the reference (apps.cpp:114-121) -- or is null: then the handle's scratch
+// stack is written while sl_set_stack_output is on (the default, the
+// reference's denoise materialises it) and nothing is written when it is off.
+static void denoise_one(System& s, const double* in, double* stack, double* out, cudaStream_t st) {
+    double* stk = stack;
+    if (!stk && s.materialize) {
+        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        stk = s.stack.p;
+    }
+    denoise(s, in, stk, out, s.delta.p, st);
+}
+
 int sl_denoise_dev(sl_system* h, const double* in, double* out, const double* K, int nK, double sigma, int scaled,
                    void* stream) {
     return guard([&] {
@@ -452,9 +471,25 @@ int sl_denoise_dev(sl_system* h, const double* in, double* out, const double* K,
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         deltas(s, K, nK, sigma, scaled, stream_of(stream));
-        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-        denoise(s, in, s.stack.p, out, s.delta.p, stream_of(stream));
+        denoise_one(s, in, nullptr, out, stream_of(stream));
+    });
+}
+
+int sl_denoise_stack_dev(sl_system* h, const double* in, double* stack, double* out, const double* K, int nK,
+                         double sigma, int scaled, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        require_dev_ptr(in, "denoise input");
+        require_dev_ptr(stack, "denoise stack output");
+        require_dev_ptr(out, "denoise output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        denoise_one(s, in, stack, out, stream_of(stream));
     });
 }
 
@@ -496,27 +531,66 @@ void fan_out(System& s, int nframes, cudaStream_t user, Fn&& per_frame) {
 // a group pass through each kernel together on one stream. SLB_LOCKSTEP=0
 // restores the per-frame fan-out over the workspace streams.
 bool lockstep_batch(const System& s, int nframes) {
-    const char* e = std::getenv("SLB_LOCKSTEP");
-    return s.fast2d && nframes > 1 && (e ? std::atoi(e) != 0 : true) && !std::getenv("SLB_DENOISE_UNFUSED");
+    return s.fast2d && nframes > 1 && s.knobs.lockstep != 0 && !s.knobs.denoise_unfused;
 }
-int lockstep_group(int nframes) { return std::max(1, std::min(nframes, env_int("SLB_LOCKSTEP_FRAMES", 2))); }
-void denoise_lockstep(System& s, const double* in, int nframes, double* out, cudaStream_t st) {
+int lockstep_group(const System& s, int nframes) { return std::max(1, std::min(nframes, s.knobs.lockstep_frames)); }
+// stack of frame group g: the caller's [frames][nb][dims] buffer, else the
+// workspace scratch (only while the handle materialises the stack)
+double* group_stack(System& s, double* user, long long f0, int group, long long sfs) {
+    if (user) return user + f0 * sfs;
+    if (!s.materialize) return nullptr;
+    s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+    return s.w->stack.p;
+}
+void denoise_lockstep(System& s, const double* in, int nframes, double* user_stack, double* out, cudaStream_t st) {
     if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-    const int group = lockstep_group(nframes);
+    const int group = lockstep_group(s, nframes);
     const int ngroups = (nframes + group - 1) / group;
     const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
     // groups spread over the workspace streams like single frames
     fan_out(s, ngroups, st, [&](int g, cudaStream_t fst) {
         const int f0 = g * group, nf = std::min(group, nframes - f0);
         const size_t off = static_cast<size_t>(f0) * s.nreal;
-        s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+        double* stk = group_stack(s, user_stack, f0, group, sfs);
         const int conc = s.concurrency;
         s.concurrency = std::max(conc, 4);  // full-machine band grouping (fast2d_cfg)
-        denoise2d_fast_batch(s, in + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs, out + off, s.nreal,
-                             s.delta.p, fst);
+        denoise2d_fast_batch(s, in + off, s.nreal, nf, stk, sfs, out + off, s.nreal, s.delta.p, fst);
         s.concurrency = conc;
     });
 }
+void denoise_batch(System& s, const double* in, int nframes, double* user_stack, double* out, cudaStream_t st) {
+    if (lockstep_batch(s, nframes)) {
+        denoise_lockstep(s, in, nframes, user_stack, out, st);
+        return;
+    }
+    const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
+    fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
+        double* stk = group_stack(s, user_stack, fr, 1, sfs);
+        denoise(s, in + static_cast<size_t>(fr) * s.nreal, stk, out + static_cast<size_t>(fr) * s.nreal, s.delta.p,
+                fst);
+    });
+}
+// Host buffers of the e2e call: pinned memory is used as is; pageable memory
+// is page-locked for the duration of the call (cudaHostRegister) so the
+// per-frame async copies overlap the kernels instead of serialising the loop.
+struct HostPin {
+    const void* p = nullptr;
+    bool registered = false;
+    HostPin(const void* ptr, size_t bytes) : p(ptr) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+            cudaGetLastError();
+            a.type = cudaMemoryTypeUnregistered;
+        }
+        if (a.type == cudaMemoryTypeUnregistered && bytes > 0) {
+            SL_CUDA(cudaHostRegister(const_cast<void*>(ptr), bytes, cudaHostRegisterDefault));
+            registered = true;
+        }
+    }
+    ~HostPin() {
+        if (registered) cudaHostUnregister(const_cast<void*>(p));
+    }
+};
 }  // namespace
 extern "C" {
 
@@ -547,6 +621,7 @@ int sl_sheardec_batch_dev(sl_system* h, const double* f, int nframes, double* co
         if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         cudaStream_t st = stream_of(stream);
         if (K) deltas(s, K, nK, sigma, scaled, st);
         const double* dl = K ? s.delta.p : nullptr;
@@ -564,6 +639,7 @@ int sl_shearrec_batch_dev(sl_system* h, const double* coeffs, int nframes, doubl
         if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         fan_out(s, nframes, stream_of(stream), [&](int fr, cudaStream_t fst) {
             rec(s, coeffs + static_cast<size_t>(fr) * s.nb() * s.nreal, f + static_cast<size_t>(fr) * s.nreal, fst);
         });
@@ -572,6 +648,11 @@ int sl_shearrec_batch_dev(sl_system* h, const double* coeffs, int nframes, doubl
 
 int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* out, const double* K, int nK,
                          double sigma, int scaled, void* stream) {
+    return sl_denoise_batch_stack_dev(h, in, nframes, nullptr, out, K, nK, sigma, scaled, stream);
+}
+
+int sl_denoise_batch_stack_dev(sl_system* h, const double* in, int nframes, double* stacks, double* out,
+                               const double* K, int nK, double sigma, int scaled, void* stream) {
     return guard([&] {
         System& s = sys_of(h);
         require_dev_ptr(in, "denoise input");
@@ -581,16 +662,9 @@ int sl_denoise_batch_dev(sl_system* h, const double* in, int nframes, double* ou
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
         cudaStream_t st = stream_of(stream);
+        CallOrder co(s, st);
         deltas(s, K, nK, sigma, scaled, st);
-        if (lockstep_batch(s, nframes)) {
-            denoise_lockstep(s, in, nframes, out, st);
-            return;
-        }
-        fan_out(s, nframes, st, [&](int fr, cudaStream_t fst) {
-            s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
-            denoise(s, in + static_cast<size_t>(fr) * s.nreal, s.w->stack.p, out + static_cast<size_t>(fr) * s.nreal,
-                    s.delta.p, fst);
-        });
+        denoise_batch(s, in, nframes, stacks, out, st);
     });
 }
 
@@ -604,15 +678,17 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         const size_t n = static_cast<size_t>(nframes) * s.nreal;
         s.io_in.alloc(n);
         s.io_out.alloc(n);
+        HostPin pin_in(in, n * sizeof(double)), pin_out(out, n * sizeof(double));
         cudaStream_t st = 0;
         deltas(s, K, nK, sigma, scaled, st);
         // measured (tools/e2e_ab.sh, 8 frames of 512^2): 3 compute streams
         // 6250 frames/s, 1: 4800, 4: 6100, 5-6: 6220, per-frame fan-out: 6100
-        const char* pe = std::getenv("SLB_HOST_PIPE");
-        const int pipe = pe ? std::atoi(pe) : (s.fast2d ? 3 : 0);
+        const int pipe = s.knobs.host_pipe >= 0 ? s.knobs.host_pipe : (s.fast2d ? 3 : 0);
+        const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
         if (pipe > 0 && nframes > 1) {
             // pipelined: all H2D in frame order on one copy stream, the fused
             // denoise of frame f on compute stream f % pipe once its H2D is
@@ -625,12 +701,11 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             SL_CUDA(cudaEventRecord(s.fork_ev, st));
             for (int k = 1; k <= P + 2; ++k) SL_CUDA(cudaStreamWaitEvent(s.ws[static_cast<size_t>(k)]->st, s.fork_ev, 0));
             const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);
-            s.concurrency = env_int("SLB_PIPE_CONC", P);  // band grouping of fast2d_cfg
+            s.concurrency = s.knobs.pipe_conc >= 1 ? s.knobs.pipe_conc : P;  // band grouping of fast2d_cfg
             // SLB_PIPE_GROUP = 2: lock-step frame pairs per compute stream (one
             // launch per pass covers both frames, as in the device batch)
-            const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, env_int("SLB_PIPE_GROUP", 1))) : 1;
+            const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, s.knobs.pipe_group)) : 1;
             if (grp > 1 && s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-            const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
             const int ngroups = (nframes + grp - 1) / grp;
             try {
                 for (int g = 0; g < ngroups; ++g) {
@@ -641,12 +716,12 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
                     SL_CUDA(cudaEventRecord(ein, cin));
                     s.w = s.ws[static_cast<size_t>(1 + g % P)].get();
                     SL_CUDA(cudaStreamWaitEvent(s.w->st, ein, 0));
-                    s.w->stack.alloc(static_cast<size_t>(grp) * sfs);
+                    double* stk = group_stack(s, nullptr, 0, grp, sfs);
                     if (grp > 1)
-                        denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs,
-                                             s.io_out.p + off, s.nreal, s.delta.p, s.w->st);
+                        denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, stk, sfs, s.io_out.p + off, s.nreal,
+                                             s.delta.p, s.w->st);
                     else
-                        denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, s.w->st);
+                        denoise(s, s.io_in.p + off, stk, s.io_out.p + off, s.delta.p, s.w->st);
                     SL_CUDA(cudaEventRecord(ec, s.w->st));
                     SL_CUDA(cudaStreamWaitEvent(cout, ec, 0));
                     SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, nf * fb, cudaMemcpyDeviceToHost, cout));
@@ -666,31 +741,27 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         } else {
             // per frame (or lock-step frame group) on its workspace stream: H2D ->
             // fused denoise -> D2H, so one group's copies overlap the other groups'
-            // kernels (both copy engines busy)
-            // single frames measured better here than lock-step pairs: the first
-            // H2D and the last D2H are one frame each (SLB_LOCKSTEP_HOST=1: pairs)
-            const char* lh = std::getenv("SLB_LOCKSTEP_HOST");
-            const bool lock = lh && std::atoi(lh) != 0;
-            const int group = (lock && lockstep_batch(s, nframes)) ? lockstep_group(nframes) : 1;
+            // kernels (both copy engines busy); single frames measured better here
+            // than lock-step pairs (SLB_LOCKSTEP_HOST=1: pairs)
+            const bool lock = s.knobs.lockstep_host != 0;
+            const int group = (lock && lockstep_batch(s, nframes)) ? lockstep_group(s, nframes) : 1;
             if (group > 1 && s.Wmin < 1e-12)
                 throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
             const int ngroups = (nframes + group - 1) / group;
-            const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
             fan_out(s, ngroups, st, [&](int g, cudaStream_t fst) {
                 const int f0 = g * group, nf = std::min(group, nframes - f0);
                 const size_t off = static_cast<size_t>(f0) * s.nreal;
                 const size_t bytes = static_cast<size_t>(nf) * s.nreal * sizeof(double);
                 SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, bytes, cudaMemcpyHostToDevice, fst));
-                s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+                double* stk = group_stack(s, nullptr, 0, group, sfs);
                 if (group > 1) {
                     const int conc = s.concurrency;
                     s.concurrency = std::max(conc, 4);
-                    denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, s.materialize ? s.w->stack.p : nullptr, sfs,
-                                         s.io_out.p + off,
-                                         s.nreal, s.delta.p, fst);
+                    denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, stk, sfs, s.io_out.p + off, s.nreal,
+                                         s.delta.p, fst);
                     s.concurrency = conc;
                 } else {
-                    denoise(s, s.io_in.p + off, s.w->stack.p, s.io_out.p + off, s.delta.p, fst);
+                    denoise(s, s.io_in.p + off, stk, s.io_out.p + off, s.delta.p, fst);
                 }
                 SL_CUDA(cudaMemcpyAsync(out + off, s.io_out.p + off, bytes, cudaMemcpyDeviceToHost, fst));
             });
@@ -706,6 +777,7 @@ int sl_sheardec_host(sl_system* h, const double* f, double* coeffs) {
         if (!f || !coeffs) throw SlError(SL_ERR_INVALID, "null host pointer");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         s.io_in.alloc(static_cast<size_t>(s.nreal));
         s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
         SL_CUDA(cudaMemcpy(s.io_in.p, f, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
@@ -722,6 +794,7 @@ int sl_shearrec_host(sl_system* h, const double* coeffs, int nbands, double* f) 
         if (!f || !coeffs) throw SlError(SL_ERR_INVALID, "null host pointer");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         s.io_out.alloc(static_cast<size_t>(s.nreal));
         s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
         SL_CUDA(cudaMemcpy(s.stack.p, coeffs, static_cast<size_t>(s.nb()) * s.nreal * sizeof(double),
@@ -739,6 +812,7 @@ int sl_hard_threshold_host(sl_system* h, const double* in, double* out, int nban
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         deltas(s, K, nK, sigma, scaled, 0);
         if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "hard_threshold: stack does not match the system");
         const size_t n = static_cast<size_t>(s.nb()) * s.nreal;
@@ -758,12 +832,12 @@ int sl_denoise_host(sl_system* h, const double* in, double* out, const double* K
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         deltas(s, K, nK, sigma, scaled, 0);
         s.io_in.alloc(static_cast<size_t>(s.nreal));
         s.io_out.alloc(static_cast<size_t>(s.nreal));
-        s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
         SL_CUDA(cudaMemcpy(s.io_in.p, in, s.nreal * sizeof(double), cudaMemcpyHostToDevice));
-        denoise(s, s.io_in.p, s.stack.p, s.io_out.p, s.delta.p, 0);
+        denoise_one(s, s.io_in.p, nullptr, s.io_out.p, 0);
         SL_CUDA(cudaMemcpy(out, s.io_out.p, s.nreal * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
@@ -778,6 +852,7 @@ int sl_inpaint_dev(sl_system* h, const double* masked, const double* mask, doubl
         require_dev_ptr(out, "inpaint output");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
         inpaint(s, masked, mask, out, iterations, delta_init, delta_min, scale_by_rms != 0, stream_of(stream));
     });
 }
@@ -789,6 +864,7 @@ int sl_inpaint_host(sl_system* h, const double* masked, const double* mask, doub
         if (!masked || !mask || !out) throw SlError(SL_ERR_INVALID, "null host pointer");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         DBuf<double> dm, dk, dout;
         dm.alloc(static_cast<size_t>(s.nreal));
         dk.alloc(static_cast<size_t>(s.nreal));
@@ -813,6 +889,8 @@ int sl_separate_dev(sl_system* directional, sl_system* isotropic, const double* 
         std::unique_lock<std::mutex> lk2(i.mu, std::defer_lock);
         if (&d != &i) lk2.lock();
         DeviceGuard dg(d.device);
+        CallOrder co(d, stream_of(stream));
+        CallOrder co2(i, stream_of(stream));
         separate(d, i, signal, curves, blobs, iterations, delta_init, delta_min, scale_by_rms != 0,
                  stream_of(stream));
     });
@@ -829,6 +907,8 @@ int sl_separate_host(sl_system* directional, sl_system* isotropic, const double*
         std::unique_lock<std::mutex> lk2(i.mu, std::defer_lock);
         if (&d != &i) lk2.lock();
         DeviceGuard dg(d.device);
+        CallOrder co(d, 0);
+        CallOrder co2(i, 0);
         DBuf<double> ds, dc, db;
         ds.alloc(static_cast<size_t>(d.nreal));
         dc.alloc(static_cast<size_t>(d.nreal));
@@ -914,6 +994,7 @@ int sl_shcf_forward_file(sl_system* h, const double* f, const char* path, int ba
         if (!f || !path) throw SlError(SL_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         File out(path, "wb");
         if (!out.f) throw SlError(SL_ERR_FORMAT, std::string("cannot write coefficient file: ") + path);
         std::vector<unsigned char> hdr(shcf_header_bytes(s, s.nb()));
@@ -948,6 +1029,7 @@ int sl_shcf_inverse_file(sl_system* h, const char* path, double* out, int bands_
         if (!out || !path) throw SlError(SL_ERR_INVALID, "null argument");
         std::lock_guard<std::mutex> lk(s.mu);
         DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
         if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
         File in(path, "rb");
         if (!in.f) throw SlError(SL_ERR_FORMAT, std::string("cannot open coefficient file: ") + path);

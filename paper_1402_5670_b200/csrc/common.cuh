@@ -146,8 +146,48 @@ static void set_smem(K kern, size_t smem) {
     done[reinterpret_cast<const void*>(kern)] = smem;
 }
 
+// ------------------------------------------------------------------ knobs
+// A/B knobs, read once when a handle is created: no
+// getenv on the launch paths. -1 = the measured default for the geometry.
+static int env_knob(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+struct Knobs {
+    int group = -1, chunk = -1, group1 = -1, group2 = -1, chunk1 = -1;  // 2D band grouping (fast2d_cfg)
+    int g3 = -1, chunk3 = -1;                                          // 3D band group / chunk
+    int lockstep = 1, lockstep_frames = 2;                              // lock-step frame groups (device batch)
+    int host_pipe = -1, pipe_conc = -1, pipe_group = 1, lockstep_host = 0;  // pipelined host batch
+    bool denoise_unfused = false, disable_fast2d = false, disable_fast3d = false;
+    double real_tol = 1e-9;
+    static Knobs from_env() {
+        Knobs k;
+        k.group = env_knob("SLB_GROUP", -1);
+        k.chunk = env_knob("SLB_CHUNK", -1);
+        k.group1 = env_knob("SLB_GROUP1", -1);
+        k.group2 = env_knob("SLB_GROUP2", -1);
+        k.chunk1 = env_knob("SLB_CHUNK1", -1);
+        k.g3 = env_knob("SLB_G3", -1);
+        k.chunk3 = env_knob("SLB_CHUNK3", -1);
+        k.lockstep = env_knob("SLB_LOCKSTEP", 1);
+        k.lockstep_frames = std::max(1, env_knob("SLB_LOCKSTEP_FRAMES", 2));
+        k.host_pipe = env_knob("SLB_HOST_PIPE", -1);
+        k.pipe_conc = env_knob("SLB_PIPE_CONC", -1);
+        k.pipe_group = std::max(1, env_knob("SLB_PIPE_GROUP", 1));
+        k.lockstep_host = env_knob("SLB_LOCKSTEP_HOST", 0);
+        k.denoise_unfused = std::getenv("SLB_DENOISE_UNFUSED") != nullptr;
+        k.disable_fast2d = std::getenv("SLB_DISABLE_FAST2D") != nullptr;
+        k.disable_fast3d = std::getenv("SLB_DISABLE_FAST3D") != nullptr;
+        if (const char* e = std::getenv("SLB_REAL_TOL")) k.real_tol = std::atof(e);
+        return k;
+    }
+};
+// knob value, or `dflt` where the knob is unset (< 1)
+static inline int knob_or(int v, int dflt) { return v >= 1 ? v : dflt; }
+
 // ------------------------------------------------------------------ system
 struct System {
+    Knobs knobs = Knobs::from_env();
     int ndim = 2;
     int n[3] = {1, 1, 1};
     int L_last = 0, H = 0, ldh = 0;
@@ -199,6 +239,7 @@ struct System {
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
     bool materialize = true;        // fused denoise writes the thresholded stack (sl_set_stack_output)
     cudaEvent_t fork_ev = nullptr;
+    cudaEvent_t last_ev = nullptr;  // completion of the previous call on this handle (any stream)
     std::vector<cudaEvent_t> pipe_ev;  // per-frame H2D / compute-done events of pipelined host batches
     DBuf<double> delta, stack, io_in, io_out;
     std::vector<double> delta_host;  // host copy of `delta` (deltas() skips unchanged uploads)
@@ -230,6 +271,7 @@ struct System {
     }
     ~System() {
         if (fork_ev) cudaEventDestroy(fork_ev);
+        if (last_ev) cudaEventDestroy(last_ev);
         for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
     }
     // Ensure n workspaces exist (1..n-1 with their own non-blocking streams).
@@ -244,14 +286,7 @@ struct System {
         if (!fork_ev) SL_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
         while (static_cast<int>(ws.size()) < n) {
             auto p = std::make_unique<Workspace>();
-            // graded priorities (workspace 1 highest): frames of a batch finish
-            // staggered, so one frame's D2H overlaps the others' kernels
-            int lo = 0, hi = 0;
-            SL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            const char* pe = std::getenv("SLB_PRIO");
-            const bool graded = pe && std::atoi(pe) != 0;  // opt-in: costs ~5 % device throughput
-            const int prio = graded ? std::min(lo, hi + static_cast<int>(ws.size()) - 1) : lo;
-            SL_CUDA(cudaStreamCreateWithPriority(&p->st, cudaStreamNonBlocking, prio));
+            SL_CUDA(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
             SL_CUDA(cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming));
             ws.push_back(std::move(p));
         }
@@ -266,6 +301,20 @@ struct System {
         plans[L] = std::move(ph);
         return p;
     }
+};
+
+// Orders one API call after the previous call on the same handle, whatever
+// stream each was issued on: the handle's scratch (workspaces, delta, stack,
+// io buffers, self-resetting counters) is shared by all calls, and the host
+// mutex only orders when work is queued, not when the GPU runs it.
+struct CallOrder {
+    System& s;
+    cudaStream_t st;
+    CallOrder(System& sys, cudaStream_t stream) : s(sys), st(stream) {
+        if (!s.last_ev) SL_CUDA(cudaEventCreateWithFlags(&s.last_ev, cudaEventDisableTiming));
+        else SL_CUDA(cudaStreamWaitEvent(st, s.last_ev, 0));
+    }
+    ~CallOrder() { cudaEventRecord(s.last_ev, st); }
 };
 
 // Brackets one kernel launch: counts it and, when profiling, records a

@@ -10,11 +10,6 @@
 #pragma once
 
 #include "fast2d_host.cuh"
-#include "tma.cuh"
-
-#ifndef SLB_ROWS_DIRECT_STORE
-#define SLB_ROWS_DIRECT_STORE 0
-#endif
 
 namespace slb {
 
@@ -99,22 +94,6 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
             zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
         }
     }
-#if SLB_ROWS_DIRECT_STORE
-    // rows 2q and 2q+1 of spectrum column k are one aligned 32-byte sector of
-    // the column-major intermediate: store straight from registers (no tile
-    // round trip through shared memory, no barriers)
-#pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            double2* dst = inter + (long long)k * n0 + r0 + 2 * q;
-            if (2 * q < nrows)
-                __stcg(dst, make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y)));
-            if (2 * q + 1 < nrows)
-                __stcg(dst + 1, make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x)));
-        }
-    }
-#else
     __syncthreads();  // all line buffers read before the tile is rewritten
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
@@ -129,168 +108,14 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
         if (rr < nrows) __stcg(inter + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
     }
-#endif
 }
 
-// TMA variant of k2_rows_fused (2V = 8 rows, 128-byte tile rows): the
-// column-major block comes in and goes out as two bulk tensor copies per CTA
-// (boxes of HB = ceil(H/2) k-rows x 8 complex rows, 128B swizzle = the tile's
-// XOR layout; out-of-range rows / k are zero-filled on load and clipped on
-// store) instead of per-thread cp.async / store loops.
-template <int L>
-struct RowsTma {
-    static constexpr int V = RowCfg<L>::V;
-    static constexpr bool OK = 2 * V == 8;
-    static constexpr int H = L / 2 + 1;
-    static constexpr int HB = (H + 1) / 2;
-    static constexpr int TILE = 2 * HB * 2 * V > V * L ? 2 * HB * 2 * V : V * L;  // double2 slots
-    static constexpr size_t SMEM = TILE * sizeof(double2) + 1024 + 16;             // + alignment + mbarrier
-};
-
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
-        "r"(phase)
-        : "memory");
-}
-
-template <int L>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
-    k2_rows_fused_tma(double* __restrict__ band, long long bbs, int n0, double scale, const double* __restrict__ delta,
-                      int band0, const double2* __restrict__ tw, int cstride, long long bzs,
-                      const __grid_constant__ CUtensorMap tmap) {
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V, H = RowsTma<L>::H, HB = RowsTma<L>::HB;
-    constexpr int KPT = (L / 2 + 1 + T - 1) / T;
-    extern __shared__ double2 smem_raw[];
-    double2* tile = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(tile + RowsTma<L>::TILE));
-    const int r0 = blockIdx.x * 2 * V;
-    const int bidx = blockIdx.y + blockIdx.z * cstride;  // band slot in the intermediate buffer
-    if (band) band += blockIdx.y * bbs + blockIdx.z * bzs;
-    const unsigned ts = static_cast<unsigned>(__cvta_generic_to_shared(tile));
-    const uint64_t tm = reinterpret_cast<uint64_t>(&tmap);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * HB * 128)
-                     : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                ts),
-            "l"(tm), "r"(2 * r0), "r"(0), "r"(bidx), "r"(bar)
-            : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-                ts + HB * 128),
-            "l"(tm), "r"(2 * r0), "r"(HB), "r"(bidx), "r"(bar)
-            : "memory");
-    }
-    mbar_wait(bar, 0);
-    const int q = threadIdx.x / T, t = threadIdx.x - q * T;
-    double2 x[E];
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        const int k = t + T * m;
-        double2 X, Y;
-        if (k < H) {
-            X = tile[tslot<V>(k, 2 * q)];
-            Y = tile[tslot<V>(k, 2 * q + 1)];
-            if (k == 0 || 2 * k == L) {
-                X.y = 0.0;
-                Y.y = 0.0;
-            }
-            x[m] = make_double2(X.x - Y.y, X.y + Y.x);
-        } else {
-            X = tile[tslot<V>(L - k, 2 * q)];
-            Y = tile[tslot<V>(L - k, 2 * q + 1)];
-            x[m] = make_double2(X.x + Y.y, Y.x - X.y);
-        }
-    }
-    __syncthreads();  // every line has gathered: the tile is dead
-    double2* lb = tile + q * LineBuf<L, false>::N;
-    reg_fft<L, +1, false>(x, lb, t, tw);
-    const double dl = delta[band0 + blockIdx.y];
-    const int ra = r0 + 2 * q;
-#pragma unroll
-    for (int m = 0; m < E; ++m) {
-        double a = x[m].x * scale, c = x[m].y * scale;
-        if (dl >= 0.0) {
-            if (fabs(a) < dl) a = 0.0;
-            if (fabs(c) < dl) c = 0.0;
-        }
-        const int i = t + T * m;
-        if (band) {
-            if (ra < n0) band[(long long)ra * L + i] = a;
-            if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
-        }
-        x[m] = make_double2(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : 0.0);
-    }
-    reg_fft<L, -1, false>(x, lb, t, tw);
-#pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
-    line_sync<T>();
-    double2 zk[KPT], zm[KPT];
-#pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            zk[u] = lb[swz<false>(k)];
-            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
-        }
-    }
-    __syncthreads();  // all line buffers read before the tile is rewritten
-#pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            tile[tslot<V>(k, 2 * q)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));
-            tile[tslot<V>(k, 2 * q + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));
-        }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
-                     "r"(2 * r0), "r"(0), "r"(bidx), "r"(ts)
-                     : "memory");
-        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tm),
-                     "r"(2 * r0), "r"(HB), "r"(bidx), "r"(ts + HB * 128)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    }
-}
-
-// rows pass of the fused denoise: the TMA kernel when the tile shape allows
-// (2V = 8) and SLB_ROWS_TMA != 0, else the cp.async one. `cstride` = band
-// slots per frame in the intermediate (lock-step batches), nslots = all slots.
-static bool rows_tma_enabled() {
-    const char* e = std::getenv("SLB_ROWS_TMA");
-    return e && std::atoi(e) == 1;
-}
+// rows pass of the fused denoise (band = null: the stack is not materialised)
 template <int L>
 static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, double2* inter, long long ibs,
                               double* band, long long bbs, int n0, int H, double scale, const double* delta,
-                              int band0, const double2* tw, long long izs, long long bzs, int cstride, int nslots) {
+                              int band0, const double2* tw, long long izs, long long bzs) {
     using RC = RowCfg<L>;
-    if constexpr (RowsTma<L>::OK) {
-        if (rows_tma_enabled()) {
-            const cuuint64_t dims[3] = {2ull * n0, static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(nslots)};
-            const cuuint64_t strides[2] = {16ull * n0, 16ull * n0 * H};
-            const cuuint32_t box[3] = {16, static_cast<cuuint32_t>(RowsTma<L>::HB), 1};
-            const CUtensorMap tm = tma_map_f64(inter, 3, dims, strides, box);
-            set_smem(k2_rows_fused_tma<L>, RowsTma<L>::SMEM);
-            k2_rows_fused_tma<L><<<grid, RC::THREADS, RowsTma<L>::SMEM, st>>>(band, bbs, n0, scale, delta, band0, tw,
-                                                                             cstride, bzs, tm);
-            check_launch("k2_rows_fused_tma");
-            return;
-        }
-    }
     auto* k = band ? k2_rows_fused<L, true> : k2_rows_fused<L, false>;
     set_smem(k, tile_smem);
     k<<<grid, RC::THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
@@ -355,7 +180,7 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
             LaunchScope ls(s, "f2_rows_fused", st, cb);
             launch_rows_fused<L1>(dim3(row_blocks, cb), row_smem, st, s.w->inter.p, nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
-                                  delta, s.lo + b0, tw1, 0, 0, 0, C);
+                                  delta, s.lo + b0, tw1, 0, 0);
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, cb);
@@ -440,7 +265,7 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
             LaunchScope ls(s, "f2_rows_fused", st, static_cast<long long>(cb) * nf);
             launch_rows_fused<L1>(dim3(row_blocks, cb, nf), row_smem, st, s.w->inter.p, nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
-                                  delta, s.lo + b0, tw1, izs, sfs, C, nf * C);
+                                  delta, s.lo + b0, tw1, izs, sfs);
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, static_cast<long long>(cb) * nf);

@@ -7,18 +7,13 @@
 
 namespace slb {
 
-static bool fast2d_supported(int n0, int n1) {
-    if (std::getenv("SLB_DISABLE_FAST2D")) return false;
+static bool fast2d_supported(const Knobs& k, int n0, int n1) {
+    if (k.disable_fast2d) return false;
     if (n0 != n1) return false;
     switch (n0) {
         case 64: case 128: case 192: case 256: case 512: case 1024: case 2048: return true;
         default: return false;
     }
-}
-
-static int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e ? std::max(1, std::atoi(e)) : dflt;
 }
 
 // Band grouping: G bands per column-pass CTA (F / accumulator reuse), C bands
@@ -37,17 +32,17 @@ static Fast2DCfg fast2d_cfg(const System& s) {
     if (!conc) {
         // 2-3 frames in flight (the pipelined host batch's 3 compute streams):
         // G = 14 at 512^2 (e2e +2 % over 7, r1p tools/ab_group1.sh)
-        const int G = s.concurrency > 1 ? env_int("SLB_GROUP2", s.n[0] >= 512 ? 14 : 4)
-                                        : env_int("SLB_GROUP1", s.n[0] >= 512 ? 7 : 4);
-        const int C = env_int("SLB_CHUNK1", std::max(G, static_cast<int>((256.0 * 1024 * 1024) / per)));
+        const int G = s.concurrency > 1 ? knob_or(s.knobs.group2, s.n[0] >= 512 ? 14 : 4)
+                                        : knob_or(s.knobs.group1, s.n[0] >= 512 ? 7 : 4);
+        const int C = knob_or(s.knobs.chunk1, std::max(G, static_cast<int>((256.0 * 1024 * 1024) / per)));
         return {G, std::max(1, C)};
     }
     // G = 28 where 28 bands fit the 64 MiB chunk (512^2: one group per chunk,
     // +1.2 % over G = 14 after the register-resident column state, r1o sweep),
     // else 14 (1024^2: chunks of 14)
     const int cfit = std::max(1, static_cast<int>((64.0 * 1024 * 1024) / per));
-    const int G = env_int("SLB_GROUP", cfit >= 28 ? 28 : 14);
-    int C = env_int("SLB_CHUNK", cfit);
+    const int G = knob_or(s.knobs.group, cfit >= 28 ? 28 : 14);
+    int C = knob_or(s.knobs.chunk, cfit);
     C = std::max(G, (C / G) * G);
     return {G, C};
 }

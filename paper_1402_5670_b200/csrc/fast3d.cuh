@@ -12,8 +12,6 @@
 // per-scale factor tables (system3d.cpp:144-186), so no filter bank is read.
 #pragma once
 
-#include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time)
-
 #include "fast2d.cuh"
 #include "kernels.cuh"
 
@@ -107,24 +105,14 @@ enum Ax0Mode : int {
 // Line (k2, k1) = contiguous N[(k2*n + k1)*n + k0]; output element (k2, i0, k1)
 // goes to R[(k2*n + i0)*n + k1], staged through the tile so each i0 writes V
 // consecutive k1 (a 128-byte run).
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-// TMA = true: the finished [n][V] tile (V = 8 double2 = one 128-byte row per
-// i0, chunks XOR-swizzled by i0 & 7 -- exactly the TMA 128B swizzle) leaves
-// through one bulk tensor store per band (tensor map over the rotated
-// buffer: k1-doubles x i0 x k2 x band) instead of a strided store loop.
-template <int L, int DIR, int MODE, bool TMA = false>
+template <int L, int DIR, int MODE>
 __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
     k3_ax0_to_rot(const double2* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int H,
                   FiltSynth3D filt, int band0, int G, int nb, const double* __restrict__ WN,
-                  const double2* __restrict__ tw, const __grid_constant__ CUtensorMap tmap) {
+                  const double2* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = Ax0Cfg<L>::V;
     constexpr int n = L;
-    extern __shared__ double2 smem_raw[];  // [L][V] tile + V line buffers (1024-byte aligned for TMA)
-    double2* tile = TMA ? reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023))
-                        : smem_raw;
+    extern __shared__ double2 tile[];  // [L][V] tile; the V line buffers alias it
     const int lines_per_k2 = n / V;
     const int k2 = blockIdx.x / lines_per_k2;
     const int k1_0 = (blockIdx.x - k2 * lines_per_k2) * V;
@@ -182,39 +170,20 @@ __global__ void __launch_bounds__(Ax0Cfg<L>::THREADS, Ax0Cfg<L>::TO_MIN_BLOCKS)
 #pragma unroll
             for (int m = 0; m < E; ++m) pn[m] = SLB_AX0_LINEFILT ? fn.at(t + T * m) : filt.get_d(bn, t + T * m, k1, k2);
         }
-        if (bb > 0) {
-            if (TMA && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncthreads();  // previous band's tile fully written out
-        }
+        if (bb > 0) __syncthreads();  // previous band's tile fully written out
         reg_fft<L, DIR, false>(x, lb, t, tw);
         __syncthreads();              // every line's FFT is done with the aliased buffers
         // publish into the [i0][v] tile, then write 128-byte rotated runs
 #pragma unroll
         for (int m = 0; m < E; ++m) tile[aslot<V>(t + T * m, li)] = x[m];
-        if constexpr (TMA) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile writes -> async proxy
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                const int bd = MODE == kAx0DecMul ? g0 + bb : static_cast<int>(blockIdx.y);
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmap)),
-                    "r"(2 * k1_0), "r"(0), "r"(k2), "r"(bd), "r"(smem_u32(tile))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        } else {
-            __syncthreads();
-            double2* o = dst + (long long)(g0 + bb) * dbs + (long long)k2 * n * n + k1_0;
-            for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
-                const int i0 = idx / V, v = idx - i0 * V;
-                __stcg(o + (long long)i0 * n + v, tile[aslot<V>(i0, v)]);
-            }
+        __syncthreads();
+        double2* o = dst + (long long)(g0 + bb) * dbs + (long long)k2 * n * n + k1_0;
+        for (int idx = threadIdx.x; idx < V * L; idx += blockDim.x) {
+            const int i0 = idx / V, v = idx - i0 * V;
+            __stcg(o + (long long)i0 * n + v, tile[aslot<V>(i0, v)]);
         }
     }
-    if (TMA && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     (void)H;
-    (void)dst;
 }
 
 // ---------------------------------------------------------------- axis 0: R -> N

@@ -1,15 +1,13 @@
 // Host orchestration of the specialised 3D path (kernels in fast3d.cuh).
 #pragma once
 #include "fast2d_host.cuh"
-#include "tma.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
-#include "fast3d_plane.cuh"
 
 namespace slb {
 
-static bool fast3d_supported(const int* n) {
-    if (std::getenv("SLB_DISABLE_FAST3D")) return false;
+static bool fast3d_supported(const Knobs& k, const int* n) {
+    if (k.disable_fast3d) return false;
     if (n[0] != n[1] || n[1] != n[2]) return false;
     switch (n[0]) {
         case 64: case 128: case 192: case 256: return true;
@@ -25,29 +23,14 @@ static bool fast3d_supported(const int* n) {
 // rotated intermediate allows (192^3: ~100 bands, 128^3: all 99), split across
 // the frames in flight, at least 16.
 static int fast3d_group(const System& s) {
-    const char* e = std::getenv("SLB_G3");
-    if (e) return std::max(1, std::atoi(e));
+    if (s.knobs.g3 >= 1) return s.knobs.g3;
     const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
     const double budget = 6.0 * 1024 * 1024 * 1024 / std::max(1, s.concurrency);
     return std::max(1, std::min(s.nb(), std::max(16, static_cast<int>(budget / per))));
 }
 static int fast3d_chunk(const System& s) {
     const double per = static_cast<double>(s.H) * s.n[0] * s.n[1] * sizeof(double2);
-    return env_int("SLB_CHUNK3", std::max(fast3d_group(s), static_cast<int>((64.0 * 1024 * 1024) / per)));
-}
-
-// Tensor map over a rotated buffer R[band][k2][i0][k1] (doubles along k1) for the
-// TMA tile stores of k3_ax0_to_rot: box = 8 complex k1 x all i0, 128B swizzle.
-static bool ax0_tma() {
-    const char* e = std::getenv("SLB_AX0_TMA");
-    return e && std::atoi(e) == 1;
-}
-static CUtensorMap rot_tensor_map(const double2* base, int n, int H, int nbands) {
-    const cuuint64_t dims[4] = {2ull * n, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(H),
-                                static_cast<cuuint64_t>(nbands)};
-    const cuuint64_t strides[3] = {16ull * n, 16ull * n * n, 16ull * n * n * H};
-    const cuuint32_t box[4] = {16, static_cast<cuuint32_t>(n), 1, 1};
-    return tma_map_f64(base, 4, dims, strides, box);
+    return knob_or(s.knobs.chunk3, std::max(fast3d_group(s), static_cast<int>((64.0 * 1024 * 1024) / per)));
 }
 
 template <int n>
@@ -95,22 +78,6 @@ struct Fast3DLaunch {
             inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw, 0, 0);
         check_launch("k2_rows_fused");
     }
-    // axis1<+1> + rows_fused + axis1<-1> as one plane pass on 2-CTA clusters
-    // (fast3d_plane.cuh); n = 128 / 192 (a 256 plane needs > 2 SMs of smem)
-    static constexpr bool kPlane = n == 128 || n == 192;
-    static bool plane_enabled() {
-        const char* e = std::getenv("SLB_PLANE3");
-        return kPlane && e && std::atoi(e) == 1;
-    }
-    void plane_fused(double2* inter, double* band, long long bbs, int nb, const double* delta, int band0) {
-        if constexpr (kPlane) {
-            set_smem(k3_plane_fused<n>, PlaneCfg<n>::SMEM);
-            LaunchScope ls(s, "f3_plane_fused", st, nb);
-            k3_plane_fused<n><<<dim3(2 * n, nb), PlaneCfg<n>::THREADS, PlaneCfg<n>::SMEM, st>>>(
-                inter, nT, band, bbs, 1.0 / static_cast<double>(s.nreal), delta, band0, tw);
-            check_launch("k3_plane_fused");
-        }
-    }
     template <int DIR>
     void axis1(double2* data, int nb) {
         set_smem(k3_lines_contig<n, DIR>, col_smem);
@@ -124,18 +91,9 @@ struct Fast3DLaunch {
         LaunchScope ls(s, nm, st, nb);
         const int G = MODE == kAx0DecMul ? std::min(fast3d_group(s), nb) : 1;
         const int groups = (nb + G - 1) / G;
-        if (ax0_tma() && AC::V == 8) {
-            const CUtensorMap tm = rot_tensor_map(dst, n, H, nb);
-            const size_t sm = ax_smem + 1024;  // room to align the tile to 1024 bytes
-            set_smem(k3_ax0_to_rot<n, DIR, MODE, true>, sm);
-            k3_ax0_to_rot<n, DIR, MODE, true><<<dim3(ax_blocks, groups), AC::THREADS, sm, st>>>(
-                src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw, tm);
-        } else {
-            CUtensorMap none{};
-            set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
-            k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, groups), AC::THREADS, ax_smem, st>>>(
-                src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw, none);
-        }
+        set_smem(k3_ax0_to_rot<n, DIR, MODE>, ax_smem);
+        k3_ax0_to_rot<n, DIR, MODE><<<dim3(ax_blocks, groups), AC::THREADS, ax_smem, st>>>(
+            src, sbs, dst, nT, H, s.synth, band0, G, nb, WN, tw);
         check_launch("k3_ax0_to_rot");
     }
     template <int DIR, int MODE>
@@ -210,13 +168,9 @@ static void denoise3d_fast_t(System& s, const double* f, double* stack, double* 
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         K.template to_rot<+1, kAx0DecMul>(s.w->F.p, 0, s.w->inter.p, cb, s.lo + b0, nullptr, "f3_ax0_dec");
-        if (Fast3DLaunch<n>::plane_enabled()) {
-            K.plane_fused(s.w->inter.p, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, cb, delta, s.lo + b0);
-        } else {
-            K.template axis1<+1>(s.w->inter.p, cb);
-            K.rows_fused(s.w->inter.p, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, cb, delta, s.lo + b0);
-            K.template axis1<-1>(s.w->inter.p, cb);
-        }
+        K.template axis1<+1>(s.w->inter.p, cb);
+        K.rows_fused(s.w->inter.p, (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, cb, delta, s.lo + b0);
+        K.template axis1<-1>(s.w->inter.p, cb);
         K.template from_rot<-1, kAx0RecAcc>(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, "f3_ax0_rec");
     }
     K.template to_rot<+1, kAx0DivW>(s.w->acc.p, 0, s.w->inter.p, 1, 0, s.WN.p, "f3_ax0_final");

@@ -116,13 +116,15 @@ static void inpaint(System& s, const double* masked, const double* mask, double*
     uniform_deltas(s, delta, lambda, iterations, scaled, dl, st);
     res.alloc(static_cast<size_t>(s.nreal));
     SL_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * s.nreal, st));  // estimate = 0
+    // the per-iteration thresholded stacks are internal: the fused passes never
+    // write them (bitwise the same result)
     for (int it = 0; it < iterations; ++it) {
         {
             LaunchScope ls(s, "inpaint_residual", st, 1);
             k_inpaint_residual<<<elem_blocks(s.nreal), 256, 0, st>>>(masked, mask, out, res.p, s.nreal);
             check_launch("k_inpaint_residual");
         }
-        denoise(s, res.p, s.stack.p, out, dl.p + static_cast<size_t>(it) * s.R, st);
+        denoise(s, res.p, nullptr, out, dl.p + static_cast<size_t>(it) * s.R, st);
     }
     SL_CUDA(cudaStreamSynchronize(st));  // dl / res are freed on return
 }
@@ -158,8 +160,8 @@ static void separate(System& dir, System& iso, const double* signal, double* cur
             k_separate_args<<<elem_blocks(dir.nreal), 256, 0, st>>>(signal, curves, blobs, a0.p, a1.p, dir.nreal);
             check_launch("k_separate_args");
         }
-        denoise(dir, a0.p, dir.stack.p, curves, d0.p + static_cast<size_t>(it) * dir.R, st);
-        denoise(iso, a1.p, iso.stack.p, blobs, d1.p + static_cast<size_t>(it) * iso.R, st);
+        denoise(dir, a0.p, nullptr, curves, d0.p + static_cast<size_t>(it) * dir.R, st);
+        denoise(iso, a1.p, nullptr, blobs, d1.p + static_cast<size_t>(it) * iso.R, st);
     }
     SL_CUDA(cudaStreamSynchronize(st));
 }

@@ -53,10 +53,10 @@ static void build_blur_2d(System& s, const Taps2& kernel, cudaStream_t st) {
     double im, re;
     std::memcpy(&im, &hm[0], 8);
     std::memcpy(&re, &hm[1], 8);
-    if (re > 0 && im / re > real_tol())
+    if (re > 0 && im / re > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "quality: blur kernel spectrum is not real (kernel not centrally symmetric)");
     s.rms.assign(1, 0.0);
-    if (fast2d_supported(s.n[0], s.n[1])) {
+    if (fast2d_supported(s.knobs, s.n[0], s.n[1])) {
         s.fast2d = true;
         s.psiT.alloc(static_cast<size_t>(s.H) * s.n[0]);
         k_half_to_colmajor<<<std::min<long long>(8192, (s.H * (long long)s.n[0] + 255) / 256), 256, 0, st>>>(

@@ -133,21 +133,25 @@ __global__ void k_synth_band(FiltSynth3DFlat f, int band, long long nhalf, doubl
 }
 
 
-// denoise = inverse(hard_threshold(forward(f))) with the stack materialised in
-// `stack`; the 2D fast path fuses the dec rows pass, the threshold and the rec
-// rows pass (fast2d_fused.cuh). SLB_DENOISE_UNFUSED=1 forces dec + rec.
+// denoise = inverse(hard_threshold(forward(f))). `stack` receives the
+// thresholded stack, or is null (the fused paths then never write it); the
+// fused 2D / 3D paths threshold in the dec epilogue and feed the rec in the
+// same pass (fast2d_fused.cuh, fast3d_host.cuh). SLB_DENOISE_UNFUSED=1 forces
+// dec + rec through a stack.
 static void denoise(System& s, const double* f, double* stack, double* out, const double* delta, cudaStream_t st) {
-    // fused paths: the thresholded stack is written only when materialised
-    // (sl_set_stack_output; the reference's denoise materialises it)
-    if (s.fast2d && !std::getenv("SLB_DENOISE_UNFUSED")) {
+    if (s.fast2d && !s.knobs.denoise_unfused) {
         if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-        denoise2d_fast(s, f, s.materialize ? stack : nullptr, out, delta, st);
+        denoise2d_fast(s, f, stack, out, delta, st);
         return;
     }
-    if (s.fast3d && !std::getenv("SLB_DENOISE_UNFUSED")) {
+    if (s.fast3d && !s.knobs.denoise_unfused) {
         if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-        denoise3d_fast(s, f, s.materialize ? stack : nullptr, out, delta, st);
+        denoise3d_fast(s, f, stack, out, delta, st);
         return;
+    }
+    if (!stack) {
+        s.w->stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+        stack = s.w->stack.p;
     }
     dec(s, f, stack, delta, st);
     rec(s, stack, out, st);

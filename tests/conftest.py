@@ -36,3 +36,16 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.fail("gpu-marked test needs a CUDA device")
     return torch.device("cuda:0")
+
+
+def kept_fp_torch(stack2d):
+    """Per band (count, sum of kept flat indices, sum of (index mod 1000003)^2) of
+    a [R, N] CUDA stack: the kept-position fingerprint oracle/gen_golden.py
+    stores from the reference's thresholded stack."""
+    import torch
+    out = np.zeros((stack2d.shape[0], 3), dtype=np.int64)
+    for b in range(stack2d.shape[0]):
+        idx = torch.nonzero(stack2d[b]).squeeze(1)
+        r = idx % 1000003
+        out[b] = (idx.numel(), int(idx.sum().item()), int((r * r).sum().item()))
+    return out

@@ -290,7 +290,8 @@ def test_host_batch_pipelines_agree(cuda, monkeypatch, pipe, group):
     frames = np.stack([P.add_gaussian_noise(P.cartoon(128), 25.0, 40 + i) for i in range(7)])
     monkeypatch.setenv("SLB_HOST_PIPE", pipe)
     monkeypatch.setenv("SLB_PIPE_GROUP", group)
-    got = P.denoise_batch(frames, s, sch)
+    sp = P.build_system_2d(128, 128, P.ScaleProfile.from_levels([1, 2]))  # knobs are read at creation
+    got = P.denoise_batch(frames, sp, sch)
     for i in range(7):
         one = P.denoise(frames[i], s, sch)
         assert np.linalg.norm(got[i] - one) <= 1e-12 * np.linalg.norm(one)
@@ -356,17 +357,3 @@ def test_stack_free_denoise_same_result(cuda):
         assert torch.equal(P.denoise_batch(x, s, sch), want)
         assert torch.equal(P.denoise(x[0], s, sch), one)
         s.set_stack_output(True)
-
-
-def test_rows_tma_matches(cuda, monkeypatch):
-    # TMA staging of the fused rows pass (SLB_ROWS_TMA=1) == the cp.async kernel, bitwise
-    import torch
-    s = P.build_system_2d(512, 512, P.ScaleProfile.from_levels([1, 1, 2, 2]))
-    sch = P.ThresholdSchedule.defaults_2d(40.0)
-    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(512), 40.0, i) for i in range(4)])).to(cuda)
-    monkeypatch.setenv("SLB_ROWS_TMA", "0")
-    want_b = P.denoise_batch(x, s, sch)
-    want_1 = P.denoise(x[0], s, sch)
-    monkeypatch.setenv("SLB_ROWS_TMA", "1")
-    assert torch.equal(P.denoise_batch(x, s, sch), want_b)
-    assert torch.equal(P.denoise(x[0], s, sch), want_1)
