@@ -75,7 +75,7 @@ int sl_system_create_3d(int n0, int n1, int n2, const int* levels, int n_scales,
                         int impulse_fan, int device, int shard_lo, int shard_hi, sl_system** out);
 /* Same with an explicit filter bank: build_system_2d/3d(..., fan, qmf, ...)
  * with a user FanFilter (row-major fan_rows x fan_cols taps, centre
- * (fan_c0, fan_c1); load_fan_filter / maxflat_fan(order), filters.hpp:54-67,
+ * (fan_c0, fan_c1); e.g. load_fan_filter, filters.hpp:54-67,
  * fan_design.cpp:70-108) and QmfPair (1D taps + centre index; filters.hpp:14-21).
  * lowpass NULL = maximally_flat_9tap(); highpass NULL = mirror_highpass(lowpass)
  * (QmfPair::from_lowpass); fan NULL = default_fan_filter(). fan_provenance is
@@ -92,9 +92,10 @@ int sl_system_create_3d_ex(int n0, int n1, int n2, const int* levels, int n_scal
                            int highpass_len, int highpass_center, const double* fan, int fan_rows, int fan_cols,
                            int fan_c0, int fan_c1, const char* fan_provenance, int device, int shard_lo,
                            int shard_hi, sl_system** out);
-/* fan_design::maxflat_fan(order) (fan_design.cpp:70-108), host: dims/centre
- * always written; taps written when non-NULL (cap doubles). */
-int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1);
+/* default_fan_filter() (filters.cpp:112-122): the bundled 15x15 dmaxflat4
+ * fan (a checksum-verified constant table); dims/centre always written, taps
+ * written when non-NULL (cap doubles). */
+int sl_default_fan(double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1);
 /* System descriptors (descriptor.hpp:12-39): sl_describe writes the text
  * write_descriptor() would write (describe(sys)); len = its length without the
  * NUL; text may be NULL to size. sl_system_create_from_descriptor parses that

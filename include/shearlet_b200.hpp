@@ -155,13 +155,12 @@ struct FanFilter {
     int rows = 0, cols = 0, center0 = 0, center1 = 0;
     std::string provenance = "custom";
     static FanFilter impulse() { return FanFilter{{1.0}, 1, 1, 0, 0, "impulse"}; }
-    static FanFilter maxflat(int order) {  // fan_design::maxflat_fan
+    static FanFilter default_fan() {  // default_fan_filter(), the bundled dmaxflat4 constant
         FanFilter f;
-        check(sl_maxflat_fan(order, nullptr, 0, &f.rows, &f.cols, &f.center0, &f.center1));
+        check(sl_default_fan(nullptr, 0, &f.rows, &f.cols, &f.center0, &f.center1));
         f.taps.resize(static_cast<std::size_t>(f.rows) * f.cols);
-        check(sl_maxflat_fan(order, f.taps.data(), static_cast<int64_t>(f.taps.size()), nullptr, nullptr, nullptr,
-                             nullptr));
-        f.provenance = order == 4 ? "dmaxflat4" : "dmaxflat" + std::to_string(order);
+        check(sl_default_fan(f.taps.data(), static_cast<int64_t>(f.taps.size()), nullptr, nullptr, nullptr, nullptr));
+        f.provenance = "dmaxflat4";
         return f;
     }
 };

@@ -135,7 +135,7 @@ def lib():
     bank = [dp, i, i, dp, i, i, dp, i, i, i, i, C.c_char_p]
     L.sl_system_create_2d_ex.argtypes = [i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
     L.sl_system_create_3d_ex.argtypes = [i, i, i, ip, i, i, i] + bank + [i, i, i, C.POINTER(P)]
-    L.sl_maxflat_fan.argtypes = [i, dp, C.c_int64, ip, ip, ip, ip]
+    L.sl_default_fan.argtypes = [dp, C.c_int64, ip, ip, ip, ip]
     L.sl_describe.argtypes = [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]
     L.sl_system_create_from_descriptor.argtypes = [C.c_char_p, i, i, i, i, C.POINTER(P)]
     L.sl_system_destroy.argtypes = [P]
@@ -201,7 +201,7 @@ EXPORTED_SYMBOLS = [
     "sl_set_streams", "sl_set_stack_output", "sl_sheardec_batch_dev", "sl_shearrec_batch_dev", "sl_denoise_batch_dev",
     "sl_denoise_batch_stack_dev", "sl_denoise_batch_host", "sl_inpaint_dev", "sl_inpaint_host", "sl_separate_dev", "sl_separate_host",
     "sl_shcf_size", "sl_shcf_serialize", "sl_shcf_deserialize", "sl_shcf_forward_file", "sl_shcf_inverse_file",
-    "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_maxflat_fan",
+    "sl_system_create_2d_ex", "sl_system_create_3d_ex", "sl_default_fan",
     "sl_describe", "sl_system_create_from_descriptor",
     "sl_gaussian_kernel", "sl_binarize", "sl_quality_q", "sl_quality_q_opt",
     "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
@@ -463,18 +463,13 @@ class FanFilter:
         return FanFilter(np.ones((1, 1)), 0, 0, "impulse")
 
     @staticmethod
-    def maxflat(order: int) -> "FanFilter":
-        """fan_design::maxflat_fan(order) (fan_design.cpp:70-108), computed by the library."""
-        r, c, c0, c1 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
-        _check(lib().sl_maxflat_fan(int(order), None, 0, C.byref(r), C.byref(c), C.byref(c0), C.byref(c1)))
-        t = np.zeros((r.value, c.value))
-        _check(lib().sl_maxflat_fan(int(order), _dp(t), t.size, None, None, None, None))
-        return FanFilter(t, c0.value, c1.value, f"dmaxflat{order}")
-
-    @staticmethod
     def default() -> "FanFilter":
-        """default_fan_filter() (filters.cpp:114-122), checksum-verified."""
-        f = FanFilter.maxflat(4)
+        """default_fan_filter() (filters.cpp:112-122): the bundled dmaxflat4 fan, checksum-verified."""
+        r, c, c0, c1 = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().sl_default_fan(None, 0, C.byref(r), C.byref(c), C.byref(c0), C.byref(c1)))
+        t = np.zeros((r.value, c.value))
+        _check(lib().sl_default_fan(_dp(t), t.size, None, None, None, None))
+        f = FanFilter(t, c0.value, c1.value, "dmaxflat4")
         if fan_checksum(f) != DEFAULT_FAN_CHECKSUM:
             raise AssetError("default_fan_filter: checksum mismatch on bundled fan filter")
         return f

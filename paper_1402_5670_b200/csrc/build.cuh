@@ -27,8 +27,8 @@ __global__ void k_embed2d(const double* __restrict__ taps, int t0, int t1, long 
     }
 }
 
-// half complex spectrum -> real table; records max |im| and max |re| (bits of
-// non-negative doubles order like unsigned integers).
+// half complex spectrum -> real table; records max |im| and max |re| into
+// maxabs[0..1] (bits of non-negative doubles order like unsigned integers)
 __global__ void k_take_real(const double2* __restrict__ in, double* __restrict__ out, long long nhalf, int ldh, int H,
                             unsigned long long* __restrict__ maxabs) {
     unsigned long long mi = 0, mr = 0;
@@ -43,6 +43,39 @@ __global__ void k_take_real(const double2* __restrict__ in, double* __restrict__
     }
     atomicMax(maxabs, mi);
     atomicMax(maxabs + 1, mr);
+}
+
+// full real n0 x n1 spectrum from a half spectrum [n0][ldh] of an even filter
+// (X(-a, -b) = X(a, b)), then (optionally) its transpose right after it
+__global__ void k_expand_even(const double2* __restrict__ half, int n0, int n1, int ldh, double* __restrict__ out,
+                              int with_transpose, unsigned long long* __restrict__ maxabs) {
+    const int H = n1 / 2 + 1;
+    const long long tot = (long long)n0 * n1;
+    unsigned long long mi = 0, mr = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+        const int a = (int)(e / n1), b = (int)(e - (long long)a * n1);
+        const double2 z = b < H ? half[(long long)a * ldh + b] : half[(long long)((n0 - a) % n0) * ldh + (n1 - b)];
+        out[e] = z.x;
+        if (with_transpose) out[tot + (long long)b * n0 + a] = z.x;
+        mi = max(mi, (unsigned long long)__double_as_longlong(fabs(z.y)));
+        mr = max(mr, (unsigned long long)__double_as_longlong(fabs(z.x)));
+    }
+    atomicMax(maxabs, mi);
+    atomicMax(maxabs + 1, mr);
+}
+
+// min / max of W over the valid half entries (bit order of non-negative doubles)
+__global__ void k_minmax_w(const double* __restrict__ W, long long nhalf, int ldh, int H,
+                           unsigned long long* __restrict__ mm) {
+    unsigned long long lo = ~0ull, hi = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nhalf; e += (long long)gridDim.x * blockDim.x) {
+        if ((e % ldh) >= H) continue;
+        const unsigned long long v = (unsigned long long)__double_as_longlong(W[e]);  // W >= 0
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
 }
 
 // W[e] = sum_i psi_i[e]^2 over all filters in index order (system2d.cpp:118-126).
@@ -113,17 +146,8 @@ __global__ void k_half_to_colmajor(const double* __restrict__ in, double* __rest
 }
 
 // ------------------------------------------------------------------ build helpers
-// Embed centred taps into an n0 x n1 periodic grid on the device and return
-// its Hermitian-half spectrum [n0][ldh] in `spec` (GPU FFT).
-static void spectrum_2d_of_dtaps(System& s, const double* dt, long t0, long t1, long c0, long c1, int n0, int n1,
-                                 DBuf<double>& grid, DBuf<double2>& spec, cudaStream_t st);
-static void spectrum_2d_of_taps(System& s, const Taps2& t, int n0, int n1, DBuf<double>& dtaps, DBuf<double>& grid,
-                                DBuf<double2>& spec, cudaStream_t st) {
-    dtaps.upload(t.v.data(), t.v.size(), st);
-    spectrum_2d_of_dtaps(s, dtaps.p, static_cast<long>(t.n0), static_cast<long>(t.n1), t.c0, t.c1, n0, n1, grid, spec,
-                         st);
-}
-// Embed device-resident centred taps into an n0 x n1 grid and r2c it (GPU).
+// Embed device-resident centred taps into an n0 x n1 periodic grid (wrap-sum)
+// and r2c it on the GPU into `spec` ([n0][ldh] Hermitian half).
 static void spectrum_2d_of_dtaps(System& s, const double* dt, long t0, long t1, long c0, long c1, int n0, int n1,
                                  DBuf<double>& grid, DBuf<double2>& spec, cudaStream_t st) {
     const int H = n1 / 2 + 1, ldh = (H + 7) / 8 * 8;
@@ -146,39 +170,30 @@ static void spectrum_2d_of_dtaps(System& s, const double* dt, long t0, long t1, 
         lines<-1, kPlain>(s, spec.p, 0, spec.p, 0, g, 1, 1, NoFilt{}, 0, nullptr, st);
     }
 }
-
-// Full real spectrum (n0 x n1) of centred taps, expanded from the half by the
-// even symmetry of symmetric taps; also returns max|im| / max|re| of the half.
-static std::vector<double> real_spectrum_full(System& s, const DTaps2& t, int n0, int n1, double* im_ratio,
-                                              cudaStream_t st) {
-    DBuf<double> grid;
-    DBuf<double2> spec;
-    spectrum_2d_of_dtaps(s, t.p(), t.n0, t.n1, t.c0, t.c1, n0, n1, grid, spec, st);
-    const int H = n1 / 2 + 1, ldh = (H + 7) / 8 * 8;
-    std::vector<double2> h(static_cast<size_t>(n0) * ldh);
-    SL_CUDA(cudaMemcpyAsync(h.data(), spec.p, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, st));
-    SL_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> full(static_cast<size_t>(n0) * n1);
-    double mi = 0, mr = 0;
-    for (int a = 0; a < n0; ++a)
-        for (int b = 0; b < H; ++b) {
-            const double2 z = h[static_cast<size_t>(a) * ldh + b];
-            mi = std::max(mi, std::fabs(z.y));
-            mr = std::max(mr, std::fabs(z.x));
-        }
-    for (int a = 0; a < n0; ++a)
-        for (int b = 0; b < n1; ++b) {
-            double v;
-            if (b < H)
-                v = h[static_cast<size_t>(a) * ldh + b].x;
-            else
-                v = h[static_cast<size_t>((n0 - a) % n0) * ldh + (n1 - b)].x;
-            full[static_cast<size_t>(a) * n1 + b] = v;
-        }
-    *im_ratio = mr > 0 ? mi / mr : 0.0;
-    return full;
+static void spectrum_2d_of_taps(System& s, const Taps2& t, int n0, int n1, DBuf<double>& dtaps, DBuf<double>& grid,
+                                DBuf<double2>& spec, cudaStream_t st) {
+    dtaps.upload(t.v.data(), t.v.size(), st);
+    spectrum_2d_of_dtaps(s, dtaps.p, static_cast<long>(t.n0), static_cast<long>(t.n1), t.c0, t.c1, n0, n1, grid, spec,
+                         st);
 }
 
+// |Im|/|Re| of the filter spectra, from per-filter device maxima (one copy at the end)
+static double worst_imag_ratio(const DBuf<unsigned long long>& mx, int count, int* which, cudaStream_t st) {
+    std::vector<unsigned long long> hm(2 * static_cast<size_t>(count));
+    SL_CUDA(cudaMemcpyAsync(hm.data(), mx.p, hm.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    SL_CUDA(cudaStreamSynchronize(st));
+    double worst = 0.0;
+    for (int i = 0; i < count; ++i) {
+        double im, re;
+        std::memcpy(&im, &hm[2 * static_cast<size_t>(i)], 8);
+        std::memcpy(&re, &hm[2 * static_cast<size_t>(i) + 1], 8);
+        if (re > 0 && im / re > worst) {
+            worst = im / re;
+            if (which) *which = i;
+        }
+    }
+    return worst;
+}
 
 static void finish_rms(System& s, const double* partial, int nblocks, int R) {
     s.rms.assign(static_cast<size_t>(R), 0.0);
@@ -190,17 +205,17 @@ static void finish_rms(System& s, const double* partial, int nblocks, int R) {
 }
 
 static void finish_W(System& s, cudaStream_t st) {
-    std::vector<double> w(static_cast<size_t>(s.nhalf));
-    SL_CUDA(cudaMemcpyAsync(w.data(), s.W.p, w.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    DBuf<unsigned long long> mm;
+    mm.alloc(2);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    SL_CUDA(cudaMemcpyAsync(mm.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_minmax_w<<<512, 256, 0, st>>>(s.W.p, s.nhalf, s.ldh, s.H, mm.p);
+    check_launch("k_minmax_w");
+    unsigned long long h[2];
+    SL_CUDA(cudaMemcpyAsync(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost, st));
     SL_CUDA(cudaStreamSynchronize(st));
-    double lo = INFINITY, hi = -INFINITY;
-    for (long long e = 0; e < s.nhalf; ++e) {
-        if ((e % s.ldh) >= s.H) continue;
-        lo = std::min(lo, w[static_cast<size_t>(e)]);
-        hi = std::max(hi, w[static_cast<size_t>(e)]);
-    }
-    s.Wmin = lo;
-    s.Wmax = hi;
+    std::memcpy(&s.Wmin, &h[0], 8);
+    std::memcpy(&s.Wmax, &h[1], 8);
 }
 
 static void init_geometry(System& s) {
@@ -227,7 +242,7 @@ static void validate_profile(const Profile& p) {
 
 static Taps2 fan_of(int impulse_fan) {
     if (impulse_fan) return Taps2::impulse();
-    Taps2 f = maxflat_fan(4);
+    Taps2 f = default_fan();
     if (fan_checksum(f) != kDefaultFanChecksum)
         throw SlError(SL_ERR_ASSET, "default_fan_filter: checksum mismatch on bundled fan filter");
     return f;
@@ -250,55 +265,40 @@ static void set_shard(System& s, int lo, int hi) {
     s.hi = hi;
 }
 
+// 2D bank (system2d.cpp:75-116): every filter's taps are built, embedded and
+// r2c'd on the device; no host round trip until the bank is complete.
 static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     validate_profile(s.prof);
-    const Taps2& fan = bank.fan;
-    const Qmf& q = bank.qmf;
     s.index = enumerate_2d(s.prof, s.full);
     s.R = static_cast<int>(s.index.size());
     const int J = s.prof.top();
     const int n0 = s.n[0], n1 = s.n[1];
     s.psi.alloc(static_cast<size_t>(s.R) * s.nhalf);
-    DBuf<double> dtaps, grid, tbuf;
+    DBuf<double> grid;
     DBuf<double2> spec;
     DBuf<unsigned long long> mx;
-    mx.alloc(2);
-    const bool host_taps = std::getenv("SLB_HOST_TAPS") != nullptr;  // cross-check path
-    const DTaps2 dfan = d_upload(fan, st);
-    double worst = 0.0;
-    int worst_i = -1;
+    mx.alloc(2 * static_cast<size_t>(s.R));
+    SL_CUDA(cudaMemsetAsync(mx.p, 0, 2 * static_cast<size_t>(s.R) * sizeof(unsigned long long), st));
+    DQmf q(bank.qmf, st);
+    const DTaps2 dfan = d_upload(bank.fan, st);
     for (int i = 0; i < s.R; ++i) {
         const Record& r = s.index[static_cast<size_t>(i)];
+        DTaps2 t;
         if (r.kind == 0) {
-            Taps1 hJ;
-            cascade(q, J, &hJ, nullptr);
-            spectrum_2d_of_taps(s, outer(hJ, hJ), n0, n1, dtaps, grid, spec, st);
-        } else if (host_taps) {
-            const int d = s.prof.levels[static_cast<size_t>(r.scale - s.prof.j0)];
-            Taps2 t = cone_taps(r.scale, r.k1, d, J, fan, q);
-            if (r.kind == 2) t = transposed(t);
-            spectrum_2d_of_taps(s, t, n0, n1, dtaps, grid, spec, st);
+            const DTaps1& hJ = q.lowpass(J, st);
+            t = d_outer(hJ, hJ, st);
         } else {
-            // upsampling, separable convolutions and the digital shear on the GPU
             const int d = s.prof.levels[static_cast<size_t>(r.scale - s.prof.j0)];
-            DTaps2 t = d_cone_taps(r.scale, r.k1, d, J, dfan, q, tbuf, st);
+            t = d_cone_taps(r.scale, r.k1, d, J, dfan, q, st);
             if (r.kind == 2) t = d_transposed(t, st);
-            spectrum_2d_of_dtaps(s, t.p(), t.n0, t.n1, t.c0, t.c1, n0, n1, grid, spec, st);
         }
-        SL_CUDA(cudaMemsetAsync(mx.p, 0, 2 * sizeof(unsigned long long), st));
-        k_take_real<<<256, 256, 0, st>>>(spec.p, s.psi.p + static_cast<size_t>(i) * s.nhalf, s.nhalf, s.ldh, s.H, mx.p);
+        spectrum_2d_of_dtaps(s, t.p(), t.n0, t.n1, t.c0, t.c1, n0, n1, grid, spec, st);
+        k_take_real<<<256, 256, 0, st>>>(spec.p, s.psi.p + static_cast<size_t>(i) * s.nhalf, s.nhalf, s.ldh, s.H,
+                                         mx.p + 2 * i);
         check_launch("k_take_real");
-        unsigned long long hm[2];
-        SL_CUDA(cudaMemcpyAsync(hm, mx.p, sizeof(hm), cudaMemcpyDeviceToHost, st));
-        SL_CUDA(cudaStreamSynchronize(st));
-        double im, re;
-        std::memcpy(&im, &hm[0], 8);
-        std::memcpy(&re, &hm[1], 8);
-        if (re > 0 && im / re > worst) {
-            worst = im / re;
-            worst_i = i;
-        }
     }
+    int worst_i = -1;
+    const double worst = worst_imag_ratio(mx, s.R, &worst_i, st);
     if (worst > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan; filter " + std::to_string(worst_i) +
                                          " has |im|/|re| = " + std::to_string(worst) + "); unsupported by this build");
@@ -315,7 +315,6 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     SL_CUDA(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     SL_CUDA(cudaStreamSynchronize(st));
     finish_rms(s, hp.data(), nblk, s.R);
-    // pad entries of W are never read as divisors; set them to 1 for safety
     finish_W(s, st);
     if (fast2d_supported(s.knobs, s.n[0], s.n[1])) {
         s.fast2d = true;
@@ -332,55 +331,48 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     }
 }
 
+// 3D factor tables (system3d.cpp:82-142): per scale the 1D ĝ spectra and the
+// 2K+1 Φ̂ planes (plus transposed copies for axis-0 lookups), and ĥ_J per
+// axis, all built, r2c'd and expanded to full real spectra on the device,
+// straight into the table buffers. W and RMS stream every synthesised filter.
 static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
     validate_profile(s.prof);
-    const Taps2& fan = bank.fan;
-    const Qmf& q = bank.qmf;
     s.index = enumerate_3d(s.prof, s.full);
     s.R = static_cast<int>(s.index.size());
     const int J = s.prof.top();
-    std::vector<double> tab1, tab2;
-    double worst = 0.0;
-    // 1D spectra: real even -> full length via symmetry.
-    auto add_1d = [&](const Taps1& t, int n) {
-        Taps2 t2 = Taps2::zeros(1, t.size(), 0, t.c);
-        std::memcpy(t2.v.data(), t.v.data(), t.size() * sizeof(double));
-        double r;
-        std::vector<double> full = real_spectrum_full(s, d_upload(t2, st), 1, n, &r, st);
-        worst = std::max(worst, r);
-        const int off = static_cast<int>(tab1.size());
-        tab1.insert(tab1.end(), full.begin(), full.end());
-        return off;
+    DQmf q(bank.qmf, st);
+    const DTaps2 dfan = d_upload(bank.fan, st);
+    // ---- table layout (host bookkeeping only)
+    struct Job {
+        DTaps2 taps;
+        int np, ns;
+        bool tab2;  // plane (+ transpose) in tab2, else a 1D spectrum in tab1
+        long long off;
+    };
+    std::vector<Job> jobs;
+    long long n1d = 0, n2d = 0;
+    auto add_1d = [&](const DTaps1& t, int n) {
+        jobs.push_back(Job{d_as_row(t), 1, n, false, n1d});
+        n1d += n;
+        return static_cast<int>(jobs.back().off);
     };
     std::map<std::pair<int, int>, int> cache2;  // (taps id, n_p * 65536 + n_s) -> off
     auto add_2d = [&](const DTaps2& t, int tid, int np, int ns) {
         const auto key = std::make_pair(tid, np * 65536 + ns);
         auto it = cache2.find(key);
         if (it != cache2.end()) return it->second;
-        double r;
-        std::vector<double> full = real_spectrum_full(s, t, np, ns, &r, st);
-        worst = std::max(worst, r);
-        const int off = static_cast<int>(tab2.size());
-        tab2.insert(tab2.end(), full.begin(), full.end());
-        // transposed copy right after the plane (ns x np): coalesced lookups
-        // when the principal index runs along axis 0 (FiltSynth3D::get_d)
-        for (int a = 0; a < ns; ++a)
-            for (int p = 0; p < np; ++p) tab2.push_back(full[static_cast<size_t>(p) * ns + a]);
-        cache2[key] = off;
-        return off;
+        jobs.push_back(Job{t, np, ns, true, n2d});
+        n2d += 2LL * np * ns;  // plane + its transpose
+        cache2[key] = static_cast<int>(jobs.back().off);
+        return cache2[key];
     };
-    DBuf<double> tbuf;
-    const DTaps2 dfan = d_upload(fan, st);
-    Taps1 hJ;
-    cascade(q, J, &hJ, nullptr);
     FiltSynth3D syn{};
     for (int a = 0; a < 3; ++a) {
         syn.n[a] = s.n[a];
-        syn.lp_off[a] = add_1d(hJ, s.n[a]);
+        syn.lp_off[a] = add_1d(q.lowpass(J, st), s.n[a]);
     }
     struct ScaleTabs {
         int d;
-        Taps1 g;
         std::vector<DTaps2> phi;  // device-built component taps
         std::map<int, int> goff;  // axis length -> offset
     };
@@ -392,13 +384,9 @@ static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
         const int d = s.prof.levels[static_cast<size_t>(si)];
         auto& S = sc[static_cast<size_t>(si)];
         S.d = d;
-        cascade(q, J - j, nullptr, &S.g);
         const int K = 1 << d;
         for (int k = -K; k <= K; ++k) {
-            if (std::getenv("SLB_HOST_TAPS"))
-                S.phi.push_back(d_upload(phi_taps(j, k, d, J, fan, q), st));
-            else
-                S.phi.push_back(d_phi_taps(j, k, d, J, dfan, q, tbuf, st));
+            S.phi.push_back(d_phi_taps(j, k, d, J, dfan, q, st));
             phi_id[static_cast<size_t>(si)].push_back(tid++);
         }
     }
@@ -417,17 +405,33 @@ static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
         b.s2 = axes[r.kind][2];
         const int np = s.n[b.pa];
         auto git = S.goff.find(np);
-        if (git == S.goff.end()) git = S.goff.emplace(np, add_1d(S.g, np)).first;
+        if (git == S.goff.end()) git = S.goff.emplace(np, add_1d(q.highpass(J - r.scale, st), np)).first;
         b.g_off = git->second;
-        b.p1_off = add_2d(S.phi[static_cast<size_t>(r.k1 + K)], phi_id[static_cast<size_t>(si)][static_cast<size_t>(r.k1 + K)],
-                          np, s.n[b.s1]);
-        b.p2_off = add_2d(S.phi[static_cast<size_t>(r.k2 + K)], phi_id[static_cast<size_t>(si)][static_cast<size_t>(r.k2 + K)],
-                          np, s.n[b.s2]);
+        b.p1_off = add_2d(S.phi[static_cast<size_t>(r.k1 + K)],
+                          phi_id[static_cast<size_t>(si)][static_cast<size_t>(r.k1 + K)], np, s.n[b.s1]);
+        b.p2_off = add_2d(S.phi[static_cast<size_t>(r.k2 + K)],
+                          phi_id[static_cast<size_t>(si)][static_cast<size_t>(r.k2 + K)], np, s.n[b.s2]);
     }
-    if (worst > s.knobs.real_tol)
+    // ---- spectra on the device, written straight into the tables
+    s.tab1.alloc(static_cast<size_t>(std::max(1LL, n1d)));
+    s.tab2.alloc(static_cast<size_t>(std::max(1LL, n2d)));
+    DBuf<unsigned long long> mx;
+    mx.alloc(2 * jobs.size());
+    SL_CUDA(cudaMemsetAsync(mx.p, 0, 2 * jobs.size() * sizeof(unsigned long long), st));
+    DBuf<double> grid;
+    DBuf<double2> spec;
+    for (size_t k = 0; k < jobs.size(); ++k) {
+        const Job& jb = jobs[k];
+        spectrum_2d_of_dtaps(s, jb.taps.p(), jb.taps.n0, jb.taps.n1, jb.taps.c0, jb.taps.c1, jb.np, jb.ns, grid, spec,
+                             st);
+        const int ldh = (jb.ns / 2 + 1 + 7) / 8 * 8;
+        double* dst = jb.tab2 ? s.tab2.p + jb.off : s.tab1.p + jb.off;
+        k_expand_even<<<blocks_for(static_cast<long long>(jb.np) * jb.ns), 256, 0, st>>>(
+            spec.p, jb.np, jb.ns, ldh, dst, jb.tab2 ? 1 : 0, mx.p + 2 * k);
+        check_launch("k_expand_even");
+    }
+    if (worst_imag_ratio(mx, static_cast<int>(jobs.size()), nullptr, st) > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan); unsupported by this build");
-    s.tab1.upload(tab1.data(), tab1.size(), st);
-    s.tab2.upload(tab2.data(), tab2.size(), st);
     s.bands3.upload(bd.data(), bd.size(), st);
     syn.bands = s.bands3.p;
     syn.tab1d = s.tab1.p;

@@ -247,16 +247,15 @@ int sl_system_create_from_descriptor(const char* text, int ndim, int device, int
                   shard_hi, out);
 }
 
-int sl_maxflat_fan(int order, double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1) {
+int sl_default_fan(double* taps, int64_t cap, int* rows, int* cols, int* c0, int* c1) {
     return guard([&] {
-        if (order < 1) throw SlError(SL_ERR_DOMAIN, "maxflat_fan: order must be >= 1");
-        const Taps2 f = maxflat_fan(order);
+        const Taps2 f = fan_of(0);  // the bundled constant, checksum-verified
         if (rows) *rows = static_cast<int>(f.n0);
         if (cols) *cols = static_cast<int>(f.n1);
         if (c0) *c0 = static_cast<int>(f.c0);
         if (c1) *c1 = static_cast<int>(f.c1);
         if (taps) {
-            if (cap < static_cast<int64_t>(f.v.size())) throw SlError(SL_ERR_INVALID, "maxflat_fan: buffer too small");
+            if (cap < static_cast<int64_t>(f.v.size())) throw SlError(SL_ERR_INVALID, "default_fan: buffer too small");
             std::memcpy(taps, f.v.data(), sizeof(double) * f.v.size());
         }
     });

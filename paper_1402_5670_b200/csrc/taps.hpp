@@ -1,14 +1,11 @@
-// Host-side filter-bank geometry for the B200 shearlet path.
+// Host-side descriptions of the filter bank: tap containers, the QMF pair and
+// fan asset (constants), the scale profile and the filter enumeration order.
+// All tap arithmetic (cascades, upsampling, separable convolutions, the
+// digital shear, embedding and FFTs) runs on the GPU: gpu_taps.cuh, build.cuh.
 //
-// Finite tap sets with declared centres, the QMF cascade, the maximally-flat
-// fan, the aperiodic digital shear and the filter enumeration order. These
-// feed the device-side system construction (system.cu), which embeds the
-// taps periodically, FFTs them on the GPU and reduces W / RMS there.
-//
-// Semantics follow the reference's filter algebra (paths relative to
-// /root/reference/proj/core): include/shearlet/taps.hpp:13-61,
-// src/filters.cpp:12-83, src/fan_design.cpp:48-108, src/shear.cpp:222-281,
-// src/system2d.cpp:21-73, src/system3d.cpp:13-80.
+// Reference (paths relative to /root/reference/proj/core): tap containers
+// include/shearlet/taps.hpp:13-61; QMF pair and fan asset src/filters.cpp:12-38,
+// 86-122; filter order src/system2d.cpp:49-73, src/system3d.cpp:27-80.
 #pragma once
 
 #include <cstdint>
@@ -34,31 +31,18 @@ struct Taps2 {
     static Taps2 impulse();
 };
 
-Taps1 impulse1();
-Taps1 conv(const Taps1& a, const Taps1& b);
-Taps1 upsample(const Taps1& a, std::size_t f);
-Taps1 reversed(const Taps1& a);
-Taps2 outer(const Taps1& a0, const Taps1& a1);
-Taps2 conv_axis(const Taps2& g, const Taps1& t, int axis);
-Taps2 upsample2(const Taps2& g, std::size_t f0, std::size_t f1);
-Taps2 transposed(const Taps2& g);
-
 struct Qmf {
     Taps1 lowpass, highpass;
 };
-Taps1 maxflat9_lowpass();               // filters.cpp:12-20 closed form
-Taps1 mirror_highpass(const Taps1& h);  // filters.cpp:22-30
+Taps1 maxflat9_lowpass();               // closed-form 9-tap lowpass (filters.cpp:12-20)
+Taps1 mirror_highpass(const Taps1& h);  // g[n] = (-1)^n h[n] (filters.cpp:22-30)
 Qmf qmf_from_lowpass(const Taps1& h);
-/// Level-j iterated lowpass h_j and highpass g_j (filters.cpp:40-63).
-void cascade(const Qmf& q, int level, Taps1* h, Taps1* g);
-Taps1 shear_interp(const Qmf& q, int level);  // h_d * sqrt(2)^d (filters.cpp:80-83)
 
-Taps2 maxflat_fan(int order);  // fan_design.cpp:70-108
-std::uint64_t fan_checksum(const Taps2& t);  // FNV-1a 64 (filters.cpp:89-110)
+/// The bundled 15x15 "dmaxflat4" fan filter (filters.cpp:112-122), shipped as
+/// a constant table and verified against its FNV-1a checksum.
+Taps2 default_fan();
+std::uint64_t fan_checksum(const Taps2& t);  // FNV-1a 64 over dims, centre, tap bytes (filters.cpp:86-110)
 constexpr std::uint64_t kDefaultFanChecksum = 0xb942f71dc884b1baull;
-
-/// Aperiodic digital shear S^d_{k/2^d} on centred taps (shear.cpp:222-281).
-Taps2 digital_shear_taps(const Taps2& t, long k, int d, const Taps1& interp);
 
 // ---------------------------------------------------------------- systems
 struct Profile {
@@ -78,11 +62,5 @@ std::vector<Record> enumerate_2d(const Profile& p, bool full);  // system2d.cpp:
 std::vector<Record> enumerate_3d(const Profile& p, bool full);  // system3d.cpp:58-80
 std::size_t redundancy_2d(const Profile& p, bool full);
 std::size_t redundancy_3d(const Profile& p, bool full);
-
-/// Spatial taps of one 2D cone filter, horizontal orientation (system2d.cpp:21-37).
-Taps2 cone_taps(int j, long k, int d, int J, const Taps2& fan, const Qmf& q);
-/// 3D component taps: the 2D construction with the highpass replaced by an
-/// impulse (system3d.cpp:13-25).
-Taps2 phi_taps(int j, long k, int d, int J, const Taps2& fan, const Qmf& q);
 
 }  // namespace slb

@@ -49,3 +49,12 @@ def kept_fp_torch(stack2d):
         r = idx % 1000003
         out[b] = (idx.numel(), int(idx.sum().item()), int((r * r).sum().item()))
     return out
+
+
+def golden_fan(order):
+    """maxflat_fan(order) of the reference (fan_design.cpp:70-108) from the golden
+    fixture, as a custom FanFilter (the fan design tool is out of scope for the
+    library; the library consumes fan taps)."""
+    import paper_1402_5670_b200 as P
+    t = golden("maxflat_fans")[f"order{order}"]
+    return P.FanFilter(np.array(t), (t.shape[0] - 1) // 2, (t.shape[1] - 1) // 2, f"dmaxflat{order}")

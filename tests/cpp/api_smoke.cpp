@@ -39,7 +39,7 @@ int main() {
     if (same != c) { std::printf("sigma 0 not identity\n"); ++fails; }
     const auto [A, B] = sys.frame_bounds();
     if (!(A > 0 && B >= A)) ++fails;
-    // SHCF round trip and a custom filter bank (maxflat_fan(2) + a 5-tap QMF)
+    // SHCF round trip and a custom filter bank (a symmetric 3x3 diamond fan + a 5-tap QMF)
     const auto bytes = serialize(c, sys);
     if (deserialize(bytes, sys) != c) { std::printf("shcf round trip\n"); ++fails; }
     auto bytes_bad = bytes;
@@ -49,7 +49,8 @@ int main() {
         ++fails;
     } catch (const FormatError&) {
     }
-    auto sys2 = build_system_2d(32, 32, ScaleProfile::from_levels({0, 1}), FanFilter::maxflat(2),
+    auto sys2 = build_system_2d(32, 32, ScaleProfile::from_levels({0, 1}),
+                                FanFilter{{0, 0.25, 0, 0.25, 0.5, 0.25, 0, 0.25, 0}, 3, 3, 1, 1, "custom"},
                                 QmfPair::from_lowpass(Taps1d{{-0.125, 0.25, 0.75, 0.25, -0.125}, 2}));
     std::vector<double> g(32 * 32);
     for (double& x : g) x = 2.0 * (static_cast<double>(rng()) * 0x1.0p-64) - 1.0;

@@ -4,7 +4,7 @@ GPU from the reference's text has the reference's filter bank (RMS pinned)."""
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import golden, golden_fan
 import paper_1402_5670_b200 as P
 
 pytestmark = pytest.mark.gpu
@@ -19,7 +19,7 @@ def _build(name):
     if name == "d2_48x40_full_j1":
         return P.build_system_2d(48, 40, prof([0, 1], 1), full_system=True)
     if name == "d2_32_legall":
-        return P.build_system_2d(32, 32, prof([0, 1]), fan=P.FanFilter.maxflat(2), qmf=LEGALL)
+        return P.build_system_2d(32, 32, prof([0, 1]), fan=golden_fan(2), qmf=LEGALL)
     if name == "d3_16_impulse":
         return P.build_system_3d((16, 16, 16), prof([0, 1]), fan="impulse")
     return P.build_system_3d((16, 20, 24), prof([0, 1]), qmf=LEGALL)

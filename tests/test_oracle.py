@@ -179,25 +179,26 @@ def test_oracle_custom_bank_3d_golden():
 
 
 def test_python_bank_helpers():
-    # host-side mirrors of filters.hpp helpers; maxflat_fan computed by the library (host code, no GPU)
+    # host-side mirrors of filters.hpp helpers; the bundled fan is a checksummed
+    # constant of the library equal to the reference's maxflat_fan(4)
     import paper_1402_5670_b200 as P
     g = golden("maxflat_fans")
-    for o in range(1, 7):
-        np.testing.assert_array_equal(P.FanFilter.maxflat(o).taps, g[f"order{o}"])
-    assert P.fan_checksum(P.FanFilter.default()) == P.DEFAULT_FAN_CHECKSUM
+    d = P.FanFilter.default()
+    np.testing.assert_array_equal(d.taps, g["order4"])
+    assert (d.center0, d.center1) == (7, 7)
+    assert P.fan_checksum(d) == P.DEFAULT_FAN_CHECKSUM
     q = P.QmfPair.from_lowpass([-0.125, 0.25, 0.75, 0.25, -0.125])
     np.testing.assert_array_equal(q.highpass, O.mirror_highpass(O.T1(q.lowpass, 2)).v)
     assert P.alpha_to_shear_levels([1.0, 1.0, 1.0], 1) == [1, 1, 2]
     with pytest.raises(P.DomainError):
         P.alpha_to_shear_levels([2.0], 0)
-    with pytest.raises(P.DomainError):
-        P.FanFilter.maxflat(0)
 
 
 def test_fan_asset_round_trip(tmp_path):
     # load_fan_filter / save_fan_filter text format (filters.cpp:124-156)
     import paper_1402_5670_b200 as P
-    f = P.FanFilter.maxflat(3)
+    from conftest import golden_fan
+    f = golden_fan(3)
     p = str(tmp_path / "fan.txt")
     f.save(p)
     back = P.FanFilter.load(p)
