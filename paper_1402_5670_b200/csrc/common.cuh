@@ -159,6 +159,7 @@ struct Knobs {
     int lockstep = 1, lockstep_frames = 2;                              // lock-step frame groups (device batch)
     int host_pipe = -1, pipe_conc = -1, pipe_group = 1, lockstep_host = 0;  // pipelined host batch
     bool denoise_unfused = false, disable_fast2d = false, disable_fast3d = false;
+    bool split3d = true;  // three-pass 3D kernels (fast3d_split.cuh); SLB_SPLIT3D=0 selects the five-pass ones
     double real_tol = 1e-9;
     static Knobs from_env() {
         Knobs k;
@@ -178,6 +179,7 @@ struct Knobs {
         k.denoise_unfused = std::getenv("SLB_DENOISE_UNFUSED") != nullptr;
         k.disable_fast2d = std::getenv("SLB_DISABLE_FAST2D") != nullptr;
         k.disable_fast3d = std::getenv("SLB_DISABLE_FAST3D") != nullptr;
+        k.split3d = env_knob("SLB_SPLIT3D", 1) != 0;
         if (const char* e = std::getenv("SLB_REAL_TOL")) k.real_tol = std::atof(e);
         return k;
     }

@@ -3,6 +3,7 @@
 #include "fast2d_host.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
+#include "fast3d_split.cuh"
 
 namespace slb {
 
@@ -178,6 +179,120 @@ static void denoise3d_fast_t(System& s, const double* f, double* stack, double* 
     K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
 }
 
+// ---------------------------------------------------------------- three-pass path (fast3d_split.cuh)
+// band group of pass A (F held in registers across it): about a quarter of the
+// chunk, so the grid has ~4x the CTAs of one group per band chunk
+static int split_group(const System& s, int cb) {
+    if (s.knobs.g3 >= 1) return s.knobs.g3;
+    return std::max(4, (cb + 3) / 4);
+}
+
+template <int n>
+struct Split3DLaunch {
+    using S = SplitShape<n>;
+    System& s;
+    cudaStream_t st;
+    long long nT;
+    const double2* tw;
+    Split3DLaunch(System& sys, cudaStream_t stream) : s(sys), st(stream) {
+        nT = static_cast<long long>(s.H) * n * n;
+        tw = s.plan(n, st).tw;
+    }
+    void dec(const double2* F, double2* Z, int nb, int band0) {
+        set_smem(k3s_dec<n>, S::AC_SMEM);
+        const int G = std::min(nb, split_group(s, nb));
+        LaunchScope ls(s, "f3s_dec", st, nb);
+        k3s_dec<n><<<dim3(S::H * S::Q, (nb + G - 1) / G), S::AC_THREADS, S::AC_SMEM, st>>>(F, Z, nT, s.synth, band0, G,
+                                                                                           nb, tw);
+        check_launch("k3s_dec");
+    }
+    template <int MODE>
+    void mid(double2* Z, double* band, const double* bandin, int nb, const double* delta, int band0) {
+        auto* k = (MODE == kMidRec || band) ? k3s_mid<n, MODE, true> : k3s_mid<n, MODE, false>;
+        set_smem(k, S::B_SMEM);
+        LaunchScope ls(s, MODE == kMidFused ? "f3s_mid" : (MODE == kMidDec ? "f3s_mid_dec" : "f3s_mid_rec"), st, nb);
+        k<<<dim3(n * (S::P / 2), nb), S::B_THREADS, S::B_SMEM, st>>>(Z, nT, band, s.nreal, bandin,
+                                                                    1.0 / static_cast<double>(s.nreal), delta, band0,
+                                                                    tw);
+        check_launch("k3s_mid");
+    }
+    void rec(const double2* Z, double2* acc, int nb, int band0, int accumulate) {
+        set_smem(k3s_rec<n>, S::AC_SMEM);
+        LaunchScope ls(s, "f3s_rec", st, nb);
+        k3s_rec<n><<<dim3(S::H * S::Q, 1), S::AC_THREADS, S::AC_SMEM, st>>>(Z, nT, acc, nb, s.synth, band0, accumulate,
+                                                                          tw);
+        check_launch("k3s_rec");
+    }
+};
+
+// F (natural layout) = FFT_0 FFT_1 R2C_2 f, with the five-pass kernels (once per call)
+template <int n>
+static void forward_natural(Fast3DLaunch<n>& K, System& s, const double* f) {
+    s.w->inter.alloc(static_cast<size_t>(K.nT));
+    s.w->F.alloc(static_cast<size_t>(K.nT));
+    K.rows_r2c(f, 0, s.w->inter.p, 1);
+    K.template axis1<-1>(s.w->inter.p, 1);
+    K.template from_rot<-1, kAx0Plain>(s.w->inter.p, s.w->F.p, 1, 0, 0, "f3_ax0_fwd");
+}
+// out = Re IFFT(acc / W) / N
+template <int n>
+static void finish_rec(Fast3DLaunch<n>& K, System& s, double* out) {
+    K.template to_rot<+1, kAx0DivW>(s.w->acc.p, 0, s.w->inter.p, 1, 0, s.WN.p, "f3_ax0_final");
+    K.template axis1<+1>(s.w->inter.p, 1);
+    K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
+}
+
+template <int n>
+static void denoise3d_split_t(System& s, const double* f, double* stack, double* out, const double* delta,
+                              cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    Split3DLaunch<n> S3(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    forward_natural<n>(K, s, f);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    s.w->acc.alloc(static_cast<size_t>(K.nT));
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        double* sb = stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr;
+        S3.dec(s.w->F.p, s.w->inter.p, cb, s.lo + b0);
+        S3.template mid<kMidFused>(s.w->inter.p, sb, nullptr, cb, delta, s.lo + b0);
+        S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+    }
+    finish_rec<n>(K, s, out);
+}
+
+template <int n>
+static void dec3d_split_t(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    Split3DLaunch<n> S3(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    forward_natural<n>(K, s, f);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        S3.dec(s.w->F.p, s.w->inter.p, cb, s.lo + b0);
+        S3.template mid<kMidDec>(s.w->inter.p, out + static_cast<size_t>(b0) * s.nreal, nullptr, cb, delta, s.lo + b0);
+    }
+}
+
+template <int n>
+static void rec3d_split_t(System& s, const double* coeffs, double* out, cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    Split3DLaunch<n> S3(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    s.w->acc.alloc(static_cast<size_t>(K.nT));
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        S3.template mid<kMidRec>(s.w->inter.p, nullptr, coeffs + static_cast<size_t>(b0) * s.nreal, cb, nullptr, 0);
+        S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+    }
+    finish_rec<n>(K, s, out);
+}
+
 #define SLB_FAST3D_DISPATCH(FN, ...)                                        \
     switch (s.n[0]) {                                                       \
         case 64: FN<64>(__VA_ARGS__); break;                                \
@@ -187,16 +302,29 @@ static void denoise3d_fast_t(System& s, const double* f, double* stack, double* 
         default: throw SlError(SL_ERR_GENERIC, "fast3d: unsupported size"); \
     }
 
+// the three-pass kernels by default (SLB_SPLIT3D=0: the five-pass ones, A/B)
 static void dec3d_fast(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
-    SLB_FAST3D_DISPATCH(dec3d_fast_t, s, f, out, delta, st)
+    if (s.knobs.split3d) {
+        SLB_FAST3D_DISPATCH(dec3d_split_t, s, f, out, delta, st)
+    } else {
+        SLB_FAST3D_DISPATCH(dec3d_fast_t, s, f, out, delta, st)
+    }
 }
 static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_t st) {
-    SLB_FAST3D_DISPATCH(rec3d_fast_t, s, coeffs, out, st)
+    if (s.knobs.split3d) {
+        SLB_FAST3D_DISPATCH(rec3d_split_t, s, coeffs, out, st)
+    } else {
+        SLB_FAST3D_DISPATCH(rec3d_fast_t, s, coeffs, out, st)
+    }
 }
 
 static void denoise3d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
                            cudaStream_t st) {
-    SLB_FAST3D_DISPATCH(denoise3d_fast_t, s, f, stack, out, delta, st)
+    if (s.knobs.split3d) {
+        SLB_FAST3D_DISPATCH(denoise3d_split_t, s, f, stack, out, delta, st)
+    } else {
+        SLB_FAST3D_DISPATCH(denoise3d_fast_t, s, f, stack, out, delta, st)
+    }
 }
 
 }  // namespace slb

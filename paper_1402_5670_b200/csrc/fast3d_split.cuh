@@ -1,0 +1,315 @@
+// Three-pass 3D dec -> threshold -> rec for cubic grids n = P * Q.
+//
+// The half spectrum of a band (k2 < H = n/2 + 1 along the real axis 2) makes
+// three HBM round trips instead of five: the axis-1 FFT is split four-step
+// style, k1 = q + Q p and i1 = a + P c, so that
+//   y[a + P c] = sum_q w_Q^{c q} w_n^{a q} sum_p w_P^{a p} X[q + Q p],
+// and each half rides along with a full axis:
+//   pass A (k3s_dec): per (k2, q): the P lines k1 = q + Q p of F * psi_b (F in
+//            registers across a band group, psi synthesised per line) get
+//            the axis-0 IFFT, then the length-P DFT across the lines and the
+//            twiddle w_n^{a q}                                  -> Z[k2][i0][q][a]
+//   pass B (k3s_mid): per (i0, a pair): the length-Q DFT across q gives the
+//            2Q rows i1 = a + P c; axis-2 c2r, 1/N, hard threshold, band
+//            store; r2c, length-Q DFT back                     -> Z'[k2][i0][q][a]
+//   pass C (k3s_rec): per (k2, q): twiddle, length-P DFT, axis-0 FFT,
+//            * psi_b, summed over the chunk's bands in registers -> acc (RMW once)
+// Z / Z' have the size of one half spectrum per band (H n n double2); pass B
+// works in place. Per band: 16 Nh (A) + 16 Nh + 8 N + 16 Nh (B) + 16 Nh (C)
+// bytes, against 5 passes (80 Nh + 8 N) in fast3d.cuh.
+// Reference: transform.cpp:39-61 (forward 3D), :94-125 (inverse 3D),
+// apps.cpp:57-81,114-121 (threshold, denoise), system3d.cpp:144-186 (psi).
+#pragma once
+
+#include "fast3d.cuh"
+
+namespace slb {
+
+template <int L>
+struct SplitCfg;
+template <>
+struct SplitCfg<64> {
+    static constexpr int P = 8, Q = 8;
+};
+template <>
+struct SplitCfg<128> {
+    static constexpr int P = 8, Q = 16;
+};
+template <>
+struct SplitCfg<192> {
+    static constexpr int P = 12, Q = 16;
+};
+template <>
+struct SplitCfg<256> {
+    static constexpr int P = 16, Q = 16;
+};
+
+template <int L>
+struct SplitShape {
+    static constexpr int T = RegPlan<L>::T, P = SplitCfg<L>::P, Q = SplitCfg<L>::Q;
+    static constexpr int LD = P + 1;                 // [L][P] tile row stride: 8 consecutive rows hit distinct banks
+    static constexpr int AC_THREADS = P * T;         // passes A / C: P axis-0 lines
+    static constexpr int B_THREADS = Q * T;          // pass B: Q pair-lines = 2Q rows
+    static constexpr int H = L / 2 + 1;
+    static constexpr size_t AC_SMEM = static_cast<size_t>(L) * LD * sizeof(double2);
+    static constexpr size_t B_SMEM = static_cast<size_t>((H * 2 * Q > Q * L) ? H * 2 * Q : Q * L) * sizeof(double2);
+#ifndef SLB_SPLIT_AC_MINB
+    static constexpr int AC_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 4);
+#else
+    static constexpr int AC_MINB = SLB_SPLIT_AC_MINB;
+#endif
+#ifndef SLB_SPLIT_B_MINB
+    static constexpr int B_MINB = L >= 256 ? 1 : 3;
+#else
+    static constexpr int B_MINB = SLB_SPLIT_B_MINB;
+#endif
+};
+
+template <int R, int DIR>
+__device__ __forceinline__ void dft_small(double2 (&v)[R]) {
+    if constexpr (R == 8)
+        bfly8<DIR>(v);
+    else if constexpr (R == 12)
+        bfly12<DIR>(v);
+    else if constexpr (R == 16)
+        bfly16<DIR>(v);
+}
+
+// ---------------------------------------------------------------- pass A
+template <int L>
+__global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_MINB)
+    k3s_dec(const double2* __restrict__ F, double2* __restrict__ Z, long long zbs, FiltSynth3D filt, int band0, int G,
+            int nb, const double2* __restrict__ tw) {
+    using S = SplitShape<L>;
+    constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
+    extern __shared__ double2 tile[];  // [n][LD]; the P line buffers alias it
+    const int k2 = blockIdx.x / Q, q = blockIdx.x - k2 * Q;
+    const int g0 = blockIdx.y * G, gn = min(G, nb - g0);
+    const int p = threadIdx.x / T, t = threadIdx.x - p * T;
+    const int k1 = q + Q * p;
+    const double2* fl = F + ((long long)k2 * n + k1) * n;
+    double2 fr[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
+    double2* lb = tile + p * LineBuf<L, false>::N;
+    for (int bb = 0; bb < gn; ++bb) {
+        const BandDesc3D bd = filt.bands[band0 + g0 + bb];
+        const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
+        double2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const double ps = fline.at(t + T * m);
+            x[m] = make_double2(fr[m].x * ps, fr[m].y * ps);
+        }
+        if (bb > 0) __syncthreads();  // the previous band's tile is copied out
+        reg_fft<L, +1, false>(x, lb, t, tw);
+        __syncthreads();  // every line is done with the aliased buffers
+#pragma unroll
+        for (int m = 0; m < E; ++m) tile[(t + T * m) * LD + p] = x[m];
+        __syncthreads();
+        // length-P DFT across the lines for each i0, twiddle w_n^{a q}
+        for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
+            double2 v[P];
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) v[pp] = tile[i0 * LD + pp];
+            dft_small<P, +1>(v);
+#pragma unroll
+            for (int a = 0; a < P; ++a) tile[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
+        }
+        __syncthreads();
+        double2* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P;
+        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
+            const int i0 = idx / P, a = idx - i0 * P;
+            __stcg(z + (long long)i0 * n + a, tile[i0 * LD + a]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- pass B
+enum SplitMid : int {
+    kMidFused = 0,  // Z -> c2r, threshold, band store, r2c -> Z' (denoise)
+    kMidDec = 1,    // Z -> c2r, threshold, band store                (forward)
+    kMidRec = 2,    // band rows -> r2c -> Z'                         (inverse)
+};
+
+template <int L, int MODE, bool STORE>
+__global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MINB)
+    k3s_mid(double2* __restrict__ Z, long long zbs, double* __restrict__ band, long long bbs,
+            const double* __restrict__ bandin, double scale, const double* __restrict__ delta, int band0,
+            const double2* __restrict__ tw) {
+    using S = SplitShape<L>;
+    constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, H = S::H, n = L;
+    constexpr int KPT = (H + T - 1) / T;
+    extern __shared__ double2 tile[];  // [H][2Q] tslot<Q>; line buffers alias it
+    const int i0 = blockIdx.x / (P / 2), a0 = 2 * (blockIdx.x - i0 * (P / 2));
+    const int bi = blockIdx.y;
+    const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
+    const int i1 = a0 + P * lq;
+    double2* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
+    double2* lb = tile + lq * LineBuf<L, false>::N;
+    double2 x[E];
+    if constexpr (MODE != kMidRec) {
+        for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
+            const int k2 = idx / (2 * Q), j = idx - k2 * 2 * Q;
+            cp_async16(tile + tslot<Q>(k2, j), zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1));
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
+        for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
+            const int e = idx / H, k2 = idx - e * H;
+            double2 v[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
+            dft_small<Q, +1>(v);
+#pragma unroll
+            for (int j = 0; j < Q; ++j) tile[tslot<Q>(k2, 2 * j + e)] = v[j];
+        }
+        __syncthreads();
+        // axis-2 c2r of the row pair (pair-packed, as k2_rows_c2r)
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int k = t + T * m;
+            double2 X, Y;
+            if (k < H) {
+                X = tile[tslot<Q>(k, 2 * lq)];
+                Y = tile[tslot<Q>(k, 2 * lq + 1)];
+                if (k == 0 || 2 * k == L) {
+                    X.y = 0.0;
+                    Y.y = 0.0;
+                }
+                x[m] = make_double2(X.x - Y.y, X.y + Y.x);
+            } else {
+                X = tile[tslot<Q>(L - k, 2 * lq)];
+                Y = tile[tslot<Q>(L - k, 2 * lq + 1)];
+                x[m] = make_double2(X.x + Y.y, Y.x - X.y);
+            }
+        }
+        __syncthreads();  // the tile becomes the line buffers
+        reg_fft<L, +1, false>(x, lb, t, tw);
+        const double dl = delta ? delta[band0 + bi] : -1.0;
+        double* r0p = band + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            double u = x[m].x * scale, w = x[m].y * scale;
+            if (dl >= 0.0) {
+                if (fabs(u) < dl) u = 0.0;
+                if (fabs(w) < dl) w = 0.0;
+            }
+            if (STORE) {
+                r0p[t + T * m] = u;
+                r0p[n + t + T * m] = w;
+            }
+            x[m] = make_double2(u, w);
+        }
+        if constexpr (MODE == kMidDec) return;
+    } else {
+        const double* r0p = bandin + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = make_double2(__ldg(r0p + t + T * m), __ldg(r0p + n + t + T * m));
+    }
+    // axis-2 r2c of the row pair (as k2_rows_r2c)
+    reg_fft<L, -1, false>(x, lb, t, tw);
+#pragma unroll
+    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
+    line_sync<T>();
+    double2 zk[KPT], zm[KPT];
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            zk[u] = lb[swz<false>(k)];
+            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
+        }
+    }
+    __syncthreads();  // all line buffers read before the tile is rewritten
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        const int k = t + T * u;
+        if (k < H) {
+            tile[tslot<Q>(k, 2 * lq)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));
+            tile[tslot<Q>(k, 2 * lq + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));
+        }
+    }
+    __syncthreads();
+    // length-Q DFT back over c for each (k2, e): slot 2c + e -> 2q + e
+    for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
+        const int e = idx / H, k2 = idx - e * H;
+        double2 v[Q];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
+        dft_small<Q, -1>(v);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) tile[tslot<Q>(k2, 2 * j + e)] = v[j];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
+        const int k2 = idx / (2 * Q), j = idx - k2 * 2 * Q;
+        __stcg(zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1), tile[tslot<Q>(k2, j)]);
+    }
+}
+
+// ---------------------------------------------------------------- pass C
+template <int L>
+__global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_MINB)
+    k3s_rec(const double2* __restrict__ Z, long long zbs, double2* __restrict__ acc, int nbands, FiltSynth3D filt,
+            int band0, int accumulate, const double2* __restrict__ tw) {
+    using S = SplitShape<L>;
+    constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
+    extern __shared__ double2 tile[];  // [n][LD]; the P line buffers alias it
+    const int k2 = blockIdx.x / Q, q = blockIdx.x - k2 * Q;
+    const int p = threadIdx.x / T, t = threadIdx.x - p * T;
+    const int k1 = q + Q * p;
+    double2* lb = tile + p * LineBuf<L, false>::N;
+    double2 ar[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) ar[m] = make_double2(0.0, 0.0);
+    for (int b = 0; b < nbands; ++b) {
+        const double2* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
+        if (b > 0) __syncthreads();  // the previous band's line buffers are free
+        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
+            const int i0 = idx / P, a = idx - i0 * P;
+            cp_async16(tile + i0 * LD + a, z + (long long)i0 * n + a);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // twiddle w_n^{-a q}, length-P DFT over a -> p, for each i0
+        for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
+            double2 v[P];
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                const double2 u = tile[i0 * LD + a];
+                v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
+            }
+            dft_small<P, -1>(v);
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) tile[i0 * LD + pp] = v[pp];
+        }
+        __syncthreads();
+        double2 x[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = tile[(t + T * m) * LD + p];
+        __syncthreads();  // all lines gathered: the tile becomes the line buffers
+        const BandDesc3D bd = filt.bands[band0 + b];
+        const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
+        reg_fft<L, -1, false>(x, lb, t, tw);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const double ps = fline.at(t + T * m);
+            ar[m].x = fma(x[m].x, ps, ar[m].x);
+            ar[m].y = fma(x[m].y, ps, ar[m].y);
+        }
+    }
+    double2* d = acc + ((long long)k2 * n + k1) * n;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        double2 v = ar[m];
+        if (accumulate) {
+            const double2 o = __ldcg(d + t + T * m);
+            v = make_double2(o.x + v.x, o.y + v.y);
+        }
+        __stcg(d + t + T * m, v);
+    }
+}
+
+}  // namespace slb

@@ -216,3 +216,27 @@ def test_largest_specialised_sizes_round_trip(cuda):
         assert (torch.linalg.norm(d - f) / torch.linalg.norm(f)).item() <= 1e-10
         del s, r, d
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n,levels", [(64, [0, 1]), (128, [1, 1]), (192, [0, 0, 1]), (256, [0, 1])])
+def test_three_pass_matches_five_pass(cuda, n, levels, monkeypatch):
+    # the three-pass path (fast3d_split.cuh, default) against the five-pass
+    # kernels (SLB_SPLIT3D=0): dec bands, rec and the fused denoise
+    import torch
+    prof = P.ScaleProfile.from_levels(levels)
+    sch = P.ThresholdSchedule.defaults_3d(0.3, len(levels))
+    x = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, (n, n, n))).to(cuda)
+    got = {}
+    for split in ("1", "0"):
+        monkeypatch.setenv("SLB_SPLIT3D", split)  # knobs are read when the handle is created
+        s = P.build_system_3d((n, n, n), prof)
+        d, st = P.denoise(x, s, sch, return_stack=True)
+        b = P.forward(x, s)
+        r = P.inverse(b, s)
+        got[split] = (d, st, b, r)
+        del s
+    (d1, st1, b1, r1), (d0, st0, b0, r0) = got["1"], got["0"]
+    rel = lambda a, b: (torch.linalg.norm(a - b) / torch.linalg.norm(b)).item()  # noqa: E731
+    assert rel(b1, b0) <= 1e-13 and rel(st1, st0) <= 1e-13
+    assert rel(d1, d0) <= 1e-13 and rel(r1, r0) <= 1e-13
+    assert rel(r1, x) <= 1e-10
