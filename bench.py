@@ -26,9 +26,10 @@ sampled during the timed region. e2e = the same metric through the host
 entry points with pinned host in/out, copies inside the timed region.
 
 Multi-GPU (torchrun, one rank per GPU): 2D frames are replicas (weak scaling,
-no collective); 3D shards the filter bank by shearlet index inside one
-process per GPU, broadcasts the volume and reduces the partial
-reconstructions (NCCL through torch.distributed).
+no collective); 3D shards the filter bank by shearlet index through the
+library's own NCCL communicator (sl_comm_create / sl_system_set_comm /
+sl_denoise_dist_dev: broadcast of the volume, sharded fused denoise, reduce of
+the half-spectrum accumulators, root-only final inverse FFT).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref:
 the unmodified reference library compiled with our FFTW-API shim, all host
@@ -325,12 +326,19 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     if is3d:
-        lo, hi = R_full * rank // world, R_full * (rank + 1) // world  # contiguous balanced band ranges
-        sysg = P.build_system_3d(dims, prof, device=local, shard=(lo, hi) if world > 1 else None)
+        sysg = P.build_system_3d(dims, prof, device=local)
     else:
         sysg = P.build_system_2d(*dims, prof, device=local)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
+    comm = None
+    if world > 1:
+        # the library's own NCCL communicator (sl_comm_create): 3D shards the
+        # bank by shearlet index (broadcast f, accumulator reduce inside the
+        # library); 2D batches keep the bank and shard by image
+        from paper_1402_5670_b200 import dist as PD
+        comm = PD.library_comm(local)
+        PD.attach(sysg, comm)
     nstreams = int(os.environ.get("SLB_STREAMS", "6"))
     if is3d:
         frames, scaling = 1, "strong"  # one volume per step whatever the rank count
@@ -366,12 +374,12 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
             return
         for i in range(frames):
             x, o = d_in_b[i], d_out_b[i]
-            if world > 1:
-                dist.broadcast(x, src=0)
-            P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
-                                      Kp, len(K), sg, 1, sp()))
-            if world > 1:
-                dist.reduce(o, dst=0, op=dist.ReduceOp.SUM)
+            if world > 1:  # in-library NCCL broadcast + sharded denoise + accumulator reduce
+                P._check(L.sl_denoise_dist_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
+                                               Kp, len(K), sg, 1, 0, sp()))
+            else:
+                P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(x.data_ptr()), C.c_void_p(o.data_ptr()),
+                                          Kp, len(K), sg, 1, sp()))
 
     def step_lone():  # b = 1: one frame through sl_denoise_dev
         P._check(L.sl_denoise_dev(sysg.handle, C.c_void_p(d_in_b[0].data_ptr()), C.c_void_p(d_out_b[0].data_ptr()),
@@ -421,7 +429,7 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
     units_step = frames * world if not is3d else 1
     value = units_step / (ms_step / 1000.0)
     k_side = max(3, min(steps, 20 if is3d else 50))
-    ms_lone, _ = timed(step_lone, k_side, 2) if not is3d else (ms_step, None)
+    ms_lone, _ = timed(step_lone, k_side, 2) if (not is3d and world == 1) else (ms_step, None)
     ms_unf, _ = timed(step_unfused, k_side, 2) if world == 1 else (None, None)
     del stack
     torch.cuda.empty_cache()
@@ -452,11 +460,7 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
         else:
             for i in range(frames):
                 xd = pinned_in[i].to(dev, non_blocking=True)
-                if world > 1:
-                    dist.broadcast(xd, src=0)
-                od = P.denoise(xd, sysg, sch)
-                if world > 1:
-                    dist.reduce(od, dst=0, op=dist.ReduceOp.SUM)
+                od = P.denoise_dist(xd, sysg, sch) if world > 1 else P.denoise(xd, sysg, sch)
                 pinned_out[i].copy_(od)
         torch.cuda.synchronize()
         if k > 0:
@@ -535,7 +539,9 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
             out["cpu_baseline"] = cpu_reference(cfg, seconds=12.0, steps=10 if not is3d else 1, warmup=1)
         except Exception as e:  # reported, never fatal
             out["cpu_baseline"] = {"value": None, "error": str(e)}
-    del sysg
+    if comm is not None:
+        sysg.set_comm(None)
+    del sysg, comm
     torch.cuda.empty_cache()
     return out
 

@@ -50,10 +50,12 @@ enum sl_status {
     SL_ERR_DEGENERATE_MASK = 9,  /* shearlet::DegenerateMaskError                */
     SL_ERR_DEGENERATE_TRUTH = 10, /* shearlet::DegenerateTruthError              */
     SL_ERR_CUDA = 20,            /* CUDA runtime failure                         */
+    SL_ERR_NCCL = 21,            /* NCCL failure / libnccl.so.2 not loadable     */
     SL_ERR_INVALID = 22,         /* null handle / bad argument at the ABI        */
 };
 
 typedef struct sl_system sl_system;
+typedef struct sl_comm sl_comm;
 
 /* Library / device queries. */
 const char* sl_version(void);
@@ -250,6 +252,32 @@ int sl_launch_count(const sl_system* sys, int64_t* count);
 int sl_phantom_cartoon(int n, double* out);            /* phantoms::cartoon        */
 int sl_phantom_cartoon_volume(int n, double* out);     /* phantoms::cartoon_volume */
 int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double sigma, uint64_t seed);
+
+/* ---- multi-GPU (one process per GPU) -------------------------
+ * The filter index -- the reference's only parallel axis (parallel_for,
+ * parallel.hpp:20-46) -- shards across GPUs: rank r owns the balanced band
+ * range sl_partition(R, nranks, r). sl_denoise_dist_dev broadcasts the
+ * input from `root` (in: device buffer on every rank, read on the root,
+ * overwritten elsewhere), runs the fused dec -> threshold -> rec of this
+ * rank's bands and NCCL-reduces the reconstruction onto the root (3D: the
+ * half-spectrum accumulators; the root alone divides by W and inverts).
+ * Batched 2D frames shard by image with no collective
+ * (sl_denoise_batch_dist_*: frames sl_partition(nframes, ...) of a globally
+ * indexed batch). NCCL is loaded at run time; SL_ERR_NCCL when absent. */
+int sl_comm_unique_id(unsigned char* id /* 128 bytes, NCCL_UNIQUE_ID_BYTES */);
+int sl_comm_create(const unsigned char* id, int nranks, int rank, int device, sl_comm** out);
+int sl_comm_destroy(sl_comm* comm);
+int sl_comm_info(const sl_comm* comm, int* nranks, int* rank, int* device);
+int sl_partition(int64_t count, int nranks, int rank, int64_t* lo, int64_t* hi);
+/* attach (or, with NULL, detach) a communicator; shard_bands != 0 restricts
+ * the handle to this rank's band range, 0 keeps the whole bank (2D batches) */
+int sl_system_set_comm(sl_system* sys, sl_comm* comm, int shard_bands);
+int sl_denoise_dist_dev(sl_system* sys, const double* in, double* out, const double* K, int nK, double sigma,
+                        int scale_by_rms, int root, void* stream);
+int sl_denoise_batch_dist_dev(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
+                              double sigma, int scale_by_rms, void* stream);
+int sl_denoise_batch_dist_host(sl_system* sys, const double* in, int nframes, double* out, const double* K, int nK,
+                               double sigma, int scale_by_rms);
 
 #ifdef __cplusplus
 }

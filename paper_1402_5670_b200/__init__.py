@@ -75,6 +75,10 @@ class DegenerateTruthError(Error):
     pass
 
 
+class NcclError(Error):
+    """NCCL failure or libnccl.so.2 not loadable (SL_ERR_NCCL)."""
+
+
 class CudaError(Error):
     pass
 
@@ -85,7 +89,7 @@ class InvalidArgument(Error):
 
 _CODES = {1: Error, 2: ShapeError, 3: ConfigError, 4: DomainError, 5: SingularFrameError,
           6: UnsupportedSizeError, 7: AssetError, 8: FormatError, 9: DegenerateMaskError, 10: DegenerateTruthError, 20: CudaError,
-          22: InvalidArgument}
+          21: NcclError, 22: InvalidArgument}
 
 # ------------------------------------------------------------------ library
 _lib = None
@@ -185,6 +189,16 @@ def lib():
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
+    u8 = C.c_char_p
+    L.sl_comm_unique_id.argtypes = [u8]
+    L.sl_comm_create.argtypes = [u8, i, i, i, C.POINTER(P)]
+    L.sl_comm_destroy.argtypes = [P]
+    L.sl_comm_info.argtypes = [P, ip, ip, ip]
+    L.sl_partition.argtypes = [C.c_int64, i, i, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+    L.sl_system_set_comm.argtypes = [P, P, i]
+    L.sl_denoise_dist_dev.argtypes = [P, P, P, dp, i, C.c_double, i, i, P]
+    L.sl_denoise_batch_dist_dev.argtypes = [P, P, i, P, dp, i, C.c_double, i, P]
+    L.sl_denoise_batch_dist_host.argtypes = [P, dp, i, dp, dp, i, C.c_double, i]
     L.sl_phantom_cartoon.argtypes = [i, dp]
     L.sl_phantom_cartoon_volume.argtypes = [i, dp]
     L.sl_add_gaussian_noise.argtypes = [dp, dp, C.c_int64, C.c_double, C.c_uint64]
@@ -207,6 +221,8 @@ EXPORTED_SYMBOLS = [
     "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
+    "sl_comm_unique_id", "sl_comm_create", "sl_comm_destroy", "sl_comm_info", "sl_partition", "sl_system_set_comm",
+    "sl_denoise_dist_dev", "sl_denoise_batch_dist_dev", "sl_denoise_batch_dist_host",
 ]
 
 
@@ -355,6 +371,16 @@ class _System:
         raw = names.raw
         return {raw[32 * i:32 * i + 32].split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i]), int(units[i]))
                 for i in range(n.value)}
+
+    def set_comm(self, comm: Optional["Comm"], shard_bands: bool = True):
+        """Attach a multi-GPU communicator (None detaches). shard_bands: this
+        rank keeps only its band range (3D / single frames); False keeps the
+        whole bank (2D batches shard by image)."""
+        _check(lib().sl_system_set_comm(self._h, comm.handle if comm else None, int(bool(comm) and shard_bands)))
+        lo, hi = C.c_int(), C.c_int()
+        _check(lib().sl_shard(self._h, C.byref(lo), C.byref(hi)))
+        self.shard = (lo.value, hi.value)
+        self._comm = comm  # keeps the communicator alive while attached
 
     def set_stack_output(self, materialize: bool = True):
         """Fused denoise writes the thresholded stack (default, as the reference) or not."""
@@ -870,6 +896,70 @@ def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule, return_stac
     frames = np.ascontiguousarray(frames, dtype=np.float64)
     out = np.empty_like(frames)
     _check(lib().sl_denoise_batch_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))
+    return out
+
+
+# ------------------------------------------------------------------ multi-GPU
+def partition(count: int, nranks: int, rank: int):
+    """[lo, hi) of `rank` in the balanced contiguous split the library uses."""
+    lo, hi = C.c_int64(), C.c_int64()
+    _check(lib().sl_partition(int(count), int(nranks), int(rank), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+class Comm:
+    """NCCL communicator owned by the library (one process per GPU)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, device: int):
+        h = C.c_void_p()
+        _check(lib().sl_comm_create(bytes(unique_id), int(nranks), int(rank), int(device), C.byref(h)))
+        self.handle, self.nranks, self.rank, self.device = h, nranks, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().sl_comm_unique_id(buf))
+        return buf.raw
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().sl_comm_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def denoise_dist(x, sys: _System, schedule: ThresholdSchedule, root: int = 0):
+    """Sharded fused denoise across the ranks of sys's communicator: x (CUDA,
+    read on the root, overwritten by the broadcast elsewhere) -> the full
+    denoised signal on the root (an unspecified buffer elsewhere)."""
+    import torch
+    K, Kp = _k_arg(schedule)
+    x = x.contiguous().to(torch.float64)
+    out = torch.empty_like(x)
+    _check(lib().sl_denoise_dist_dev(sys.handle, C.c_void_p(x.data_ptr()), C.c_void_p(out.data_ptr()), Kp, len(K),
+                                     float(schedule.sigma), int(schedule.scale_by_filter_norm), int(root),
+                                     _stream_ptr(x.device.index)))
+    return out
+
+
+def denoise_batch_dist(frames, sys: _System, schedule: ThresholdSchedule, out=None):
+    """This rank's share (partition(nframes, ...)) of a globally indexed batch;
+    the other frames of `out` are left untouched. No collective."""
+    _check_batch(frames, sys)
+    K, Kp = _k_arg(schedule)
+    args = (Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm))
+    if _is_cuda_tensor(frames):
+        import torch
+        frames = frames.contiguous().to(torch.float64)
+        out = torch.zeros_like(frames) if out is None else out
+        _check(lib().sl_denoise_batch_dist_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
+                                               C.c_void_p(out.data_ptr()), *args, _stream_ptr(frames.device.index)))
+        return out
+    frames = np.ascontiguousarray(frames, dtype=np.float64)
+    out = np.zeros_like(frames) if out is None else out
+    _check(lib().sl_denoise_batch_dist_host(sys.handle, _dp(frames), int(frames.shape[0]), _dp(out), *args))
     return out
 
 

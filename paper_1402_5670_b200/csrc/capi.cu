@@ -16,12 +16,14 @@
 #include "image_io.cuh"
 #include "descriptor.cuh"
 #include "quality.cuh"
+#include "comm.cuh"
 
 // ====================================================================== C ABI
 using namespace slb;
 
 struct sl_system {
     System s;
+    sl_comm* comm = nullptr;  // sl_system_set_comm: multi-GPU (one process per GPU)
 };
 
 namespace {
@@ -1262,6 +1264,131 @@ int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double s
             out[i] += sigma * g;
         }
     });
+}
+
+// ---- multi-GPU: NCCL communicators and the sharded hot path (comm.cuh) ----
+int sl_comm_unique_id(unsigned char* id) {
+    return guard([&] {
+        if (!id) throw SlError(SL_ERR_INVALID, "null id buffer");
+        ncclUniqueId u;
+        SL_NCCL(nccl().getUniqueId(&u));
+        std::memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+int sl_comm_create(const unsigned char* id, int nranks, int rank, int device, sl_comm** out) {
+    return guard([&] {
+        if (!id || !out) throw SlError(SL_ERR_INVALID, "null argument");
+        *out = nullptr;
+        long long lo, hi;
+        shard_of(1, nranks, rank, &lo, &hi);  // validates nranks / rank
+        DeviceGuard dg(device);
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+        auto c = std::make_unique<sl_comm>();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->device = device;
+        SL_NCCL(nccl().commInitRank(&c->comm, nranks, u, rank));
+        *out = c.release();
+    });
+}
+
+int sl_comm_destroy(sl_comm* comm) {
+    return guard([&] {
+        if (!comm) return;
+        DeviceGuard dg(comm->device);
+        if (comm->comm) SL_NCCL(nccl().commDestroy(comm->comm));
+        delete comm;
+    });
+}
+
+int sl_comm_info(const sl_comm* comm, int* nranks, int* rank, int* device) {
+    return guard([&] {
+        if (!comm) throw SlError(SL_ERR_INVALID, "null communicator");
+        if (nranks) *nranks = comm->nranks;
+        if (rank) *rank = comm->rank;
+        if (device) *device = comm->device;
+    });
+}
+
+int sl_partition(int64_t count, int nranks, int rank, int64_t* lo, int64_t* hi) {
+    return guard([&] {
+        if (count < 0) throw SlError(SL_ERR_SHAPE, "negative count");
+        long long a, b;
+        shard_of(count, nranks, rank, &a, &b);
+        if (lo) *lo = a;
+        if (hi) *hi = b;
+    });
+}
+
+int sl_system_set_comm(sl_system* h, sl_comm* comm, int shard_bands) {
+    return guard([&] {
+        System& s = sys_of(h);
+        std::lock_guard<std::mutex> lk(s.mu);
+        if (comm && comm->device != s.device) throw SlError(SL_ERR_CONFIG, "communicator and system on different devices");
+        h->comm = comm;
+        if (comm && shard_bands) {
+            long long lo, hi;
+            shard_of(s.R, comm->nranks, comm->rank, &lo, &hi);
+            if (lo >= hi) throw SlError(SL_ERR_CONFIG, "more ranks than shearlets");
+            set_shard(s, static_cast<int>(lo), static_cast<int>(hi));
+        } else {
+            set_shard(s, 0, s.R);
+        }
+    });
+}
+
+int sl_denoise_dist_dev(sl_system* h, const double* in, double* out, const double* K, int nK, double sigma, int scaled,
+                        int root, void* stream) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (!h->comm) throw SlError(SL_ERR_CONFIG, "denoise_dist: no communicator (sl_system_set_comm)");
+        if (root < 0 || root >= h->comm->nranks) throw SlError(SL_ERR_CONFIG, "denoise_dist: bad root rank");
+        if (h->comm->rank == root) {
+            require_dev_ptr(in, "denoise input");
+            require_dev_ptr(out, "denoise output");
+        }
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        denoise_dist(s, *h->comm, in ? in : s.io_in.p, out, root, stream_of(stream));
+    });
+}
+
+// 2D frames shard by image: this rank denoises frames [lo, hi) of the
+// nframes-frame batch (global in / out indexing), no collective.
+int sl_denoise_batch_dist_host(sl_system* h, const double* in, int nframes, double* out, const double* K, int nK,
+                               double sigma, int scaled) {
+    long long lo = 0, hi = nframes;
+    const int rc = guard([&] {
+        if (!h) throw SlError(SL_ERR_INVALID, "null system handle");
+        if (!h->comm) throw SlError(SL_ERR_CONFIG, "denoise_batch_dist: no communicator (sl_system_set_comm)");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        shard_of(nframes, h->comm->nranks, h->comm->rank, &lo, &hi);
+    });
+    if (rc) return rc;
+    if (hi <= lo) return SL_OK;
+    const size_t off = static_cast<size_t>(lo) * static_cast<size_t>(h->s.nreal);
+    return sl_denoise_batch_host(h, in + off, static_cast<int>(hi - lo), out + off, K, nK, sigma, scaled);
+}
+
+int sl_denoise_batch_dist_dev(sl_system* h, const double* in, int nframes, double* out, const double* K, int nK,
+                              double sigma, int scaled, void* stream) {
+    long long lo = 0, hi = nframes;
+    const int rc = guard([&] {
+        if (!h) throw SlError(SL_ERR_INVALID, "null system handle");
+        if (!h->comm) throw SlError(SL_ERR_CONFIG, "denoise_batch_dist: no communicator (sl_system_set_comm)");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        shard_of(nframes, h->comm->nranks, h->comm->rank, &lo, &hi);
+    });
+    if (rc) return rc;
+    if (hi <= lo) return SL_OK;
+    const size_t off = static_cast<size_t>(lo) * static_cast<size_t>(h->s.nreal);
+    return sl_denoise_batch_stack_dev(h, in + off, static_cast<int>(hi - lo), nullptr, out + off, K, nK, sigma, scaled,
+                                      stream);
 }
 
 }  // extern "C"

@@ -242,6 +242,9 @@ static void finish_rec(Fast3DLaunch<n>& K, System& s, double* out) {
     K.rows_c2r(s.w->inter.p, out, 0, 1, nullptr, 0);
 }
 
+// fused denoise of this handle's bands up to the half-spectrum accumulator
+// sum_b FFT(thr(band_b)) psi_b in s.w->acc (natural layout); out = null stops
+// there (the distributed path reduces the accumulators across ranks first)
 template <int n>
 static void denoise3d_split_t(System& s, const double* f, double* stack, double* out, const double* delta,
                               cudaStream_t st) {
@@ -259,6 +262,14 @@ static void denoise3d_split_t(System& s, const double* f, double* stack, double*
         S3.template mid<kMidFused>(s.w->inter.p, sb, nullptr, cb, delta, s.lo + b0);
         S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
     }
+    if (out) finish_rec<n>(K, s, out);
+}
+
+// out = Re IFFT(acc / W) / N of an accumulator in s.w->acc
+template <int n>
+static void finish3d_t(System& s, double* out, cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    s.w->inter.alloc(static_cast<size_t>(K.nT));
     finish_rec<n>(K, s, out);
 }
 
@@ -317,6 +328,8 @@ static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_
         SLB_FAST3D_DISPATCH(rec3d_fast_t, s, coeffs, out, st)
     }
 }
+
+static void finish3d_fast(System& s, double* out, cudaStream_t st) { SLB_FAST3D_DISPATCH(finish3d_t, s, out, st) }
 
 static void denoise3d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
                            cudaStream_t st) {

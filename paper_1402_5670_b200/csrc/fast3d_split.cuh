@@ -65,6 +65,12 @@ struct SplitShape {
 #endif
 };
 
+// pass A keeps its F lines in registers across the band group (1) or reloads
+// them per band from L2 (0: 24 fewer registers at 192)
+#ifndef SLB_SPLIT_REGF
+#define SLB_SPLIT_REGF 1
+#endif
+
 template <int R, int DIR>
 __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
     if constexpr (R == 8)
@@ -89,8 +95,10 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     const int k1 = q + Q * p;
     const double2* fl = F + ((long long)k2 * n + k1) * n;
     double2 fr[E];
+    if (SLB_SPLIT_REGF) {
 #pragma unroll
-    for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
+        for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
+    }
     double2* lb = tile + p * LineBuf<L, false>::N;
     for (int bb = 0; bb < gn; ++bb) {
         const BandDesc3D bd = filt.bands[band0 + g0 + bb];
@@ -99,7 +107,8 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const double ps = fline.at(t + T * m);
-            x[m] = make_double2(fr[m].x * ps, fr[m].y * ps);
+            const double2 f = SLB_SPLIT_REGF ? fr[m] : __ldg(fl + t + T * m);
+            x[m] = make_double2(f.x * ps, f.y * ps);
         }
         if (bb > 0) __syncthreads();  // the previous band's tile is copied out
         reg_fft<L, +1, false>(x, lb, t, tw);

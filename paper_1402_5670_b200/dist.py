@@ -13,7 +13,7 @@ here.
 """
 from __future__ import annotations
 
-from typing import Callable, Tuple
+from typing import Callable, Optional, Tuple
 
 
 def shard_range(R: int, rank: int, world: int) -> Tuple[int, int]:
@@ -54,3 +54,22 @@ def sharded_inverse(coeffs, sys, group=None, root: int = 0):
     part = inverse(coeffs, sys)
     dist.reduce(part, dst=root, op=dist.ReduceOp.SUM, group=group)
     return part
+
+
+def library_comm(device: int, group=None):
+    """The library's own NCCL communicator over the ranks of a torch.distributed
+    group: rank 0 creates the NCCL unique id, torch.distributed broadcasts it
+    (any backend, gloo included), every rank joins (sl_comm_create)."""
+    import torch.distributed as dist
+    from . import Comm
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    box = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return Comm(box[0], world, rank, device)
+
+
+def attach(sys, comm, shard_bands: Optional[bool] = None):
+    """Attach `comm` to a system: 3D shards the bank by shearlet index, 2D keeps
+    the whole bank (frames shard by image)."""
+    sys.set_comm(comm, sys.ndim == 3 if shard_bands is None else shard_bands)
+    return sys

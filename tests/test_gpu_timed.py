@@ -135,3 +135,30 @@ def test_calls_on_two_streams_are_ordered(cuda):
     assert rel_l2(d0.cpu().numpy(), want[0]) == 0.0
     assert rel_l2(h1, want[1]) == 0.0
     assert rel_l2(d2.cpu().numpy(), want[2]) == 0.0
+
+
+def test_in_library_nccl_single_rank(cuda):
+    # the in-library NCCL path (broadcast, sharded fused denoise, accumulator
+    # reduce, root-only finish) on a one-rank communicator: equals the plain
+    # fused denoise; 2D batches keep the bank and take all frames
+    import torch
+    dev = cuda.index or 0
+    comm = P.Comm(P.Comm.unique_id(), 1, 0, dev)
+    s3 = P.build_system_3d((64, 64, 64), P.ScaleProfile.from_levels([0, 1]))
+    sch3 = P.ThresholdSchedule.defaults_3d(0.3, 2)
+    x = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, (64, 64, 64))).to(cuda)
+    want = P.denoise(x, s3, sch3)
+    s3.set_comm(comm)
+    assert s3.shard == (0, s3.redundancy())
+    got = P.denoise_dist(x.clone(), s3, sch3)
+    assert (torch.linalg.norm(got - want) / torch.linalg.norm(want)).item() <= 1e-13
+    s2 = P.build_system_2d(128, 128, P.ScaleProfile.from_levels([1, 1]))
+    sch2 = P.ThresholdSchedule.defaults_2d(20.0, 2)
+    fr = np.stack([P.add_gaussian_noise(P.cartoon(128), 20.0, i) for i in range(3)])
+    base = P.denoise_batch(fr, s2, sch2)
+    s2.set_comm(comm, shard_bands=False)
+    np.testing.assert_allclose(P.denoise_batch_dist(fr, s2, sch2), base, rtol=0, atol=1e-12 * np.abs(base).max())
+    g2 = P.denoise_dist(torch.from_numpy(fr[0]).to(cuda), s2, sch2).cpu().numpy()
+    assert rel_l2(g2, P.denoise(fr[0], s2, sch2)) <= 1e-12
+    s2.set_comm(None)
+    s3.set_comm(None)

@@ -82,3 +82,40 @@ def test_gloo_world2_shard_reduce_equals_full(dims, levels):
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) <= 1e-12
+
+
+def test_library_partition_matches_shard_range():
+    # the C-ABI partition (sl_partition, host code: no GPU needed) is the split
+    # the in-library NCCL path uses; it equals dist.shard_range
+    import paper_1402_5670_b200 as P
+    for R in (17, 49, 99, 292):
+        for world in (1, 2, 3, 8):
+            for r in range(world):
+                assert P.partition(R, world, r) == shard_range(R, r, world)
+    with pytest.raises(P.ConfigError):
+        P.partition(10, 2, 2)
+
+
+def _lib_id_worker(rank, world, port, q):
+    # the library communicator's unique id travels over torch.distributed (gloo
+    # here); creating the NCCL communicator itself needs a GPU per rank
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    box = [b"\x01" * 128 if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    q.put((rank, box[0] == b"\x01" * 128))
+    dist.destroy_process_group()
+
+
+def test_unique_id_broadcast_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_lib_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert got == {0: True, 1: True}
