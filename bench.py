@@ -546,6 +546,50 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
     return out
 
 
+def run_fp32(steps, warmup, local):
+    """The optional fp32 mode at the headline 2D config (reported separately,
+    never as the headline): the same lock-step 8-frame fused denoise with every
+    FFT pass in fp32 (sl_denoise_batch_f32_dev), device-timed like the fp64 line."""
+    import ctypes as C
+    import torch
+    import paper_1402_5670_b200 as P
+    cfg = CONFIGS["2d512"]
+    dev = torch.device("cuda", local)
+    s = P.build_system_2d(*cfg["dims"], P.ScaleProfile.from_levels(cfg["levels"]), device=local, dtype="f32")
+    sch = schedule_for(P, cfg)
+    frames = cfg["batch"]
+    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(512), cfg["sigma"], i) for i in range(frames)]))
+    x = x.to(dev).float()
+    o = torch.empty_like(x)
+    K = np.ascontiguousarray(sch.per_scale_factors, dtype=np.float64)
+    Kp = K.ctypes.data_as(C.POINTER(C.c_double))
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def step():
+        P._check(P.lib().sl_denoise_batch_f32_dev(s.handle, C.c_void_p(x.data_ptr()), frames, None,
+                                                  C.c_void_p(o.data_ptr()), Kp, len(K), float(sch.sigma), 1,
+                                                  P._stream_ptr(local)))
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        flush.zero_()
+        a.record()
+        step()
+        b.record()
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+    R = P.redundancy_2d(P.ScaleProfile.from_levels(cfg["levels"]))
+    nbytes = path_bytes(cfg, R, frames, "fused", 2) / 2  # fp32: every term halved (SURVEY 8d)
+    peak, _ = hbm_peak()
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"metric": "2D 512^2 dec+thr+rec frames/s, fp32 mode (nScales=4, R=49)", "value": frames / (ms / 1e3),
+            "unit": "frames/s", "ms_per_step": ms, "steps": steps, "dtype": "f32",
+            "path_roofline": {"bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak},
+            "note": "optional fp32 mode (within 1e-5 of the fp64 reference, tests/test_gpu_fp32.py); not the headline"}
+
+
 # ------------------------------------------------------------------ main
 def reference_line(name, steps, warmup, ngpus):
     cfg = CONFIGS[name]
@@ -598,6 +642,8 @@ def main():
         if rank == 0:
             w3["steps"], w3["warmup"] = k3, max(3, args.warmup)
             line["workloads"] = {"3d192": w3}
+            if world == 1:
+                line["workloads"]["2d512_f32"] = run_fp32(args.steps, max(3, args.warmup), local)
     if rank == 0:
         line.update(steps=args.steps, warmup=args.warmup)
         print(json.dumps(line), flush=True)

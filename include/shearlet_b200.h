@@ -253,6 +253,22 @@ int sl_phantom_cartoon(int n, double* out);            /* phantoms::cartoon     
 int sl_phantom_cartoon_volume(int n, double* out);     /* phantoms::cartoon_volume */
 int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double sigma, uint64_t seed);
 
+/* ---- optional fp32 mode (north_star: "within 1e-5 in an optional float32
+ * mode"; the reference itself is fp64 only, grid.hpp:78-85) ------------------
+ * sl_system_set_precision(sys, 32) rounds the handle's filter tables to
+ * float (square 2D fast-path grids: 64..2048 and 192) and enables the *_f32
+ * entry points, which take float signals / stacks and run every FFT pass in
+ * fp32. Thresholds (K sigma RMS) are compared in fp64. */
+int sl_system_set_precision(sl_system* sys, int bits);
+int sl_sheardec_f32_dev(sl_system* sys, const float* f, float* coeffs, const double* K, int nK, double sigma,
+                        int scale_by_rms, void* stream);
+int sl_shearrec_f32_dev(sl_system* sys, const float* coeffs, int nbands, float* f, void* stream);
+/* fused denoise; stack may be NULL (then the scratch stack, when materialised) */
+int sl_denoise_f32_dev(sl_system* sys, const float* in, float* stack, float* out, const double* K, int nK,
+                       double sigma, int scale_by_rms, void* stream);
+int sl_denoise_batch_f32_dev(sl_system* sys, const float* in, int nframes, float* stacks, float* out,
+                             const double* K, int nK, double sigma, int scale_by_rms, void* stream);
+
 /* ---- multi-GPU (one process per GPU) -------------------------
  * The filter index -- the reference's only parallel axis (parallel_for,
  * parallel.hpp:20-46) -- shards across GPUs: rank r owns the balanced band

@@ -189,6 +189,11 @@ def lib():
     L.sl_profile.argtypes = [P, i]
     L.sl_pass_stats.argtypes = [P, i, C.c_char_p, dp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), ip]
     L.sl_launch_count.argtypes = [P, C.POINTER(C.c_int64)]
+    L.sl_system_set_precision.argtypes = [P, i]
+    L.sl_sheardec_f32_dev.argtypes = [P, P, P, dp, i, C.c_double, i, P]
+    L.sl_shearrec_f32_dev.argtypes = [P, P, i, P, P]
+    L.sl_denoise_f32_dev.argtypes = [P, P, P, P, dp, i, C.c_double, i, P]
+    L.sl_denoise_batch_f32_dev.argtypes = [P, P, i, P, P, dp, i, C.c_double, i, P]
     u8 = C.c_char_p
     L.sl_comm_unique_id.argtypes = [u8]
     L.sl_comm_create.argtypes = [u8, i, i, i, C.POINTER(P)]
@@ -221,6 +226,8 @@ EXPORTED_SYMBOLS = [
     "sl_load_pgm", "sl_save_pgm", "sl_load_svol", "sl_save_svol",
     "sl_phantom_cartoon", "sl_phantom_cartoon_volume",
     "sl_add_gaussian_noise",
+    "sl_system_set_precision", "sl_sheardec_f32_dev", "sl_shearrec_f32_dev", "sl_denoise_f32_dev",
+    "sl_denoise_batch_f32_dev",
     "sl_comm_unique_id", "sl_comm_create", "sl_comm_destroy", "sl_comm_info", "sl_partition", "sl_system_set_comm",
     "sl_denoise_dist_dev", "sl_denoise_batch_dist_dev", "sl_denoise_batch_dist_host",
 ]
@@ -570,9 +577,10 @@ def _bank_args(fan, qmf):
 
 
 def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair] = None,
-                    full_system: bool = False, device: int = 0, shard=None) -> ShearletSystem2D:
+                    full_system: bool = False, device: int = 0, shard=None, dtype: str = "f64") -> ShearletSystem2D:
     """build_system_2d (system2d.hpp:66-69). fan: None/"dmaxflat4" (default_fan_filter), "impulse" or a
-    FanFilter; qmf: None (maximally_flat_9tap) or a QmfPair."""
+    FanFilter; qmf: None (maximally_flat_9tap) or a QmfPair. dtype "f32" also prepares the optional
+    fp32 mode (float32 CUDA tensors then run the fp32 kernels; fp64 stays available)."""
     profile.validate()
     lv, lvp = _levels_arg(profile)
     h = C.c_void_p()
@@ -580,7 +588,12 @@ def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan=None, qmf: 
     args, _keep = _bank_args(fan, qmf)
     _check(lib().sl_system_create_2d_ex(int(rows), int(cols), lvp, len(lv), profile.coarsest_scale_offset,
                                         int(full_system), *args, int(device), int(lo), int(hi), C.byref(h)))
-    return ShearletSystem2D(h, rows, cols, profile, full_system, device)
+    sys = ShearletSystem2D(h, rows, cols, profile, full_system, device)
+    if dtype == "f32":
+        _check(lib().sl_system_set_precision(h, 32))
+    elif dtype != "f64":
+        raise ConfigError("dtype must be 'f64' or 'f32'")
+    return sys
 
 
 def build_system_3d(dims, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair] = None,
@@ -739,6 +752,11 @@ def _k_arg(schedule: ThresholdSchedule):
     return K, K.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def _is_f32(x) -> bool:
+    import torch
+    return _is_cuda_tensor(x) and x.dtype == torch.float32
+
+
 def forward(f, sys: _System, threads: int = 0):
     """Undecimated analysis band_i = Re IDFT(conj(psi_i) DFT(f)) (transform.hpp:27-31).
 
@@ -746,6 +764,13 @@ def forward(f, sys: _System, threads: int = 0):
     `threads` is accepted for API parity; the GPU grid replaces host threads."""
     _check_signal(f, sys, "forward")
     L = lib()
+    if _is_f32(f):  # fp32 mode (sys built with dtype="f32")
+        import torch
+        f = f.contiguous()
+        out = torch.empty((sys.n_bands,) + tuple(sys.shape), dtype=torch.float32, device=f.device)
+        _check(L.sl_sheardec_f32_dev(sys.handle, C.c_void_p(f.data_ptr()), C.c_void_p(out.data_ptr()), None, 0,
+                                     0.0, 0, _stream_ptr(f.device.index)))
+        return out
     if _is_cuda_tensor(f):
         import torch
         f = f.contiguous().to(torch.float64)
@@ -764,6 +789,13 @@ def inverse(coeffs, sys: _System, threads: int = 0):
     if tuple(coeffs.shape[1:]) != tuple(sys.shape) or coeffs.shape[0] != sys.n_bands:
         raise ShapeError("inverse: coefficient stack does not match the system")
     L = lib()
+    if _is_f32(coeffs):
+        import torch
+        coeffs = coeffs.contiguous()
+        out = torch.empty(tuple(sys.shape), dtype=torch.float32, device=coeffs.device)
+        _check(L.sl_shearrec_f32_dev(sys.handle, C.c_void_p(coeffs.data_ptr()), int(coeffs.shape[0]),
+                                     C.c_void_p(out.data_ptr()), _stream_ptr(coeffs.device.index)))
+        return out
     if _is_cuda_tensor(coeffs):
         import torch
         coeffs = coeffs.contiguous().to(torch.float64)
@@ -816,6 +848,17 @@ def denoise(noisy, sys: _System, schedule: ThresholdSchedule, threads: int = 0, 
     _check_signal(noisy, sys, "forward")
     K, Kp = _k_arg(schedule)
     L = lib()
+    if _is_f32(noisy):
+        import torch
+        noisy = noisy.contiguous()
+        out = torch.empty_like(noisy)
+        stack = torch.empty((sys.n_bands,) + tuple(sys.shape), dtype=torch.float32, device=noisy.device) \
+            if return_stack else None
+        _check(L.sl_denoise_f32_dev(sys.handle, C.c_void_p(noisy.data_ptr()),
+                                    C.c_void_p(stack.data_ptr() if stack is not None else None),
+                                    C.c_void_p(out.data_ptr()), Kp, len(K), float(schedule.sigma),
+                                    int(schedule.scale_by_filter_norm), _stream_ptr(noisy.device.index)))
+        return (out, stack) if return_stack else out
     if _is_cuda_tensor(noisy):
         import torch
         noisy = noisy.contiguous().to(torch.float64)
@@ -877,6 +920,16 @@ def denoise_batch(frames, sys: _System, schedule: ThresholdSchedule, return_stac
     _check_batch(frames, sys)
     K, Kp = _k_arg(schedule)
     args = (Kp, len(K), float(schedule.sigma), int(schedule.scale_by_filter_norm))
+    if _is_f32(frames):
+        import torch
+        frames = frames.contiguous()
+        out = torch.empty_like(frames)
+        st = torch.empty((frames.shape[0], sys.n_bands) + tuple(sys.shape), dtype=torch.float32,
+                         device=frames.device) if return_stacks else None
+        _check(lib().sl_denoise_batch_f32_dev(sys.handle, C.c_void_p(frames.data_ptr()), int(frames.shape[0]),
+                                              C.c_void_p(st.data_ptr() if st is not None else None),
+                                              C.c_void_p(out.data_ptr()), *args, _stream_ptr(frames.device.index)))
+        return (out, st) if return_stacks else out
     if _is_cuda_tensor(frames):
         import torch
         frames = frames.contiguous().to(torch.float64)

@@ -1266,6 +1266,133 @@ int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double s
     });
 }
 
+// ---- optional fp32 mode (north_star: within 1e-5 of the fp64 reference) ----
+}  // extern "C"
+namespace {
+__global__ void k_to_f32(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = static_cast<float>(in[i]);
+}
+System& fp32_sys(sl_system* h) {
+    System& s = sys_of(h);
+    if (!s.fp32) throw SlError(SL_ERR_CONFIG, "fp32 entry point: call sl_system_set_precision(sys, 32) first");
+    return s;
+}
+}  // namespace
+extern "C" {
+
+int sl_system_set_precision(sl_system* h, int bits) {
+    return guard([&] {
+        System& s = sys_of(h);
+        if (bits != 32 && bits != 64) throw SlError(SL_ERR_CONFIG, "precision must be 32 or 64 bits");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, 0);
+        if (bits == 64) {
+            s.fp32 = false;
+            s.psiT32.release();
+            s.WT32.release();
+            return;
+        }
+        if (!s.fast2d)
+            throw SlError(SL_ERR_UNSUPPORTED_SIZE,
+                          "fp32 mode: square 2D grids of 64..2048 (power of two or 192) only");
+        const long long np = static_cast<long long>(s.R) * s.H * s.n[0], nw = static_cast<long long>(s.H) * s.n[0];
+        s.psiT32.alloc(static_cast<size_t>(np));
+        s.WT32.alloc(static_cast<size_t>(nw));
+        k_to_f32<<<1024, 256>>>(s.psiT.p, s.psiT32.p, np);
+        check_launch("k_to_f32");
+        k_to_f32<<<256, 256>>>(s.WT.p, s.WT32.p, nw);
+        check_launch("k_to_f32");
+        SL_CUDA(cudaDeviceSynchronize());
+        s.fp32 = true;
+    });
+}
+
+int sl_sheardec_f32_dev(sl_system* h, const float* f, float* coeffs, const double* K, int nK, double sigma, int scaled,
+                        void* stream) {
+    return guard([&] {
+        System& s = fp32_sys(h);
+        require_dev_ptr(f, "sheardec input");
+        require_dev_ptr(coeffs, "sheardec output");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
+        if (K) deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        dec2d_fast_f32(s, f, coeffs, K ? s.delta.p : nullptr, stream_of(stream));
+    });
+}
+
+int sl_shearrec_f32_dev(sl_system* h, const float* coeffs, int nbands, float* f, void* stream) {
+    return guard([&] {
+        System& s = fp32_sys(h);
+        if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "inverse: coefficient stack does not match the system");
+        require_dev_ptr(coeffs, "shearrec input");
+        require_dev_ptr(f, "shearrec output");
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
+        rec2d_fast_f32(s, coeffs, f, stream_of(stream));
+    });
+}
+
+int sl_denoise_f32_dev(sl_system* h, const float* in, float* stack, float* out, const double* K, int nK, double sigma,
+                       int scaled, void* stream) {
+    return guard([&] {
+        System& s = fp32_sys(h);
+        require_dev_ptr(in, "denoise input");
+        require_dev_ptr(out, "denoise output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        CallOrder co(s, stream_of(stream));
+        deltas(s, K, nK, sigma, scaled, stream_of(stream));
+        float* stk = stack;
+        if (!stk && s.materialize) {  // scratch stack, sized for fp64 (fp32 uses the front half)
+            s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
+            stk = reinterpret_cast<float*>(s.stack.p);
+        }
+        denoise2d_fast_f32(s, in, stk, out, s.delta.p, stream_of(stream));
+    });
+}
+
+int sl_denoise_batch_f32_dev(sl_system* h, const float* in, int nframes, float* stacks, float* out, const double* K,
+                             int nK, double sigma, int scaled, void* stream) {
+    return guard([&] {
+        System& s = fp32_sys(h);
+        require_dev_ptr(in, "denoise input");
+        require_dev_ptr(out, "denoise output");
+        if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");
+        if (nframes < 0) throw SlError(SL_ERR_SHAPE, "negative frame count");
+        if (s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
+        std::lock_guard<std::mutex> lk(s.mu);
+        DeviceGuard dg(s.device);
+        cudaStream_t st = stream_of(stream);
+        CallOrder co(s, st);
+        deltas(s, K, nK, sigma, scaled, st);
+        const int group = lockstep_group(s, nframes);
+        const int ngroups = (nframes + group - 1) / group;
+        const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
+        fan_out(s, ngroups, st, [&](int g, cudaStream_t fst) {
+            const int f0 = g * group, nf = std::min(group, nframes - f0);
+            const size_t off = static_cast<size_t>(f0) * s.nreal;
+            float* stk = nullptr;
+            if (stacks) {
+                stk = stacks + static_cast<size_t>(f0) * sfs;
+            } else if (s.materialize) {
+                s.w->stack.alloc(static_cast<size_t>(group) * sfs);
+                stk = reinterpret_cast<float*>(s.w->stack.p);
+            }
+            const int conc = s.concurrency;
+            s.concurrency = std::max(conc, 4);
+            denoise2d_fast_batch_f32(s, in + off, s.nreal, nf, stk, sfs, out + off, s.nreal, s.delta.p, fst);
+            s.concurrency = conc;
+        });
+    });
+}
+
 // ---- multi-GPU: NCCL communicators and the sharded hot path (comm.cuh) ----
 int sl_comm_unique_id(unsigned char* id) {
     return guard([&] {

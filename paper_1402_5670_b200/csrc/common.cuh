@@ -76,6 +76,7 @@ struct DBuf {
 struct PlanHolder {
     FftPlan plan;
     DBuf<double2> tw;
+    DBuf<float2> tw32;
 };
 
 static std::vector<int> factor_radices(int L) {
@@ -111,6 +112,10 @@ static void make_plan(int L, PlanHolder& ph, cudaStream_t st) {
     }
     ph.tw.upload(tw.data(), tw.size(), st);
     ph.plan.tw = ph.tw.p;
+    std::vector<float2> t32(tw.size());
+    for (size_t k = 0; k < tw.size(); ++k) t32[k] = make_float2(static_cast<float>(tw[k].x), static_cast<float>(tw[k].y));
+    ph.tw32.upload(t32.data(), t32.size(), st);
+    ph.plan.tw32 = ph.tw32.p;
 }
 
 // ------------------------------------------------------------------ launch helpers
@@ -214,6 +219,10 @@ struct System {
     // 2D fast path (fast2d.cuh): column-major halves psi^T [R][H][n0], W^T [H][n0]
     bool fast2d = false;
     DBuf<double> psiT, WT;
+    // optional fp32 mode (sl_system_set_precision(32)): the same tables rounded
+    // to float, used by the *_f32 entry points
+    bool fp32 = false;
+    DBuf<float> psiT32, WT32;
     // 3D fast path (fast3d.cuh): W in the natural [k2][k1][k0] layout
     bool fast3d = false;
     DBuf<double> WN;

@@ -23,6 +23,20 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// one complex element: 16 bytes (double2, .cg: L2 only) or 8 bytes (float2, .ca)
+template <class C>
+__device__ __forceinline__ void cp_async_c(C* smem, const C* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if constexpr (sizeof(C) == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+// dynamic shared memory typed per instantiation (fp64 / fp32 kernels share the symbol)
+#define SLB_DYN_SMEM(C, name)                                      \
+    extern __shared__ __align__(16) unsigned char slb_dyn_smem[]; \
+    C* name = reinterpret_cast<C*>(slb_dyn_smem)
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -78,18 +92,18 @@ struct ColCfg {
 };
 
 // dynamic shared memory of the kernels (line buffers padded, LineBuf<L>)
-template <int L>
+template <int L, class C = double2>
 static size_t row_smem_bytes(int H) {  // [H][2V] tile; V padded line buffers alias it
     using RC = RowCfg<L>;
-    return std::max(static_cast<size_t>(2 * RC::V) * H, static_cast<size_t>(RC::V) * LineBuf<L, false>::N) * sizeof(double2);
+    return std::max(static_cast<size_t>(2 * RC::V) * H, static_cast<size_t>(RC::V) * LineBuf<L, false>::N) * sizeof(C);
 }
-template <int L>
+template <int L, class C = double2>
 static size_t col1_smem_bytes() {  // one padded exchange buffer per line
-    return static_cast<size_t>(ColCfg<L>::LINES) * LineBuf<L>::N * sizeof(double2);
+    return static_cast<size_t>(ColCfg<L>::LINES) * LineBuf<L>::N * sizeof(C);
 }
-template <int L>
+template <int L, class C = double2>
 static size_t col2_smem_bytes() {  // exchange buffer + a second L-line (F column / accumulator)
-    return static_cast<size_t>(ColCfg<L>::LINES) * (LineBuf<L>::N + L) * sizeof(double2);
+    return static_cast<size_t>(ColCfg<L>::LINES) * (LineBuf<L>::N + L) * sizeof(C);
 }
 
 // accumulator in registers (measured: cols_rec<512> -6 %, <1024> -10 %); at
@@ -103,20 +117,21 @@ struct ColRec {
     static constexpr bool REGACC = SLB_COLREC_REGACC;
 #endif
 };
-template <int L>
+template <int L, class C = double2>
 static size_t colrec_smem_bytes() {  // register accumulator: exchange buffers only
-    return ColRec<L>::REGACC ? col1_smem_bytes<L>() : col2_smem_bytes<L>();
+    return ColRec<L>::REGACC ? col1_smem_bytes<L, C>() : col2_smem_bytes<L, C>();
 }
 
 // ---------------------------------------------------------------- rows c2r
 // In : src[k1 * n0 + r] (column-major half spectrum), bands strided by sbs.
 // Out: dst[r * L + i] real rows, scaled, optionally thresholded (delta >= 0).
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(RowCfg<L>::THREADS)
-    k2_rows_c2r(const double2* __restrict__ src, long long sbs, double* __restrict__ dst, long long dbs, int n0,
-                int H, double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw) {
+    k2_rows_c2r(const C* __restrict__ src, long long sbs, RealOf<C>* __restrict__ dst, long long dbs, int n0,
+                int H, RealOf<C> scale, const double* __restrict__ delta, int band0, const C* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
-    extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers of L
+    using R = RealOf<C>;
+    SLB_DYN_SMEM(C, tile);  // [H][2V] swizzled tile, then V line buffers of L
     const int r0 = blockIdx.x * 2 * V;
     src += blockIdx.y * sbs;
     dst += blockIdx.y * dbs;
@@ -126,18 +141,18 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
         if (rr < nrows)
-            cp_async16(tile + tslot<V>(k, rr), src + (long long)k * n0 + r0 + rr);
+            cp_async_c(tile + tslot<V>(k, rr), src + (long long)k * n0 + r0 + rr);
         else
-            tile[tslot<V>(k, rr)] = make_double2(0.0, 0.0);
+            tile[tslot<V>(k, rr)] = mkc<C>(0.0, 0.0);
     }
     cp_async_wait_all();
     __syncthreads();
     const int q = threadIdx.x / T, t = threadIdx.x - q * T;
-    double2 x[E];
+    C x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int k = t + T * m;
-        double2 X, Y;
+        C X, Y;
         if (k < H) {
             X = tile[tslot<V>(k, 2 * q)];
             Y = tile[tslot<V>(k, 2 * q + 1)];
@@ -145,23 +160,23 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
                 X.y = 0.0;
                 Y.y = 0.0;
             }
-            x[m] = make_double2(X.x - Y.y, X.y + Y.x);  // X + iY
+            x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);  // X + iY
         } else {
             X = tile[tslot<V>(L - k, 2 * q)];
             Y = tile[tslot<V>(L - k, 2 * q + 1)];
-            x[m] = make_double2(X.x + Y.y, Y.x - X.y);  // conj(X) + i conj(Y)
+            x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);  // conj(X) + i conj(Y)
         }
     }
     // the tile is dead once every line has gathered its inputs: the line
     // exchange buffers alias it (H*2V >= V*L), halving shared memory per CTA
     __syncthreads();
-    double2* lb = tile + q * LineBuf<L, false>::N;
+    C* lb = tile + q * LineBuf<L, false>::N;
     reg_fft<L, +1, false>(x, lb, t, tw);
     const double dl = delta ? delta[band0 + blockIdx.y] : -1.0;
     const int ra = r0 + 2 * q;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-        double a = x[m].x * scale, b = x[m].y * scale;
+        R a = x[m].x * scale, b = x[m].y * scale;
         if (dl >= 0.0) {
             if (fabs(a) < dl) a = 0.0;
             if (fabs(b) < dl) b = 0.0;
@@ -174,33 +189,34 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
 
 // ---------------------------------------------------------------- rows r2c
 // In : real rows src[r * L + i]; Out: column-major half spectrum dst[k1 * n0 + r].
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(RowCfg<L>::THREADS)
-    k2_rows_r2c(const double* __restrict__ src, long long sbs, double2* __restrict__ dst, long long dbs, int n0,
-                int H, const double2* __restrict__ tw) {
+    k2_rows_r2c(const RealOf<C>* __restrict__ src, long long sbs, C* __restrict__ dst, long long dbs, int n0,
+                int H, const C* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    using R = RealOf<C>;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;  // split outputs per thread
-    extern __shared__ double2 tile[];            // [H][2V] swizzled tile, then V line buffers
+    SLB_DYN_SMEM(C, tile);            // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
     src += blockIdx.y * sbs;
     dst += blockIdx.y * dbs;
     const int q = threadIdx.x / T, t = threadIdx.x - q * T;
     const int ra = r0 + 2 * q;
-    double2 x[E];
+    C x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int i = t + T * m;
-        const double a = ra < n0 ? __ldg(src + (long long)ra * L + i) : 0.0;
-        const double b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : 0.0;
-        x[m] = make_double2(a, b);
+        const R a = ra < n0 ? __ldg(src + (long long)ra * L + i) : R(0);
+        const R b = ra + 1 < n0 ? __ldg(src + (long long)(ra + 1) * L + i) : R(0);
+        x[m] = mkc<C>(a, b);
     }
-    double2* lb = tile + q * LineBuf<L, false>::N;  // line buffers alias the (not yet used) output tile
+    C* lb = tile + q * LineBuf<L, false>::N;  // line buffers alias the (not yet used) output tile
     reg_fft<L, -1, false>(x, lb, t, tw);
     // Z in registers (element t + T m); publish to the line buffer, then split
 #pragma unroll
     for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
     line_sync<T>();
-    double2 zk[KPT], zm[KPT];
+    C zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
@@ -214,8 +230,8 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            tile[tslot<V>(k, 2 * q)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));      // X
-            tile[tslot<V>(k, 2 * q + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));  // Y
+            tile[tslot<V>(k, 2 * q)] = mkc<C>(R(0.5) * (zk[u].x + zm[u].x), R(0.5) * (zk[u].y - zm[u].y));      // X
+            tile[tslot<V>(k, 2 * q + 1)] = mkc<C>(R(0.5) * (zk[u].y + zm[u].y), R(0.5) * (zm[u].x - zk[u].x));  // Y
         }
     }
     __syncthreads();
@@ -245,63 +261,64 @@ struct ColDec {
     static constexpr int MIN_BLOCKS = SLB_COLDEC_MINB;
 #endif
 };
-template <int L>
+template <int L, class C = double2>
 static size_t coldec_smem_bytes() {
-    return ColDec<L>::REGF ? col1_smem_bytes<L>() : col2_smem_bytes<L>();
+    return ColDec<L>::REGF ? col1_smem_bytes<L, C>() : col2_smem_bytes<L, C>();
 }
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
-    k2_cols_dec(const double2* __restrict__ FT, const double* __restrict__ psiT, long long pbs,
-                double2* __restrict__ inter, long long ibs, int H, int band0, int G, int nb,
-                const double2* __restrict__ tw, long long fzs = 0, long long izs = 0) {
+    k2_cols_dec(const C* __restrict__ FT, const RealOf<C>* __restrict__ psiT, long long pbs,
+                C* __restrict__ inter, long long ibs, int H, int band0, int G, int nb,
+                const C* __restrict__ tw, long long fzs = 0, long long izs = 0) {
     FT += blockIdx.z * fzs;  // blockIdx.z: frame of a lock-step batch
     inter += blockIdx.z * izs;
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
-    extern __shared__ double2 lbuf[];  // per line: [exchange L][F column L]
+    using R = RealOf<C>;
+    SLB_DYN_SMEM(C, lbuf);  // per line: [exchange L][F column L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
-    double2* sm = lbuf + li * (LineBuf<L>::N + (ColDec<L>::REGF ? 0 : L));
-    double2* fs = sm + LineBuf<L>::N;
-    double2 fr[E];
+    C* sm = lbuf + li * (LineBuf<L>::N + (ColDec<L>::REGF ? 0 : L));
+    C* fs = sm + LineBuf<L>::N;
+    C fr[E];
     if (ColDec<L>::REGF) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) fr[m] = valid ? __ldg(FT + (long long)k1 * L + t + T * m) : make_double2(0.0, 0.0);
+        for (int m = 0; m < E; ++m) fr[m] = valid ? __ldg(FT + (long long)k1 * L + t + T * m) : mkc<C>(0.0, 0.0);
     } else {
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             if (valid)
-                cp_async16(fs + t + T * m, FT + (long long)k1 * L + t + T * m);
+                cp_async_c(fs + t + T * m, FT + (long long)k1 * L + t + T * m);
             else
-                fs[t + T * m] = make_double2(0.0, 0.0);
+                fs[t + T * m] = mkc<C>(0.0, 0.0);
         }
         cp_async_wait_all();
     }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
     // psi of band b+1 is loaded while band b is in the FFT
-    double p[E];
+    R p[E];
     {
-        const double* ps = psiT + (long long)(band0 + g0) * pbs + (long long)k1 * L;
+        const R* ps = psiT + (long long)(band0 + g0) * pbs + (long long)k1 * L;
 #pragma unroll
-        for (int m = 0; m < E; ++m) p[m] = (valid && gn > 0) ? __ldg(ps + t + T * m) : 0.0;
+        for (int m = 0; m < E; ++m) p[m] = (valid && gn > 0) ? __ldg(ps + t + T * m) : R(0);
     }
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
-        double2 x[E];
+        C x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double2 fv = ColDec<L>::REGF ? fr[m] : fs[t + T * m];
-            x[m] = make_double2(fv.x * p[m], fv.y * p[m]);  // conj(psi) * F, psi real
+            const C fv = ColDec<L>::REGF ? fr[m] : fs[t + T * m];
+            x[m] = mkc<C>(fv.x * p[m], fv.y * p[m]);  // conj(psi) * F, psi real
         }
         if (bb + 1 < gn) {
-            const double* ps = psiT + (long long)(band0 + b + 1) * pbs + (long long)k1 * L;
+            const R* ps = psiT + (long long)(band0 + b + 1) * pbs + (long long)k1 * L;
 #pragma unroll
-            for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
+            for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
         reg_fft<L, +1>(x, sm, t, tw);
         if (valid) {
-            double2* o = inter + (long long)b * ibs + (long long)k1 * L;
+            C* o = inter + (long long)b * ibs + (long long)k1 * L;
 #pragma unroll
             for (int m = 0; m < E; ++m) __stcg(o + t + T * m, x[m]);
         }
@@ -312,21 +329,22 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
 // final rec column pass for one line: IFFT_0((sum_s slot[s]) / W) -> out; also
 // the plain forward column FFT (F = FFT_0 of the rows pass) when W == nullptr &&
 // DIR < 0. Slots are summed in index order (deterministic).
-template <int L, int DIR>
-__device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots, long long sbs, int nslots,
-                                              const double* __restrict__ WT, double2* __restrict__ out, int k1,
-                                              bool valid, double2* sm, int t, const double2* __restrict__ tw) {
+template <int L, int DIR, class C = double2>
+__device__ __forceinline__ void cols_sum_line(const C* __restrict__ slots, long long sbs, int nslots,
+                                              const RealOf<C>* __restrict__ WT, C* __restrict__ out, int k1,
+                                              bool valid, C* sm, int t, const C* __restrict__ tw) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
-    double2 x[E];
+    using R = RealOf<C>;
+    C x[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) x[m] = make_double2(0.0, 0.0);
+    for (int m = 0; m < E; ++m) x[m] = mkc<C>(0.0, 0.0);
     if (valid) {
         // slots summed in order; two slots' loads in flight per step
         int s = 0;
         for (; s + 1 < nslots; s += 2) {
-            const double2* in0 = slots + (long long)s * sbs + (long long)k1 * L;
-            const double2* in1 = in0 + sbs;
-            double2 u[E], v[E];
+            const C* in0 = slots + (long long)s * sbs + (long long)k1 * L;
+            const C* in1 = in0 + sbs;
+            C u[E], v[E];
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 u[m] = __ldcg(in0 + t + T * m);
@@ -336,21 +354,21 @@ __device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots,
             for (int m = 0; m < E; ++m) x[m] = cadd(cadd(x[m], u[m]), v[m]);
         }
         for (; s < nslots; ++s) {
-            const double2* in = slots + (long long)s * sbs + (long long)k1 * L;
+            const C* in = slots + (long long)s * sbs + (long long)k1 * L;
 #pragma unroll
             for (int m = 0; m < E; ++m) x[m] = cadd(x[m], __ldcg(in + t + T * m));
         }
         if (WT) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
-                const double w = __ldg(WT + (long long)k1 * L + t + T * m);
-                x[m] = make_double2(x[m].x / w, x[m].y / w);
+                const R w = __ldg(WT + (long long)k1 * L + t + T * m);
+                x[m] = mkc<C>(x[m].x / w, x[m].y / w);
             }
         }
     }
     reg_fft<L, DIR>(x, sm, t, tw);
     if (valid) {
-        double2* o = out + (long long)k1 * L;
+        C* o = out + (long long)k1 * L;
 #pragma unroll
         for (int m = 0; m < E; ++m) __stcg(o + t + T * m, x[m]);
     }
@@ -360,47 +378,48 @@ __device__ __forceinline__ void cols_sum_line(const double2* __restrict__ slots,
 #ifndef SLB_COLREC_MINB
 #define SLB_COLREC_MINB ColCfg<L>::MIN_BLOCKS
 #endif
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
-    k2_cols_rec(const double2* __restrict__ inter, long long ibs, const double* __restrict__ psiT, long long pbs,
-                double2* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
-                const double2* __restrict__ tw, int* __restrict__ done, int nslots, const double* __restrict__ WT,
-                double2* __restrict__ fout, long long izs = 0, long long szs = 0, long long fozs = 0) {
+    k2_cols_rec(const C* __restrict__ inter, long long ibs, const RealOf<C>* __restrict__ psiT, long long pbs,
+                C* __restrict__ slots, long long sbs, int H, int band0, int G, int nb, int slot0,
+                const C* __restrict__ tw, int* __restrict__ done, int nslots, const RealOf<C>* __restrict__ WT,
+                C* __restrict__ fout, long long izs = 0, long long szs = 0, long long fozs = 0) {
     inter += blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
     slots += blockIdx.z * szs;
     fout += blockIdx.z * fozs;
     if (done) done += blockIdx.z * gridDim.x;
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
-    extern __shared__ double2 lbuf[];  // per line: [exchange L][accumulator L]
+    using R = RealOf<C>;
+    SLB_DYN_SMEM(C, lbuf);  // per line: [exchange L][accumulator L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
     // per line: [exchange L] (+ [accumulator L] unless it lives in registers)
-    double2* sm = lbuf + li * (LineBuf<L>::N + (ColRec<L>::REGACC ? 0 : L));
-    double2* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
-    double2 ar[E];
+    C* sm = lbuf + li * (LineBuf<L>::N + (ColRec<L>::REGACC ? 0 : L));
+    C* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
+    C ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-        ar[m] = make_double2(0.0, 0.0);
+        ar[m] = mkc<C>(0.0, 0.0);
         if (!ColRec<L>::REGACC) acc[t + T * m] = ar[m];
     }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
-        double2 x[E];
-        const double2* in = inter + (long long)b * ibs + (long long)k1 * L;
+        C x[E];
+        const C* in = inter + (long long)b * ibs + (long long)k1 * L;
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : make_double2(0.0, 0.0);
+        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : mkc<C>(0.0, 0.0);
         // the band's psi is loaded before the FFT so its latency overlaps it
-        double p[E];
-        const double* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+        R p[E];
+        const R* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
 #pragma unroll
-        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : 0.0;
+        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         reg_fft<L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            double2 a = ColRec<L>::REGACC ? ar[m] : acc[t + T * m];
+            C a = ColRec<L>::REGACC ? ar[m] : acc[t + T * m];
             a.x = fma(x[m].x, p[m], a.x);
             a.y = fma(x[m].y, p[m], a.y);
             if (ColRec<L>::REGACC)
@@ -411,7 +430,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
         line_sync<T>();
     }
     if (valid) {
-        double2* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
+        C* o = slots + (long long)(slot0 + blockIdx.y) * sbs + (long long)k1 * L;
 #pragma unroll
         for (int m = 0; m < E; ++m) __stcg(o + t + T * m, ColRec<L>::REGACC ? ar[m] : acc[t + T * m]);
     }
@@ -430,21 +449,21 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     __syncthreads();
     if (!last) return;
     __threadfence();
-    cols_sum_line<L, +1>(slots, sbs, nslots, WT, fout, k1, valid, sm, t, tw);
+    cols_sum_line<L, +1, C>(slots, sbs, nslots, WT, fout, k1, valid, sm, t, tw);
 }
 
-template <int L, int DIR>
+template <int L, int DIR, class C = double2>
 __global__ void __launch_bounds__(ColCfg<L>::THREADS)
-    k2_cols_sum(const double2* __restrict__ slots, long long sbs, int nslots, const double* __restrict__ WT,
-                double2* __restrict__ out, int H, const double2* __restrict__ tw, long long szs = 0,
+    k2_cols_sum(const C* __restrict__ slots, long long sbs, int nslots, const RealOf<C>* __restrict__ WT,
+                C* __restrict__ out, int H, const C* __restrict__ tw, long long szs = 0,
                 long long ozs = 0) {
     slots += blockIdx.z * szs;  // blockIdx.z: frame of a lock-step batch
     out += blockIdx.z * ozs;
     constexpr int T = RegPlan<L>::T;
-    extern __shared__ double2 lbuf[];
+    SLB_DYN_SMEM(C, lbuf);
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
-    cols_sum_line<L, DIR>(slots, sbs, nslots, WT, out, k1, k1 < H, lbuf + li * LineBuf<L>::N, t, tw);
+    cols_sum_line<L, DIR, C>(slots, sbs, nslots, WT, out, k1, k1 < H, lbuf + li * LineBuf<L>::N, t, tw);
 }
 
 }  // namespace slb

@@ -16,14 +16,15 @@ namespace slb {
 // STORE = false: the stack is not materialised (sl_set_stack_output, band
 // null); a separate instantiation so the stack-writing variant keeps its
 // register allocation (a runtime null test spilled 136 B/thread at L = 128)
-template <int L, bool STORE = true>
+template <int L, bool STORE = true, class C = double2>
 __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
-    k2_rows_fused(double2* __restrict__ inter, long long ibs, double* __restrict__ band, long long bbs, int n0, int H,
-                  double scale, const double* __restrict__ delta, int band0, const double2* __restrict__ tw,
+    k2_rows_fused(C* __restrict__ inter, long long ibs, RealOf<C>* __restrict__ band, long long bbs, int n0, int H,
+                  RealOf<C> scale, const double* __restrict__ delta, int band0, const C* __restrict__ tw,
                   long long izs = 0, long long bzs = 0) {
     constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    using R = RealOf<C>;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;
-    extern __shared__ double2 tile[];  // [H][2V] swizzled tile, then V line buffers
+    SLB_DYN_SMEM(C, tile);  // [H][2V] swizzled tile, then V line buffers
     const int r0 = blockIdx.x * 2 * V;
     inter += blockIdx.y * ibs + blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
     // STORE = false keeps a (never taken) runtime test on the stores: ptxas
@@ -36,18 +37,18 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
         const int k = idx / (2 * V), rr = idx - k * 2 * V;
         if (rr < nrows)
-            cp_async16(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
+            cp_async_c(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
         else
-            tile[tslot<V>(k, rr)] = make_double2(0.0, 0.0);
+            tile[tslot<V>(k, rr)] = mkc<C>(0.0, 0.0);
     }
     cp_async_wait_all();
     __syncthreads();
     const int q = threadIdx.x / T, t = threadIdx.x - q * T;
-    double2 x[E];
+    C x[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const int k = t + T * m;
-        double2 X, Y;
+        C X, Y;
         if (k < H) {
             X = tile[tslot<V>(k, 2 * q)];
             Y = tile[tslot<V>(k, 2 * q + 1)];
@@ -55,21 +56,21 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
                 X.y = 0.0;
                 Y.y = 0.0;
             }
-            x[m] = make_double2(X.x - Y.y, X.y + Y.x);
+            x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
         } else {
             X = tile[tslot<V>(L - k, 2 * q)];
             Y = tile[tslot<V>(L - k, 2 * q + 1)];
-            x[m] = make_double2(X.x + Y.y, Y.x - X.y);
+            x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
         }
     }
     __syncthreads();              // every line has gathered: the tile is dead
-    double2* lb = tile + q * LineBuf<L, false>::N;   // line buffers alias it (smem sized for both)
+    C* lb = tile + q * LineBuf<L, false>::N;   // line buffers alias it (smem sized for both)
     reg_fft<L, +1, false>(x, lb, t, tw);
     const double dl = delta[band0 + blockIdx.y];
     const int ra = r0 + 2 * q;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-        double a = x[m].x * scale, c = x[m].y * scale;
+        R a = x[m].x * scale, c = x[m].y * scale;
         if (dl >= 0.0) {
             if (fabs(a) < dl) a = 0.0;
             if (fabs(c) < dl) c = 0.0;
@@ -79,13 +80,13 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
             if (ra < n0) band[(long long)ra * L + i] = a;
             if (ra + 1 < n0) band[(long long)(ra + 1) * L + i] = c;
         }
-        x[m] = make_double2(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : 0.0);  // rec input: the thresholded rows
+        x[m] = mkc<C>(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : R(0));  // rec input: the thresholded rows
     }
     reg_fft<L, -1, false>(x, lb, t, tw);
 #pragma unroll
     for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
     line_sync<T>();
-    double2 zk[KPT], zm[KPT];
+    C zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
@@ -99,8 +100,8 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            tile[tslot<V>(k, 2 * q)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));
-            tile[tslot<V>(k, 2 * q + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));
+            tile[tslot<V>(k, 2 * q)] = mkc<C>(R(0.5) * (zk[u].x + zm[u].x), R(0.5) * (zk[u].y - zm[u].y));
+            tile[tslot<V>(k, 2 * q + 1)] = mkc<C>(R(0.5) * (zk[u].y + zm[u].y), R(0.5) * (zm[u].x - zk[u].x));
         }
     }
     __syncthreads();
@@ -111,20 +112,20 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
 }
 
 // rows pass of the fused denoise (band = null: the stack is not materialised)
-template <int L>
-static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, double2* inter, long long ibs,
-                              double* band, long long bbs, int n0, int H, double scale, const double* delta,
-                              int band0, const double2* tw, long long izs, long long bzs) {
+template <int L, class C = double2>
+static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, C* inter, long long ibs,
+                              RealOf<C>* band, long long bbs, int n0, int H, double scale, const double* delta,
+                              int band0, const C* tw, long long izs, long long bzs) {
     using RC = RowCfg<L>;
-    auto* k = band ? k2_rows_fused<L, true> : k2_rows_fused<L, false>;
+    auto* k = band ? k2_rows_fused<L, true, C> : k2_rows_fused<L, false, C>;
     set_smem(k, tile_smem);
     k<<<grid, RC::THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
     check_launch("k2_rows_fused");
 }
 
 // denoise with the stack materialised in `stack` ([nb][n0][n1]).
-template <int L0, int L1>
-static void denoise2d_fast_t(System& s, const double* f, double* stack, double* out, const double* delta,
+template <int L0, int L1, class CX = double2>
+static void denoise2d_fast_t(System& s, const RealOf<CX>* f, RealOf<CX>* stack, RealOf<CX>* out, const double* delta,
                              cudaStream_t st) {
     const int n0 = s.n[0], H = s.H;
     const long long nhT = static_cast<long long>(H) * n0;
@@ -136,19 +137,19 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     int nslots = 0;
     for (int b0 = 0; b0 < nb; b0 += C) nslots += (std::min(C, nb - b0) + cfg.G - 1) / cfg.G;
     s.w->slots.alloc(static_cast<size_t>(nslots) * nhT);
-    const double2* tw0 = s.plan(L0, st).tw;
-    const double2* tw1 = s.plan(L1, st).tw;
+    const CX* tw0 = Prec2D<CX>::tw(s.plan(L0, st));
+    const CX* tw1 = Prec2D<CX>::tw(s.plan(L1, st));
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = row_smem_bytes<L1>(H);
-    const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = coldec_smem_bytes<L0>();
-    set_smem(k2_rows_r2c<L1>, row_smem);
-    set_smem(k2_rows_c2r<L1>, row_smem);
-    set_smem(k2_cols_sum<L0, -1>, col_smem);
-    set_smem(k2_cols_sum<L0, +1>, col_smem);
-    set_smem(k2_cols_dec<L0>, col2_smem);
-    set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
+    const size_t row_smem = row_smem_bytes<L1, CX>(H);
+    const size_t col_smem = col1_smem_bytes<L0, CX>();
+    const size_t col2_smem = coldec_smem_bytes<L0, CX>();
+    set_smem(k2_rows_r2c<L1, CX>, row_smem);
+    set_smem(k2_rows_c2r<L1, CX>, row_smem);
+    set_smem(k2_cols_sum<L0, -1, CX>, col_smem);
+    set_smem(k2_cols_sum<L0, +1, CX>, col_smem);
+    set_smem(k2_cols_dec<L0, CX>, col2_smem);
+    set_smem(k2_cols_rec<L0, CX>, colrec_smem_bytes<L0, CX>());
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     if (s.w->done.n < static_cast<size_t>(col_blocks)) {  // zeroed once; the kernel resets its counters
@@ -157,28 +158,28 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
     }
     {
         LaunchScope ls(s, "f2_rows_r2c", st, 1);
-        k2_rows_r2c<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(f, 0, s.w->inter.p, 0, n0, H, tw1);
+        k2_rows_r2c<L1, CX><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(f, 0, ws_as<CX>(s.w->inter), 0, n0, H, tw1);
         check_launch("k2_rows_r2c");
     }
     {
         LaunchScope ls(s, "f2_cols_fwd", st, 1);
-        k2_cols_sum<L0, -1><<<col_blocks, CC::THREADS, col_smem, st>>>(s.w->inter.p, 0, 1, nullptr, s.w->F.p, H, tw0);
+        k2_cols_sum<L0, -1, CX><<<col_blocks, CC::THREADS, col_smem, st>>>(ws_as<CX>(s.w->inter), 0, 1, nullptr, ws_as<CX>(s.w->F), H, tw0);
         check_launch("k2_cols_sum");
     }
-    const double scale = 1.0 / static_cast<double>(s.nreal);
+    const RealOf<CX> scale = RealOf<CX>(1.0 / static_cast<double>(s.nreal));
     int slot0 = 0;
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         const int groups = (cb + cfg.G - 1) / cfg.G;
         {
             LaunchScope ls(s, "f2_cols_dec", st, cb);
-            k2_cols_dec<L0><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
-                s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0);
+            k2_cols_dec<L0, CX><<<dim3(col_blocks, groups), CC::THREADS, col2_smem, st>>>(
+                ws_as<CX>(s.w->F), Prec2D<CX>::psiT(s), nhT, ws_as<CX>(s.w->inter), nhT, H, s.lo + b0, cfg.G, cb, tw0);
             check_launch("k2_cols_dec");
         }
         {
             LaunchScope ls(s, "f2_rows_fused", st, cb);
-            launch_rows_fused<L1>(dim3(row_blocks, cb), row_smem, st, s.w->inter.p, nhT,
+            launch_rows_fused<L1, CX>(dim3(row_blocks, cb), row_smem, st, ws_as<CX>(s.w->inter), nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
                                   delta, s.lo + b0, tw1, 0, 0);
         }
@@ -186,16 +187,16 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
             LaunchScope ls(s, "f2_cols_rec", st, cb);
             // the last chunk's CTAs also finish the reconstruction (k2_cols_rec)
             const bool fin = b0 + cb >= nb;
-            k2_cols_rec<L0><<<dim3(col_blocks, groups), CC::THREADS, colrec_smem_bytes<L0>(), st>>>(
-                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
-                fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p);
+            k2_cols_rec<L0, CX><<<dim3(col_blocks, groups), CC::THREADS, colrec_smem_bytes<L0, CX>(), st>>>(
+                ws_as<CX>(s.w->inter), nhT, Prec2D<CX>::psiT(s), nhT, ws_as<CX>(s.w->slots), nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
+                fin ? s.w->done.p : nullptr, nslots, Prec2D<CX>::WT(s), ws_as<CX>(s.w->inter));
             check_launch("k2_cols_rec");
         }
         slot0 += groups;
     }
     {
         LaunchScope ls(s, "f2_rows_c2r", st, 1);
-        k2_rows_c2r<L1><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(s.w->inter.p, 0, out, 0, n0, H, scale,
+        k2_rows_c2r<L1, CX><<<dim3(row_blocks, 1), RC::THREADS, row_smem, st>>>(ws_as<CX>(s.w->inter), 0, out, 0, n0, H, scale,
                                                                             nullptr, 0, tw1);
         check_launch("k2_rows_c2r");
     }
@@ -205,9 +206,9 @@ static void denoise2d_fast_t(System& s, const double* f, double* stack, double* 
 // launch per pass covering every frame (blockIdx.z), so each band's psi is read
 // once from HBM for all frames (L2 hits for the rest) and launches/tails are
 // amortised over the batch. Per-frame stacks at stack + f * sfs.
-template <int L0, int L1>
-static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, int nf, double* stack, long long sfs,
-                                   double* out, long long ofs, const double* delta, cudaStream_t st) {
+template <int L0, int L1, class CX = double2>
+static void denoise2d_fast_batch_t(System& s, const RealOf<CX>* f, long long ffs, int nf, RealOf<CX>* stack,
+                                   long long sfs, RealOf<CX>* out, long long ofs, const double* delta, cudaStream_t st) {
     const int n0 = s.n[0], H = s.H;
     const long long nhT = static_cast<long long>(H) * n0;
     const Fast2DCfg cfg = fast2d_cfg(s);
@@ -220,18 +221,18 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
     for (int b0 = 0; b0 < nb; b0 += C) nslots += (std::min(C, nb - b0) + cfg.G - 1) / cfg.G;
     const long long szs = static_cast<long long>(nslots) * nhT;
     s.w->slots.alloc(static_cast<size_t>(nf) * szs);
-    const double2* tw0 = s.plan(L0, st).tw;
-    const double2* tw1 = s.plan(L1, st).tw;
+    const CX* tw0 = Prec2D<CX>::tw(s.plan(L0, st));
+    const CX* tw1 = Prec2D<CX>::tw(s.plan(L1, st));
     using RC = RowCfg<L1>;
     using CC = ColCfg<L0>;
-    const size_t row_smem = row_smem_bytes<L1>(H);
-    const size_t col_smem = col1_smem_bytes<L0>();
-    const size_t col2_smem = coldec_smem_bytes<L0>();
-    set_smem(k2_rows_r2c<L1>, row_smem);
-    set_smem(k2_rows_c2r<L1>, row_smem);
-    set_smem(k2_cols_sum<L0, -1>, col_smem);
-    set_smem(k2_cols_dec<L0>, col2_smem);
-    set_smem(k2_cols_rec<L0>, colrec_smem_bytes<L0>());
+    const size_t row_smem = row_smem_bytes<L1, CX>(H);
+    const size_t col_smem = col1_smem_bytes<L0, CX>();
+    const size_t col2_smem = coldec_smem_bytes<L0, CX>();
+    set_smem(k2_rows_r2c<L1, CX>, row_smem);
+    set_smem(k2_rows_c2r<L1, CX>, row_smem);
+    set_smem(k2_cols_sum<L0, -1, CX>, col_smem);
+    set_smem(k2_cols_dec<L0, CX>, col2_smem);
+    set_smem(k2_cols_rec<L0, CX>, colrec_smem_bytes<L0, CX>());
     const int row_blocks = (n0 + 2 * RC::V - 1) / (2 * RC::V);
     const int col_blocks = (H + CC::LINES - 1) / CC::LINES;
     const size_t ndone = static_cast<size_t>(col_blocks) * nf;
@@ -241,45 +242,45 @@ static void denoise2d_fast_batch_t(System& s, const double* f, long long ffs, in
     }
     {  // F^T of every frame
         LaunchScope ls(s, "f2_rows_r2c", st, nf);
-        k2_rows_r2c<L1><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(f, ffs, s.w->inter.p, izs, n0, H, tw1);
+        k2_rows_r2c<L1, CX><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(f, ffs, ws_as<CX>(s.w->inter), izs, n0, H, tw1);
         check_launch("k2_rows_r2c");
     }
     {
         LaunchScope ls(s, "f2_cols_fwd", st, nf);
-        k2_cols_sum<L0, -1><<<dim3(col_blocks, 1, nf), CC::THREADS, col_smem, st>>>(s.w->inter.p, 0, 1, nullptr,
-                                                                                  s.w->F.p, H, tw0, izs, nhT);
+        k2_cols_sum<L0, -1, CX><<<dim3(col_blocks, 1, nf), CC::THREADS, col_smem, st>>>(ws_as<CX>(s.w->inter), 0, 1, nullptr,
+                                                                                  ws_as<CX>(s.w->F), H, tw0, izs, nhT);
         check_launch("k2_cols_sum");
     }
-    const double scale = 1.0 / static_cast<double>(s.nreal);
+    const RealOf<CX> scale = RealOf<CX>(1.0 / static_cast<double>(s.nreal));
     int slot0 = 0;
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         const int groups = (cb + cfg.G - 1) / cfg.G;
         {
             LaunchScope ls(s, "f2_cols_dec", st, static_cast<long long>(cb) * nf);
-            k2_cols_dec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, col2_smem, st>>>(
-                s.w->F.p, s.psiT.p, nhT, s.w->inter.p, nhT, H, s.lo + b0, cfg.G, cb, tw0, nhT, izs);
+            k2_cols_dec<L0, CX><<<dim3(col_blocks, groups, nf), CC::THREADS, col2_smem, st>>>(
+                ws_as<CX>(s.w->F), Prec2D<CX>::psiT(s), nhT, ws_as<CX>(s.w->inter), nhT, H, s.lo + b0, cfg.G, cb, tw0, nhT, izs);
             check_launch("k2_cols_dec");
         }
         {
             LaunchScope ls(s, "f2_rows_fused", st, static_cast<long long>(cb) * nf);
-            launch_rows_fused<L1>(dim3(row_blocks, cb, nf), row_smem, st, s.w->inter.p, nhT,
+            launch_rows_fused<L1, CX>(dim3(row_blocks, cb, nf), row_smem, st, ws_as<CX>(s.w->inter), nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
                                   delta, s.lo + b0, tw1, izs, sfs);
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, static_cast<long long>(cb) * nf);
             const bool fin = b0 + cb >= nb;
-            k2_cols_rec<L0><<<dim3(col_blocks, groups, nf), CC::THREADS, colrec_smem_bytes<L0>(), st>>>(
-                s.w->inter.p, nhT, s.psiT.p, nhT, s.w->slots.p, nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
-                fin ? s.w->done.p : nullptr, nslots, s.WT.p, s.w->inter.p, izs, szs, izs);
+            k2_cols_rec<L0, CX><<<dim3(col_blocks, groups, nf), CC::THREADS, colrec_smem_bytes<L0, CX>(), st>>>(
+                ws_as<CX>(s.w->inter), nhT, Prec2D<CX>::psiT(s), nhT, ws_as<CX>(s.w->slots), nhT, H, s.lo + b0, cfg.G, cb, slot0, tw0,
+                fin ? s.w->done.p : nullptr, nslots, Prec2D<CX>::WT(s), ws_as<CX>(s.w->inter), izs, szs, izs);
             check_launch("k2_cols_rec");
         }
         slot0 += groups;
     }
     {
         LaunchScope ls(s, "f2_rows_c2r", st, nf);
-        k2_rows_c2r<L1><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(s.w->inter.p, izs, out, ofs, n0, H,
+        k2_rows_c2r<L1, CX><<<dim3(row_blocks, nf), RC::THREADS, row_smem, st>>>(ws_as<CX>(s.w->inter), izs, out, ofs, n0, H,
                                                                              scale, nullptr, 0, tw1);
         check_launch("k2_rows_c2r");
     }
@@ -293,6 +294,16 @@ static void denoise2d_fast_batch(System& s, const double* f, long long ffs, int 
 static void denoise2d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
                            cudaStream_t st) {
     SLB_FAST2D_DISPATCH(denoise2d_fast_t, s, f, stack, out, delta, st)
+}
+
+// fp32 mode (sl_system_set_precision(32)): the same passes on float2 spectra
+static void denoise2d_fast_f32(System& s, const float* f, float* stack, float* out, const double* delta,
+                               cudaStream_t st) {
+    SLB_FAST2D_DISPATCH_F32(denoise2d_fast_t, s, f, stack, out, delta, st)
+}
+static void denoise2d_fast_batch_f32(System& s, const float* f, long long ffs, int nf, float* stack, long long sfs,
+                                     float* out, long long ofs, const double* delta, cudaStream_t st) {
+    SLB_FAST2D_DISPATCH_F32(denoise2d_fast_batch_t, s, f, ffs, nf, stack, sfs, out, ofs, delta, st)
 }
 
 }  // namespace slb

@@ -4,7 +4,8 @@
 // complex values in registers. Thread t holds elements t + T*m (m < E) both on
 // entry and on exit, so global loads/stores of a line are coalesced across
 // the T threads without any staging. Between radix stages the line goes
-// through a private shared-memory buffer of L double2 with an XOR swizzle
+// through a private shared-memory buffer of L complex values (double2 in
+// the fp64 path, float2 in the fp32 mode) with an XOR swizzle
 // (e ^ ((e >> 3) & 7)) that makes both the strided Stockham writes and the
 // contiguous reads bank-conflict free; lines of T <= 32 threads synchronise
 // with __syncwarp, wider lines with a named barrier per line.
@@ -102,15 +103,16 @@ __device__ __forceinline__ void line_sync() {
 }
 
 // radix-16 = 4 x 4 with internal twiddles w16^{n1 k2}
-template <int DIR>
-__device__ __forceinline__ void bfly16(double2* a) {
-    constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173, r2 = 0.70710678118654752440;
+template <int DIR, class C>
+__device__ __forceinline__ void bfly16(C* a) {
+    using Rl = RealOf<C>;
+    constexpr Rl c1 = Rl(0.92387953251128675613), s1 = Rl(0.38268343236508977173), r2 = Rl(0.70710678118654752440);
     // stage 1: four radix-4 over n2 (stride 4), n1 = 0..3
 #pragma unroll
     for (int n1 = 0; n1 < 4; ++n1) bfly4<DIR>(a[n1], a[n1 + 4], a[n1 + 8], a[n1 + 12]);
     // a[n1 + 4 k1] now holds sum_n2 x[n1 + 4 n2] w4^{n2 k1}; twiddle by w16^{n1 k1}
-    auto tw = [](double2 v, double c, double s) {  // v * (c + DIR i s)
-        return make_double2(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
+    auto tw = [](C v, Rl c, Rl s) {  // v * (c + DIR i s)
+        return mkc<C>(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
     };
     a[5] = tw(a[5], c1, s1);     // n1=1,k1=1: w^1
     a[9] = tw(a[9], r2, r2);     // n1=1,k1=2: w^2
@@ -122,10 +124,10 @@ __device__ __forceinline__ void bfly16(double2* a) {
     a[11] = tw(a[11], -r2, r2);  // n1=3,k1=2: w^6
     a[15] = tw(a[15], -c1, -s1); // n1=3,k1=3: w^9
     // stage 2: radix-4 over n1 for each k1; output index k1 + 4 k2
-    double2 o[16];
+    C o[16];
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
-        double2 b0 = a[4 * k1], b1 = a[4 * k1 + 1], b2 = a[4 * k1 + 2], b3 = a[4 * k1 + 3];
+        C b0 = a[4 * k1], b1 = a[4 * k1 + 1], b2 = a[4 * k1 + 2], b3 = a[4 * k1 + 3];
         bfly4<DIR>(b0, b1, b2, b3);
         o[k1] = b0;
         o[k1 + 4] = b1;
@@ -138,24 +140,26 @@ __device__ __forceinline__ void bfly16(double2* a) {
 
 // radix-12 = 4 x 3: n = n1 + 3 n2, radix-4 over n2, twiddle w12^{n1 k1},
 // radix-3 over n1; output index k1 + 4 k2
-template <int DIR>
-__device__ __forceinline__ void bfly12(double2* a) {
-    constexpr double h = 0.86602540378443864676;  // sqrt(3)/2
+template <int DIR, class C>
+__device__ __forceinline__ void bfly12(C* a) {
+    using Rl = RealOf<C>;
+    constexpr Rl h = Rl(0.86602540378443864676);  // sqrt(3)/2
+    constexpr Rl half = Rl(0.5);
 #pragma unroll
     for (int n1 = 0; n1 < 3; ++n1) bfly4<DIR>(a[n1], a[n1 + 3], a[n1 + 6], a[n1 + 9]);
-    auto tw = [](double2 v, double c, double s) {  // v * (c + DIR i s)
-        return make_double2(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
+    auto tw = [](C v, Rl c, Rl s) {  // v * (c + DIR i s)
+        return mkc<C>(v.x * c - DIR * v.y * s, v.y * c + DIR * v.x * s);
     };
-    a[4] = tw(a[4], h, 0.5);      // n1=1,k1=1: w^1
-    a[7] = tw(a[7], 0.5, h);      // n1=1,k1=2: w^2
+    a[4] = tw(a[4], h, half);     // n1=1,k1=1: w^1
+    a[7] = tw(a[7], half, h);     // n1=1,k1=2: w^2
     a[10] = mul_di<DIR>(a[10]);   // n1=1,k1=3: w^3
-    a[5] = tw(a[5], 0.5, h);      // n1=2,k1=1: w^2
-    a[8] = tw(a[8], -0.5, h);     // n1=2,k1=2: w^4
-    a[11] = make_double2(-a[11].x, -a[11].y);  // n1=2,k1=3: w^6
-    double2 o[12];
+    a[5] = tw(a[5], half, h);     // n1=2,k1=1: w^2
+    a[8] = tw(a[8], -half, h);    // n1=2,k1=2: w^4
+    a[11] = mkc<C>(-a[11].x, -a[11].y);  // n1=2,k1=3: w^6
+    C o[12];
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) {
-        double2 b0 = a[3 * k1], b1 = a[3 * k1 + 1], b2 = a[3 * k1 + 2];
+        C b0 = a[3 * k1], b1 = a[3 * k1 + 1], b2 = a[3 * k1 + 2];
         bfly3<DIR>(b0, b1, b2);
         o[k1] = b0;
         o[k1 + 4] = b1;
@@ -167,9 +171,10 @@ __device__ __forceinline__ void bfly12(double2* a) {
 
 // radix-32 = radix-2 over two radix-16 halves (decimation in time):
 // X[k] = E[k] + w32^k O[k], X[k+16] = E[k] - w32^k O[k].
-template <int DIR>
-__device__ __forceinline__ void bfly32(double2* a) {
-    double2 e[16], o[16];
+template <int DIR, class C>
+__device__ __forceinline__ void bfly32(C* a) {
+    using Rl = RealOf<C>;
+    C e[16], o[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         e[i] = a[2 * i];
@@ -196,18 +201,18 @@ __device__ __forceinline__ void bfly32(double2* a) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         // w32^k = cos(2 pi k/32) + DIR i sin(2 pi k/32); sin(2 pi k/32) = cos(2 pi (8-k)/32)
-        const double cs = c[k];
-        const double sn = k <= 8 ? c[8 - k] : c[k - 8];
-        const double2 t = k == 0 ? o[0] : make_double2(o[k].x * cs - DIR * o[k].y * sn, o[k].y * cs + DIR * o[k].x * sn);
+        const Rl cs = Rl(c[k]);
+        const Rl sn = Rl(k <= 8 ? c[8 - k] : c[k - 8]);
+        const C t = k == 0 ? o[0] : mkc<C>(o[k].x * cs - DIR * o[k].y * sn, o[k].y * cs + DIR * o[k].x * sn);
         a[k] = cadd(e[k], t);
         a[k + 16] = csub(e[k], t);
     }
 }
 
 // Butterfly of radix R on x[q + B*r], r < R.
-template <int R, int DIR, int E>
-__device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
-    double2 v[R];
+template <int R, int DIR, int E, class C>
+__device__ __forceinline__ void bfly_strided(C (&x)[E], int q, int B) {
+    C v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = x[q + B * r];
     if constexpr (R == 2) {
@@ -229,7 +234,7 @@ __device__ __forceinline__ void bfly_strided(double2 (&x)[E], int q, int B) {
     for (int r = 0; r < R; ++r) x[q + B * r] = v[r];
 }
 
-template <int L, int DIR, int S, bool PAD>
+template <int L, int DIR, int S, bool PAD, class C = double2>
 struct RegStage {
     using P = RegPlan<L>;
     static constexpr int R = P::R[S];
@@ -239,7 +244,7 @@ struct RegStage {
     static constexpr int NS = plan_ns<L>(S);
     static_assert(E % R == 0, "radix must divide the per-thread element count");
 
-    __device__ __forceinline__ static void run(double2 (&x)[E], double2* sm, int t, const double2* __restrict__ tw) {
+    __device__ __forceinline__ static void run(C (&x)[E], C* sm, int t, const C* __restrict__ tw) {
 #pragma unroll
         for (int q = 0; q < B; ++q) {
             const int j = t + T * q;
@@ -248,8 +253,8 @@ struct RegStage {
                 // one table load per butterfly; w^2..w^(R-1) by complex products
                 // (error ~3 ulp, far inside the 1e-10 budget) instead of R-1
                 // loads through the L1 data pipe
-                const double2 w1 = twiddle<DIR>(tw, jm * (L / (NS * R)));
-                double2 wp[R];
+                const C w1 = twiddle<DIR>(tw, jm * (L / (NS * R)));
+                C wp[R];
                 wp[1] = w1;
 #pragma unroll
                 for (int r = 2; r < R; ++r) wp[r] = (r & 1) ? cmul(wp[r - 1], w1) : cmul(wp[r / 2], wp[r / 2]);
@@ -277,16 +282,15 @@ struct RegStage {
                 for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD>(j + r * (L / R2))];
             }
             line_sync<T>();
-            RegStage<L, DIR, S + 1, PAD>::run(x, sm, t, tw);
+            RegStage<L, DIR, S + 1, PAD, C>::run(x, sm, t, tw);
         }
     }
 };
 
 // In/out: x[m] = element t + T*m of the line. sm: the line's L-element buffer.
-template <int L, int DIR, bool PAD = true>
-__device__ __forceinline__ void reg_fft(double2 (&x)[RegPlan<L>::E], double2* sm, int t,
-                                        const double2* __restrict__ tw) {
-    RegStage<L, DIR, 0, PAD>::run(x, sm, t, tw);
+template <int L, int DIR, bool PAD = true, class C>
+__device__ __forceinline__ void reg_fft(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
+    RegStage<L, DIR, 0, PAD, C>::run(x, sm, t, tw);
 }
 
 }  // namespace slb
