@@ -64,7 +64,12 @@ def launches(path, out):
 
 # pass names bench.py reports -> kernel whose grid y counts the bands of a launch
 PASS_KERNEL = {"f2_rows_fused": "k2_rows_fused", "f3_rows_fused": "k2_rows_fused",
-               "f2_rows_c2r_thr": "k2_rows_c2r", "f3_axis1": "k3_lines_contig"}
+               "f2_cols_dec": "k2_cols_dec", "f2_cols_rec": "k2_cols_rec",
+               "f2_rows_c2r_thr": "k2_rows_c2r", "f3_axis1": "k3_lines_contig",
+               "f3s_dec": "k3s_dec", "f3s_mid": "k3s_mid", "f3s_rec": "k3s_rec"}
+# kernels whose grid y is not the band count of the launch: bands per launch
+# of the capture driver (tools/prof3d.py: a 12-band shard in one chunk)
+BANDS_OVERRIDE = {"k3s_dec": 12, "k3s_rec": 12}
 
 
 def traffic(rep, out, config):
@@ -81,7 +86,7 @@ def traffic(rep, out, config):
     per_kernel = {}
     for r in rows[2:]:
         k = r[h.index("Kernel Name")].split("<")[0].replace("void ", "")
-        gy = int(r[h.index("launch__grid_dim_y")])
+        gy = BANDS_OVERRIDE.get(k, int(r[h.index("launch__grid_dim_y")]))
         b = col(r, "dram__bytes_read.sum") + col(r, "dram__bytes_write.sum")
         per_kernel.setdefault(k, []).append(b / max(gy, 1))
     doc = json.load(open(out)) if os.path.exists(out) else {}
