@@ -96,9 +96,25 @@ static void denoise_dist(System& s, sl_comm& c, const double* in, double* out, i
         stk = s.stack.p;
     }
     if (s.fast3d && s.knobs.split3d && !s.knobs.denoise_unfused) {
-        denoise3d_fast(s, s.io_in.p, stk, nullptr, s.delta.p, st);  // stops at the accumulator
-        const size_t na = s.w->acc.n;
-        SL_NCCL(api.reduce(s.w->acc.p, s.w->acc.p, 2 * na, ncclFloat64, ncclSum, root, c.comm, st));
+        // the accumulator slab [k2lo, k2hi) is final once the last chunk's pass C
+        // has covered it: its ncclReduce runs on the communication stream while
+        // pass C works on the next slab (chunked reduce overlapping the last band group)
+        s.ensure_workspaces(2);
+        if (!s.comm_ev.size()) s.ensure_comm_events(8);
+        cudaStream_t cs = s.ws[1]->st;
+        const long long plane = static_cast<long long>(s.n[0]) * s.n[1];  // double2 per k2 plane (natural layout)
+        int slab = 0;
+        denoise3d_split_acc(s, s.io_in.p, stk, s.delta.p, st, [&](int k2lo, int k2hi) {
+            cudaEvent_t ev = s.comm_ev[static_cast<size_t>(slab++ % 8)];
+            SL_CUDA(cudaEventRecord(ev, st));
+            SL_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+            double2* a = s.w->acc.p + k2lo * plane;
+            SL_NCCL(api.reduce(a, a, static_cast<size_t>(2 * (k2hi - k2lo) * plane), ncclFloat64, ncclSum, root,
+                               c.comm, cs));
+        });
+        cudaEvent_t done = s.comm_ev[static_cast<size_t>(slab % 8)];
+        SL_CUDA(cudaEventRecord(done, cs));
+        SL_CUDA(cudaStreamWaitEvent(st, done, 0));
         if (c.rank == root) finish3d_fast(s, out, st);
         return;
     }

@@ -252,6 +252,7 @@ struct System {
     cudaEvent_t fork_ev = nullptr;
     cudaEvent_t last_ev = nullptr;  // completion of the previous call on this handle (any stream)
     std::vector<cudaEvent_t> pipe_ev;  // per-frame H2D / compute-done events of pipelined host batches
+    std::vector<cudaEvent_t> comm_ev;  // slab-ready events of the overlapped multi-GPU reduce
     DBuf<double> delta, stack, io_in, io_out;
     std::vector<double> delta_host;  // host copy of `delta` (deltas() skips unchanged uploads)
     int chunk = 1;
@@ -284,6 +285,7 @@ struct System {
         if (fork_ev) cudaEventDestroy(fork_ev);
         if (last_ev) cudaEventDestroy(last_ev);
         for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+        for (cudaEvent_t e : comm_ev) cudaEventDestroy(e);
     }
     // Ensure n workspaces exist (1..n-1 with their own non-blocking streams).
     void ensure_pipe_events(size_t n) {
@@ -291,6 +293,13 @@ struct System {
             cudaEvent_t e;
             SL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             pipe_ev.push_back(e);
+        }
+    }
+    void ensure_comm_events(size_t n) {
+        while (comm_ev.size() < n) {
+            cudaEvent_t e;
+            SL_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            comm_ev.push_back(e);
         }
     }
     void ensure_workspaces(int n) {

@@ -1,5 +1,6 @@
 // Host orchestration of the specialised 3D path (kernels in fast3d.cuh).
 #pragma once
+#include <functional>
 #include "fast2d_host.cuh"
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
@@ -216,11 +217,12 @@ struct Split3DLaunch {
                                                                     tw);
         check_launch("k3s_mid");
     }
-    void rec(const double2* Z, double2* acc, int nb, int band0, int accumulate) {
+    void rec(const double2* Z, double2* acc, int nb, int band0, int accumulate, int k2lo = 0, int k2hi = -1) {
         set_smem(k3s_rec<n>, S::AC_SMEM);
+        if (k2hi < 0) k2hi = S::H;
         LaunchScope ls(s, "f3s_rec", st, nb);
-        k3s_rec<n><<<dim3(S::H * S::Q, 1), S::AC_THREADS, S::AC_SMEM, st>>>(Z, nT, acc, nb, s.synth, band0, accumulate,
-                                                                          tw);
+        k3s_rec<n><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, S::AC_SMEM, st>>>(
+            Z, nT, acc, nb, s.synth, band0, accumulate, tw, k2lo * S::Q);
         check_launch("k3s_rec");
     }
 };
@@ -244,10 +246,14 @@ static void finish_rec(Fast3DLaunch<n>& K, System& s, double* out) {
 
 // fused denoise of this handle's bands up to the half-spectrum accumulator
 // sum_b FFT(thr(band_b)) psi_b in s.w->acc (natural layout); out = null stops
-// there (the distributed path reduces the accumulators across ranks first)
+// there (the distributed path reduces the accumulators across ranks first).
+// slab_done(k2lo, k2hi), when set, runs after the last chunk's pass C has been
+// issued for the accumulator slab [k2lo, k2hi) -- the slab is final on this
+// rank from that point of the stream on (the multi-GPU reduce overlaps the rest)
+using SlabHook = std::function<void(int, int)>;
 template <int n>
 static void denoise3d_split_t(System& s, const double* f, double* stack, double* out, const double* delta,
-                              cudaStream_t st) {
+                              cudaStream_t st, const SlabHook& slab_done = nullptr) {
     Fast3DLaunch<n> K(s, st);
     Split3DLaunch<n> S3(s, st);
     const int nb = s.nb();
@@ -260,7 +266,16 @@ static void denoise3d_split_t(System& s, const double* f, double* stack, double*
         double* sb = stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr;
         S3.dec(s.w->F.p, s.w->inter.p, cb, s.lo + b0);
         S3.template mid<kMidFused>(s.w->inter.p, sb, nullptr, cb, delta, s.lo + b0);
-        S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+        if (slab_done && b0 + cb >= nb) {
+            constexpr int kSlabs = 4;
+            for (int j = 0; j < kSlabs; ++j) {
+                const int lo = SplitShape<n>::H * j / kSlabs, hi = SplitShape<n>::H * (j + 1) / kSlabs;
+                S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, lo, hi);
+                slab_done(lo, hi);
+            }
+        } else {
+            S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+        }
     }
     if (out) finish_rec<n>(K, s, out);
 }
@@ -330,6 +345,18 @@ static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_
 }
 
 static void finish3d_fast(System& s, double* out, cudaStream_t st) { SLB_FAST3D_DISPATCH(finish3d_t, s, out, st) }
+
+// the distributed variant: stop at the accumulator, calling slab_done per slab
+static void denoise3d_split_acc(System& s, const double* f, double* stack, const double* delta, cudaStream_t st,
+                                const SlabHook& slab_done) {
+    switch (s.n[0]) {
+        case 64: denoise3d_split_t<64>(s, f, stack, nullptr, delta, st, slab_done); break;
+        case 128: denoise3d_split_t<128>(s, f, stack, nullptr, delta, st, slab_done); break;
+        case 192: denoise3d_split_t<192>(s, f, stack, nullptr, delta, st, slab_done); break;
+        case 256: denoise3d_split_t<256>(s, f, stack, nullptr, delta, st, slab_done); break;
+        default: throw SlError(SL_ERR_GENERIC, "fast3d: unsupported size");
+    }
+}
 
 static void denoise3d_fast(System& s, const double* f, double* stack, double* out, const double* delta,
                            cudaStream_t st) {

@@ -262,11 +262,12 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
 template <int L>
 __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_MINB)
     k3s_rec(const double2* __restrict__ Z, long long zbs, double2* __restrict__ acc, int nbands, FiltSynth3D filt,
-            int band0, int accumulate, const double2* __restrict__ tw) {
+            int band0, int accumulate, const double2* __restrict__ tw, int bx0 = 0) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
     extern __shared__ double2 tile[];  // [n][LD]; the P line buffers alias it
-    const int k2 = blockIdx.x / Q, q = blockIdx.x - k2 * Q;
+    const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
+    const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
     double2* lb = tile + p * LineBuf<L, false>::N;
