@@ -65,6 +65,11 @@ struct RowCfg {
     static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
 #endif
     static constexpr int THREADS = V * T;
+#ifndef SLB_ROWS_PAD
+    static constexpr bool PAD = false;  // padded line buffers in the fused rows kernel (A/B: -DSLB_ROWS_PAD=1)
+#else
+    static constexpr bool PAD = SLB_ROWS_PAD;
+#endif
 #ifndef SLB_FUSED_MINB
     // explicit occupancy targets (measured): without them ptxas takes 124-154
     // registers; 4 CTAs/SM (<= 64 registers) except 192 (12 CTAs of 64 threads,
@@ -95,7 +100,7 @@ struct ColCfg {
 template <int L, class C = double2>
 static size_t row_smem_bytes(int H) {  // [H][2V] tile; V padded line buffers alias it
     using RC = RowCfg<L>;
-    return std::max(static_cast<size_t>(2 * RC::V) * H, static_cast<size_t>(RC::V) * LineBuf<L, false>::N) * sizeof(C);
+    return std::max(static_cast<size_t>(2 * RC::V) * H, static_cast<size_t>(RC::V) * LineBuf<L, RC::PAD>::N) * sizeof(C);
 }
 template <int L, class C = double2>
 static size_t col1_smem_bytes() {  // one padded exchange buffer per line

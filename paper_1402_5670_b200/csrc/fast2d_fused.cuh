@@ -64,8 +64,9 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         }
     }
     __syncthreads();              // every line has gathered: the tile is dead
-    C* lb = tile + q * LineBuf<L, false>::N;   // line buffers alias it (smem sized for both)
-    reg_fft<L, +1, false>(x, lb, t, tw);
+    constexpr bool PAD = RowCfg<L>::PAD;
+    C* lb = tile + q * LineBuf<L, PAD>::N;   // line buffers alias it (smem sized for both)
+    reg_fft<L, +1, PAD>(x, lb, t, tw);
     const double dl = delta[band0 + blockIdx.y];
     const int ra = r0 + 2 * q;
 #pragma unroll
@@ -82,17 +83,17 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         }
         x[m] = mkc<C>(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : R(0));  // rec input: the thresholded rows
     }
-    reg_fft<L, -1, false>(x, lb, t, tw);
+    reg_fft<L, -1, PAD>(x, lb, t, tw);
 #pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
+    for (int m = 0; m < E; ++m) lb[swz<PAD>(t + T * m)] = x[m];
     line_sync<T>();
     C zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            zk[u] = lb[swz<false>(k)];
-            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
+            zk[u] = lb[swz<PAD>(k)];
+            zm[u] = lb[swz<PAD>(k == 0 ? 0 : L - k)];
         }
     }
     __syncthreads();  // all line buffers read before the tile is rewritten

@@ -44,6 +44,12 @@ struct SplitCfg<256> {
     static constexpr int P = 16, Q = 16;
 };
 
+// padded line buffers (e + e/8: conflict-free strided Stockham stores) in the
+// FFT exchanges of the split kernels; the tiles they alias grow to fit
+#ifndef SLB_SPLIT_PAD
+#define SLB_SPLIT_PAD 0
+#endif
+
 template <int L>
 struct SplitShape {
     static constexpr int T = RegPlan<L>::T, P = SplitCfg<L>::P, Q = SplitCfg<L>::Q;
@@ -51,8 +57,10 @@ struct SplitShape {
     static constexpr int AC_THREADS = P * T;         // passes A / C: P axis-0 lines
     static constexpr int B_THREADS = Q * T;          // pass B: Q pair-lines = 2Q rows
     static constexpr int H = L / 2 + 1;
-    static constexpr size_t AC_SMEM = static_cast<size_t>(L) * LD * sizeof(double2);
-    static constexpr size_t B_SMEM = static_cast<size_t>((H * 2 * Q > Q * L) ? H * 2 * Q : Q * L) * sizeof(double2);
+    static constexpr bool PAD = SLB_SPLIT_PAD;
+    static constexpr int LB = LineBuf<L, PAD>::N;    // line buffer stride (double2)
+    static constexpr size_t AC_SMEM = static_cast<size_t>((L * LD > P * LB) ? L * LD : P * LB) * sizeof(double2);
+    static constexpr size_t B_SMEM = static_cast<size_t>((H * 2 * Q > Q * LB) ? H * 2 * Q : Q * LB) * sizeof(double2);
 #ifndef SLB_SPLIT_AC_MINB
     static constexpr int AC_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 4);
 #else
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
 #pragma unroll
         for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
     }
-    double2* lb = tile + p * LineBuf<L, false>::N;
+    double2* lb = tile + p * S::LB;
     for (int bb = 0; bb < gn; ++bb) {
         const BandDesc3D bd = filt.bands[band0 + g0 + bb];
         const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
@@ -111,7 +119,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
             x[m] = make_double2(f.x * ps, f.y * ps);
         }
         if (bb > 0) __syncthreads();  // the previous band's tile is copied out
-        reg_fft<L, +1, false>(x, lb, t, tw);
+        reg_fft<L, +1, S::PAD>(x, lb, t, tw);
         __syncthreads();  // every line is done with the aliased buffers
 #pragma unroll
         for (int m = 0; m < E; ++m) tile[(t + T * m) * LD + p] = x[m];
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
     double2* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
-    double2* lb = tile + lq * LineBuf<L, false>::N;
+    double2* lb = tile + lq * S::LB;
     double2 x[E];
     if constexpr (MODE != kMidRec) {
         for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
@@ -195,7 +203,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
             }
         }
         __syncthreads();  // the tile becomes the line buffers
-        reg_fft<L, +1, false>(x, lb, t, tw);
+        reg_fft<L, +1, S::PAD>(x, lb, t, tw);
         const double dl = delta ? delta[band0 + bi] : -1.0;
         double* r0p = band + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
 #pragma unroll
@@ -218,17 +226,17 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
         for (int m = 0; m < E; ++m) x[m] = make_double2(__ldg(r0p + t + T * m), __ldg(r0p + n + t + T * m));
     }
     // axis-2 r2c of the row pair (as k2_rows_r2c)
-    reg_fft<L, -1, false>(x, lb, t, tw);
+    reg_fft<L, -1, S::PAD>(x, lb, t, tw);
 #pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
+    for (int m = 0; m < E; ++m) lb[swz<S::PAD>(t + T * m)] = x[m];
     line_sync<T>();
     double2 zk[KPT], zm[KPT];
 #pragma unroll
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            zk[u] = lb[swz<false>(k)];
-            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
+            zk[u] = lb[swz<S::PAD>(k)];
+            zm[u] = lb[swz<S::PAD>(k == 0 ? 0 : L - k)];
         }
     }
     __syncthreads();  // all line buffers read before the tile is rewritten
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
-    double2* lb = tile + p * LineBuf<L, false>::N;
+    double2* lb = tile + p * S::LB;
     double2 ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) ar[m] = make_double2(0.0, 0.0);
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
         const BandDesc3D bd = filt.bands[band0 + b];
         const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
-        reg_fft<L, -1, false>(x, lb, t, tw);
+        reg_fft<L, -1, S::PAD>(x, lb, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const double ps = fline.at(t + T * m);
