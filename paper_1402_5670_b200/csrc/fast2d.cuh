@@ -17,6 +17,11 @@
 
 #include "fft_reg.cuh"
 
+// r2c mirror pairs by warp shuffles where a line fits one warp segment (T <= 32)
+#ifndef SLB_ROWS_SHFL
+#define SLB_ROWS_SHFL 1
+#endif
+
 namespace slb {
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -121,6 +126,11 @@ struct ColRec {
 #else
     static constexpr bool REGACC = SLB_COLREC_REGACC;
 #endif
+#ifndef SLB_COLREC_PF
+    static constexpr bool PF = false;  // register prefetch of the next band (A/B)
+#else
+    static constexpr bool PF = SLB_COLREC_PF;
+#endif
 };
 template <int L, class C = double2>
 static size_t colrec_smem_bytes() {  // register accumulator: exchange buffers only
@@ -217,17 +227,22 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     }
     C* lb = tile + q * LineBuf<L, false>::N;  // line buffers alias the (not yet used) output tile
     reg_fft<L, -1, false>(x, lb, t, tw);
-    // Z in registers (element t + T m); publish to the line buffer, then split
-#pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
-    line_sync<T>();
+    // Z in registers (element t + T m); mirror pairs by warp shuffles, or
+    // through the line buffer for lines wider than a warp
     C zk[KPT], zm[KPT];
+    if constexpr (T <= 32 && SLB_ROWS_SHFL) {
+        mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);
+    } else {
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            zk[u] = lb[swz<false>(k)];
-            zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
+        for (int m = 0; m < E; ++m) lb[swz<false>(t + T * m)] = x[m];
+        line_sync<T>();
+#pragma unroll
+        for (int u = 0; u < KPT; ++u) {
+            const int k = t + T * u;
+            if (k < H) {
+                zk[u] = lb[swz<false>(k)];
+                zm[u] = lb[swz<false>(k == 0 ? 0 : L - k)];
+            }
         }
     }
     __syncthreads();  // all line buffers read before the tile is written
@@ -410,17 +425,48 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
+    // PF: band b+1's line and psi are loaded into registers while band b is in
+    // the FFT (the kernel is DRAM-latency bound at ~4 warps per scheduler)
+    constexpr bool PF = ColRec<L>::PF;
+    C xn[E];
+    R pn[E];
+    if (PF && gn > 0) {
+        const C* in = inter + (long long)g0 * ibs + (long long)k1 * L;
+        const R* ps = psiT + (long long)(band0 + g0) * pbs + (long long)k1 * L;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            xn[m] = valid ? __ldcg(in + t + T * m) : mkc<C>(0.0, 0.0);
+            pn[m] = valid ? __ldg(ps + t + T * m) : R(0);
+        }
+    }
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
         C x[E];
-        const C* in = inter + (long long)b * ibs + (long long)k1 * L;
-#pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : mkc<C>(0.0, 0.0);
-        // the band's psi is loaded before the FFT so its latency overlaps it
         R p[E];
-        const R* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+        if (PF) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
+            for (int m = 0; m < E; ++m) {
+                x[m] = xn[m];
+                p[m] = pn[m];
+            }
+            if (bb + 1 < gn) {
+                const C* in = inter + (long long)(b + 1) * ibs + (long long)k1 * L;
+                const R* ps = psiT + (long long)(band0 + b + 1) * pbs + (long long)k1 * L;
+#pragma unroll
+                for (int m = 0; m < E; ++m) {
+                    xn[m] = valid ? __ldcg(in + t + T * m) : mkc<C>(0.0, 0.0);
+                    pn[m] = valid ? __ldg(ps + t + T * m) : R(0);
+                }
+            }
+        } else {
+            const C* in = inter + (long long)b * ibs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) x[m] = valid ? __ldcg(in + t + T * m) : mkc<C>(0.0, 0.0);
+            // the band's psi is loaded before the FFT so its latency overlaps it
+            const R* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
+        }
         reg_fft<L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {

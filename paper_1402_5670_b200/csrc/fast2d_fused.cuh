@@ -84,16 +84,20 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         x[m] = mkc<C>(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : R(0));  // rec input: the thresholded rows
     }
     reg_fft<L, -1, PAD>(x, lb, t, tw);
-#pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<PAD>(t + T * m)] = x[m];
-    line_sync<T>();
     C zk[KPT], zm[KPT];
+    if constexpr (T <= 32 && SLB_ROWS_SHFL) {
+        mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
+    } else {
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            zk[u] = lb[swz<PAD>(k)];
-            zm[u] = lb[swz<PAD>(k == 0 ? 0 : L - k)];
+        for (int m = 0; m < E; ++m) lb[swz<PAD>(t + T * m)] = x[m];
+        line_sync<T>();
+#pragma unroll
+        for (int u = 0; u < KPT; ++u) {
+            const int k = t + T * u;
+            if (k < H) {
+                zk[u] = lb[swz<PAD>(k)];
+                zm[u] = lb[swz<PAD>(k == 0 ? 0 : L - k)];
+            }
         }
     }
     __syncthreads();  // all line buffers read before the tile is rewritten

@@ -227,16 +227,20 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     }
     // axis-2 r2c of the row pair (as k2_rows_r2c)
     reg_fft<L, -1, S::PAD>(x, lb, t, tw);
-#pragma unroll
-    for (int m = 0; m < E; ++m) lb[swz<S::PAD>(t + T * m)] = x[m];
-    line_sync<T>();
     double2 zk[KPT], zm[KPT];
+    if constexpr (T <= 32 && SLB_ROWS_SHFL) {
+        mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
+    } else {
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int k = t + T * u;
-        if (k < H) {
-            zk[u] = lb[swz<S::PAD>(k)];
-            zm[u] = lb[swz<S::PAD>(k == 0 ? 0 : L - k)];
+        for (int m = 0; m < E; ++m) lb[swz<S::PAD>(t + T * m)] = x[m];
+        line_sync<T>();
+#pragma unroll
+        for (int u = 0; u < KPT; ++u) {
+            const int k = t + T * u;
+            if (k < H) {
+                zk[u] = lb[swz<S::PAD>(k)];
+                zm[u] = lb[swz<S::PAD>(k == 0 ? 0 : L - k)];
+            }
         }
     }
     __syncthreads();  // all line buffers read before the tile is rewritten

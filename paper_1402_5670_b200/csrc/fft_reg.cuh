@@ -287,6 +287,26 @@ struct RegStage {
     }
 };
 
+// Mirror pairs of a line held in registers (x[m] = Z[t + T m] on the T lanes
+// of one warp segment, T <= 32): zk[u] = Z[k], zm[u] = Z[(L - k) mod L] for
+// k = t + T u, by warp shuffles instead of a shared-memory round trip --
+// (L - k) lives on lane (T - t) mod T at register E - 1 - u (lane 0: its own
+// register (E - u) mod E). The r2c split of pair-packed rows needs exactly these.
+template <int L, int T, int E, int KPT, class C>
+__device__ __forceinline__ void mirror_pairs_shfl(const C (&x)[E], C (&zk)[KPT], C (&zm)[KPT], int t) {
+    static_assert(T <= 32 && (T & (T - 1)) == 0 && T * E == L, "one power-of-two warp segment per line");
+    static_assert(KPT <= E, "split outputs within the line");
+    const int src = (T - t) & (T - 1);
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+        zk[u] = x[u];
+        C v;
+        v.x = __shfl_sync(0xffffffffu, x[E - 1 - u].x, src, T);
+        v.y = __shfl_sync(0xffffffffu, x[E - 1 - u].y, src, T);
+        zm[u] = t == 0 ? x[(E - u) % E] : v;
+    }
+}
+
 // In/out: x[m] = element t + T*m of the line. sm: the line's L-element buffer.
 template <int L, int DIR, bool PAD = true, class C>
 __device__ __forceinline__ void reg_fft(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
