@@ -152,6 +152,24 @@ def gen_banks():
     save("maxflat_fans", **{f"order{o}": ref.maxflat_fan(o)[0] for o in range(1, 7)})
 
 
+def gen_asym():
+    """An asymmetric fan (maxflat_fan(2) with its centre moved off the middle):
+    the filters are real in space but not centrally symmetric, so psi_hat is
+    complex (Hermitian) -- the reference stores full complex grids
+    (system2d.hpp:38) and accepts any fan (filters.hpp:64)."""
+    t, c0, c1 = ref.maxflat_fan(2)
+    fan = (t, c0 + 1, c1)
+    for n, lv, name in ((32, [0, 1], "bank_2d_32_asym"), (64, [0, 0, 1], "bank_2d_64_asym")):
+        s = ref.RefSystem2D(n, n, lv, fan=fan)
+        f = O.random_grid((n, n), 13 + n)
+        b = s.forward(f)
+        K = [2.0] * len(lv)
+        thr = s.hard_threshold(b, K, 0.2)
+        save(name, f=f, levels=np.array(lv), fan=t, fan_c=np.array([c0 + 1, c1]), index=s.index(),
+             filter_norms=s.filter_norms(), frame_weight=s.frame_weight(), bands=b, rec=s.inverse(b),
+             K=np.array(K), sigma=0.2, den=s.inverse(thr), filter1=s.filter(1))
+
+
 def gen_io():
     """PGM (8/16-bit) and SVOL bytes written by the reference (image_io.cpp:77-159)."""
     import tempfile
@@ -217,13 +235,16 @@ def gen_acceptance():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 128^3 / 192^3 fixtures")
-    ap.add_argument("--only", choices=["cfg2", "cfg5"], help="regenerate one timed-config fixture")
+    ap.add_argument("--only", choices=["cfg2", "cfg5", "asym"], help="regenerate one fixture")
     a = ap.parse_args()
     if not ref.available():
         sys.exit("build the reference first: make -C oracle ref")
     if a.only == "cfg2":
         noisy = ref.add_noise(ref.cartoon(512), 40.0, 7)
         gen_2d_stats("cfg2_denoise512_1122", 512, [1, 1, 2, 2], noisy, K=[2.5, 2.5, 2.5, 3.8], sigma=40.0)
+        return
+    if a.only == "asym":
+        gen_asym()
         return
     if a.only == "cfg5":
         noisy3 = ref.add_noise(ref.cartoon_volume(192), 40.0, 3)
@@ -284,6 +305,7 @@ def main():
     save("shcf_3d_8x12x10_0", levels=np.array([0]), bands=b3,
          shcf=np.frombuffer(ref.serialize(s3, b3), dtype=np.uint8))
     gen_banks()
+    gen_asym()
     gen_io()
     gen_descriptors()
     gen_quality()

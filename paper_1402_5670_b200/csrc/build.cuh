@@ -131,6 +131,27 @@ struct FiltTable2DGet {
     FiltTable2D t;
     __device__ __forceinline__ double get(int band, long long e) const { return t.get(band, e); }
 };
+// complex filter spectra (asymmetric fans)
+struct FiltTable2DCplx {
+    const double2* psi;
+    long long nhalf;
+    __device__ __forceinline__ double2 get(int band, long long e) const { return __ldg(psi + (long long)band * nhalf + e); }
+};
+// |psi| of complex spectra, for the W / RMS reductions (sum of |psi|^2)
+struct FiltTable2DAbs {
+    const double2* psi;
+    long long nhalf;
+    __device__ __forceinline__ double get(int band, long long e) const {
+        const double2 z = __ldg(psi + (long long)band * nhalf + e);
+        return sqrt(z.x * z.x + z.y * z.y);
+    }
+};
+// half complex spectrum (pad columns zeroed) into the complex table
+__global__ void k_take_complex(const double2* __restrict__ in, double2* __restrict__ out, long long nhalf, int ldh,
+                               int H) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nhalf; e += (long long)gridDim.x * blockDim.x)
+        out[e] = (e % ldh) >= H ? make_double2(0.0, 0.0) : in[e];
+}
 
 // [R][n0][ldh] row-major real halves -> [R][H][n0] column-major (fast 2D path)
 __global__ void k_half_to_colmajor(const double* __restrict__ in, double* __restrict__ out, int R, int n0, int H,
@@ -281,6 +302,7 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
     SL_CUDA(cudaMemsetAsync(mx.p, 0, 2 * static_cast<size_t>(s.R) * sizeof(unsigned long long), st));
     DQmf q(bank.qmf, st);
     const DTaps2 dfan = d_upload(bank.fan, st);
+    s.psiC.alloc(static_cast<size_t>(s.R) * s.nhalf);  // released again for real (symmetric) banks
     for (int i = 0; i < s.R; ++i) {
         const Record& r = s.index[static_cast<size_t>(i)];
         DTaps2 t;
@@ -296,27 +318,44 @@ static void build_2d(System& s, const Bank& bank, cudaStream_t st) {
         k_take_real<<<256, 256, 0, st>>>(spec.p, s.psi.p + static_cast<size_t>(i) * s.nhalf, s.nhalf, s.ldh, s.H,
                                          mx.p + 2 * i);
         check_launch("k_take_real");
+        k_take_complex<<<256, 256, 0, st>>>(spec.p, s.psiC.p + static_cast<size_t>(i) * s.nhalf, s.nhalf, s.ldh, s.H);
+        check_launch("k_take_complex");
     }
     int worst_i = -1;
     const double worst = worst_imag_ratio(mx, s.R, &worst_i, st);
-    if (worst > s.knobs.real_tol)
-        throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan; filter " + std::to_string(worst_i) +
-                                         " has |im|/|re| = " + std::to_string(worst) + "); unsupported by this build");
+    // centrally symmetric banks (every default and maxflat fan) have real
+    // spectra: real tables and the fast path. Asymmetric fans keep the
+    // complex (Hermitian) spectra the reference stores (system2d.hpp:38) and
+    // run the generic path.
+    s.cplx = worst > s.knobs.real_tol;
     s.W.alloc(static_cast<size_t>(s.nhalf));
-    k_weight2d<<<1024, 256, 0, st>>>(s.psi.p, s.R, s.nhalf, s.W.p);
-    check_launch("k_weight2d");
     const int nblk = 128;
     DBuf<double> part;
     part.alloc(static_cast<size_t>(s.R) * nblk);
-    FiltTable2DGet f{FiltTable2D{s.psi.p, s.nhalf}};
-    k_energy<<<dim3(nblk, s.R), 256, 0, st>>>(f, s.nhalf, s.ldh, s.H, s.L_last, part.p);
-    check_launch("k_energy");
+    if (s.cplx) {
+        FiltTable2DAbs fa{s.psiC.p, s.nhalf};
+        k_weight_synth<<<1024, 256, 0, st>>>(fa, s.R, s.nhalf, s.ldh, s.H, s.W.p);
+        check_launch("k_weight_synth");
+        k_energy<<<dim3(nblk, s.R), 256, 0, st>>>(fa, s.nhalf, s.ldh, s.H, s.L_last, part.p);
+        check_launch("k_energy");
+    } else {
+        k_weight2d<<<1024, 256, 0, st>>>(s.psi.p, s.R, s.nhalf, s.W.p);
+        check_launch("k_weight2d");
+        FiltTable2DGet f{FiltTable2D{s.psi.p, s.nhalf}};
+        k_energy<<<dim3(nblk, s.R), 256, 0, st>>>(f, s.nhalf, s.ldh, s.H, s.L_last, part.p);
+        check_launch("k_energy");
+    }
     std::vector<double> hp(static_cast<size_t>(s.R) * nblk);
     SL_CUDA(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
     SL_CUDA(cudaStreamSynchronize(st));
     finish_rms(s, hp.data(), nblk, s.R);
     finish_W(s, st);
-    if (fast2d_supported(s.knobs, s.n[0], s.n[1])) {
+    if (s.cplx) {
+        s.psi.release();
+    } else {
+        s.psiC.release();
+    }
+    if (!s.cplx && fast2d_supported(s.knobs, s.n[0], s.n[1])) {
         s.fast2d = true;
         s.psiT.alloc(static_cast<size_t>(s.R) * s.H * s.n[0]);
         s.WT.alloc(static_cast<size_t>(s.H) * s.n[0]);

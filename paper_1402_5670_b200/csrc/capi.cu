@@ -359,6 +359,26 @@ int sl_filter_spectrum(sl_system* h, int i, double* out) {
         DeviceGuard dg(s.device);
         CallOrder co(s, 0);
         std::vector<double> half(static_cast<size_t>(s.nhalf));
+        std::vector<double2> halfc;
+        if (s.ndim == 2 && s.cplx) {
+            // complex (Hermitian) spectrum of an asymmetric fan: psi(-xi) = conj(psi(xi))
+            halfc.resize(static_cast<size_t>(s.nhalf));
+            SL_CUDA(cudaMemcpy(halfc.data(), s.psiC.p + static_cast<size_t>(i) * s.nhalf, halfc.size() * sizeof(double2),
+                               cudaMemcpyDeviceToHost));
+            const long long rows = s.nrows;
+            const int L = s.L_last;
+            for (long long r = 0; r < rows; ++r) {
+                const long long rr = (s.n[0] - r) % s.n[0];
+                for (int k = 0; k < L; ++k) {
+                    const bool lo = k < s.H;
+                    const double2 z = lo ? halfc[static_cast<size_t>(r * s.ldh + k)]
+                                         : halfc[static_cast<size_t>(rr * s.ldh + (L - k))];
+                    out[2 * (r * L + k)] = z.x;
+                    out[2 * (r * L + k) + 1] = lo ? z.y : -z.y;
+                }
+            }
+            return;
+        }
         if (s.ndim == 2) {
             SL_CUDA(cudaMemcpy(half.data(), s.psi.p + static_cast<size_t>(i) * s.nhalf, half.size() * sizeof(double),
                                cudaMemcpyDeviceToHost));

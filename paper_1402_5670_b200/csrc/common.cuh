@@ -216,6 +216,10 @@ struct System {
 
     std::map<int, std::unique_ptr<PlanHolder>> plans;
     DBuf<double> psi;   // 2D: [R][nhalf] real
+    // asymmetric fans: complex (Hermitian) filter spectra [R][nhalf]; such a
+    // system runs the generic 2D path (the fast path assumes real filters)
+    bool cplx = false;
+    DBuf<double2> psiC;
     // 2D fast path (fast2d.cuh): column-major halves psi^T [R][H][n0], W^T [H][n0]
     bool fast2d = false;
     DBuf<double> psiT, WT;

@@ -232,6 +232,17 @@ struct LineGeom {
     long long nhalf;  // elements per spectrum (band stride)
 };
 
+// filter multiply of the generic lines pass: real (centrally symmetric
+// filters) or complex (asymmetric fans) spectra; the dec side takes conj(psi)
+template <bool CONJ>
+__device__ __forceinline__ double2 filt_mul(double2 z, double p) {
+    return cscale(z, p);
+}
+template <bool CONJ>
+__device__ __forceinline__ double2 filt_mul(double2 z, double2 p) {
+    return cmul(z, CONJ ? cconj(p) : p);
+}
+
 template <int DIR, int MODE, class Filt>
 __global__ void k_lines(const double2* __restrict__ src, long long src_bstride, double2* __restrict__ dst,
                         long long dst_bstride, LineGeom g, FftPlan p, int V, Filt filt, int band_base,
@@ -256,7 +267,7 @@ __global__ void k_lines(const double2* __restrict__ src, long long src_bstride, 
             const long long e = base + (long long)i * g.istride + v;
             z = src[e];
             if (MODE == kDecMul) {
-                z = cscale(z, filt.get(band, e));
+                z = filt_mul<true>(z, filt.get(band, e));
             } else if (MODE == kDivW) {
                 const double w = __ldg(W + e);
                 z = make_double2(z.x / w, z.y / w);
@@ -272,7 +283,7 @@ __global__ void k_lines(const double2* __restrict__ src, long long src_bstride, 
         if (c < g.cw && (c % g.ldh) < g.H) {
             const long long e = base + (long long)i * g.istride + v;
             double2 z = r[v * ld + i];
-            if (MODE == kRecMul) z = cscale(z, filt.get(band, e));
+            if (MODE == kRecMul) z = filt_mul<false>(z, filt.get(band, e));
             dst[e] = z;
         }
     }

@@ -104,7 +104,9 @@ static void dec(System& s, const double* f, double* out, const double* delta, cu
         return;
     }
     forward_spectrum(s, f, st);
-    if (s.ndim == 2)
+    if (s.ndim == 2 && s.cplx)
+        dec_bands(s, FiltTable2DCplx{s.psiC.p, s.nhalf}, out, delta, st);
+    else if (s.ndim == 2)
         dec_bands(s, FiltTable2DGet{FiltTable2D{s.psi.p, s.nhalf}}, out, delta, st);
     else
         dec_bands(s, FiltSynth3DFlat{s.synth, s.ldh}, out, delta, st);
@@ -120,7 +122,9 @@ static void rec(System& s, const double* coeffs, double* out, cudaStream_t st) {
         rec3d_fast(s, coeffs, out, st);
         return;
     }
-    if (s.ndim == 2)
+    if (s.ndim == 2 && s.cplx)
+        rec_bands(s, FiltTable2DCplx{s.psiC.p, s.nhalf}, coeffs, out, st);
+    else if (s.ndim == 2)
         rec_bands(s, FiltTable2DGet{FiltTable2D{s.psi.p, s.nhalf}}, coeffs, out, st);
     else
         rec_bands(s, FiltSynth3DFlat{s.synth, s.ldh}, coeffs, out, st);
