@@ -20,7 +20,7 @@ def test_asymmetric_fan_matches_reference(cuda, name):
     f = g["f"]
     n = f.shape[0]
     s = P.build_system_2d(n, n, P.ScaleProfile.from_levels(list(g["levels"])), fan=fan)
-    np.testing.assert_array_equal(s.index_records, g["index"])
+    np.testing.assert_array_equal(s.index_records[:, :3], g["index"])
     np.testing.assert_allclose(s.filter_norms, g["filter_norms"], rtol=1e-12)
     np.testing.assert_allclose(s.frame_weight, g["frame_weight"], rtol=1e-12, atol=1e-14)
     psi1 = s.filter_freq(1)

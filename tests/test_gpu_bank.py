@@ -55,10 +55,14 @@ def test_default_bank_equals_explicit(cuda):
     np.testing.assert_array_equal(P.forward(f, a), P.forward(f, b))
 
 
-def test_asymmetric_fan_rejected(cuda):
-    # the half-spectrum design needs real filter spectra; an off-centre fan is refused loudly
+def test_asymmetric_fan_2d_complex_3d_rejected(cuda):
+    # 2D keeps complex filter tables for an off-centre fan (tests/test_gpu_asym.py);
+    # the 3D factor tables assume real spectra, so 3D refuses it loudly
     fan = P.FanFilter(np.array([[0.0, 1.0, 0.5]]), 0, 0, "asym")
+    s = P.build_system_2d(32, 32, P.ScaleProfile.from_levels([0, 1]), fan=fan)
+    f = np.random.default_rng(1).uniform(-1, 1, (32, 32))
+    assert rel_l2(P.inverse(P.forward(f, s), s), f) <= 1e-10
     with pytest.raises(P.DomainError):
-        P.build_system_2d(32, 32, P.ScaleProfile.from_levels([0, 1]), fan=fan)
+        P.build_system_3d((16, 16, 16), P.ScaleProfile.from_levels([0, 1]), fan=fan)
     with pytest.raises(P.InvalidArgument):
         P.build_system_2d(32, 32, P.ScaleProfile.from_levels([0, 1]), fan=P.FanFilter(np.zeros((0, 3)), 0, 0))
