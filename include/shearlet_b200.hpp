@@ -31,6 +31,7 @@ struct UnsupportedSizeError : Error { using Error::Error; };
 struct DegenerateMaskError : Error { using Error::Error; };
 struct DegenerateTruthError : Error { using Error::Error; };
 struct CudaError : Error { using Error::Error; };
+struct NcclError : Error { using Error::Error; };
 
 inline void check(int rc) {
     if (rc == SL_OK) return;
@@ -46,6 +47,7 @@ inline void check(int rc) {
         case SL_ERR_DEGENERATE_MASK: throw DegenerateMaskError(m);
         case SL_ERR_DEGENERATE_TRUTH: throw DegenerateTruthError(m);
         case SL_ERR_CUDA: throw CudaError(m);
+        case SL_ERR_NCCL: throw NcclError(m);
         default: throw Error(m);
     }
 }
@@ -105,6 +107,8 @@ class ShearletSystem {
     std::size_t n_bands() const { return static_cast<std::size_t>(nb_); }
     std::size_t size() const { return ndim_ == 2 ? dims_[0] * dims_[1] : dims_[0] * dims_[1] * dims_[2]; }
     int ndim() const { return ndim_; }
+    /// optional fp32 mode (2D fast-path grids): prepares the float tables
+    void set_precision(int bits) const { check(sl_system_set_precision(h_.get(), bits)); }
     std::pair<double, double> frame_bounds() const {
         double a, b;
         check(sl_frame_bounds(h_.get(), &a, &b));
@@ -354,6 +358,47 @@ inline std::pair<double, int> quality_q_opt(const std::vector<double>& recovered
     check(sl_quality_q_opt(rows, cols, recovered.data(), truth.data(), g.taps.data(), g.size, g.size, g.center,
                            g.center, device, &q, &d, nullptr));
     return {q, d};
+}
+
+// ---- fused denoise returning the thresholded stack (host value semantics over
+// a device round trip is the _host entry points' job; this one takes device
+// pointers, as a caller already holding device buffers would)
+inline void denoise_with_stack_dev(const ShearletSystem& s, const double* d_in, double* d_stack, double* d_out,
+                                   const ThresholdSchedule& sch, void* stream = nullptr) {
+    check(sl_denoise_stack_dev(s.handle(), d_in, d_stack, d_out, sch.per_scale_factors.data(),
+                               static_cast<int>(sch.per_scale_factors.size()), sch.sigma,
+                               sch.scale_by_filter_norm ? 1 : 0, stream));
+}
+
+// ---- multi-GPU: one process per GPU, the library's own NCCL communicator
+class Comm {
+  public:
+    static std::vector<unsigned char> unique_id() {
+        std::vector<unsigned char> id(128);
+        check(sl_comm_unique_id(id.data()));
+        return id;
+    }
+    Comm(const std::vector<unsigned char>& id, int nranks, int rank, int device) : c_(nullptr, &sl_comm_destroy) {
+        if (id.size() != 128) throw ConfigError("Comm: the NCCL unique id has 128 bytes");
+        sl_comm* c = nullptr;
+        check(sl_comm_create(id.data(), nranks, rank, device, &c));
+        c_.reset(c);
+    }
+    sl_comm* handle() const { return c_.get(); }
+
+  private:
+    std::unique_ptr<sl_comm, int (*)(sl_comm*)> c_;
+};
+/// attach (shard_bands: 3D / single frames) or detach (comm = nullptr)
+inline void set_comm(const ShearletSystem& s, const Comm* comm, bool shard_bands = true) {
+    check(sl_system_set_comm(s.handle(), comm ? comm->handle() : nullptr, shard_bands ? 1 : 0));
+}
+/// sharded fused denoise; d_in read on the root, d_out written on the root
+inline void denoise_dist_dev(const ShearletSystem& s, const double* d_in, double* d_out, const ThresholdSchedule& sch,
+                             int root = 0, void* stream = nullptr) {
+    check(sl_denoise_dist_dev(s.handle(), d_in, d_out, sch.per_scale_factors.data(),
+                              static_cast<int>(sch.per_scale_factors.size()), sch.sigma,
+                              sch.scale_by_filter_norm ? 1 : 0, root, stream));
 }
 
 }  // namespace shearlet_b200
