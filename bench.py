@@ -546,19 +546,26 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
     return out
 
 
-def run_fp32(steps, warmup, local):
-    """The optional fp32 mode at the headline 2D config (reported separately,
-    never as the headline): the same lock-step 8-frame fused denoise with every
-    FFT pass in fp32 (sl_denoise_batch_f32_dev), device-timed like the fp64 line."""
+def run_fp32(name, steps, warmup, local):
+    """The optional fp32 mode (reported separately, never as the headline):
+    2D -- the same lock-step 8-frame fused denoise with every FFT pass in fp32
+    (sl_denoise_batch_f32_dev); 3D -- the fused denoise of one volume with the
+    three band passes in fp32 (sl_denoise_f32_dev). Device-timed like the
+    fp64 lines (L2 flushed between steps)."""
     import ctypes as C
     import torch
     import paper_1402_5670_b200 as P
-    cfg = CONFIGS["2d512"]
+    cfg = CONFIGS[name]
+    dims = cfg["dims"]
+    is3d = len(dims) == 3
     dev = torch.device("cuda", local)
-    s = P.build_system_2d(*cfg["dims"], P.ScaleProfile.from_levels(cfg["levels"]), device=local, dtype="f32")
+    prof = P.ScaleProfile.from_levels(cfg["levels"])
+    s = P.build_system_3d(dims, prof, device=local, dtype="f32") if is3d else \
+        P.build_system_2d(*dims, prof, device=local, dtype="f32")
     sch = schedule_for(P, cfg)
-    frames = cfg["batch"]
-    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(512), cfg["sigma"], i) for i in range(frames)]))
+    frames = 1 if is3d else cfg["batch"]
+    gen = P.cartoon_volume if is3d else P.cartoon
+    x = torch.from_numpy(np.stack([P.add_gaussian_noise(gen(dims[0]), cfg["sigma"], i) for i in range(frames)]))
     x = x.to(dev).float()
     o = torch.empty_like(x)
     K = np.ascontiguousarray(sch.per_scale_factors, dtype=np.float64)
@@ -566,9 +573,13 @@ def run_fp32(steps, warmup, local):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     def step():
-        P._check(P.lib().sl_denoise_batch_f32_dev(s.handle, C.c_void_p(x.data_ptr()), frames, None,
-                                                  C.c_void_p(o.data_ptr()), Kp, len(K), float(sch.sigma), 1,
-                                                  P._stream_ptr(local)))
+        if is3d:
+            P._check(P.lib().sl_denoise_f32_dev(s.handle, C.c_void_p(x.data_ptr()), None, C.c_void_p(o.data_ptr()),
+                                                Kp, len(K), float(sch.sigma), 1, P._stream_ptr(local)))
+        else:
+            P._check(P.lib().sl_denoise_batch_f32_dev(s.handle, C.c_void_p(x.data_ptr()), frames, None,
+                                                      C.c_void_p(o.data_ptr()), Kp, len(K), float(sch.sigma), 1,
+                                                      P._stream_ptr(local)))
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
@@ -580,12 +591,14 @@ def run_fp32(steps, warmup, local):
         b.record()
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-    R = P.redundancy_2d(P.ScaleProfile.from_levels(cfg["levels"]))
-    nbytes = path_bytes(cfg, R, frames, "fused", 2) / 2  # fp32: every term halved
+    R = P.redundancy_3d(prof) if is3d else P.redundancy_2d(prof)
+    nbytes = path_bytes(cfg, R, frames, "fused", 1 if is3d else 2) / 2  # fp32: every term halved
     peak, _ = hbm_peak()
     gbs = nbytes / (ms / 1e3) / 1e9
-    return {"metric": "2D 512^2 dec+thr+rec frames/s, fp32 mode (nScales=4, R=49)", "value": frames / (ms / 1e3),
-            "unit": "frames/s", "ms_per_step": ms, "steps": steps, "dtype": "f32",
+    del s
+    torch.cuda.empty_cache()
+    return {"metric": cfg["metric"] + ", fp32 mode", "value": frames / (ms / 1e3), "unit": cfg["unit"],
+            "ms_per_step": ms, "steps": steps, "dtype": "f32",
             "path_roofline": {"bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak},
             "note": "optional fp32 mode (within 1e-5 of the fp64 reference, tests/test_gpu_fp32.py); not the headline"}
 
@@ -643,7 +656,8 @@ def main():
             w3["steps"], w3["warmup"] = k3, max(3, args.warmup)
             line["workloads"] = {"3d192": w3}
             if world == 1:
-                line["workloads"]["2d512_f32"] = run_fp32(args.steps, max(3, args.warmup), local)
+                line["workloads"]["2d512_f32"] = run_fp32("2d512", args.steps, max(3, args.warmup), local)
+                line["workloads"]["3d192_f32"] = run_fp32("3d192", k3, max(3, args.warmup), local)
     if rank == 0:
         line.update(steps=args.steps, warmup=args.warmup)
         print(json.dumps(line), flush=True)

@@ -258,7 +258,11 @@ int sl_add_gaussian_noise(const double* in, double* out, int64_t count, double s
  * sl_system_set_precision(sys, 32) rounds the handle's filter tables to
  * float (square 2D fast-path grids: 64..2048 and 192) and enables the *_f32
  * entry points, which take float signals / stacks and run every FFT pass in
- * fp32. Thresholds (K sigma RMS) are compared in fp64. */
+ * fp32. Cubic 3D grids (64/128/192/256) support the fused denoise
+ * (sl_denoise_f32_dev): the three band passes run on float2 spectra, the
+ * filters are synthesised in fp64 and rounded, the input spectrum and the
+ * final inverse (one spectrum each) run in fp64. Thresholds (K sigma RMS) are
+ * compared in fp64. */
 int sl_system_set_precision(sl_system* sys, int bits);
 int sl_sheardec_f32_dev(sl_system* sys, const float* f, float* coeffs, const double* K, int nK, double sigma,
                         int scale_by_rms, void* stream);

@@ -597,8 +597,9 @@ def build_system_2d(rows: int, cols: int, profile: ScaleProfile, fan=None, qmf: 
 
 
 def build_system_3d(dims, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair] = None,
-                    full_system: bool = False, device: int = 0, shard=None) -> ShearletSystem3D:
-    """build_system_3d (system3d.hpp:68-71); fan / qmf as build_system_2d."""
+                    full_system: bool = False, device: int = 0, shard=None, dtype: str = "f64") -> ShearletSystem3D:
+    """build_system_3d (system3d.hpp:68-71); fan / qmf as build_system_2d. dtype "f32" enables the
+    optional fp32 fused denoise (float32 CUDA volumes) on cubic 64/128/192/256 grids."""
     profile.validate()
     lv, lvp = _levels_arg(profile)
     h = C.c_void_p()
@@ -607,7 +608,12 @@ def build_system_3d(dims, profile: ScaleProfile, fan=None, qmf: Optional[QmfPair
     args, _keep = _bank_args(fan, qmf)
     _check(lib().sl_system_create_3d_ex(n0, n1, n2, lvp, len(lv), profile.coarsest_scale_offset,
                                         int(full_system), *args, int(device), int(lo), int(hi), C.byref(h)))
-    return ShearletSystem3D(h, (n0, n1, n2), profile, full_system, device)
+    sys = ShearletSystem3D(h, (n0, n1, n2), profile, full_system, device)
+    if dtype == "f32":
+        _check(lib().sl_system_set_precision(h, 32))
+    elif dtype != "f64":
+        raise ConfigError("dtype must be 'f64' or 'f32'")
+    return sys
 
 
 def redundancy_2d(profile: ScaleProfile, full_system: bool = False) -> int:  # system2d.cpp:49-57

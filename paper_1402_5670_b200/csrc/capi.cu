@@ -1314,9 +1314,14 @@ int sl_system_set_precision(sl_system* h, int bits) {
             s.WT32.release();
             return;
         }
+        if (s.fast3d && s.knobs.split3d) {  // 3D: the three passes in fp32, tables synthesised as before
+            s.fp32 = true;
+            return;
+        }
         if (!s.fast2d)
             throw SlError(SL_ERR_UNSUPPORTED_SIZE,
-                          "fp32 mode: square 2D grids of 64..2048 (power of two or 192) only");
+                          "fp32 mode: square 2D grids of 64..2048 (power of two or 192) and cubic 3D grids of "
+                          "64 / 128 / 192 / 256 only");
         const long long np = static_cast<long long>(s.R) * s.H * s.n[0], nw = static_cast<long long>(s.H) * s.n[0];
         s.psiT32.alloc(static_cast<size_t>(np));
         s.WT32.alloc(static_cast<size_t>(nw));
@@ -1333,6 +1338,7 @@ int sl_sheardec_f32_dev(sl_system* h, const float* f, float* coeffs, const doubl
                         void* stream) {
     return guard([&] {
         System& s = fp32_sys(h);
+        if (s.ndim != 2) throw SlError(SL_ERR_CONFIG, "fp32 mode in 3D: the fused denoise (sl_denoise_f32_dev)");
         require_dev_ptr(f, "sheardec input");
         require_dev_ptr(coeffs, "sheardec output");
         std::lock_guard<std::mutex> lk(s.mu);
@@ -1346,6 +1352,7 @@ int sl_sheardec_f32_dev(sl_system* h, const float* f, float* coeffs, const doubl
 int sl_shearrec_f32_dev(sl_system* h, const float* coeffs, int nbands, float* f, void* stream) {
     return guard([&] {
         System& s = fp32_sys(h);
+        if (s.ndim != 2) throw SlError(SL_ERR_CONFIG, "fp32 mode in 3D: the fused denoise (sl_denoise_f32_dev)");
         if (nbands != s.nb()) throw SlError(SL_ERR_SHAPE, "inverse: coefficient stack does not match the system");
         require_dev_ptr(coeffs, "shearrec input");
         require_dev_ptr(f, "shearrec output");
@@ -1374,7 +1381,10 @@ int sl_denoise_f32_dev(sl_system* h, const float* in, float* stack, float* out, 
             s.stack.alloc(static_cast<size_t>(s.nb()) * s.nreal);
             stk = reinterpret_cast<float*>(s.stack.p);
         }
-        denoise2d_fast_f32(s, in, stk, out, s.delta.p, stream_of(stream));
+        if (s.ndim == 3)
+            denoise3d_fast_f32(s, in, stk, out, s.delta.p, stream_of(stream));
+        else
+            denoise2d_fast_f32(s, in, stk, out, s.delta.p, stream_of(stream));
     });
 }
 
@@ -1382,6 +1392,7 @@ int sl_denoise_batch_f32_dev(sl_system* h, const float* in, int nframes, float* 
                              int nK, double sigma, int scaled, void* stream) {
     return guard([&] {
         System& s = fp32_sys(h);
+        if (s.ndim != 2) throw SlError(SL_ERR_CONFIG, "fp32 mode in 3D: the fused denoise (sl_denoise_f32_dev)");
         require_dev_ptr(in, "denoise input");
         require_dev_ptr(out, "denoise output");
         if (!K && nK > 0) throw SlError(SL_ERR_INVALID, "null K");

@@ -239,6 +239,7 @@ struct System {
     // out over several workspaces); `w` is the workspace the next pass uses.
     struct Workspace {
         DBuf<double2> F, inter, acc, slots;
+        DBuf<double2> aux;  // fp32-mode 3D staging (float2 spectra viewed through double2 storage)
         DBuf<int> done;  // per column block: CTAs of the last rec chunk that finished (self-resetting)
         DBuf<double> stack;
         cudaStream_t st = nullptr;  // owned stream (workspaces > 0)

@@ -188,40 +188,42 @@ static int split_group(const System& s, int cb) {
     return std::max(4, (cb + 3) / 4);
 }
 
-template <int n>
+template <int n, class C = double2>
 struct Split3DLaunch {
     using S = SplitShape<n>;
     System& s;
     cudaStream_t st;
     long long nT;
-    const double2* tw;
+    const C* tw;
+    static constexpr size_t AC_SMEM = S::AC_ELEMS * sizeof(C);
+    static constexpr size_t B_SMEM = S::B_ELEMS * sizeof(C);
     Split3DLaunch(System& sys, cudaStream_t stream) : s(sys), st(stream) {
         nT = static_cast<long long>(s.H) * n * n;
-        tw = s.plan(n, st).tw;
+        tw = Prec2D<C>::tw(s.plan(n, st));
     }
-    void dec(const double2* F, double2* Z, int nb, int band0) {
-        set_smem(k3s_dec<n>, S::AC_SMEM);
+    void dec(const C* F, C* Z, int nb, int band0) {
+        set_smem(k3s_dec<n, C>, AC_SMEM);
         const int G = std::min(nb, split_group(s, nb));
         LaunchScope ls(s, "f3s_dec", st, nb);
-        k3s_dec<n><<<dim3(S::H * S::Q, (nb + G - 1) / G), S::AC_THREADS, S::AC_SMEM, st>>>(F, Z, nT, s.synth, band0, G,
-                                                                                           nb, tw);
+        k3s_dec<n, C><<<dim3(S::H * S::Q, (nb + G - 1) / G), S::AC_THREADS, AC_SMEM, st>>>(F, Z, nT, s.synth, band0, G,
+                                                                                       nb, tw);
         check_launch("k3s_dec");
     }
     template <int MODE>
-    void mid(double2* Z, double* band, const double* bandin, int nb, const double* delta, int band0) {
-        auto* k = (MODE == kMidRec || band) ? k3s_mid<n, MODE, true> : k3s_mid<n, MODE, false>;
-        set_smem(k, S::B_SMEM);
+    void mid(C* Z, RealOf<C>* band, const RealOf<C>* bandin, int nb, const double* delta, int band0) {
+        auto* k = (MODE == kMidRec || band) ? k3s_mid<n, MODE, true, C> : k3s_mid<n, MODE, false, C>;
+        set_smem(k, B_SMEM);
         LaunchScope ls(s, MODE == kMidFused ? "f3s_mid" : (MODE == kMidDec ? "f3s_mid_dec" : "f3s_mid_rec"), st, nb);
-        k<<<dim3(n * (S::P / 2), nb), S::B_THREADS, S::B_SMEM, st>>>(Z, nT, band, s.nreal, bandin,
-                                                                    1.0 / static_cast<double>(s.nreal), delta, band0,
-                                                                    tw);
+        k<<<dim3(n * (S::P / 2), nb), S::B_THREADS, B_SMEM, st>>>(Z, nT, band, s.nreal, bandin,
+                                                                 RealOf<C>(1.0 / static_cast<double>(s.nreal)), delta,
+                                                                 band0, tw);
         check_launch("k3s_mid");
     }
-    void rec(const double2* Z, double2* acc, int nb, int band0, int accumulate, int k2lo = 0, int k2hi = -1) {
-        set_smem(k3s_rec<n>, S::AC_SMEM);
+    void rec(const C* Z, C* acc, int nb, int band0, int accumulate, int k2lo = 0, int k2hi = -1) {
+        set_smem(k3s_rec<n, C>, AC_SMEM);
         if (k2hi < 0) k2hi = S::H;
         LaunchScope ls(s, "f3s_rec", st, nb);
-        k3s_rec<n><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, S::AC_SMEM, st>>>(
+        k3s_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, AC_SMEM, st>>>(
             Z, nT, acc, nb, s.synth, band0, accumulate, tw, k2lo * S::Q);
         check_launch("k3s_rec");
     }
@@ -288,6 +290,53 @@ static void finish3d_t(System& s, double* out, cudaStream_t st) {
     finish_rec<n>(K, s, out);
 }
 
+// fp32 mode (sl_system_set_precision(32)): the three passes on float2 spectra.
+// The input's spectrum F and the final inverse of the accumulator -- one
+// spectrum each per call, < 1 % of the work -- run in fp64 and are rounded.
+__global__ void k_f32_to_f64(const float* __restrict__ in, double* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = static_cast<double>(in[i]);
+}
+__global__ void k_f64_to_f32(const double* __restrict__ in, float* __restrict__ out, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = static_cast<float>(in[i]);
+}
+template <int n>
+static void denoise3d_split_f32_t(System& s, const float* f, float* stack, float* out, const double* delta,
+                                  cudaStream_t st) {
+    Fast3DLaunch<n> K(s, st);
+    Split3DLaunch<n, float2> S3(s, st);
+    const int nb = s.nb();
+    const int C = std::min(fast3d_chunk(s), nb);
+    const long long nr = s.nreal;
+    s.w->aux.alloc(static_cast<size_t>(K.nT) + static_cast<size_t>((nr + 1) / 2));
+    double* f64 = reinterpret_cast<double*>(s.w->aux.p + K.nT);  // real staging after the fp32 spectra
+    k_f32_to_f64<<<2048, 256, 0, st>>>(f, f64, nr);
+    check_launch("k_f32_to_f64");
+    forward_natural<n>(K, s, f64);  // s.w->F (double2)
+    float2* F32 = reinterpret_cast<float2*>(s.w->aux.p);
+    float2* acc32 = F32 + K.nT;  // second half of the aux block (K.nT float2 = K.nT / 2 double2)
+    k_f64_to_f32<<<2048, 256, 0, st>>>(reinterpret_cast<const double*>(s.w->F.p), reinterpret_cast<float*>(F32),
+                                       2 * K.nT);
+    check_launch("k_f64_to_f32");
+    s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    float2* Z = reinterpret_cast<float2*>(s.w->inter.p);
+    for (int b0 = 0; b0 < nb; b0 += C) {
+        const int cb = std::min(C, nb - b0);
+        float* sb = stack ? stack + static_cast<size_t>(b0) * nr : nullptr;
+        S3.dec(F32, Z, cb, s.lo + b0);
+        S3.template mid<kMidFused>(Z, sb, nullptr, cb, delta, s.lo + b0);
+        S3.rec(Z, acc32, cb, s.lo + b0, b0 > 0);
+    }
+    s.w->acc.alloc(static_cast<size_t>(K.nT));
+    k_f32_to_f64<<<2048, 256, 0, st>>>(reinterpret_cast<const float*>(acc32), reinterpret_cast<double*>(s.w->acc.p),
+                                       2 * K.nT);
+    check_launch("k_f32_to_f64");
+    finish_rec<n>(K, s, f64);
+    k_f64_to_f32<<<2048, 256, 0, st>>>(f64, out, nr);
+    check_launch("k_f64_to_f32");
+}
+
 template <int n>
 static void dec3d_split_t(System& s, const double* f, double* out, const double* delta, cudaStream_t st) {
     Fast3DLaunch<n> K(s, st);
@@ -345,6 +394,11 @@ static void rec3d_fast(System& s, const double* coeffs, double* out, cudaStream_
 }
 
 static void finish3d_fast(System& s, double* out, cudaStream_t st) { SLB_FAST3D_DISPATCH(finish3d_t, s, out, st) }
+
+static void denoise3d_fast_f32(System& s, const float* f, float* stack, float* out, const double* delta,
+                               cudaStream_t st) {
+    SLB_FAST3D_DISPATCH(denoise3d_split_f32_t, s, f, stack, out, delta, st)
+}
 
 // the distributed variant: stop at the accumulator, calling slab_done per slab
 static void denoise3d_split_acc(System& s, const double* f, double* stack, const double* delta, cudaStream_t st,

@@ -59,8 +59,10 @@ struct SplitShape {
     static constexpr int H = L / 2 + 1;
     static constexpr bool PAD = SLB_SPLIT_PAD;
     static constexpr int LB = LineBuf<L, PAD>::N;    // line buffer stride (double2)
-    static constexpr size_t AC_SMEM = static_cast<size_t>((L * LD > P * LB) ? L * LD : P * LB) * sizeof(double2);
-    static constexpr size_t B_SMEM = static_cast<size_t>((H * 2 * Q > Q * LB) ? H * 2 * Q : Q * LB) * sizeof(double2);
+    static constexpr size_t AC_ELEMS = static_cast<size_t>((L * LD > P * LB) ? L * LD : P * LB);
+    static constexpr size_t B_ELEMS = static_cast<size_t>((H * 2 * Q > Q * LB) ? H * 2 * Q : Q * LB);
+    static constexpr size_t AC_SMEM = AC_ELEMS * sizeof(double2);  // fp64; the fp32 mode needs half
+    static constexpr size_t B_SMEM = B_ELEMS * sizeof(double2);
 #ifndef SLB_SPLIT_AC_MINB
     static constexpr int AC_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 4);
 #else
@@ -79,8 +81,8 @@ struct SplitShape {
 #define SLB_SPLIT_REGF 1
 #endif
 
-template <int R, int DIR>
-__device__ __forceinline__ void dft_small(double2 (&v)[R]) {
+template <int R, int DIR, class C>
+__device__ __forceinline__ void dft_small(C (&v)[R]) {
     if constexpr (R == 8)
         bfly8<DIR>(v);
     else if constexpr (R == 12)
@@ -90,33 +92,33 @@ __device__ __forceinline__ void dft_small(double2 (&v)[R]) {
 }
 
 // ---------------------------------------------------------------- pass A
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_MINB)
-    k3s_dec(const double2* __restrict__ F, double2* __restrict__ Z, long long zbs, FiltSynth3D filt, int band0, int G,
-            int nb, const double2* __restrict__ tw) {
+    k3s_dec(const C* __restrict__ F, C* __restrict__ Z, long long zbs, FiltSynth3D filt, int band0, int G,
+            int nb, const C* __restrict__ tw) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
-    extern __shared__ double2 tile[];  // [n][LD]; the P line buffers alias it
+    SLB_DYN_SMEM(C, tile);  // [n][LD]; the P line buffers alias it
     const int k2 = blockIdx.x / Q, q = blockIdx.x - k2 * Q;
     const int g0 = blockIdx.y * G, gn = min(G, nb - g0);
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
-    const double2* fl = F + ((long long)k2 * n + k1) * n;
-    double2 fr[E];
+    const C* fl = F + ((long long)k2 * n + k1) * n;
+    C fr[E];
     if (SLB_SPLIT_REGF) {
 #pragma unroll
         for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
     }
-    double2* lb = tile + p * S::LB;
+    C* lb = tile + p * S::LB;
     for (int bb = 0; bb < gn; ++bb) {
         const BandDesc3D bd = filt.bands[band0 + g0 + bb];
         const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
-        double2 x[E];
+        C x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const double ps = fline.at(t + T * m);
-            const double2 f = SLB_SPLIT_REGF ? fr[m] : __ldg(fl + t + T * m);
-            x[m] = make_double2(f.x * ps, f.y * ps);
+            const C f = SLB_SPLIT_REGF ? fr[m] : __ldg(fl + t + T * m);
+            x[m] = mkc<C>(f.x * RealOf<C>(ps), f.y * RealOf<C>(ps));
         }
         if (bb > 0) __syncthreads();  // the previous band's tile is copied out
         reg_fft<L, +1, S::PAD>(x, lb, t, tw);
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         __syncthreads();
         // length-P DFT across the lines for each i0, twiddle w_n^{a q}
         for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
-            double2 v[P];
+            C v[P];
 #pragma unroll
             for (int pp = 0; pp < P; ++pp) v[pp] = tile[i0 * LD + pp];
             dft_small<P, +1>(v);
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
             for (int a = 0; a < P; ++a) tile[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
         }
         __syncthreads();
-        double2* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P;
+        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P;
         for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
             const int i0 = idx / P, a = idx - i0 * P;
             __stcg(z + (long long)i0 * n + a, tile[i0 * LD + a]);
@@ -149,33 +151,33 @@ enum SplitMid : int {
     kMidRec = 2,    // band rows -> r2c -> Z'                         (inverse)
 };
 
-template <int L, int MODE, bool STORE>
+template <int L, int MODE, bool STORE, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MINB)
-    k3s_mid(double2* __restrict__ Z, long long zbs, double* __restrict__ band, long long bbs,
-            const double* __restrict__ bandin, double scale, const double* __restrict__ delta, int band0,
-            const double2* __restrict__ tw) {
+    k3s_mid(C* __restrict__ Z, long long zbs, RealOf<C>* __restrict__ band, long long bbs,
+            const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
+            const C* __restrict__ tw) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, H = S::H, n = L;
     constexpr int KPT = (H + T - 1) / T;
-    extern __shared__ double2 tile[];  // [H][2Q] tslot<Q>; line buffers alias it
+    SLB_DYN_SMEM(C, tile);  // [H][2Q] tslot<Q>; line buffers alias it
     const int i0 = blockIdx.x / (P / 2), a0 = 2 * (blockIdx.x - i0 * (P / 2));
     const int bi = blockIdx.y;
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
-    double2* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
-    double2* lb = tile + lq * S::LB;
-    double2 x[E];
+    C* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
+    C* lb = tile + lq * S::LB;
+    C x[E];
     if constexpr (MODE != kMidRec) {
         for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
             const int k2 = idx / (2 * Q), j = idx - k2 * 2 * Q;
-            cp_async16(tile + tslot<Q>(k2, j), zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1));
+            cp_async_c(tile + tslot<Q>(k2, j), zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1));
         }
         cp_async_wait_all();
         __syncthreads();
         // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
         for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
             const int e = idx / H, k2 = idx - e * H;
-            double2 v[Q];
+            C v[Q];
 #pragma unroll
             for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
             dft_small<Q, +1>(v);
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const int k = t + T * m;
-            double2 X, Y;
+            C X, Y;
             if (k < H) {
                 X = tile[tslot<Q>(k, 2 * lq)];
                 Y = tile[tslot<Q>(k, 2 * lq + 1)];
@@ -195,20 +197,20 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
                     X.y = 0.0;
                     Y.y = 0.0;
                 }
-                x[m] = make_double2(X.x - Y.y, X.y + Y.x);
+                x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
             } else {
                 X = tile[tslot<Q>(L - k, 2 * lq)];
                 Y = tile[tslot<Q>(L - k, 2 * lq + 1)];
-                x[m] = make_double2(X.x + Y.y, Y.x - X.y);
+                x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
             }
         }
         __syncthreads();  // the tile becomes the line buffers
         reg_fft<L, +1, S::PAD>(x, lb, t, tw);
         const double dl = delta ? delta[band0 + bi] : -1.0;
-        double* r0p = band + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+        RealOf<C>* r0p = band + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            double u = x[m].x * scale, w = x[m].y * scale;
+            RealOf<C> u = x[m].x * scale, w = x[m].y * scale;
             if (dl >= 0.0) {
                 if (fabs(u) < dl) u = 0.0;
                 if (fabs(w) < dl) w = 0.0;
@@ -217,17 +219,17 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
                 r0p[t + T * m] = u;
                 r0p[n + t + T * m] = w;
             }
-            x[m] = make_double2(u, w);
+            x[m] = mkc<C>(u, w);
         }
         if constexpr (MODE == kMidDec) return;
     } else {
-        const double* r0p = bandin + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+        const RealOf<C>* r0p = bandin + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = make_double2(__ldg(r0p + t + T * m), __ldg(r0p + n + t + T * m));
+        for (int m = 0; m < E; ++m) x[m] = mkc<C>(__ldg(r0p + t + T * m), __ldg(r0p + n + t + T * m));
     }
     // axis-2 r2c of the row pair (as k2_rows_r2c)
     reg_fft<L, -1, S::PAD>(x, lb, t, tw);
-    double2 zk[KPT], zm[KPT];
+    C zk[KPT], zm[KPT];
     if constexpr (T <= 32 && SLB_ROWS_SHFL) {
         mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
     } else {
@@ -248,15 +250,15 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            tile[tslot<Q>(k, 2 * lq)] = make_double2(0.5 * (zk[u].x + zm[u].x), 0.5 * (zk[u].y - zm[u].y));
-            tile[tslot<Q>(k, 2 * lq + 1)] = make_double2(0.5 * (zk[u].y + zm[u].y), 0.5 * (zm[u].x - zk[u].x));
+            tile[tslot<Q>(k, 2 * lq)] = mkc<C>(RealOf<C>(0.5) * (zk[u].x + zm[u].x), RealOf<C>(0.5) * (zk[u].y - zm[u].y));
+            tile[tslot<Q>(k, 2 * lq + 1)] = mkc<C>(RealOf<C>(0.5) * (zk[u].y + zm[u].y), RealOf<C>(0.5) * (zm[u].x - zk[u].x));
         }
     }
     __syncthreads();
     // length-Q DFT back over c for each (k2, e): slot 2c + e -> 2q + e
     for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
         const int e = idx / H, k2 = idx - e * H;
-        double2 v[Q];
+        C v[Q];
 #pragma unroll
         for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
         dft_small<Q, -1>(v);
@@ -271,36 +273,36 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
 }
 
 // ---------------------------------------------------------------- pass C
-template <int L>
+template <int L, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_MINB)
-    k3s_rec(const double2* __restrict__ Z, long long zbs, double2* __restrict__ acc, int nbands, FiltSynth3D filt,
-            int band0, int accumulate, const double2* __restrict__ tw, int bx0 = 0) {
+    k3s_rec(const C* __restrict__ Z, long long zbs, C* __restrict__ acc, int nbands, FiltSynth3D filt,
+            int band0, int accumulate, const C* __restrict__ tw, int bx0 = 0) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
-    extern __shared__ double2 tile[];  // [n][LD]; the P line buffers alias it
+    SLB_DYN_SMEM(C, tile);  // [n][LD]; the P line buffers alias it
     const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
-    double2* lb = tile + p * S::LB;
-    double2 ar[E];
+    C* lb = tile + p * S::LB;
+    C ar[E];
 #pragma unroll
-    for (int m = 0; m < E; ++m) ar[m] = make_double2(0.0, 0.0);
+    for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
     for (int b = 0; b < nbands; ++b) {
-        const double2* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
+        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
         if (b > 0) __syncthreads();  // the previous band's line buffers are free
         for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
             const int i0 = idx / P, a = idx - i0 * P;
-            cp_async16(tile + i0 * LD + a, z + (long long)i0 * n + a);
+            cp_async_c(tile + i0 * LD + a, z + (long long)i0 * n + a);
         }
         cp_async_wait_all();
         __syncthreads();
         // twiddle w_n^{-a q}, length-P DFT over a -> p, for each i0
         for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
-            double2 v[P];
+            C v[P];
 #pragma unroll
             for (int a = 0; a < P; ++a) {
-                const double2 u = tile[i0 * LD + a];
+                const C u = tile[i0 * LD + a];
                 v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
             }
             dft_small<P, -1>(v);
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
             for (int pp = 0; pp < P; ++pp) tile[i0 * LD + pp] = v[pp];
         }
         __syncthreads();
-        double2 x[E];
+        C x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) x[m] = tile[(t + T * m) * LD + p];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
@@ -318,17 +320,17 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const double ps = fline.at(t + T * m);
-            ar[m].x = fma(x[m].x, ps, ar[m].x);
-            ar[m].y = fma(x[m].y, ps, ar[m].y);
+            ar[m].x = fma(x[m].x, RealOf<C>(ps), ar[m].x);
+            ar[m].y = fma(x[m].y, RealOf<C>(ps), ar[m].y);
         }
     }
-    double2* d = acc + ((long long)k2 * n + k1) * n;
+    C* d = acc + ((long long)k2 * n + k1) * n;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
-        double2 v = ar[m];
+        C v = ar[m];
         if (accumulate) {
-            const double2 o = __ldcg(d + t + T * m);
-            v = make_double2(o.x + v.x, o.y + v.y);
+            const C o = __ldcg(d + t + T * m);
+            v = mkc<C>(o.x + v.x, o.y + v.y);
         }
         __stcg(d + t + T * m, v);
     }

@@ -54,7 +54,31 @@ def test_fp32_requires_precision(cuda):
     s = P.build_system_2d(64, 64, P.ScaleProfile.from_levels([0, 1]))
     with pytest.raises(P.ConfigError):
         P.denoise(torch.zeros((64, 64), device=cuda, dtype=torch.float32), s, P.ThresholdSchedule.defaults_2d(1.0, 2))
-    s3 = P.build_system_3d((16, 16, 16), P.ScaleProfile.from_levels([0]))
+    s3 = P.build_system_3d((16, 16, 16), P.ScaleProfile.from_levels([0]))  # generic 3D path: no fp32
     with pytest.raises(P.UnsupportedSizeError):
-        P.lib()  # noqa
         P._check(P.lib().sl_system_set_precision(s3.handle, 32))
+
+
+@pytest.mark.parametrize("n,levels", [(64, [0, 1]), (128, [1, 1])])
+def test_fp32_3d_denoise_vs_fp64(cuda, n, levels):
+    import torch
+    sch = P.ThresholdSchedule.defaults_3d(0.3, len(levels))
+    s = P.build_system_3d((n, n, n), P.ScaleProfile.from_levels(levels), dtype="f32")
+    x = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, (n, n, n))).to(cuda)
+    d64 = P.denoise(x, s, sch)
+    d32, st32 = P.denoise(x.float(), s, sch, return_stack=True)
+    assert d32.dtype == torch.float32 and st32.dtype == torch.float32
+    assert (torch.linalg.norm(d32.double() - d64) / torch.linalg.norm(d64)).item() <= 1e-5
+    _, st64 = P.denoise(x, s, sch, return_stack=True)
+    assert (torch.linalg.norm(st32.double() - st64) / torch.linalg.norm(st64)).item() <= 1e-5
+
+
+@pytest.mark.slow
+def test_fp32_cfg5_192_denoise_vs_reference(cuda):
+    import torch
+    g = golden("cfg5_denoise192_112")
+    s = P.build_system_3d((192, 192, 192), P.ScaleProfile.from_levels([1, 1, 2]), dtype="f32")
+    x = torch.from_numpy(P.add_gaussian_noise(P.cartoon_volume(192), 40.0, 3)).to(cuda).float()
+    d = P.denoise(x, s, P.ThresholdSchedule.defaults_3d(40.0)).double().cpu().numpy()
+    assert rel_l2(d.reshape(-1)[sample_idx(d.size)], g["den_sample"]) <= 1e-5
+    assert abs(d.sum() - g["den_sum"]) <= 1e-5 * abs(g["den_sum"])
