@@ -61,16 +61,26 @@ def test_fp32_requires_precision(cuda):
 
 @pytest.mark.parametrize("n,levels", [(64, [0, 1]), (128, [1, 1])])
 def test_fp32_3d_denoise_vs_fp64(cuda, n, levels):
+    # sigma 0: the fused pipeline as a pure fp32 round trip, within 1e-5 of fp64;
+    # sigma > 0: fp32 rounding may move a coefficient within ~1e-7 of its
+    # threshold across it, so the denoised volumes agree to the flipped
+    # coefficients' share and the kept counts almost exactly
     import torch
-    sch = P.ThresholdSchedule.defaults_3d(0.3, len(levels))
     s = P.build_system_3d((n, n, n), P.ScaleProfile.from_levels(levels), dtype="f32")
     x = torch.from_numpy(np.random.default_rng(n).uniform(-1, 1, (n, n, n))).to(cuda)
-    d64 = P.denoise(x, s, sch)
+    rel = lambda a, b: (torch.linalg.norm(a.double() - b) / torch.linalg.norm(b)).item()  # noqa: E731
+    s0 = P.ThresholdSchedule.defaults_3d(0.0, len(levels))
+    r32 = P.denoise(x.float(), s, s0)
+    assert r32.dtype == torch.float32
+    assert rel(r32, x) <= 1e-5
+    sch = P.ThresholdSchedule.defaults_3d(0.3, len(levels))
+    d64, st64 = P.denoise(x, s, sch, return_stack=True)
     d32, st32 = P.denoise(x.float(), s, sch, return_stack=True)
-    assert d32.dtype == torch.float32 and st32.dtype == torch.float32
-    assert (torch.linalg.norm(d32.double() - d64) / torch.linalg.norm(d64)).item() <= 1e-5
-    _, st64 = P.denoise(x, s, sch, return_stack=True)
-    assert (torch.linalg.norm(st32.double() - st64) / torch.linalg.norm(st64)).item() <= 1e-5
+    assert st32.dtype == torch.float32
+    assert rel(d32, d64) <= 1e-3
+    k64 = torch.count_nonzero(st64.reshape(st64.shape[0], -1), dim=1)
+    k32 = torch.count_nonzero(st32.reshape(st32.shape[0], -1), dim=1)
+    assert (k32 - k64).abs().sum().item() <= 1e-4 * k64.sum().item()
 
 
 @pytest.mark.slow
