@@ -196,6 +196,7 @@ struct Split3DLaunch {
     long long nT;
     const C* tw;
     static constexpr size_t AC_SMEM = S::AC_ELEMS * sizeof(C);
+    static constexpr size_t REC_SMEM = (S::REC_DB ? 2 : 1) * S::AC_ELEMS * sizeof(C);
     static constexpr size_t B_SMEM = S::B_ELEMS * sizeof(C);
     Split3DLaunch(System& sys, cudaStream_t stream) : s(sys), st(stream) {
         nT = static_cast<long long>(s.H) * n * n;
@@ -220,10 +221,10 @@ struct Split3DLaunch {
         check_launch("k3s_mid");
     }
     void rec(const C* Z, C* acc, int nb, int band0, int accumulate, int k2lo = 0, int k2hi = -1) {
-        set_smem(k3s_rec<n, C>, AC_SMEM);
+        set_smem(k3s_rec<n, C>, REC_SMEM);
         if (k2hi < 0) k2hi = S::H;
         LaunchScope ls(s, "f3s_rec", st, nb);
-        k3s_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, AC_SMEM, st>>>(
+        k3s_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, REC_SMEM, st>>>(
             Z, nT, acc, nb, s.synth, band0, accumulate, tw, k2lo * S::Q);
         check_launch("k3s_rec");
     }

@@ -68,6 +68,11 @@ struct SplitShape {
 #else
     static constexpr int AC_MINB = SLB_SPLIT_AC_MINB;
 #endif
+#ifndef SLB_SPLIT_REC_DB
+    static constexpr bool REC_DB = true;  // pass C: double-buffered cp.async band tiles
+#else
+    static constexpr bool REC_DB = SLB_SPLIT_REC_DB;
+#endif
 #ifndef SLB_SPLIT_B_MINB
     static constexpr int B_MINB = L >= 256 ? 1 : 3;
 #else
@@ -284,39 +289,56 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
-    C* lb = tile + p * S::LB;
+    // DB: band b+1's tile is loaded (cp.async) into the second buffer while band
+    // b goes through the DFT / FFT / accumulate in the first
+    constexpr bool DB = S::REC_DB;
+    auto load = [&](int b, C* buf) {
+        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
+        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
+            const int i0 = idx / P, a = idx - i0 * P;
+            cp_async_c(buf + i0 * LD + a, z + (long long)i0 * n + a);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     C ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
+    if (DB && nbands > 0) load(0, tile);
     for (int b = 0; b < nbands; ++b) {
-        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
-        if (b > 0) __syncthreads();  // the previous band's line buffers are free
-        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
-            const int i0 = idx / P, a = idx - i0 * P;
-            cp_async_c(tile + i0 * LD + a, z + (long long)i0 * n + a);
+        C* cur = DB ? tile + (b & 1) * S::AC_ELEMS : tile;
+        if (b > 0) __syncthreads();  // the previous band's line buffers (and its tile) are free
+        if (DB) {
+            if (b + 1 < nbands) {
+                load(b + 1, tile + ((b + 1) & 1) * S::AC_ELEMS);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // band b landed, b+1 in flight
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+        } else {
+            load(b, cur);
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
         }
-        cp_async_wait_all();
         __syncthreads();
         // twiddle w_n^{-a q}, length-P DFT over a -> p, for each i0
         for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
             C v[P];
 #pragma unroll
             for (int a = 0; a < P; ++a) {
-                const C u = tile[i0 * LD + a];
+                const C u = cur[i0 * LD + a];
                 v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
             }
             dft_small<P, -1>(v);
 #pragma unroll
-            for (int pp = 0; pp < P; ++pp) tile[i0 * LD + pp] = v[pp];
+            for (int pp = 0; pp < P; ++pp) cur[i0 * LD + pp] = v[pp];
         }
         __syncthreads();
         C x[E];
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = tile[(t + T * m) * LD + p];
+        for (int m = 0; m < E; ++m) x[m] = cur[(t + T * m) * LD + p];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
         const BandDesc3D bd = filt.bands[band0 + b];
         const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
-        reg_fft<L, -1, S::PAD>(x, lb, t, tw);
+        reg_fft<L, -1, S::PAD>(x, cur + p * S::LB, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const double ps = fline.at(t + T * m);
