@@ -68,6 +68,11 @@ struct SplitShape {
 #else
     static constexpr int AC_MINB = SLB_SPLIT_AC_MINB;
 #endif
+#ifndef SLB_SPLIT_DEC_PF
+    static constexpr bool DEC_PF = false;  // pass A: next band's filter line prefetched (A/B)
+#else
+    static constexpr bool DEC_PF = SLB_SPLIT_DEC_PF;
+#endif
 #ifndef SLB_SPLIT_REC_DB
     static constexpr bool REC_DB = true;  // pass C: double-buffered cp.async band tiles
 #else
@@ -115,15 +120,28 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         for (int m = 0; m < E; ++m) fr[m] = __ldg(fl + t + T * m);
     }
     C* lb = tile + p * S::LB;
+    // PF: band b+1's filter line is synthesised (table loads in flight) while band b is in the FFT
+    constexpr bool PF = S::DEC_PF;
+    double pn[E];
+    if (PF && gn > 0) {
+        const FiltSynth3D::Ax0Line f0 = filt.ax0_line(filt.bands[band0 + g0], k1, k2);
+#pragma unroll
+        for (int m = 0; m < E; ++m) pn[m] = f0.at(t + T * m);
+    }
     for (int bb = 0; bb < gn; ++bb) {
         const BandDesc3D bd = filt.bands[band0 + g0 + bb];
         const FiltSynth3D::Ax0Line fline = filt.ax0_line(bd, k1, k2);
         C x[E];
 #pragma unroll
         for (int m = 0; m < E; ++m) {
-            const double ps = fline.at(t + T * m);
+            const double ps = PF ? pn[m] : fline.at(t + T * m);
             const C f = SLB_SPLIT_REGF ? fr[m] : __ldg(fl + t + T * m);
             x[m] = mkc<C>(f.x * RealOf<C>(ps), f.y * RealOf<C>(ps));
+        }
+        if (PF && bb + 1 < gn) {
+            const FiltSynth3D::Ax0Line fn = filt.ax0_line(filt.bands[band0 + g0 + bb + 1], k1, k2);
+#pragma unroll
+            for (int m = 0; m < E; ++m) pn[m] = fn.at(t + T * m);
         }
         if (bb > 0) __syncthreads();  // the previous band's tile is copied out
         reg_fft<L, +1, S::PAD>(x, lb, t, tw);
