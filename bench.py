@@ -7,9 +7,10 @@
 BASELINE.json's metric has two halves; the default run measures both:
   * the headline line: 2D 512^2 (configs[1]), nScales=4 shear levels
     [1,1,2,2] (R=49); one step = decompose -> hard_threshold(defaults_2d(40),
-    RMS-scaled) -> reconstruct of 8 distinct noisy cartoon frames through the
-    fused device batch (sl_denoise_batch_dev: lock-step frame pairs, each
-    frame's 103 MB thresholded stack materialised in HBM);
+    RMS-scaled) -> reconstruct of a streamed batch of 32 distinct noisy cartoon
+    frames through the fused device batch (sl_denoise_batch_dev: lock-step
+    frame pairs over the handle's streams, each frame's 103 MB thresholded
+    stack materialised in HBM);
   * "workloads": {"3d192": ...}: 3D 192^3 SL3D_2 [1,1,2] (R=292, configs[4]),
     one step = the fused denoise of one noisy cartoon volume (sl_denoise_dev,
     16.5 GB stack materialised), timed the same way.
@@ -56,9 +57,9 @@ FP64_FLOP_PER_CLK_SM = 128  # 64 DFMA / clk / SM (tools/fp64_peak.cu measured 34
 
 CONFIGS = {
     # name: dims, shear levels, sigma, frames per step per rank, unit, metric
-    "2d512": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s",
+    "2d512": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=32, unit="frames/s",
                   metric="2D 512^2 dec+thr+rec frames/s (nScales=4, R=49)", baseline_cfg=1),
-    "2d512_nostack": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=8, unit="frames/s", nostack=True,
+    "2d512_nostack": dict(dims=(512, 512), levels=[1, 1, 2, 2], sigma=40.0, batch=32, unit="frames/s", nostack=True,
                           metric="2D 512^2 denoise frames/s, coefficient stack not materialised (nScales=4, R=49)",
                           baseline_cfg=1),
     "2d256": dict(dims=(256, 256), levels=[1, 1], sigma=40.0, batch=32, unit="frames/s",
@@ -529,7 +530,8 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
         "e2e": {"value": e2e_value, "unit": cfg["unit"], "h2d_bytes_per_step": frames * N * 8,
                 "d2h_bytes_per_step": frames * N * 8,
                 "api": ("sl_denoise_batch_host (pinned host in/out; H2D in frame order on a copy stream, fused "
-                        "dec/thr/rec on 3 compute streams, D2H in frame order on a second copy stream)" if not is3d
+                        "dec/thr/rec on 4 compute streams (one head frame, then lock-step pairs), D2H in frame "
+                        "order on a second copy stream)" if not is3d
                         else "denoise (sl_denoise_dev) with pinned H2D/D2H")},
         "clocks": clocks,
     }

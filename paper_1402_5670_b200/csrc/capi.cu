@@ -708,7 +708,12 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         deltas(s, K, nK, sigma, scaled, st);
         // measured (tools/e2e_ab.sh, 8 frames of 512^2): 3 compute streams
         // 6250 frames/s, 1: 4800, 4: 6100, 5-6: 6220, per-frame fan-out: 6100
-        const int pipe = s.knobs.host_pipe >= 0 ? s.knobs.host_pipe : (s.fast2d ? 3 : 0);
+        // schedule (profiles/r2_e2e_sweep.log): below 16 frames 3 compute streams of
+        // single frames; from 16 frames 4 streams of lock-step pairs after one
+        // single head frame (compute starts after one frame's H2D) -- e2e 0.92 of
+        // the device batch at 32 frames vs 0.88 with singles
+        const bool many = nframes >= 16;
+        const int pipe = s.knobs.host_pipe >= 0 ? s.knobs.host_pipe : (s.fast2d ? (many ? 4 : 3) : 0);
         const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
         if (pipe > 0 && nframes > 1) {
             // pipelined: all H2D in frame order on one copy stream, the fused
@@ -725,20 +730,30 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             s.concurrency = s.knobs.pipe_conc >= 1 ? s.knobs.pipe_conc : P;  // band grouping of fast2d_cfg
             // SLB_PIPE_GROUP = 2: lock-step frame pairs per compute stream (one
             // launch per pass covers both frames, as in the device batch)
-            const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, s.knobs.pipe_group)) : 1;
+            const int want_grp = s.knobs.pipe_group >= 1 ? s.knobs.pipe_group : (many ? 2 : 1);
+            const int head = s.knobs.pipe_head >= 0 ? s.knobs.pipe_head : (many ? 1 : 0);
+            const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, want_grp)) : 1;
             if (grp > 1 && s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
-            const int ngroups = (nframes + grp - 1) / grp;
+            // segments: the first `head` frames alone (compute starts after one
+            // frame's H2D), then lock-step groups of grp frames
+            std::vector<std::pair<int, int>> seg;
+            for (int f0 = 0; f0 < nframes;) {
+                const int nf = static_cast<int>(seg.size()) < head ? 1 : std::min(grp, nframes - f0);
+                seg.emplace_back(f0, nf);
+                f0 += nf;
+            }
+            s.ensure_pipe_events(2 * seg.size());
             try {
-                for (int g = 0; g < ngroups; ++g) {
-                    const int f0 = g * grp, nf = std::min(grp, nframes - f0);
+                for (size_t g = 0; g < seg.size(); ++g) {
+                    const int f0 = seg[g].first, nf = seg[g].second;
                     const size_t off = static_cast<size_t>(f0) * s.nreal;
-                    cudaEvent_t ein = s.pipe_ev[2 * static_cast<size_t>(g)], ec = s.pipe_ev[2 * static_cast<size_t>(g) + 1];
+                    cudaEvent_t ein = s.pipe_ev[2 * g], ec = s.pipe_ev[2 * g + 1];
                     SL_CUDA(cudaMemcpyAsync(s.io_in.p + off, in + off, nf * fb, cudaMemcpyHostToDevice, cin));
                     SL_CUDA(cudaEventRecord(ein, cin));
                     s.w = s.ws[static_cast<size_t>(1 + g % P)].get();
                     SL_CUDA(cudaStreamWaitEvent(s.w->st, ein, 0));
-                    double* stk = group_stack(s, nullptr, 0, grp, sfs);
-                    if (grp > 1)
+                    double* stk = group_stack(s, nullptr, 0, std::max(grp, nf), sfs);
+                    if (nf > 1)
                         denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, stk, sfs, s.io_out.p + off, s.nreal,
                                              s.delta.p, s.w->st);
                     else

@@ -280,19 +280,21 @@ def test_batched_api_matches_per_frame(cuda):
         P.denoise_batch(ft[:, :128], s, sch)
 
 
-@pytest.mark.parametrize("pipe,group", [("0", "1"), ("1", "1"), ("3", "1"), ("6", "1"), ("3", "2"), ("2", "3")])
+@pytest.mark.parametrize("pipe,group", [("0", "1"), ("1", "1"), ("3", "1"), ("6", "1"), ("3", "2"), ("2", "3"),
+                                        ("-1", "-1")])
 def test_host_batch_pipelines_agree(cuda, monkeypatch, pipe, group):
     # the pipelined host batch (copy streams + SLB_HOST_PIPE compute streams,
     # SLB_PIPE_GROUP lock-step frames per stream, ragged last group) and the
     # per-frame fan-out return the per-frame result for every frame
     s = system(128, 128, [1, 2])
     sch = P.ThresholdSchedule.defaults_2d(25.0, 2)
-    frames = np.stack([P.add_gaussian_noise(P.cartoon(128), 25.0, 40 + i) for i in range(7)])
+    nfr = 7 if pipe != "-1" else 19  # auto schedule: >= 16 frames take head frame + lock-step pairs
+    frames = np.stack([P.add_gaussian_noise(P.cartoon(128), 25.0, 40 + i) for i in range(nfr)])
     monkeypatch.setenv("SLB_HOST_PIPE", pipe)
     monkeypatch.setenv("SLB_PIPE_GROUP", group)
     sp = P.build_system_2d(128, 128, P.ScaleProfile.from_levels([1, 2]))  # knobs are read at creation
     got = P.denoise_batch(frames, sp, sch)
-    for i in range(7):
+    for i in range(nfr):
         one = P.denoise(frames[i], s, sch)
         assert np.linalg.norm(got[i] - one) <= 1e-12 * np.linalg.norm(one)
 
