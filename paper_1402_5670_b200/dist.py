@@ -39,6 +39,34 @@ def sharded_denoise(x, local_partial: Callable, group=None, root: int = 0):
     return part
 
 
+def sharded_denoise_accumulator(x, local_accumulator: Callable, finish: Callable, group=None, root: int = 0,
+                                slabs: int = 4):
+    """The library's 3D schedule (csrc/comm.cuh denoise_dist), with
+    torch.distributed collectives: broadcast x from `root`; every rank forms the
+    half-spectrum accumulator sum_b FFT(thr c_b) psi_b of its bands; the
+    accumulators are sum-reduced onto the root in `slabs` contiguous slabs along
+    the first axis (the order the library overlaps with its last band group);
+    only the root runs finish(acc) (divide by W, inverse FFT). Returns finish's
+    result on the root, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    dist.broadcast(x, src=root, group=group)
+    acc = local_accumulator(x)
+    n0 = acc.shape[0]
+    for j in range(slabs):
+        lo, hi = n0 * j // slabs, n0 * (j + 1) // slabs
+        if hi > lo:
+            part = acc[lo:hi].contiguous()
+            if torch.is_complex(part):  # gloo reduces real tensors: view complex as (re, im) pairs
+                pr = torch.view_as_real(part).contiguous()
+                dist.reduce(pr, dst=root, op=dist.ReduceOp.SUM, group=group)
+                part = torch.view_as_complex(pr)
+            else:
+                dist.reduce(part, dst=root, op=dist.ReduceOp.SUM, group=group)
+            acc[lo:hi] = part
+    return finish(acc) if dist.get_rank(group) == root else None
+
+
 def sharded_forward_thresholded(x, sys, schedule, group=None, root: int = 0):
     """Device path: broadcast then this rank's thresholded bands."""
     import torch.distributed as dist

@@ -119,3 +119,50 @@ def test_unique_id_broadcast_world2():
     for p in ps:
         p.join(timeout=60)
     assert got == {0: True, 1: True}
+
+
+def _acc_worker(rank, world, port, dims, levels, q):
+    # the library's multi-GPU 3D schedule on CPU: broadcast, per-rank accumulator of
+    # its bands (numpy oracle), slab-wise sum-reduce onto the root, root-only finish
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import shearlet_np as O
+    from paper_1402_5670_b200.dist import sharded_denoise_accumulator
+    s = O.build_system_3d(dims, levels)
+    lo, hi = shard_range(s.R, rank, world)
+    x = torch.zeros(dims, dtype=torch.float64)
+    if rank == 0:
+        x = torch.from_numpy(np.random.default_rng(6).uniform(-1, 1, dims))
+    K = [3.0] * len(levels)
+
+    def local_acc(xt):
+        F = np.fft.fftn(xt.numpy())
+        acc = np.zeros(dims, dtype=np.complex128)
+        for i in range(lo, hi):
+            band = np.real(np.fft.ifftn(np.conj(s.filter_freq(i)) * F))
+            r = s.index[i]
+            if r[1] >= 0:  # hard threshold of the non-lowpass bands (apps.cpp:57-81)
+                band[np.abs(band) < K[r[1]] * 0.3 * s.filter_norms[i]] = 0.0
+            acc += np.fft.fftn(band) * s.filter_freq(i)
+        return torch.from_numpy(acc)
+
+    out = sharded_denoise_accumulator(x, local_acc, lambda a: np.real(np.fft.ifftn(a.numpy() / s.frame_weight)))
+    if rank == 0:
+        full = O.inverse_3d(O.hard_threshold(O.forward_3d(x.numpy(), s), s.index, 0, s.filter_norms, K, 0.3), s)
+        q.put(float(np.linalg.norm(out - full) / np.linalg.norm(full)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world3_accumulator_reduce_equals_full_denoise():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_acc_worker, args=(r, 3, port, (12, 12, 12), [0], q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=10) <= 1e-12
