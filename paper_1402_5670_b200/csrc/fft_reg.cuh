@@ -40,7 +40,9 @@ SLB_REG_PLAN(128, 16, 8, 4, 4)
 SLB_PLAN128
 #endif
 SLB_REG_PLAN(256, 32, 8, 8, 4)
-#ifndef SLB_PLAN512
+#if defined(SLB_PLAN512_WIDE)
+SLB_REG_PLAN(512, 16, 32, 16)  // one exchange per line, 32 complex per thread
+#elif !defined(SLB_PLAN512)
 SLB_REG_PLAN(512, 64, 8, 8, 8)
 #else
 SLB_PLAN512
@@ -80,16 +82,39 @@ constexpr int plan_ns(int s) {
 // address is a per-thread base plus a compile-time offset (no per-access XOR).
 // The rows kernels keep the unpadded XOR swizzle (PAD = false): their line
 // buffers alias a staging tile sized for L-element lines, and measured faster.
-template <bool PAD = true>
+// Length 192 (radix 12 first) uses e -> e + e/24 in both modes: the stride-12
+// stores of the radix-12 stage (e = 12 t + r) land on 8 distinct 16-byte bank
+// groups per quarter-warp (4 t + t/2 mod 8), which neither the XOR swizzle nor
+// the e/8 pad achieves (both 2-way), and aligned runs of 8 stay distinct.
+// Plans whose first radix is 16 or 32 (one thread holds 16t..16t+15 or
+// 32t..32t+31 before the first store) XOR the 16-byte slot with e >> 4 / e >> 5
+// instead, in both modes.
+#ifndef SLB_SWZ192
+#define SLB_SWZ192 1
+#endif
+template <int L>
+struct SwzShift {
+    static constexpr int value = RegPlan<L>::R[0] == 32 ? 5 : (RegPlan<L>::R[0] == 16 ? 4 : 3);
+};
+template <>
+struct SwzShift<0> {
+    static constexpr int value = 3;
+};
+template <bool PAD = true, int L = 0>
 __device__ __forceinline__ int swz(int e) {
-    if constexpr (PAD)
+    if constexpr (L == 192 && SLB_SWZ192)
+        return e + static_cast<int>(static_cast<unsigned>(e) / 24u);
+    else if constexpr (SwzShift<L>::value != 3)
+        return e ^ ((e >> SwzShift<L>::value) & 7);
+    else if constexpr (PAD)
         return e + (e >> 3);
     else
         return e ^ ((e >> 3) & 7);
 }
 template <int L, bool PAD = true>
 struct LineBuf {
-    static constexpr int N = PAD ? L + L / 8 : L;  // double2 slots per line buffer
+    static constexpr int N = (L == 192 && SLB_SWZ192) ? L + L / 24
+                             : (SwzShift<L>::value != 3 ? L : (PAD ? L + L / 8 : L));  // double2 slots per line buffer
 };
 
 template <int T>
@@ -270,7 +295,7 @@ struct RegStage {
                 const int jm = j % NS;
                 const int base = (j - jm) * R + jm;
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[swz<PAD>(base + r * NS)] = x[q + B * r];
+                for (int r = 0; r < R; ++r) sm[swz<PAD, L>(base + r * NS)] = x[q + B * r];
             }
             line_sync<T>();
             constexpr int R2 = P::R[S + 1];
@@ -279,7 +304,7 @@ struct RegStage {
             for (int q = 0; q < B2; ++q) {
                 const int j = t + T * q;
 #pragma unroll
-                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD>(j + r * (L / R2))];
+                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD, L>(j + r * (L / R2))];
             }
             line_sync<T>();
             RegStage<L, DIR, S + 1, PAD, C>::run(x, sm, t, tw);
