@@ -153,8 +153,11 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     const int nrows = min(2 * V, n0 - r0);
     // all tile loads in flight at once (cp.async, 16 B each, L2 only); the
     // smem slot order follows the global order so each warp's writes are dense
-    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
-        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+    // thread -> fixed slot rr, k-rows strided by a compile-time step
+    constexpr int KS = RowCfg<L>::THREADS / (2 * V);
+    const int rr = threadIdx.x % (2 * V);
+#pragma unroll 4
+    for (int k = threadIdx.x / (2 * V); k < H; k += KS) {
         if (rr < nrows)
             cp_async_c(tile + tslot<V>(k, rr), src + (long long)k * n0 + r0 + rr);
         else
@@ -256,10 +259,11 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
     }
     __syncthreads();
     const int nrows = min(2 * V, n0 - r0);
-    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
-        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+    constexpr int KS = RowCfg<L>::THREADS / (2 * V);
+    const int rr = threadIdx.x % (2 * V);
+#pragma unroll 4
+    for (int k = threadIdx.x / (2 * V); k < H; k += KS)
         if (rr < nrows) __stcg(dst + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
-    }
 }
 
 // ---------------------------------------------------------------- column lines

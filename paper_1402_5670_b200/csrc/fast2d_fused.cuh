@@ -34,8 +34,11 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     constexpr bool kTest = !STORE || L == 2048;
     if (!kTest || band) band += blockIdx.y * bbs + blockIdx.z * bzs;
     const int nrows = min(2 * V, n0 - r0);
-    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
-        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+    // thread -> fixed slot rr, k-rows strided by a compile-time step
+    constexpr int KS = RowCfg<L>::THREADS / (2 * V);
+    const int rr = threadIdx.x % (2 * V);
+#pragma unroll 4
+    for (int k = threadIdx.x / (2 * V); k < H; k += KS) {
         if (rr < nrows)
             cp_async_c(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
         else
@@ -110,10 +113,9 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         }
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < H * 2 * V; idx += blockDim.x) {
-        const int k = idx / (2 * V), rr = idx - k * 2 * V;
+#pragma unroll 4
+    for (int k = threadIdx.x / (2 * V); k < H; k += KS)
         if (rr < nrows) __stcg(inter + (long long)k * n0 + r0 + rr, tile[tslot<V>(k, rr)]);
-    }
 }
 
 // rows pass of the fused denoise (band = null: the stack is not materialised)

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         for (int m = 0; m < E; ++m) tile[(t + T * m) * LD + p] = x[m];
         __syncthreads();
         // length-P DFT across the lines for each i0, twiddle w_n^{a q}
-        for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
+        for (int i0 = threadIdx.x; i0 < n; i0 += S::AC_THREADS) {
             C v[P];
 #pragma unroll
             for (int pp = 0; pp < P; ++pp) v[pp] = tile[i0 * LD + pp];
@@ -159,11 +159,12 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
             for (int a = 0; a < P; ++a) tile[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
         }
         __syncthreads();
-        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P;
-        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
-            const int i0 = idx / P, a = idx - i0 * P;
-            __stcg(z + (long long)i0 * n + a, tile[i0 * LD + a]);
-        }
+        // the CTA's P * T threads cover T rows i0 of P entries per step (row
+        // offsets by compile-time strides, no per-element division)
+        const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
+        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P + (long long)si0 * n + sa;
+#pragma unroll 4
+        for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, tile[(si0 + T * j) * LD + sa]);
     }
 }
 
@@ -189,16 +190,18 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     const int i1 = a0 + P * lq;
     C* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
     C* lb = tile + lq * S::LB;
+    constexpr int KST = S::B_THREADS / (2 * Q);  // k2 rows per tile-copy step
+    const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
     C x[E];
     if constexpr (MODE != kMidRec) {
-        for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
-            const int k2 = idx / (2 * Q), j = idx - k2 * 2 * Q;
-            cp_async_c(tile + tslot<Q>(k2, j), zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1));
-        }
+        // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
+#pragma unroll 4
+        for (int k2 = sk2; k2 < H; k2 += KST)
+            cp_async_c(tile + tslot<Q>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1));
         cp_async_wait_all();
         __syncthreads();
         // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
-        for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
+        for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
             const int e = idx / H, k2 = idx - e * H;
             C v[Q];
 #pragma unroll
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     }
     __syncthreads();
     // length-Q DFT back over c for each (k2, e): slot 2c + e -> 2q + e
-    for (int idx = threadIdx.x; idx < 2 * H; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
         const int e = idx / H, k2 = idx - e * H;
         C v[Q];
 #pragma unroll
@@ -289,10 +292,9 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
         for (int j = 0; j < Q; ++j) tile[tslot<Q>(k2, 2 * j + e)] = v[j];
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < H * 2 * Q; idx += blockDim.x) {
-        const int k2 = idx / (2 * Q), j = idx - k2 * 2 * Q;
-        __stcg(zb + (long long)k2 * n * n + (j >> 1) * P + (j & 1), tile[tslot<Q>(k2, j)]);
-    }
+#pragma unroll 4
+    for (int k2 = sk2; k2 < H; k2 += KST)
+        __stcg(zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1), tile[tslot<Q>(k2, sj)]);
 }
 
 // ---------------------------------------------------------------- pass C
@@ -310,12 +312,11 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     // DB: band b+1's tile is loaded (cp.async) into the second buffer while band
     // b goes through the DFT / FFT / accumulate in the first
     constexpr bool DB = S::REC_DB;
+    const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
     auto load = [&](int b, C* buf) {
-        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P;
-        for (int idx = threadIdx.x; idx < n * P; idx += blockDim.x) {
-            const int i0 = idx / P, a = idx - i0 * P;
-            cp_async_c(buf + i0 * LD + a, z + (long long)i0 * n + a);
-        }
+        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P + (long long)si0 * n + sa;
+#pragma unroll 4
+        for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     C ar[E];
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         }
         __syncthreads();
         // twiddle w_n^{-a q}, length-P DFT over a -> p, for each i0
-        for (int i0 = threadIdx.x; i0 < n; i0 += blockDim.x) {
+        for (int i0 = threadIdx.x; i0 < n; i0 += S::AC_THREADS) {
             C v[P];
 #pragma unroll
             for (int a = 0; a < P; ++a) {
