@@ -79,7 +79,8 @@ struct SplitShape {
     static constexpr bool REC_DB = SLB_SPLIT_REC_DB;
 #endif
 #ifndef SLB_SPLIT_B_MINB
-    static constexpr int B_MINB = L >= 256 ? 1 : 3;
+    // 192: 2 CTAs/SM at <= 128 registers (no spills) measured +1.3 % on pass B over 3 at <= 85 (72 B spilled)
+    static constexpr int B_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 3);
 #else
     static constexpr int B_MINB = SLB_SPLIT_B_MINB;
 #endif
@@ -168,6 +169,51 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     }
 }
 
+// The pair-packed c2r input of rows (2 lq, 2 lq + 1) with each half-spectrum
+// entry read from the tile once: x[k] = X[k] + i Y[k] (k < H) and
+// x[L - k] = conj(X[k]) + i conj(Y[k]) are formed by the thread owning k; the
+// mirrored values travel to their owner (lane (T - t) mod T, register E - 1 - u)
+// by warp shuffles (lane 0 keeps its own, register E - u). Needs L = T E with
+// T a power of two <= 32 and the mirrored registers m > (H - 1) / T.
+#ifndef SLB_SPLIT_C2R_SHFL
+#define SLB_SPLIT_C2R_SHFL 1
+#endif
+template <int L, int T, int E, int Q, class C>
+__device__ __forceinline__ void c2r_pack_shfl(const C* __restrict__ tile, int lq, int t, C (&x)[E]) {
+    constexpr int H = L / 2 + 1;
+    constexpr int UD = (H - 1) / T;  // registers u < UD are direct on every lane; u = UD on lane 0 only (k = L/2 when T | L/2)
+    static_assert(T <= 32 && (T & (T - 1)) == 0 && T * E == L, "one power-of-two warp segment per line");
+    static_assert(L % 2 == 0 && (L / 2) % T == 0, "k = L/2 sits on lane 0");
+    C mir[UD];
+#pragma unroll
+    for (int u = 0; u <= UD; ++u) {
+        const int k = t + T * u;
+        if (u < UD || t == 0) {
+            C X = tile[tslot<Q>(k, 2 * lq)];
+            C Y = tile[tslot<Q>(k, 2 * lq + 1)];
+            if (u < UD) mir[u] = mkc<C>(X.x + Y.y, Y.x - X.y);  // the value at L - k
+            if (k == 0 || 2 * k == L) {
+                X.y = 0.0;
+                Y.y = 0.0;
+            }
+            x[u] = mkc<C>(X.x - Y.y, X.y + Y.x);
+        }
+    }
+    const int src = (T - t) & (T - 1);
+#pragma unroll
+    for (int m = UD; m < E; ++m) {
+        // lane t >= 1: k = t + T m mirrors k' = (T - t) + T (E - 1 - m) on lane T - t
+        C v;
+        v.x = __shfl_sync(0xffffffffu, mir[E - 1 - m < UD ? E - 1 - m : 0].x, src, T);
+        v.y = __shfl_sync(0xffffffffu, mir[E - 1 - m < UD ? E - 1 - m : 0].y, src, T);
+        if (t != 0) {
+            x[m] = v;
+        } else if (m > UD) {
+            x[m] = mir[E - m];  // lane 0: k = T m mirrors T (E - m), its own register
+        }
+    }
+}
+
 // ---------------------------------------------------------------- pass B
 enum SplitMid : int {
     kMidFused = 0,  // Z -> c2r, threshold, band store, r2c -> Z' (denoise)
@@ -212,22 +258,26 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
         }
         __syncthreads();
         // axis-2 c2r of the row pair (pair-packed, as k2_rows_c2r)
+        if constexpr (T <= 32 && SLB_SPLIT_C2R_SHFL) {
+            c2r_pack_shfl<L, T, E, Q>(tile, lq, t, x);
+        } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) {
-            const int k = t + T * m;
-            C X, Y;
-            if (k < H) {
-                X = tile[tslot<Q>(k, 2 * lq)];
-                Y = tile[tslot<Q>(k, 2 * lq + 1)];
-                if (k == 0 || 2 * k == L) {
-                    X.y = 0.0;
-                    Y.y = 0.0;
+            for (int m = 0; m < E; ++m) {
+                const int k = t + T * m;
+                C X, Y;
+                if (k < H) {
+                    X = tile[tslot<Q>(k, 2 * lq)];
+                    Y = tile[tslot<Q>(k, 2 * lq + 1)];
+                    if (k == 0 || 2 * k == L) {
+                        X.y = 0.0;
+                        Y.y = 0.0;
+                    }
+                    x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
+                } else {
+                    X = tile[tslot<Q>(L - k, 2 * lq)];
+                    Y = tile[tslot<Q>(L - k, 2 * lq + 1)];
+                    x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
                 }
-                x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
-            } else {
-                X = tile[tslot<Q>(L - k, 2 * lq)];
-                Y = tile[tslot<Q>(L - k, 2 * lq + 1)];
-                x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
             }
         }
         __syncthreads();  // the tile becomes the line buffers
