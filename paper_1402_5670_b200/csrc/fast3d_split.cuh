@@ -78,6 +78,17 @@ struct SplitShape {
 #else
     static constexpr bool REC_DB = SLB_SPLIT_REC_DB;
 #endif
+#ifndef SLB_SPLIT_B_DIRECT
+    // pass B's Q-DFTs straight from / to Z in registers (measured: 128^3 pass B -6 %, 192^3 +5 %)
+    static constexpr bool B_DIRECT = L <= 128;
+#else
+    static constexpr bool B_DIRECT = SLB_SPLIT_B_DIRECT;
+#endif
+#ifndef SLB_SPLIT_B_SWZ
+    static constexpr bool B_SWZ = true;  // the (k, e)-pair conflict-free tile swizzle (192^3 pass B -0.6 % with cp.async too)
+#else
+    static constexpr bool B_SWZ = SLB_SPLIT_B_SWZ;
+#endif
 #ifndef SLB_SPLIT_B_MINB
     // 192: 2 CTAs/SM at <= 128 registers (no spills) measured +1.3 % on pass B over 3 at <= 85 (72 B spilled)
     static constexpr int B_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 3);
@@ -169,6 +180,20 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     }
 }
 
+// Pass B tile [H][2Q]: slot rr of row k XOR-swizzled with a function of k mod 8
+// that keeps the per-line accesses (8 consecutive k, fixed rr), the row copies
+// (consecutive rr) and the (k, e)-pair Q-DFT accesses (4 consecutive k x 2 e,
+// slot 2 j + e) bank-conflict free for 16-byte elements. DIRECT: the Q-DFTs
+// read / write Z straight from / to registers (no cp.async staging, no tile
+// round trip for the copy-out).
+template <int Q, bool DIRECT>
+__device__ __forceinline__ int bslot(int k, int rr) {
+    if constexpr (DIRECT)
+        return k * (2 * Q) + (rr ^ (((k & 3) << 1) | ((k >> 2) & 1)));
+    else
+        return tslot<Q>(k, rr);
+}
+
 // The pair-packed c2r input of rows (2 lq, 2 lq + 1) with each half-spectrum
 // entry read from the tile once: x[k] = X[k] + i Y[k] (k < H) and
 // x[L - k] = conj(X[k]) + i conj(Y[k]) are formed by the thread owning k; the
@@ -178,7 +203,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
 #ifndef SLB_SPLIT_C2R_SHFL
 #define SLB_SPLIT_C2R_SHFL 1
 #endif
-template <int L, int T, int E, int Q, class C>
+template <int L, int T, int E, int Q, bool DIRECT, class C>
 __device__ __forceinline__ void c2r_pack_shfl(const C* __restrict__ tile, int lq, int t, C (&x)[E]) {
     constexpr int H = L / 2 + 1;
     constexpr int UD = (H - 1) / T;  // registers u < UD are direct on every lane; u = UD on lane 0 only (k = L/2 when T | L/2)
@@ -189,8 +214,8 @@ __device__ __forceinline__ void c2r_pack_shfl(const C* __restrict__ tile, int lq
     for (int u = 0; u <= UD; ++u) {
         const int k = t + T * u;
         if (u < UD || t == 0) {
-            C X = tile[tslot<Q>(k, 2 * lq)];
-            C Y = tile[tslot<Q>(k, 2 * lq + 1)];
+            C X = tile[bslot<Q, DIRECT>(k, 2 * lq)];
+            C Y = tile[bslot<Q, DIRECT>(k, 2 * lq + 1)];
             if (u < UD) mir[u] = mkc<C>(X.x + Y.y, Y.x - X.y);  // the value at L - k
             if (k == 0 || 2 * k == L) {
                 X.y = 0.0;
@@ -229,7 +254,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, H = S::H, n = L;
     constexpr int KPT = (H + T - 1) / T;
-    SLB_DYN_SMEM(C, tile);  // [H][2Q] tslot<Q>; line buffers alias it
+    SLB_DYN_SMEM(C, tile);  // [H][2Q] bslot<Q>; line buffers alias it
     const int i0 = blockIdx.x / (P / 2), a0 = 2 * (blockIdx.x - i0 * (P / 2));
     const int bi = blockIdx.y;
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
@@ -237,45 +262,60 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     C* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
     C* lb = tile + lq * S::LB;
     constexpr int KST = S::B_THREADS / (2 * Q);  // k2 rows per tile-copy step
-    const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
+    [[maybe_unused]] const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
     C x[E];
     if constexpr (MODE != kMidRec) {
-        // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
+        if constexpr (S::B_DIRECT) {
+            // length-Q DFT over q for each (k2, e) straight from Z (lane pairs e = 0, 1
+            // read one 32-byte sector per q), result into slot 2c + e
+            for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
+                const int k2 = idx >> 1, e = idx & 1;
+                const C* zq = zb + (long long)k2 * n * n + e;
+                C v[Q];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) v[j] = __ldcg(zq + j * P);
+                dft_small<Q, +1>(v);
+#pragma unroll
+                for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+            }
+        } else {
+            // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
 #pragma unroll 4
-        for (int k2 = sk2; k2 < H; k2 += KST)
-            cp_async_c(tile + tslot<Q>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1));
-        cp_async_wait_all();
-        __syncthreads();
-        // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
-        for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
-            const int e = idx / H, k2 = idx - e * H;
-            C v[Q];
+            for (int k2 = sk2; k2 < H; k2 += KST)
+                cp_async_c(tile + bslot<Q, S::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1));
+            cp_async_wait_all();
+            __syncthreads();
+            // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
+            for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
+                const int e = idx / H, k2 = idx - e * H;
+                C v[Q];
 #pragma unroll
-            for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
-            dft_small<Q, +1>(v);
+                for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+                dft_small<Q, +1>(v);
 #pragma unroll
-            for (int j = 0; j < Q; ++j) tile[tslot<Q>(k2, 2 * j + e)] = v[j];
+                for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+            }
         }
         __syncthreads();
         // axis-2 c2r of the row pair (pair-packed, as k2_rows_c2r)
         if constexpr (T <= 32 && SLB_SPLIT_C2R_SHFL) {
-            c2r_pack_shfl<L, T, E, Q>(tile, lq, t, x);
+            c2r_pack_shfl<L, T, E, Q, S::B_SWZ>(tile, lq, t, x);
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int k = t + T * m;
                 C X, Y;
                 if (k < H) {
-                    X = tile[tslot<Q>(k, 2 * lq)];
-                    Y = tile[tslot<Q>(k, 2 * lq + 1)];
+                    X = tile[bslot<Q, S::B_SWZ>(k, 2 * lq)];
+                    Y = tile[bslot<Q, S::B_SWZ>(k, 2 * lq + 1)];
                     if (k == 0 || 2 * k == L) {
                         X.y = 0.0;
                         Y.y = 0.0;
                     }
                     x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
                 } else {
-                    X = tile[tslot<Q>(L - k, 2 * lq)];
-                    Y = tile[tslot<Q>(L - k, 2 * lq + 1)];
+                    X = tile[bslot<Q, S::B_SWZ>(L - k, 2 * lq)];
+                    Y = tile[bslot<Q, S::B_SWZ>(L - k, 2 * lq + 1)];
                     x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
                 }
             }
@@ -326,25 +366,38 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            tile[tslot<Q>(k, 2 * lq)] = mkc<C>(RealOf<C>(0.5) * (zk[u].x + zm[u].x), RealOf<C>(0.5) * (zk[u].y - zm[u].y));
-            tile[tslot<Q>(k, 2 * lq + 1)] = mkc<C>(RealOf<C>(0.5) * (zk[u].y + zm[u].y), RealOf<C>(0.5) * (zm[u].x - zk[u].x));
+            tile[bslot<Q, S::B_SWZ>(k, 2 * lq)] = mkc<C>(RealOf<C>(0.5) * (zk[u].x + zm[u].x), RealOf<C>(0.5) * (zk[u].y - zm[u].y));
+            tile[bslot<Q, S::B_SWZ>(k, 2 * lq + 1)] = mkc<C>(RealOf<C>(0.5) * (zk[u].y + zm[u].y), RealOf<C>(0.5) * (zm[u].x - zk[u].x));
         }
     }
     __syncthreads();
-    // length-Q DFT back over c for each (k2, e): slot 2c + e -> 2q + e
-    for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
-        const int e = idx / H, k2 = idx - e * H;
-        C v[Q];
+    // length-Q DFT back over c for each (k2, e): slot 2c + e -> q
+    if constexpr (S::B_DIRECT) {
+        for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
+            const int k2 = idx >> 1, e = idx & 1;
+            C v[Q];
 #pragma unroll
-        for (int j = 0; j < Q; ++j) v[j] = tile[tslot<Q>(k2, 2 * j + e)];
-        dft_small<Q, -1>(v);
+            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+            dft_small<Q, -1>(v);
+            C* zq = zb + (long long)k2 * n * n + e;
 #pragma unroll
-        for (int j = 0; j < Q; ++j) tile[tslot<Q>(k2, 2 * j + e)] = v[j];
-    }
-    __syncthreads();
+            for (int j = 0; j < Q; ++j) __stcg(zq + j * P, v[j]);
+        }
+    } else {
+        for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
+            const int e = idx / H, k2 = idx - e * H;
+            C v[Q];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+            dft_small<Q, -1>(v);
+#pragma unroll
+            for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+        }
+        __syncthreads();
 #pragma unroll 4
-    for (int k2 = sk2; k2 < H; k2 += KST)
-        __stcg(zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1), tile[tslot<Q>(k2, sj)]);
+        for (int k2 = sk2; k2 < H; k2 += KST)
+            __stcg(zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1), tile[bslot<Q, S::B_SWZ>(k2, sj)]);
+    }
 }
 
 // ---------------------------------------------------------------- pass C
