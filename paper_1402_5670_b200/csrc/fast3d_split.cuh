@@ -78,6 +78,12 @@ struct SplitShape {
 #else
     static constexpr bool REC_DB = SLB_SPLIT_REC_DB;
 #endif
+#ifndef SLB_SPLIT_ZQUAD
+    // quad-interleaved Z rows (zrow): measured 192^3 +0.7 % (pass B -5 %, A / C +3-4 %), 128^3 -5 %
+    static constexpr bool ZQUAD = L == 192;
+#else
+    static constexpr bool ZQUAD = SLB_SPLIT_ZQUAD;
+#endif
 #ifndef SLB_SPLIT_B_DIRECT
     // pass B's Q-DFTs straight from / to Z in registers (measured: 128^3 pass B -6 %, 192^3 +5 %)
     static constexpr bool B_DIRECT = L <= 128;
@@ -96,6 +102,22 @@ struct SplitShape {
     static constexpr int B_MINB = SLB_SPLIT_B_MINB;
 #endif
 };
+
+// Offset of (q, a) inside one n-long Z row. ZQUAD: a is split into quads
+// a = 4 aq + ar and the row is [aq][q][ar], so pass A / C's per-(k2, q) tiles
+// move 64-byte runs and pass B's per-(i0, a pair) tiles 32-byte chunks at a
+// 64-byte stride (8 lines per warp access instead of 16 for pass B; 3 lines per
+// i0 for A / C instead of 2). Otherwise [q][a]: 192-byte runs for A / C, 32-byte
+// chunks at a P * 16-byte stride for B.
+template <int P, int Q, bool QUAD>
+__host__ __device__ __forceinline__ int zrow(int q, int a) {
+    if constexpr (QUAD) {
+        static_assert(P % 4 == 0, "quads of a");
+        return (a >> 2) * (4 * Q) + q * 4 + (a & 3);
+    } else {
+        return q * P + a;
+    }
+}
 
 // pass A keeps its F lines in registers across the band group (1) or reloads
 // them per band from L2 (0: 24 fewer registers at 192)
@@ -174,7 +196,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         // the CTA's P * T threads cover T rows i0 of P entries per step (row
         // offsets by compile-time strides, no per-element division)
         const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
-        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + q * P + (long long)si0 * n + sa;
+        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + zrow<P, Q, S::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
         for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, tile[(si0 + T * j) * LD + sa]);
     }
@@ -259,7 +281,8 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     const int bi = blockIdx.y;
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
-    C* zb = Z + (long long)bi * zbs + (long long)i0 * n + a0;  // + k2 n n + q P + e
+    C* zb = Z + (long long)bi * zbs + (long long)i0 * n + zrow<P, Q, S::ZQUAD>(0, a0);  // + k2 n n + q ZS + e
+    constexpr int ZS = S::ZQUAD ? 4 : P;  // distance between consecutive q at fixed a
     C* lb = tile + lq * S::LB;
     constexpr int KST = S::B_THREADS / (2 * Q);  // k2 rows per tile-copy step
     [[maybe_unused]] const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
@@ -273,7 +296,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
                 const C* zq = zb + (long long)k2 * n * n + e;
                 C v[Q];
 #pragma unroll
-                for (int j = 0; j < Q; ++j) v[j] = __ldcg(zq + j * P);
+                for (int j = 0; j < Q; ++j) v[j] = __ldcg(zq + j * ZS);
                 dft_small<Q, +1>(v);
 #pragma unroll
                 for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
@@ -282,7 +305,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
             // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
 #pragma unroll 4
             for (int k2 = sk2; k2 < H; k2 += KST)
-                cp_async_c(tile + bslot<Q, S::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1));
+                cp_async_c(tile + bslot<Q, S::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
             cp_async_wait_all();
             __syncthreads();
             // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
@@ -381,7 +404,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
             dft_small<Q, -1>(v);
             C* zq = zb + (long long)k2 * n * n + e;
 #pragma unroll
-            for (int j = 0; j < Q; ++j) __stcg(zq + j * P, v[j]);
+            for (int j = 0; j < Q; ++j) __stcg(zq + j * ZS, v[j]);
         }
     } else {
         for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
@@ -396,7 +419,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
         __syncthreads();
 #pragma unroll 4
         for (int k2 = sk2; k2 < H; k2 += KST)
-            __stcg(zb + (long long)k2 * n * n + (sj >> 1) * P + (sj & 1), tile[bslot<Q, S::B_SWZ>(k2, sj)]);
+            __stcg(zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1), tile[bslot<Q, S::B_SWZ>(k2, sj)]);
     }
 }
 
@@ -417,7 +440,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     constexpr bool DB = S::REC_DB;
     const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
     auto load = [&](int b, C* buf) {
-        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + q * P + (long long)si0 * n + sa;
+        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + zrow<P, Q, S::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
         for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
         asm volatile("cp.async.commit_group;" ::: "memory");
