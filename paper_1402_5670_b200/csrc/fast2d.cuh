@@ -237,14 +237,14 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS)
         mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);
     } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) lb[swz<false, L>(t + T * m)] = x[m];
+        for (int m = 0; m < E; ++m) lb[swz<false, L, sizeof(C)>(t + T * m)] = x[m];
         line_sync<T>();
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
             const int k = t + T * u;
             if (k < H) {
-                zk[u] = lb[swz<false, L>(k)];
-                zm[u] = lb[swz<false, L>(k == 0 ? 0 : L - k)];
+                zk[u] = lb[swz<false, L, sizeof(C)>(k)];
+                zm[u] = lb[swz<false, L, sizeof(C)>(k == 0 ? 0 : L - k)];
             }
         }
     }

@@ -92,14 +92,14 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
     } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) lb[swz<PAD, L>(t + T * m)] = x[m];
+        for (int m = 0; m < E; ++m) lb[swz<PAD, L, sizeof(C)>(t + T * m)] = x[m];
         line_sync<T>();
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
             const int k = t + T * u;
             if (k < H) {
-                zk[u] = lb[swz<PAD, L>(k)];
-                zm[u] = lb[swz<PAD, L>(k == 0 ? 0 : L - k)];
+                zk[u] = lb[swz<PAD, L, sizeof(C)>(k)];
+                zm[u] = lb[swz<PAD, L, sizeof(C)>(k == 0 ? 0 : L - k)];
             }
         }
     }

@@ -101,6 +101,7 @@ struct SplitShape {
 #else
     static constexpr int B_MINB = SLB_SPLIT_B_MINB;
 #endif
+
 };
 
 // Offset of (q, a) inside one n-long Z row. ZQUAD: a is split into quads
@@ -118,6 +119,22 @@ __host__ __device__ __forceinline__ int zrow(int q, int a) {
         return q * P + a;
     }
 }
+
+// pass B occupancy: the fp32 mode keeps 3 CTAs/SM below 256 (measured 2.6 %
+// faster than 2 at 192), fp64 takes SplitShape::B_MINB
+template <int L, class C>
+struct SplitMinB {
+    static constexpr int value = sizeof(C) == 16 ? SplitShape<L>::B_MINB : (L >= 256 ? 1 : 3);
+};
+// layout choices per precision: the fp32 mode (8-byte elements) measured 7 %
+// faster at 192^3 with neither the quad-interleaved Z rows nor the pass-B swizzle
+// (profiles/r2_ab_f32_layout.log)
+template <int L, class C>
+struct SplitLayout {
+    static constexpr bool ZQUAD = sizeof(C) == 16 && SplitShape<L>::ZQUAD;
+    static constexpr bool B_SWZ = sizeof(C) == 16 && SplitShape<L>::B_SWZ;
+    static constexpr bool B_DIRECT = sizeof(C) == 16 && SplitShape<L>::B_DIRECT;  // measured in fp64 only
+};
 
 // pass A keeps its F lines in registers across the band group (1) or reloads
 // them per band from L2 (0: 24 fewer registers at 192)
@@ -196,7 +213,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
         // the CTA's P * T threads cover T rows i0 of P entries per step (row
         // offsets by compile-time strides, no per-element division)
         const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
-        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + zrow<P, Q, S::ZQUAD>(q, sa) + (long long)si0 * n;
+        C* z = Z + (long long)(g0 + bb) * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
         for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, tile[(si0 + T * j) * LD + sa]);
     }
@@ -269,7 +286,7 @@ enum SplitMid : int {
 };
 
 template <int L, int MODE, bool STORE, class C = double2>
-__global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MINB)
+__global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::value)
     k3s_mid(C* __restrict__ Z, long long zbs, RealOf<C>* __restrict__ band, long long bbs,
             const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
             const C* __restrict__ tw) {
@@ -281,14 +298,14 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     const int bi = blockIdx.y;
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
-    C* zb = Z + (long long)bi * zbs + (long long)i0 * n + zrow<P, Q, S::ZQUAD>(0, a0);  // + k2 n n + q ZS + e
-    constexpr int ZS = S::ZQUAD ? 4 : P;  // distance between consecutive q at fixed a
+    C* zb = Z + (long long)bi * zbs + (long long)i0 * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(0, a0);  // + k2 n n + q ZS + e
+    constexpr int ZS = SplitLayout<L, C>::ZQUAD ? 4 : P;  // distance between consecutive q at fixed a
     C* lb = tile + lq * S::LB;
     constexpr int KST = S::B_THREADS / (2 * Q);  // k2 rows per tile-copy step
     [[maybe_unused]] const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
     C x[E];
     if constexpr (MODE != kMidRec) {
-        if constexpr (S::B_DIRECT) {
+        if constexpr (SplitLayout<L, C>::B_DIRECT) {
             // length-Q DFT over q for each (k2, e) straight from Z (lane pairs e = 0, 1
             // read one 32-byte sector per q), result into slot 2c + e
             for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
@@ -299,13 +316,13 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
                 for (int j = 0; j < Q; ++j) v[j] = __ldcg(zq + j * ZS);
                 dft_small<Q, +1>(v);
 #pragma unroll
-                for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+                for (int j = 0; j < Q; ++j) tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)] = v[j];
             }
         } else {
             // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
 #pragma unroll 4
             for (int k2 = sk2; k2 < H; k2 += KST)
-                cp_async_c(tile + bslot<Q, S::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
+                cp_async_c(tile + bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
             cp_async_wait_all();
             __syncthreads();
             // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
@@ -313,32 +330,32 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
                 const int e = idx / H, k2 = idx - e * H;
                 C v[Q];
 #pragma unroll
-                for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+                for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)];
                 dft_small<Q, +1>(v);
 #pragma unroll
-                for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+                for (int j = 0; j < Q; ++j) tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)] = v[j];
             }
         }
         __syncthreads();
         // axis-2 c2r of the row pair (pair-packed, as k2_rows_c2r)
         if constexpr (T <= 32 && SLB_SPLIT_C2R_SHFL) {
-            c2r_pack_shfl<L, T, E, Q, S::B_SWZ>(tile, lq, t, x);
+            c2r_pack_shfl<L, T, E, Q, SplitLayout<L, C>::B_SWZ>(tile, lq, t, x);
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 const int k = t + T * m;
                 C X, Y;
                 if (k < H) {
-                    X = tile[bslot<Q, S::B_SWZ>(k, 2 * lq)];
-                    Y = tile[bslot<Q, S::B_SWZ>(k, 2 * lq + 1)];
+                    X = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k, 2 * lq)];
+                    Y = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k, 2 * lq + 1)];
                     if (k == 0 || 2 * k == L) {
                         X.y = 0.0;
                         Y.y = 0.0;
                     }
                     x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
                 } else {
-                    X = tile[bslot<Q, S::B_SWZ>(L - k, 2 * lq)];
-                    Y = tile[bslot<Q, S::B_SWZ>(L - k, 2 * lq + 1)];
+                    X = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(L - k, 2 * lq)];
+                    Y = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(L - k, 2 * lq + 1)];
                     x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
                 }
             }
@@ -373,14 +390,14 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
         mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
     } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) lb[swz<S::PAD, L>(t + T * m)] = x[m];
+        for (int m = 0; m < E; ++m) lb[swz<S::PAD, L, sizeof(C)>(t + T * m)] = x[m];
         line_sync<T>();
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
             const int k = t + T * u;
             if (k < H) {
-                zk[u] = lb[swz<S::PAD, L>(k)];
-                zm[u] = lb[swz<S::PAD, L>(k == 0 ? 0 : L - k)];
+                zk[u] = lb[swz<S::PAD, L, sizeof(C)>(k)];
+                zm[u] = lb[swz<S::PAD, L, sizeof(C)>(k == 0 ? 0 : L - k)];
             }
         }
     }
@@ -389,18 +406,18 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
     for (int u = 0; u < KPT; ++u) {
         const int k = t + T * u;
         if (k < H) {
-            tile[bslot<Q, S::B_SWZ>(k, 2 * lq)] = mkc<C>(RealOf<C>(0.5) * (zk[u].x + zm[u].x), RealOf<C>(0.5) * (zk[u].y - zm[u].y));
-            tile[bslot<Q, S::B_SWZ>(k, 2 * lq + 1)] = mkc<C>(RealOf<C>(0.5) * (zk[u].y + zm[u].y), RealOf<C>(0.5) * (zm[u].x - zk[u].x));
+            tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k, 2 * lq)] = mkc<C>(RealOf<C>(0.5) * (zk[u].x + zm[u].x), RealOf<C>(0.5) * (zk[u].y - zm[u].y));
+            tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k, 2 * lq + 1)] = mkc<C>(RealOf<C>(0.5) * (zk[u].y + zm[u].y), RealOf<C>(0.5) * (zm[u].x - zk[u].x));
         }
     }
     __syncthreads();
     // length-Q DFT back over c for each (k2, e): slot 2c + e -> q
-    if constexpr (S::B_DIRECT) {
+    if constexpr (SplitLayout<L, C>::B_DIRECT) {
         for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
             const int k2 = idx >> 1, e = idx & 1;
             C v[Q];
 #pragma unroll
-            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)];
             dft_small<Q, -1>(v);
             C* zq = zb + (long long)k2 * n * n + e;
 #pragma unroll
@@ -411,15 +428,15 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitShape<L>::B_MIN
             const int e = idx / H, k2 = idx - e * H;
             C v[Q];
 #pragma unroll
-            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)];
+            for (int j = 0; j < Q; ++j) v[j] = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)];
             dft_small<Q, -1>(v);
 #pragma unroll
-            for (int j = 0; j < Q; ++j) tile[bslot<Q, S::B_SWZ>(k2, 2 * j + e)] = v[j];
+            for (int j = 0; j < Q; ++j) tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)] = v[j];
         }
         __syncthreads();
 #pragma unroll 4
         for (int k2 = sk2; k2 < H; k2 += KST)
-            __stcg(zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1), tile[bslot<Q, S::B_SWZ>(k2, sj)]);
+            __stcg(zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1), tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj)]);
     }
 }
 
@@ -440,7 +457,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, SplitShape<L>::AC_M
     constexpr bool DB = S::REC_DB;
     const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
     auto load = [&](int b, C* buf) {
-        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + zrow<P, Q, S::ZQUAD>(q, sa) + (long long)si0 * n;
+        const C* z = Z + (long long)b * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
         for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
         asm volatile("cp.async.commit_group;" ::: "memory");
