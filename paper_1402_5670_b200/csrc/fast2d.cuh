@@ -131,9 +131,19 @@ struct ColRec {
 #else
     static constexpr bool PF = SLB_COLREC_PF;
 #endif
+    // CPA: band b+1's line is copied (cp.async, double-buffered per line) while
+    // band b is in the FFT. Measured: the kernel alone -5 %, but the 4-stream
+    // lock-step batch -3 % (51 KB instead of 18 KB of smem per CTA crowds out the
+    // concurrently resident passes; profiles/r2_ab_colrec_cpa.log) -> opt-in
+#ifndef SLB_COLREC_CPA
+    static constexpr bool CPA = false;
+#else
+    static constexpr bool CPA = !PF && REGACC && SLB_COLREC_CPA;
+#endif
 };
 template <int L, class C = double2>
-static size_t colrec_smem_bytes() {  // register accumulator: exchange buffers only
+static size_t colrec_smem_bytes() {  // register accumulator: exchange buffers (+ 2 staged lines per line with CPA)
+    if (ColRec<L>::CPA) return static_cast<size_t>(ColCfg<L>::LINES) * (LineBuf<L>::N + 2 * L) * sizeof(C);
     return ColRec<L>::REGACC ? col1_smem_bytes<L, C>() : col2_smem_bytes<L, C>();
 }
 
@@ -419,7 +429,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;
     const bool valid = k1 < H;
     // per line: [exchange L] (+ [accumulator L] unless it lives in registers)
-    C* sm = lbuf + li * (LineBuf<L>::N + (ColRec<L>::REGACC ? 0 : L));
+    C* sm = lbuf + li * (LineBuf<L>::N + (ColRec<L>::CPA ? 2 * L : (ColRec<L>::REGACC ? 0 : L)));
     C* acc = sm + LineBuf<L>::N;  // thread t owns acc[t + T m]
     C ar[E];
 #pragma unroll
@@ -443,11 +453,35 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
             pn[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
     }
+    constexpr bool CPA = ColRec<L>::CPA;
+    C* stg = sm + LineBuf<L>::N;  // CPA: two staged lines [2][L] after the exchange buffer
+    auto stage = [&](int b, int buf) {  // each thread copies exactly the elements it reads back
+        if (valid) {
+            const C* in = inter + (long long)b * ibs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) cp_async_c(stg + buf * L + t + T * m, in + t + T * m);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (CPA && gn > 0) stage(g0, 0);
     for (int bb = 0; bb < gn; ++bb) {
         const int b = g0 + bb;
         C x[E];
         R p[E];
-        if (PF) {
+        if (CPA) {
+            if (bb + 1 < gn) {
+                stage(b + 1, (bb + 1) & 1);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // band b landed, b+1 in flight
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            const C* cur = stg + (bb & 1) * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) x[m] = valid ? cur[t + T * m] : mkc<C>(0.0, 0.0);
+            const R* ps = psiT + (long long)(band0 + b) * pbs + (long long)k1 * L;
+#pragma unroll
+            for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
+        } else if (PF) {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
                 x[m] = xn[m];
