@@ -732,13 +732,17 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             // launch per pass covers both frames, as in the device batch)
             const int want_grp = s.knobs.pipe_group >= 1 ? s.knobs.pipe_group : (many ? 2 : 1);
             const int head = s.knobs.pipe_head >= 0 ? s.knobs.pipe_head : (many ? 1 : 0);
+            // the last `tail` frames alone too: the compute streams finish single
+            // frames instead of pairs, so less D2H is left after the last kernel
+            const int tail = s.knobs.pipe_tail >= 0 ? s.knobs.pipe_tail : 0;
             const int grp = lockstep_batch(s, nframes) ? std::max(1, std::min(nframes, want_grp)) : 1;
             if (grp > 1 && s.Wmin < 1e-12) throw SlError(SL_ERR_SINGULAR_FRAME, "inverse: frame weight below 1e-12");
             // segments: the first `head` frames alone (compute starts after one
             // frame's H2D), then lock-step groups of grp frames
             std::vector<std::pair<int, int>> seg;
             for (int f0 = 0; f0 < nframes;) {
-                const int nf = static_cast<int>(seg.size()) < head ? 1 : std::min(grp, nframes - f0);
+                const bool single = static_cast<int>(seg.size()) < head || nframes - f0 <= tail;
+                const int nf = single ? 1 : std::min(grp, nframes - f0);
                 seg.emplace_back(f0, nf);
                 f0 += nf;
             }
