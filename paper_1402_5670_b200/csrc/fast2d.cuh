@@ -70,6 +70,9 @@ struct RowCfg {
     static constexpr int V = (SLB_ROW_THREADS / T) > 0 ? SLB_ROW_THREADS / T : 1;
 #endif
     static constexpr int THREADS = V * T;
+    // the fused rows kernel: the same V row pairs with its own line split
+    static constexpr int FUSED_T = FusedRowPlan<L>::T;
+    static constexpr int FUSED_THREADS = V * FUSED_T;
 #ifndef SLB_ROWS_PAD
     static constexpr bool PAD = false;  // padded line buffers in the fused rows kernel (A/B: -DSLB_ROWS_PAD=1)
 #else

@@ -17,11 +17,11 @@ namespace slb {
 // null); a separate instantiation so the stack-writing variant keeps its
 // register allocation (a runtime null test spilled 136 B/thread at L = 128)
 template <int L, bool STORE = true, class C = double2>
-__global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
+__global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
     k2_rows_fused(C* __restrict__ inter, long long ibs, RealOf<C>* __restrict__ band, long long bbs, int n0, int H,
                   RealOf<C> scale, const double* __restrict__ delta, int band0, const C* __restrict__ tw,
                   long long izs = 0, long long bzs = 0) {
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E, V = RowCfg<L>::V;
+    constexpr int T = FusedRowPlan<L>::T, E = FusedRowPlan<L>::E, V = RowCfg<L>::V;
     using R = RealOf<C>;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;
     SLB_DYN_SMEM(C, tile);  // [H][2V] swizzled tile, then V line buffers
@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     if (!kTest || band) band += blockIdx.y * bbs + blockIdx.z * bzs;
     const int nrows = min(2 * V, n0 - r0);
     // thread -> fixed slot rr, k-rows strided by a compile-time step
-    constexpr int KS = RowCfg<L>::THREADS / (2 * V);
+    constexpr int KS = RowCfg<L>::FUSED_THREADS / (2 * V);
     const int rr = threadIdx.x % (2 * V);
 #pragma unroll 4
     for (int k = threadIdx.x / (2 * V); k < H; k += KS) {
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
     __syncthreads();              // every line has gathered: the tile is dead
     constexpr bool PAD = RowCfg<L>::PAD;
     C* lb = tile + q * LineBuf<L, PAD>::N;   // line buffers alias it (smem sized for both)
-    reg_fft<L, +1, PAD>(x, lb, t, tw);
+    reg_fft_p<FusedRowPlan<L>, L, +1, PAD>(x, lb, t, tw);
     const double dl = delta[band0 + blockIdx.y];
     const int ra = r0 + 2 * q;
 #pragma unroll
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(RowCfg<L>::THREADS, RowCfg<L>::FUSED_MIN_BLOCK
         }
         x[m] = mkc<C>(ra < n0 ? a : 0.0, ra + 1 < n0 ? c : R(0));  // rec input: the thresholded rows
     }
-    reg_fft<L, -1, PAD>(x, lb, t, tw);
+    reg_fft_p<FusedRowPlan<L>, L, -1, PAD>(x, lb, t, tw);
     C zk[KPT], zm[KPT];
     if constexpr (T <= 32 && SLB_ROWS_SHFL) {
         mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
@@ -126,7 +126,7 @@ static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, C* i
     using RC = RowCfg<L>;
     auto* k = band ? k2_rows_fused<L, true, C> : k2_rows_fused<L, false, C>;
     set_smem(k, tile_smem);
-    k<<<grid, RC::THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
+    k<<<grid, RC::FUSED_THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
     check_launch("k2_rows_fused");
 }
 

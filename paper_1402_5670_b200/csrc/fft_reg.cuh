@@ -67,6 +67,21 @@ SLB_REG_PLAN(1024, 64, 16, 8, 8)
 SLB_REG_PLAN(2048, 128, 16, 16, 8)
 SLB_REG_PLAN(192, 8, 8, 8, 3)
 #endif
+// plan of the fused rows kernel (k2_rows_fused): RegPlan<L> except 512, which
+// runs 32 threads x 16 complex per line there (warp-synchronous exchanges, r2c
+// mirror pairs by shuffles): measured 2D 512^2 batch +5 % over 64 x 8
+// (profiles/r2_ab_fused_rowplan.log; -DSLB_FUSEDPLAN512_T64 restores 64 x 8)
+template <int L>
+struct FusedRowPlan : RegPlan<L> {};
+#ifndef SLB_FUSEDPLAN512_T64
+template <>
+struct FusedRowPlan<512> {
+    static constexpr int T = 32;
+    static constexpr int E = 16;
+    static constexpr int R[] = {8, 8, 8};
+    static constexpr int NST = 3;
+};
+#endif
 #undef SLB_REG_PLAN
 
 template <int L>
@@ -259,14 +274,24 @@ __device__ __forceinline__ void bfly_strided(C (&x)[E], int q, int B) {
     for (int r = 0; r < R; ++r) x[q + B * r] = v[r];
 }
 
-template <int L, int DIR, int S, bool PAD, class C = double2>
+// product of the first S radices of plan PL
+template <class PL, int S>
+struct PlanNS {
+    static constexpr int value = PlanNS<PL, S - 1>::value * PL::R[S - 1];
+};
+template <class PL>
+struct PlanNS<PL, 0> {
+    static constexpr int value = 1;
+};
+
+template <int L, int DIR, int S, bool PAD, class C = double2, class PL = RegPlan<L>>
 struct RegStage {
-    using P = RegPlan<L>;
+    using P = PL;
     static constexpr int R = P::R[S];
     static constexpr int E = P::E;
     static constexpr int T = P::T;
     static constexpr int B = E / R;
-    static constexpr int NS = plan_ns<L>(S);
+    static constexpr int NS = PlanNS<PL, S>::value;
     static_assert(E % R == 0, "radix must divide the per-thread element count");
 
     __device__ __forceinline__ static void run(C (&x)[E], C* sm, int t, const C* __restrict__ tw) {
@@ -307,7 +332,7 @@ struct RegStage {
                 for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD, L, sizeof(C)>(j + r * (L / R2))];
             }
             line_sync<T>();
-            RegStage<L, DIR, S + 1, PAD, C>::run(x, sm, t, tw);
+            RegStage<L, DIR, S + 1, PAD, C, PL>::run(x, sm, t, tw);
         }
     }
 };
@@ -336,6 +361,13 @@ __device__ __forceinline__ void mirror_pairs_shfl(const C (&x)[E], C (&zk)[KPT],
 template <int L, int DIR, bool PAD = true, class C>
 __device__ __forceinline__ void reg_fft(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
     RegStage<L, DIR, 0, PAD, C>::run(x, sm, t, tw);
+}
+// the same with an explicit plan (a kernel family may use another T / E split
+// of the same length; the first radix must match RegPlan<L>'s for the swizzle)
+template <class PL, int L, int DIR, bool PAD = true, class C>
+__device__ __forceinline__ void reg_fft_p(C (&x)[PL::E], C* sm, int t, const C* __restrict__ tw) {
+    static_assert(PL::R[0] == RegPlan<L>::R[0], "line-buffer swizzle follows RegPlan<L>'s first radix");
+    RegStage<L, DIR, 0, PAD, C, PL>::run(x, sm, t, tw);
 }
 
 }  // namespace slb
