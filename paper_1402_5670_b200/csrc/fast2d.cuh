@@ -89,7 +89,7 @@ struct RowCfg {
 };
 template <int L>
 struct ColCfg {
-    static constexpr int T = RegPlan<L>::T;
+    static constexpr int T = ColPlan<L>::T;
 #ifndef SLB_COL_THREADS
     static constexpr int LINES = (128 / T) > 0 ? 128 / T : 1;
 #else
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
                 const C* __restrict__ tw, long long fzs = 0, long long izs = 0) {
     FT += blockIdx.z * fzs;  // blockIdx.z: frame of a lock-step batch
     inter += blockIdx.z * izs;
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    constexpr int T = ColPlan<L>::T, E = ColPlan<L>::E;
     using R = RealOf<C>;
     SLB_DYN_SMEM(C, lbuf);  // per line: [exchange L][F column L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
 #pragma unroll
             for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
-        reg_fft<L, +1>(x, sm, t, tw);
+        reg_fft_p<ColPlan<L>, L, +1>(x, sm, t, tw);
         if (valid) {
             C* o = inter + (long long)b * ibs + (long long)k1 * L;
 #pragma unroll
@@ -370,7 +370,7 @@ template <int L, int DIR, class C = double2>
 __device__ __forceinline__ void cols_sum_line(const C* __restrict__ slots, long long sbs, int nslots,
                                               const RealOf<C>* __restrict__ WT, C* __restrict__ out, int k1,
                                               bool valid, C* sm, int t, const C* __restrict__ tw) {
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    constexpr int T = ColPlan<L>::T, E = ColPlan<L>::E;
     using R = RealOf<C>;
     C x[E];
 #pragma unroll
@@ -403,7 +403,7 @@ __device__ __forceinline__ void cols_sum_line(const C* __restrict__ slots, long 
             }
         }
     }
-    reg_fft<L, DIR>(x, sm, t, tw);
+    reg_fft_p<ColPlan<L>, L, DIR>(x, sm, t, tw);
     if (valid) {
         C* o = out + (long long)k1 * L;
 #pragma unroll
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
     slots += blockIdx.z * szs;
     fout += blockIdx.z * fozs;
     if (done) done += blockIdx.z * gridDim.x;
-    constexpr int T = RegPlan<L>::T, E = RegPlan<L>::E;
+    constexpr int T = ColPlan<L>::T, E = ColPlan<L>::E;
     using R = RealOf<C>;
     SLB_DYN_SMEM(C, lbuf);  // per line: [exchange L][accumulator L]
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
 #pragma unroll
             for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
-        reg_fft<L, -1>(x, sm, t, tw);
+        reg_fft_p<ColPlan<L>, L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             C a = ColRec<L>::REGACC ? ar[m] : acc[t + T * m];
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS)
                 long long ozs = 0) {
     slots += blockIdx.z * szs;  // blockIdx.z: frame of a lock-step batch
     out += blockIdx.z * ozs;
-    constexpr int T = RegPlan<L>::T;
+    constexpr int T = ColPlan<L>::T;
     SLB_DYN_SMEM(C, lbuf);
     const int li = threadIdx.x / T, t = threadIdx.x - li * T;
     const int k1 = blockIdx.x * ColCfg<L>::LINES + li;

@@ -82,6 +82,19 @@ struct FusedRowPlan<512> {
     static constexpr int NST = 3;
 };
 #endif
+// plan of the 2D column kernels (k2_cols_dec / rec / sum): RegPlan<L> unless a
+// column-specific split is selected (A/B: -DSLB_COLPLAN512_T32)
+template <int L>
+struct ColPlan : RegPlan<L> {};
+#ifdef SLB_COLPLAN512_T32
+template <>
+struct ColPlan<512> {
+    static constexpr int T = 32;
+    static constexpr int E = 16;
+    static constexpr int R[] = {8, 8, 8};
+    static constexpr int NST = 3;
+};
+#endif
 #undef SLB_REG_PLAN
 
 template <int L>
