@@ -472,6 +472,7 @@ static void build_3d(System& s, const Bank& bank, cudaStream_t st) {
     if (worst_imag_ratio(mx, static_cast<int>(jobs.size()), nullptr, st) > s.knobs.real_tol)
         throw SlError(SL_ERR_DOMAIN, "filter spectra are not real (asymmetric fan); unsupported by this build");
     s.bands3.upload(bd.data(), bd.size(), st);
+    s.bands3_host = bd;
     syn.bands = s.bands3.p;
     syn.tab1d = s.tab1.p;
     syn.tab2d = s.tab2.p;

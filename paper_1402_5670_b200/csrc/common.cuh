@@ -165,6 +165,8 @@ struct Knobs {
     int host_pipe = -1, pipe_conc = -1, pipe_group = -1, pipe_head = -1, pipe_tail = -1, lockstep_host = 0;  // pipelined host batch (-1: auto)
     bool denoise_unfused = false, disable_fast2d = false, disable_fast3d = false;
     bool split3d = true;  // three-pass 3D kernels (fast3d_split.cuh); SLB_SPLIT3D=0 selects the five-pass ones
+    bool group3d = true;  // shear-group passes A / C (fast3d_group.cuh); SLB_GROUP3D=0: one axis-0 FFT per band
+    bool t3 = true;       // pyramid-3 bands in the transposed frame (SLB_T3=0: singleton groups)
     double real_tol = 1e-9;
     static Knobs from_env() {
         Knobs k;
@@ -187,6 +189,8 @@ struct Knobs {
         k.disable_fast2d = std::getenv("SLB_DISABLE_FAST2D") != nullptr;
         k.disable_fast3d = std::getenv("SLB_DISABLE_FAST3D") != nullptr;
         k.split3d = env_knob("SLB_SPLIT3D", 1) != 0;
+        k.group3d = env_knob("SLB_GROUP3D", 1) != 0;
+        k.t3 = env_knob("SLB_T3", 1) != 0;
         if (const char* e = std::getenv("SLB_REAL_TOL")) k.real_tol = std::atof(e);
         return k;
     }
@@ -235,12 +239,14 @@ struct System {
     DBuf<double> W;     // [nhalf]
     // 3D synthesis tables
     DBuf<BandDesc3D> bands3;
+    std::vector<BandDesc3D> bands3_host;  // the same descriptors (shear-group planning on the host)
     DBuf<double> tab1, tab2;
     FiltSynth3D synth{};
     // scratch: one workspace per concurrent stream (batched calls fan frames
     // out over several workspaces); `w` is the workspace the next pass uses.
     struct Workspace {
         DBuf<double2> F, inter, acc, slots;
+        DBuf<double2> FT, accT;  // 3D transposed frame (pyramid-3 shear groups): F^T and its accumulator
         DBuf<double2> aux;  // fp32-mode 3D staging (float2 spectra viewed through double2 storage)
         DBuf<int> done;  // per column block: CTAs of the last rec chunk that finished (self-resetting)
         DBuf<double> stack;

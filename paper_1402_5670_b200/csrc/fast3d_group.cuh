@@ -1,0 +1,294 @@
+// Shear-group passes A / C of the three-pass 3D path (fast3d_split.cuh).
+//
+// Every 3D shearlet spectrum is a product of factors that each depend on two
+// of the three frequency indices (system3d.cpp:144-186):
+//   psi_b(k) = g(k_pa) Phi_{s1(b)}(k_pa, k_s1) Phi_{s2(b)}(k_pa, k_s2).
+// On an axis-0 line (k1, k2 fixed) of a band whose principal axis is 1 or 2
+// (pyramids 4 / 5) only Phi_{s1(b)}(k_pa, k0) varies, and it is the same for
+// every band of the pyramid and scale with the same first shear -- the
+// 2^l + 1 (or 2^l - 1) bands of one "shear group", consecutive in the band
+// order (index loop k2 innermost, taps.cpp: enumerate_3d). So
+//   dec: IFFT_0(F psi_b) = s_b(k1, k2) IFFT_0(F A)         (A = shared row)
+//   rec: sum_b psi_b FFT_0(y_b) = A FFT_0(sum_b s_b(k1, k2) y_b)
+// and passes A / C run ONE axis-0 FFT per group instead of one per band; per
+// band only the length-P DFT across the CTA's lines (and its Z tile) is left.
+// Pyramid-3 bands (principal axis 0) factor the same way after swapping axes 0
+// and 1 of the problem: the spectrum F^T[k2][k0][k1] goes through the same
+// kernels, pass B stores the coefficient rows transposed (k3s_mid, `tb`), and
+// their reconstruction sums into a transposed accumulator that is added back
+// once. The lowpass factors as hJ(k0) * (hJ(k1) hJ(k2)).
+// Reference: transform.cpp:39-61,94-125 (forward / inverse 3D), apps.cpp:114-121.
+#pragma once
+
+#include "fast3d_split.cuh"
+
+namespace slb {
+
+enum GroupType : int {
+    kGrpFull = 0,  // one band, the full axis-0 filter line (pyramid 3 without the transposed frame)
+    kGrpRowK1 = 1, // A = Phi_{s1}(k1, .), s_b = g(k1) Phi_{s2}(k1, k2)   (pyramid 4; pyramid 3 transposed)
+    kGrpRowK2 = 2, // A = Phi_{s1}(k2, .), s_b = g(k2) Phi_{s2}(k2, k1)   (pyramid 5)
+    kGrpLow = 3,   // A = hJ(.),           s_b = hJ(k1) hJ(k2)            (lowpass)
+};
+constexpr int kMaxGroups = 128;  // groups per launch (the host splits longer lists)
+constexpr int kMaxGroupLen = 16; // bands per group (the host splits longer runs)
+
+struct SplitGroups {
+    int count;
+    int zb0;  // global band index of Z slot 0 (the chunk's first band)
+    int first[kMaxGroups];  // global band index of each group's first band
+    unsigned char len[kMaxGroups];
+    unsigned char type[kMaxGroups];
+};
+
+template <int L>
+struct GroupShape {
+    using S = SplitShape<L>;
+    static_assert(S::AC_THREADS >= L, "one thread per output row i0 in the across-line DFTs");
+    static constexpr size_t SC_BYTES = static_cast<size_t>(kMaxGroupLen) * S::P * sizeof(double);
+    template <class C>
+    static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars
+        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES;
+    }
+#ifndef SLB_GROUP_A_MINB
+    static constexpr int A_MINB = 2;
+#else
+    static constexpr int A_MINB = SLB_GROUP_A_MINB;
+#endif
+#ifndef SLB_GROUP_C_MINB
+    static constexpr int C_MINB = 2;
+#else
+    static constexpr int C_MINB = SLB_GROUP_C_MINB;
+#endif
+};
+
+// the group's shared axis-0 row (unscaled): A[k0], or the full filter line (kGrpFull)
+struct GroupRow {
+    const double* A;
+    FiltSynth3D::Ax0Line full;
+    bool is_full;
+    __device__ __forceinline__ double at(int k0) const { return is_full ? full.at(k0) : __ldg(A + k0); }
+};
+__device__ __forceinline__ GroupRow group_row(const FiltSynth3D& f, const BandDesc3D& d, int type, int k1, int k2,
+                                              int n) {
+    GroupRow r{};
+    r.is_full = type == kGrpFull;
+    if (r.is_full)
+        r.full = f.ax0_line(d, k1, k2);
+    else if (type == kGrpLow)
+        r.A = f.tab1d + f.lp_off[0];
+    else
+        r.A = f.tab2d + d.p1_off + static_cast<long long>(type == kGrpRowK1 ? k1 : k2) * n;
+    return r;
+}
+// per-band, per-line scalar s_b(k1, k2)
+__device__ __forceinline__ double group_scalar(const FiltSynth3D& f, const BandDesc3D& d, int type, int k1, int k2,
+                                               int n) {
+    switch (type) {
+        case kGrpRowK1: return __ldg(f.tab1d + d.g_off + k1) * __ldg(f.tab2d + d.p2_off + (long long)k1 * n + k2);
+        case kGrpRowK2: return __ldg(f.tab1d + d.g_off + k2) * __ldg(f.tab2d + d.p2_off + (long long)k2 * n + k1);
+        case kGrpLow: return __ldg(f.tab1d + f.lp_off[1] + k1) * __ldg(f.tab1d + f.lp_off[2] + k2);
+        default: return 1.0;
+    }
+}
+
+// ---------------------------------------------------------------- pass A (groups)
+// grid (group, k2 * Q + q): consecutive CTAs share the CTA's F lines in L2.
+template <int L, class C = double2>
+__global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MINB)
+    k3g_dec(const C* __restrict__ F, C* __restrict__ Z, long long zbs, FiltSynth3D filt,
+            const __grid_constant__ SplitGroups grp, const C* __restrict__ tw) {
+    using S = SplitShape<L>;
+    using R = RealOf<C>;
+    constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
+    SLB_DYN_SMEM(C, tile);  // [2][n][LD] output tiles; the line buffers and the Y staging alias tile 0
+    R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);  // [len][P]
+    const int gi = blockIdx.x;
+    const int k2 = blockIdx.y / Q, q = blockIdx.y - k2 * Q;
+    const int p = threadIdx.x / T, t = threadIdx.x - p * T;
+    const int k1 = q + Q * p;
+    const int b0 = grp.first[gi], nbg = grp.len[gi], type = grp.type[gi];
+    // the group's shared line: IFFT_0(F * A)
+    C x[E];
+    {
+        const BandDesc3D bd0 = filt.bands[b0];
+        const GroupRow row = group_row(filt, bd0, type, k1, k2, n);
+        const C* fl = F + ((long long)k2 * n + k1) * n;
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const C f = __ldg(fl + t + T * m);
+            const R a = R(row.at(t + T * m));
+            x[m] = mkc<C>(f.x * a, f.y * a);
+        }
+    }
+    if (threadIdx.x < nbg * P) {
+        const int bb = threadIdx.x / P, pp = threadIdx.x - bb * P;
+        sc[threadIdx.x] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
+    }
+    reg_fft<L, +1, S::PAD>(x, tile + p * S::LB, t, tw);
+    __syncthreads();  // every line is done with the aliased buffers
+#pragma unroll
+    for (int m = 0; m < E; ++m) tile[(t + T * m) * LD + p] = x[m];
+    __syncthreads();
+    const int i0 = threadIdx.x;
+    C y[P];
+    if (i0 < n) {
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) y[pp] = tile[i0 * LD + pp];
+    }
+    const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
+    for (int bb = 0; bb < nbg; ++bb) {
+        // band bb writes tile (bb + 1) & 1: tile 0 (the Y staging) is first
+        // rewritten at bb = 1, after the bb = 0 barrier every Y read precedes
+        C* buf = tile + ((bb + 1) & 1) * S::AC_ELEMS;
+        if (i0 < n) {
+            C v[P];
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) {
+                const R s = type == kGrpFull ? R(1) : sc[bb * P + pp];
+                v[pp] = mkc<C>(y[pp].x * s, y[pp].y * s);
+            }
+            dft_small<P, +1>(v);
+#pragma unroll
+            for (int a = 0; a < P; ++a) buf[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
+        }
+        __syncthreads();
+        C* z = Z + (long long)(b0 + bb - grp.zb0) * zbs + (long long)k2 * n * n +
+               zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) + (long long)si0 * n;
+#pragma unroll 4
+        for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, buf[(si0 + T * j) * LD + sa]);
+    }
+}
+
+// ---------------------------------------------------------------- pass C (groups)
+// per (k2, q): for every group, sum_b s_b * (twiddle, length-P DFT of Z'_b) in
+// registers (one thread per row i0), then one axis-0 FFT, * A, into acc.
+template <int L, class C = double2>
+__global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MINB)
+    k3g_rec(const C* __restrict__ Z, long long zbs, C* __restrict__ acc, FiltSynth3D filt,
+            const __grid_constant__ SplitGroups grp, int accumulate, const C* __restrict__ tw, int bx0 = 0) {
+    using S = SplitShape<L>;
+    using R = RealOf<C>;
+    constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
+    SLB_DYN_SMEM(C, tile);  // [2][n][LD] band tiles (cp.async double buffer)
+    R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);
+    const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
+    const int k2 = bx / Q, q = bx - k2 * Q;
+    const int p = threadIdx.x / T, t = threadIdx.x - p * T;
+    const int k1 = q + Q * p;
+    const int i0 = threadIdx.x;
+    const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
+    auto load = [&](int slot, C* buf) {
+        const C* z = Z + (long long)slot * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) +
+                     (long long)si0 * n;
+#pragma unroll 4
+        for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    C ar[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
+    if (grp.count > 0) load(grp.first[0] - grp.zb0, tile);
+    int it = 0;  // flat band counter (tile it & 1)
+    for (int gi = 0; gi < grp.count; ++gi) {
+        const int b0 = grp.first[gi], nbg = grp.len[gi], type = grp.type[gi];
+        if (threadIdx.x < nbg * P) {  // the previous group's scalars were last read before its closing barriers
+            const int bb = threadIdx.x / P, pp = threadIdx.x - bb * P;
+            sc[threadIdx.x] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
+        }
+        C ag[P];
+#pragma unroll
+        for (int pp = 0; pp < P; ++pp) ag[pp] = mkc<C>(0.0, 0.0);
+        C* cur = tile;
+        for (int bb = 0; bb < nbg; ++bb, ++it) {
+            cur = tile + (it & 1) * S::AC_ELEMS;
+            if (it > 0) __syncthreads();  // tile (it + 1) & 1 is free (read by band it - 1 / the group end)
+            int nslot = -1;
+            if (bb + 1 < nbg)
+                nslot = b0 + bb + 1 - grp.zb0;
+            else if (gi + 1 < grp.count)
+                nslot = grp.first[gi + 1] - grp.zb0;
+            if (nslot >= 0) {
+                load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");  // band it landed, the next in flight
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
+            if (i0 < n) {
+                C v[P];
+#pragma unroll
+                for (int a = 0; a < P; ++a) {
+                    const C u = cur[i0 * LD + a];
+                    v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
+                }
+                dft_small<P, -1>(v);
+#pragma unroll
+                for (int pp = 0; pp < P; ++pp) {
+                    const R s = type == kGrpFull ? R(1) : sc[bb * P + pp];
+                    ag[pp].x = fma(v[pp].x, s, ag[pp].x);
+                    ag[pp].y = fma(v[pp].y, s, ag[pp].y);
+                }
+            }
+        }
+        // group end: the rows' sums back into lines through the last band's tile
+        __syncthreads();  // every row read its last tile
+        if (i0 < n) {
+#pragma unroll
+            for (int pp = 0; pp < P; ++pp) cur[i0 * LD + pp] = ag[pp];
+        }
+        __syncthreads();
+        C x[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) x[m] = cur[(t + T * m) * LD + p];
+        __syncthreads();  // all lines gathered: the tile becomes the line buffers
+        const BandDesc3D bd0 = filt.bands[b0];
+        const GroupRow row = group_row(filt, bd0, type, k1, k2, n);
+        reg_fft<L, -1, S::PAD>(x, cur + p * S::LB, t, tw);
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const R a = R(row.at(t + T * m));
+            ar[m].x = fma(x[m].x, a, ar[m].x);
+            ar[m].y = fma(x[m].y, a, ar[m].y);
+        }
+    }
+    C* d = acc + ((long long)k2 * n + k1) * n;
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        C v = ar[m];
+        if (accumulate) {
+            const C o = __ldcg(d + t + T * m);
+            v = mkc<C>(o.x + v.x, o.y + v.y);
+        }
+        __stcg(d + t + T * m, v);
+    }
+}
+
+// out[k2][a][b] = in[k2][b][a] (add: +=) for the planes k2 in [k2lo, k2hi):
+// F -> F^T for the transposed frame, and the transposed accumulator back.
+template <class C>
+__global__ void k3_plane_transpose(const C* __restrict__ in, C* __restrict__ out, int n, int k2lo, int add) {
+    __shared__ C tl[32][33];
+    const int k2 = blockIdx.z + k2lo;
+    const long long pb = (long long)k2 * n * n;
+    const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = by + j, c = bx + threadIdx.x;
+        if (r < n && c < n) tl[j][threadIdx.x] = __ldcs(in + pb + (long long)r * n + c);
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int r = bx + j, c = by + threadIdx.x;  // out row = in column
+        if (r < n && c < n) {
+            C v = tl[threadIdx.x][j];
+            C* o = out + pb + (long long)r * n + c;
+            if (add) {
+                const C w = *o;
+                v = mkc<C>(w.x + v.x, w.y + v.y);
+            }
+            *o = v;
+        }
+    }
+}
+
+}  // namespace slb

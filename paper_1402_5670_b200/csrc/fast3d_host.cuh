@@ -5,6 +5,7 @@
 #include "fast3d.cuh"
 #include "fast2d_fused.cuh"
 #include "fast3d_split.cuh"
+#include "fast3d_group.cuh"
 
 namespace slb {
 
@@ -211,14 +212,54 @@ struct Split3DLaunch {
         check_launch("k3s_dec");
     }
     template <int MODE>
-    void mid(C* Z, RealOf<C>* band, const RealOf<C>* bandin, int nb, const double* delta, int band0) {
+    void mid(C* Z, RealOf<C>* band, const RealOf<C>* bandin, int nb, const double* delta, int band0,
+             const BandDesc3D* tb = nullptr) {
         auto* k = (MODE == kMidRec || band) ? k3s_mid<n, MODE, true, C> : k3s_mid<n, MODE, false, C>;
         set_smem(k, B_SMEM);
         LaunchScope ls(s, MODE == kMidFused ? "f3s_mid" : (MODE == kMidDec ? "f3s_mid_dec" : "f3s_mid_rec"), st, nb);
         k<<<dim3(n * (S::P / 2), nb), S::B_THREADS, B_SMEM, st>>>(Z, nT, band, s.nreal, bandin,
                                                                  RealOf<C>(1.0 / static_cast<double>(s.nreal)), delta,
-                                                                 band0, tw);
+                                                                 band0, tw, tb);
         check_launch("k3s_mid");
+    }
+    // shear-group passes (fast3d_group.cuh)
+    static constexpr size_t G_SMEM = GroupShape<n>::template smem<C>();
+    void gdec(const C* F, C* Z, const SplitGroups& g) {
+        if constexpr (n > 192) {
+            throw SlError(SL_ERR_GENERIC, "shear-group passes: n <= 192");
+        } else {
+        if (g.count == 0) return;
+        set_smem(k3g_dec<n, C>, G_SMEM);
+        int nbands = 0;
+        for (int i = 0; i < g.count; ++i) nbands += g.len[i];
+        LaunchScope ls(s, "f3g_dec", st, nbands);
+        k3g_dec<n, C><<<dim3(g.count, S::H * S::Q), S::AC_THREADS, G_SMEM, st>>>(F, Z, nT, s.synth, g, tw);
+        check_launch("k3g_dec");
+        }
+    }
+    void grec(const C* Z, C* acc, const SplitGroups& g, int accumulate, int k2lo = 0, int k2hi = -1) {
+        if constexpr (n > 192) {
+            throw SlError(SL_ERR_GENERIC, "shear-group passes: n <= 192");
+        } else {
+        if (g.count == 0) return;
+        set_smem(k3g_rec<n, C>, G_SMEM);
+        if (k2hi < 0) k2hi = S::H;
+        int nbands = 0;
+        for (int i = 0; i < g.count; ++i) nbands += g.len[i];
+        LaunchScope ls(s, "f3g_rec", st, nbands);
+        k3g_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, G_SMEM, st>>>(Z, nT, acc, s.synth, g, accumulate,
+                                                                                   tw, k2lo * S::Q);
+        check_launch("k3g_rec");
+        }
+    }
+    // out[k2] (+)= in[k2]^T for planes [k2lo, k2hi)
+    void transpose(const C* in, C* out, int add, int k2lo = 0, int k2hi = -1) {
+        if (k2hi < 0) k2hi = S::H;
+        if (k2hi <= k2lo) return;
+        LaunchScope ls(s, "f3_transpose", st, 1);
+        k3_plane_transpose<C><<<dim3((n + 31) / 32, (n + 31) / 32, k2hi - k2lo), dim3(32, 8), 0, st>>>(in, out, n, k2lo,
+                                                                                                   add);
+        check_launch("k3_plane_transpose");
     }
     void rec(const C* Z, C* acc, int nb, int band0, int accumulate, int k2lo = 0, int k2hi = -1) {
         set_smem(k3s_rec<n, C>, REC_SMEM);
@@ -254,6 +295,116 @@ static void finish_rec(Fast3DLaunch<n>& K, System& s, double* out) {
 // issued for the accumulator slab [k2lo, k2hi) -- the slab is final on this
 // rank from that point of the stream on (the multi-GPU reduce overlaps the rest)
 using SlabHook = std::function<void(int, int)>;
+
+// Passes A / C of a band chunk: per band (k3s_dec / k3s_rec) or by shear
+// groups (k3g_dec / k3g_rec, fast3d_group.cuh; n <= 192), the pyramid-3 bands
+// in the frame with axes 0 and 1 swapped (F^T in, accT out, folded back once).
+template <int n, class C>
+struct SplitPasses {
+    System& s;
+    Split3DLaunch<n, C>& S3;
+    bool grouped = false, t3 = false;
+    const C* F = nullptr;
+    const C* FT = nullptr;
+    C* acc = nullptr;
+    C* accT = nullptr;
+    bool acc_w = false, accT_w = false, folded = false;
+    struct Chunk {
+        std::vector<SplitGroups> norm, trans;
+    };
+    // F: the input spectrum (null for rec-only calls); acc: the accumulator
+    // (null for dec-only calls). The transposed frame needs fp64 buffers.
+    SplitPasses(System& sys, Split3DLaunch<n, C>& l, const C* f, C* a) : s(sys), S3(l), F(f), acc(a) {
+        grouped = s.knobs.group3d && n <= 192;
+        if (grouped && s.knobs.t3 && sizeof(C) == sizeof(double2))
+            for (int b = s.lo; b < s.hi && !t3; ++b) t3 = s.bands3_host[static_cast<size_t>(b)].kind == 3;
+        if (!t3) return;
+        const size_t nT = static_cast<size_t>(S3.nT);
+        if (F) {
+            s.w->FT.alloc(nT);
+            FT = reinterpret_cast<const C*>(s.w->FT.p);
+            S3.transpose(F, reinterpret_cast<C*>(s.w->FT.p), 0);
+        }
+        if (acc) {
+            s.w->accT.alloc(nT);
+            accT = reinterpret_cast<C*>(s.w->accT.p);
+        }
+    }
+    const BandDesc3D* tb() const { return t3 ? s.bands3.p : nullptr; }
+    // shear groups of the global bands [gb0, gb0 + cb): consecutive bands of one
+    // pyramid / scale / first shear (same shared row) form a group
+    Chunk plan(int gb0, int cb) const {
+        Chunk ck;
+        if (!grouped) return ck;
+        struct Prev {
+            int band = -2, type = -1, p1 = -1, kind = -1;
+        } pn, pt;
+        for (int b = gb0; b < gb0 + cb; ++b) {
+            const BandDesc3D& d = s.bands3_host[static_cast<size_t>(b)];
+            const bool tr = t3 && d.kind == 3;
+            const int type = d.kind == 0 ? kGrpLow : (d.kind == 3 ? (tr ? kGrpRowK1 : kGrpFull) : (d.kind == 4 ? kGrpRowK1 : kGrpRowK2));
+            std::vector<SplitGroups>& v = tr ? ck.trans : ck.norm;
+            Prev& pv = tr ? pt : pn;
+            const bool ext = (type == kGrpRowK1 || type == kGrpRowK2) && pv.band == b - 1 && pv.type == type &&
+                             pv.p1 == d.p1_off && pv.kind == d.kind && v.back().len[v.back().count - 1] < kMaxGroupLen;
+            if (ext) {
+                ++v.back().len[v.back().count - 1];
+            } else {
+                if (v.empty() || v.back().count == kMaxGroups) {
+                    v.emplace_back();
+                    std::memset(&v.back(), 0, sizeof(SplitGroups));
+                    v.back().zb0 = gb0;
+                }
+                SplitGroups& g = v.back();
+                g.first[g.count] = b;
+                g.len[g.count] = 1;
+                g.type[g.count] = static_cast<unsigned char>(type);
+                ++g.count;
+            }
+            pv = Prev{b, type, d.p1_off, d.kind};
+        }
+        return ck;
+    }
+    void dec(C* Z, int gb0, int cb, const Chunk& ck) {
+        if (!grouped) {
+            S3.dec(F, Z, cb, gb0);
+            return;
+        }
+        for (const SplitGroups& g : ck.norm) S3.gdec(F, Z, g);
+        for (const SplitGroups& g : ck.trans) S3.gdec(FT, Z, g);
+    }
+    // pass C of the chunk for the accumulator planes [k2lo, k2hi)
+    void rec(const C* Z, int gb0, int cb, const Chunk& ck, int k2lo = 0, int k2hi = -1) {
+        if (!grouped) {
+            S3.rec(Z, acc, cb, gb0, acc_w, k2lo, k2hi);
+            return;
+        }
+        bool aw = acc_w, tw = accT_w;
+        for (const SplitGroups& g : ck.norm) {
+            S3.grec(Z, acc, g, aw, k2lo, k2hi);
+            aw = true;
+        }
+        for (const SplitGroups& g : ck.trans) {
+            S3.grec(Z, accT, g, tw, k2lo, k2hi);
+            tw = true;
+        }
+    }
+    void done_chunk(const Chunk& ck, int cb) {
+        acc_w = acc_w || (grouped ? !ck.norm.empty() : cb > 0);
+        accT_w = accT_w || !ck.trans.empty();
+    }
+    // acc (+)= accT^T for the planes [k2lo, k2hi); call after done_chunk of the last chunk
+    void fold(int k2lo = 0, int k2hi = -1) {
+        if (accT_w) S3.transpose(accT, acc, acc_w ? 1 : 0, k2lo, k2hi);
+    }
+};
+
+// fused denoise of this handle's bands up to the half-spectrum accumulator
+// sum_b FFT(thr(band_b)) psi_b in s.w->acc (natural layout); out = null stops
+// there (the distributed path reduces the accumulators across ranks first).
+// slab_done(k2lo, k2hi), when set, runs after the last chunk's pass C has been
+// issued for the accumulator slab [k2lo, k2hi) -- the slab is final on this
+// rank from that point of the stream on (the multi-GPU reduce overlaps the rest)
 template <int n>
 static void denoise3d_split_t(System& s, const double* f, double* stack, double* out, const double* delta,
                               cudaStream_t st, const SlabHook& slab_done = nullptr) {
@@ -264,22 +415,32 @@ static void denoise3d_split_t(System& s, const double* f, double* stack, double*
     forward_natural<n>(K, s, f);
     s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
     s.w->acc.alloc(static_cast<size_t>(K.nT));
+    SplitPasses<n, double2> SP(s, S3, s.w->F.p, s.w->acc.p);
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         double* sb = stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr;
-        S3.dec(s.w->F.p, s.w->inter.p, cb, s.lo + b0);
-        S3.template mid<kMidFused>(s.w->inter.p, sb, nullptr, cb, delta, s.lo + b0);
+        const auto ck = SP.plan(s.lo + b0, cb);
+        SP.dec(s.w->inter.p, s.lo + b0, cb, ck);
+        S3.template mid<kMidFused>(s.w->inter.p, sb, nullptr, cb, delta, s.lo + b0, SP.tb());
         if (slab_done && b0 + cb >= nb) {
             constexpr int kSlabs = 4;
+            const bool aw = SP.acc_w, tw = SP.accT_w;
             for (int j = 0; j < kSlabs; ++j) {
                 const int lo = SplitShape<n>::H * j / kSlabs, hi = SplitShape<n>::H * (j + 1) / kSlabs;
-                S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0, lo, hi);
+                SP.acc_w = aw;
+                SP.accT_w = tw;
+                SP.rec(s.w->inter.p, s.lo + b0, cb, ck, lo, hi);
+                SP.done_chunk(ck, cb);
+                SP.fold(lo, hi);
                 slab_done(lo, hi);
             }
+            SP.folded = true;
         } else {
-            S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+            SP.rec(s.w->inter.p, s.lo + b0, cb, ck);
+            SP.done_chunk(ck, cb);
         }
     }
+    if (!SP.folded) SP.fold();
     if (out) finish_rec<n>(K, s, out);
 }
 
@@ -322,12 +483,15 @@ static void denoise3d_split_f32_t(System& s, const float* f, float* stack, float
     check_launch("k_f64_to_f32");
     s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
     float2* Z = reinterpret_cast<float2*>(s.w->inter.p);
+    SplitPasses<n, float2> SP(s, S3, F32, acc32);  // shear groups, no transposed frame (fp64 buffers)
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         float* sb = stack ? stack + static_cast<size_t>(b0) * nr : nullptr;
-        S3.dec(F32, Z, cb, s.lo + b0);
+        const auto ck = SP.plan(s.lo + b0, cb);
+        SP.dec(Z, s.lo + b0, cb, ck);
         S3.template mid<kMidFused>(Z, sb, nullptr, cb, delta, s.lo + b0);
-        S3.rec(Z, acc32, cb, s.lo + b0, b0 > 0);
+        SP.rec(Z, s.lo + b0, cb, ck);
+        SP.done_chunk(ck, cb);
     }
     s.w->acc.alloc(static_cast<size_t>(K.nT));
     k_f32_to_f64<<<2048, 256, 0, st>>>(reinterpret_cast<const float*>(acc32), reinterpret_cast<double*>(s.w->acc.p),
@@ -346,10 +510,13 @@ static void dec3d_split_t(System& s, const double* f, double* out, const double*
     const int C = std::min(fast3d_chunk(s), nb);
     forward_natural<n>(K, s, f);
     s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
+    SplitPasses<n, double2> SP(s, S3, s.w->F.p, nullptr);
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
-        S3.dec(s.w->F.p, s.w->inter.p, cb, s.lo + b0);
-        S3.template mid<kMidDec>(s.w->inter.p, out + static_cast<size_t>(b0) * s.nreal, nullptr, cb, delta, s.lo + b0);
+        const auto ck = SP.plan(s.lo + b0, cb);
+        SP.dec(s.w->inter.p, s.lo + b0, cb, ck);
+        S3.template mid<kMidDec>(s.w->inter.p, out + static_cast<size_t>(b0) * s.nreal, nullptr, cb, delta, s.lo + b0,
+                                 SP.tb());
     }
 }
 
@@ -361,11 +528,16 @@ static void rec3d_split_t(System& s, const double* coeffs, double* out, cudaStre
     const int C = std::min(fast3d_chunk(s), nb);
     s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
     s.w->acc.alloc(static_cast<size_t>(K.nT));
+    SplitPasses<n, double2> SP(s, S3, nullptr, s.w->acc.p);
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
-        S3.template mid<kMidRec>(s.w->inter.p, nullptr, coeffs + static_cast<size_t>(b0) * s.nreal, cb, nullptr, 0);
-        S3.rec(s.w->inter.p, s.w->acc.p, cb, s.lo + b0, b0 > 0);
+        const auto ck = SP.plan(s.lo + b0, cb);
+        S3.template mid<kMidRec>(s.w->inter.p, nullptr, coeffs + static_cast<size_t>(b0) * s.nreal, cb, nullptr,
+                                 s.lo + b0, SP.tb());
+        SP.rec(s.w->inter.p, s.lo + b0, cb, ck);
+        SP.done_chunk(ck, cb);
     }
+    SP.fold();
     finish_rec<n>(K, s, out);
 }
 

@@ -289,7 +289,7 @@ template <int L, int MODE, bool STORE, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::value)
     k3s_mid(C* __restrict__ Z, long long zbs, RealOf<C>* __restrict__ band, long long bbs,
             const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
-            const C* __restrict__ tw) {
+            const C* __restrict__ tw, const BandDesc3D* __restrict__ tb = nullptr) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, H = S::H, n = L;
     constexpr int KPT = (H + T - 1) / T;
@@ -298,6 +298,11 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
     const int bi = blockIdx.y;
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
+    // tb: pyramid-3 bands run in the frame with axes 0 and 1 swapped
+    // (fast3d_group.cuh); their rows (i0, i1) are the coefficient's rows (i1, i0)
+    const bool trs = tb != nullptr && tb[band0 + bi].kind == 3;
+    const long long roff = trs ? ((long long)i1 * n + i0) * n : ((long long)i0 * n + i1) * n;
+    const long long rstep = trs ? (long long)n * n : (long long)n;  // row i1 + 1
     C* zb = Z + (long long)bi * zbs + (long long)i0 * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(0, a0);  // + k2 n n + q ZS + e
     constexpr int ZS = SplitLayout<L, C>::ZQUAD ? 4 : P;  // distance between consecutive q at fixed a
     C* lb = tile + lq * S::LB;
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
         __syncthreads();  // the tile becomes the line buffers
         reg_fft<L, +1, S::PAD>(x, lb, t, tw);
         const double dl = delta ? delta[band0 + bi] : -1.0;
-        RealOf<C>* r0p = band + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+        RealOf<C>* r0p = band + (long long)bi * bbs + roff;
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             RealOf<C> u = x[m].x * scale, w = x[m].y * scale;
@@ -373,15 +378,15 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
             }
             if (STORE) {
                 r0p[t + T * m] = u;
-                r0p[n + t + T * m] = w;
+                r0p[rstep + t + T * m] = w;
             }
             x[m] = mkc<C>(u, w);
         }
         if constexpr (MODE == kMidDec) return;
     } else {
-        const RealOf<C>* r0p = bandin + (long long)bi * bbs + ((long long)i0 * n + i1) * n;
+        const RealOf<C>* r0p = bandin + (long long)bi * bbs + roff;
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = mkc<C>(__ldg(r0p + t + T * m), __ldg(r0p + n + t + T * m));
+        for (int m = 0; m < E; ++m) x[m] = mkc<C>(__ldg(r0p + t + T * m), __ldg(r0p + rstep + t + T * m));
     }
     // axis-2 r2c of the row pair (as k2_rows_r2c)
     reg_fft<L, -1, S::PAD>(x, lb, t, tw);
