@@ -134,6 +134,11 @@ struct SplitLayout {
     static constexpr bool ZQUAD = sizeof(C) == 16 && SplitShape<L>::ZQUAD;
     static constexpr bool B_SWZ = sizeof(C) == 16 && SplitShape<L>::B_SWZ;
     static constexpr bool B_DIRECT = sizeof(C) == 16 && SplitShape<L>::B_DIRECT;  // measured in fp64 only
+#ifndef SLB_SPLIT_B_X1
+    static constexpr bool X1 = true;  // 192-point pass-B rows with one exchange per FFT (fft192_a / _b)
+#else
+    static constexpr bool X1 = SLB_SPLIT_B_X1;
+#endif
 };
 
 // pass A keeps its F lines in registers across the band group (1) or reloads
@@ -285,17 +290,22 @@ enum SplitMid : int {
     kMidRec = 2,    // band rows -> r2c -> Z'                         (inverse)
 };
 
-template <int L, int MODE, bool STORE, class C = double2>
-__global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::value)
-    k3s_mid(C* __restrict__ Z, long long zbs, RealOf<C>* __restrict__ band, long long bbs,
-            const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
-            const C* __restrict__ tw, const BandDesc3D* __restrict__ tb = nullptr) {
+// One pass-B work item (i0 = bx / (P/2), a pair, band bi) on the CTA's tile.
+// preloaded: the caller already staged the item's Z tile (cp.async, waited and
+// synchronised). A persistent variant that overlapped the next item's tile
+// load with the current item measured 6.7 % slower at 192^3
+// (profiles/r2b_ab_passB_persistent.log): the two resident CTAs per SM already
+// overlap each other's load and compute phases.
+template <int L, int MODE, bool STORE, class C>
+__device__ __forceinline__ void mid_item(C* __restrict__ tile, bool preloaded, int bx, int bi, C* __restrict__ Z,
+                                         long long zbs, RealOf<C>* __restrict__ band, long long bbs,
+                                         const RealOf<C>* __restrict__ bandin, RealOf<C> scale,
+                                         const double* __restrict__ delta, int band0, const C* __restrict__ tw,
+                                         const BandDesc3D* __restrict__ tb) {
     using S = SplitShape<L>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, H = S::H, n = L;
     constexpr int KPT = (H + T - 1) / T;
-    SLB_DYN_SMEM(C, tile);  // [H][2Q] bslot<Q>; line buffers alias it
-    const int i0 = blockIdx.x / (P / 2), a0 = 2 * (blockIdx.x - i0 * (P / 2));
-    const int bi = blockIdx.y;
+    const int i0 = bx / (P / 2), a0 = 2 * (bx - i0 * (P / 2));
     const int lq = threadIdx.x / T, t = threadIdx.x - lq * T;  // pair-line c = lq: rows i1, i1 + 1
     const int i1 = a0 + P * lq;
     // tb: pyramid-3 bands run in the frame with axes 0 and 1 swapped
@@ -308,7 +318,10 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
     C* lb = tile + lq * S::LB;
     constexpr int KST = S::B_THREADS / (2 * Q);  // k2 rows per tile-copy step
     [[maybe_unused]] const int sj = threadIdx.x % (2 * Q), sk2 = threadIdx.x / (2 * Q);
-    C x[E];
+    // X1: 192-point rows with one exchange per FFT (fft192_a / fft192_b, 12 x 16)
+    constexpr bool X1 = L == 192 && SplitLayout<L, C>::X1;
+    C x[X1 ? 16 : E];
+    auto& xe = *reinterpret_cast<C(*)[E]>(&x[0]);  // the 16-major view (x[m] = element t + T m)
     if constexpr (MODE != kMidRec) {
         if constexpr (SplitLayout<L, C>::B_DIRECT) {
             // length-Q DFT over q for each (k2, e) straight from Z (lane pairs e = 0, 1
@@ -324,12 +337,14 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
                 for (int j = 0; j < Q; ++j) tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)] = v[j];
             }
         } else {
-            // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
+            if (!preloaded) {
+                // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
 #pragma unroll 4
-            for (int k2 = sk2; k2 < H; k2 += KST)
-                cp_async_c(tile + bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
-            cp_async_wait_all();
-            __syncthreads();
+                for (int k2 = sk2; k2 < H; k2 += KST)
+                    cp_async_c(tile + bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
+                cp_async_wait_all();
+                __syncthreads();
+            }
             // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
             for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
                 const int e = idx / H, k2 = idx - e * H;
@@ -344,7 +359,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
         __syncthreads();
         // axis-2 c2r of the row pair (pair-packed, as k2_rows_c2r)
         if constexpr (T <= 32 && SLB_SPLIT_C2R_SHFL) {
-            c2r_pack_shfl<L, T, E, Q, SplitLayout<L, C>::B_SWZ>(tile, lq, t, x);
+            c2r_pack_shfl<L, T, E, Q, SplitLayout<L, C>::B_SWZ>(tile, lq, t, xe);
         } else {
 #pragma unroll
             for (int m = 0; m < E; ++m) {
@@ -357,45 +372,64 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
                         X.y = 0.0;
                         Y.y = 0.0;
                     }
-                    x[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
+                    xe[m] = mkc<C>(X.x - Y.y, X.y + Y.x);
                 } else {
                     X = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(L - k, 2 * lq)];
                     Y = tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(L - k, 2 * lq + 1)];
-                    x[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
+                    xe[m] = mkc<C>(X.x + Y.y, Y.x - X.y);
                 }
             }
         }
         __syncthreads();  // the tile becomes the line buffers
-        reg_fft<L, +1, S::PAD>(x, lb, t, tw);
         const double dl = delta ? delta[band0 + bi] : -1.0;
         RealOf<C>* r0p = band + (long long)bi * bbs + roff;
-#pragma unroll
-        for (int m = 0; m < E; ++m) {
-            RealOf<C> u = x[m].x * scale, w = x[m].y * scale;
+        auto thr_store = [&](C& v, int pos) {
+            RealOf<C> u = v.x * scale, w = v.y * scale;
             if (dl >= 0.0) {
                 if (fabs(u) < dl) u = 0.0;
                 if (fabs(w) < dl) w = 0.0;
             }
             if (STORE) {
-                r0p[t + T * m] = u;
-                r0p[rstep + t + T * m] = w;
+                r0p[pos] = u;
+                r0p[rstep + pos] = w;
             }
-            x[m] = mkc<C>(u, w);
+            v = mkc<C>(u, w);
+        };
+        if constexpr (X1) {
+            fft192_a<+1>(x, lb, t, tw);  // -> 12-major
+            if (t < 12) {
+#pragma unroll
+                for (int r = 0; r < 16; ++r) thr_store(x[r], t + 12 * r);
+            }
+        } else {
+            reg_fft<L, +1, S::PAD>(xe, lb, t, tw);
+#pragma unroll
+            for (int m = 0; m < E; ++m) thr_store(xe[m], t + T * m);
         }
         if constexpr (MODE == kMidDec) return;
     } else {
         const RealOf<C>* r0p = bandin + (long long)bi * bbs + roff;
+        if constexpr (X1) {
+            if (t < 12) {
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = mkc<C>(__ldg(r0p + t + T * m), __ldg(r0p + rstep + t + T * m));
+                for (int r = 0; r < 16; ++r) x[r] = mkc<C>(__ldg(r0p + t + 12 * r), __ldg(r0p + rstep + t + 12 * r));
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < E; ++m) xe[m] = mkc<C>(__ldg(r0p + t + T * m), __ldg(r0p + rstep + t + T * m));
+        }
     }
     // axis-2 r2c of the row pair (as k2_rows_r2c)
-    reg_fft<L, -1, S::PAD>(x, lb, t, tw);
+    if constexpr (X1)
+        fft192_b<-1>(x, lb, t, tw);  // 12-major -> 16-major
+    else
+        reg_fft<L, -1, S::PAD>(xe, lb, t, tw);
     C zk[KPT], zm[KPT];
     if constexpr (T <= 32 && SLB_ROWS_SHFL) {
-        mirror_pairs_shfl<L, T, E, KPT>(x, zk, zm, t);  // warp shuffles, no shared-memory round trip
+        mirror_pairs_shfl<L, T, E, KPT>(xe, zk, zm, t);  // warp shuffles, no shared-memory round trip
     } else {
 #pragma unroll
-        for (int m = 0; m < E; ++m) lb[swz<S::PAD, L, sizeof(C)>(t + T * m)] = x[m];
+        for (int m = 0; m < E; ++m) lb[swz<S::PAD, L, sizeof(C)>(t + T * m)] = xe[m];
         line_sync<T>();
 #pragma unroll
         for (int u = 0; u < KPT; ++u) {
@@ -443,6 +477,16 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
         for (int k2 = sk2; k2 < H; k2 += KST)
             __stcg(zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1), tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj)]);
     }
+}
+
+template <int L, int MODE, bool STORE, class C = double2>
+__global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::value)
+    k3s_mid(C* __restrict__ Z, long long zbs, RealOf<C>* __restrict__ band, long long bbs,
+            const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
+            const C* __restrict__ tw, const BandDesc3D* __restrict__ tb = nullptr) {
+    SLB_DYN_SMEM(C, tile);  // [H][2Q] bslot<Q>; line buffers alias it
+    mid_item<L, MODE, STORE, C>(tile, false, blockIdx.x, blockIdx.y, Z, zbs, band, bbs, bandin, scale, delta, band0,
+                                tw, tb);
 }
 
 // ---------------------------------------------------------------- pass C

@@ -370,6 +370,60 @@ __device__ __forceinline__ void mirror_pairs_shfl(const C (&x)[E], C (&zk)[KPT],
     }
 }
 
+// 192-point lines with ONE shared-memory exchange (radix 12 x 16) on 16
+// threads (the axis-2 rows of the 3D pass B), instead of the (12, 4, 4)
+// RegPlan's two:
+//   16-major layout: x[m] = element t + 16 m, m < 12, all 16 threads;
+//   12-major layout: x[r] = element t + 12 r, r < 16, threads t < 12 only.
+// fft192_a: 16-major in -> 12-major out (radix 12, exchange, radix 16);
+// fft192_b: 12-major in -> 16-major out (radix 16, exchange, radix 12).
+// Stockham stages as RegStage (w = e^{DIR 2 pi i / 192}); twiddle powers by a
+// running product (~15 ulp, far inside the 1e-10 budget). Exchange slots:
+// e + e/24 for the radix-12 stores / 12-major loads, e ^ ((e >> 4) & 7) for the
+// radix-16 stores / 16-major loads (both conflict-free per quarter warp).
+__device__ __forceinline__ int swz192a(int e) { return e + static_cast<int>(static_cast<unsigned>(e) / 24u); }
+__device__ __forceinline__ int swz192b(int e) { return e ^ ((e >> 4) & 7); }
+template <int DIR, class C>
+__device__ __forceinline__ void fft192_a(C (&x)[16], C* sm, int t, const C* __restrict__ tw) {
+    bfly12<DIR>(x);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) sm[swz192a(12 * t + k)] = x[k];
+    __syncwarp();
+    if (t < 12) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = sm[swz192a(t + 12 * r)];
+        const C w1 = twiddle<DIR>(tw, t);
+        C wr = w1;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+            x[r] = cmul(x[r], wr);
+            if (r + 1 < 16) wr = cmul(wr, w1);
+        }
+        bfly16<DIR>(x);
+    }
+    __syncwarp();
+}
+template <int DIR, class C>
+__device__ __forceinline__ void fft192_b(C (&x)[16], C* sm, int t, const C* __restrict__ tw) {
+    if (t < 12) {
+        bfly16<DIR>(x);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sm[swz192b(16 * t + k)] = x[k];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 12; ++m) x[m] = sm[swz192b(t + 16 * m)];
+    const C w1 = twiddle<DIR>(tw, t);
+    C wr = w1;
+#pragma unroll
+    for (int m = 1; m < 12; ++m) {
+        x[m] = cmul(x[m], wr);
+        if (m + 1 < 12) wr = cmul(wr, w1);
+    }
+    bfly12<DIR>(x);
+    __syncwarp();
+}
+
 // In/out: x[m] = element t + T*m of the line. sm: the line's L-element buffer.
 template <int L, int DIR, bool PAD = true, class C>
 __device__ __forceinline__ void reg_fft(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
