@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
             x[m] = mkc<C>(f.x * a, f.y * a);
         }
     }
-    if (threadIdx.x < nbg * P) {
-        const int bb = threadIdx.x / P, pp = threadIdx.x - bb * P;
-        sc[threadIdx.x] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
+    for (int i = threadIdx.x; i < nbg * P; i += S::AC_THREADS) {  // groups of up to kMaxGroupLen bands
+        const int bb = i / P, pp = i - bb * P;
+        sc[i] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
     }
     reg_fft<L, +1, S::PAD>(x, tile + p * S::LB, t, tw);
     __syncthreads();  // every line is done with the aliased buffers
@@ -192,9 +192,10 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
     int it = 0;  // flat band counter (tile it & 1)
     for (int gi = 0; gi < grp.count; ++gi) {
         const int b0 = grp.first[gi], nbg = grp.len[gi], type = grp.type[gi];
-        if (threadIdx.x < nbg * P) {  // the previous group's scalars were last read before its closing barriers
-            const int bb = threadIdx.x / P, pp = threadIdx.x - bb * P;
-            sc[threadIdx.x] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
+        // the previous group's scalars were last read before its closing barriers
+        for (int i = threadIdx.x; i < nbg * P; i += S::AC_THREADS) {
+            const int bb = i / P, pp = i - bb * P;
+            sc[i] = R(group_scalar(filt, filt.bands[b0 + bb], type, q + Q * pp, k2, n));
         }
         C ag[P];
 #pragma unroll

@@ -240,3 +240,40 @@ def test_three_pass_matches_five_pass(cuda, n, levels, monkeypatch):
     assert rel(b1, b0) <= 1e-13 and rel(st1, st0) <= 1e-13
     assert rel(d1, d0) <= 1e-13 and rel(r1, r0) <= 1e-13
     assert rel(r1, x) <= 1e-10
+
+
+@pytest.mark.parametrize("n,levels,env", [
+    (64, [0, 1], {}),
+    (64, [2, 2, 2], {"SLB_T3": "0"}),      # > 128 singleton groups: the launch lists split
+    (128, [1, 1], {"SLB_CHUNK3": "7"}),     # chunk boundaries cut shear groups
+    (192, [0, 0, 1], {}),
+])
+def test_shear_groups_match_per_band_passes(cuda, n, levels, env, monkeypatch):
+    # passes A / C by shear groups (fast3d_group.cuh: one axis-0 FFT per group,
+    # pyramid-3 bands in the axis-swapped frame) against one FFT per band
+    # (SLB_GROUP3D=0): dec bands, the fused denoise and its stack, rec, and fp32
+    import torch
+    prof = P.ScaleProfile.from_levels(levels)
+    sch = P.ThresholdSchedule.defaults_3d(0.3, len(levels))
+    x = torch.from_numpy(np.random.default_rng(n + len(levels)).uniform(-1, 1, (n, n, n))).to(cuda)
+    got = {}
+    for grp in ("1", "0"):
+        monkeypatch.setenv("SLB_GROUP3D", grp)  # knobs are read when the handle is created
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        s = P.build_system_3d((n, n, n), prof)
+        d, st = P.denoise(x, s, sch, return_stack=True)
+        b = P.forward(x, s)
+        r = P.inverse(b, s)
+        s32 = P.build_system_3d((n, n, n), prof, dtype="f32")
+        d32 = P.denoise(x.float(), s32, P.ThresholdSchedule.defaults_3d(0.0, len(levels)))
+        got[grp] = (d, st, b, r, d32)
+        del s, s32
+    (d1, st1, b1, r1, f1), (d0, st0, b0, r0, f0) = got["1"], got["0"]
+    rel = lambda a, b: (torch.linalg.norm(a.double() - b.double()) / torch.linalg.norm(b.double())).item()  # noqa: E731
+    assert rel(b1, b0) <= 1e-13 and rel(st1, st0) <= 1e-13
+    assert rel(d1, d0) <= 1e-13 and rel(r1, r0) <= 1e-13
+    assert rel(r1, x) <= 1e-10
+    # thresholded support identical (values within the 1e-13 above)
+    assert torch.equal(st1 != 0, st0 != 0)
+    assert rel(f1, f0) <= 1e-5 and rel(f1, x) <= 1e-5
