@@ -153,6 +153,8 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
             for (int a = 0; a < P; ++a) buf[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
         }
         __syncthreads();
+        // (32-byte STG.256 stores of a pairs measured 2 % slower here and in
+        // pass B's copy-out: profiles/r2b_ab_stg256_pairs.log)
         C* z = Z + (long long)(b0 + bb - grp.zb0) * zbs + (long long)k2 * n * n +
                zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
