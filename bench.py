@@ -180,6 +180,11 @@ def pass_bytes(name, dims, G3=None):
         "f3s_dec": 16 * Nh + 16 * Nh / G3,          # Z write (+ F once per group)
         "f3s_mid": 16 * Nh + 8 * N + 16 * Nh,       # Z read, thresholded band write, Z' write
         "f3s_rec": 16 * Nh + 32 * Nh / G3,          # Z' read (+ accumulator RMW once per group)
+        # shear-group passes A / C (fast3d_group.cuh): F read and accumulator
+        # RMW once per shear group (~8 bands at SL3D_2), charged here per band
+        "f3g_dec": 16 * Nh + 16 * Nh / 8,           # Z write (+ F once per group)
+        "f3g_rec": 16 * Nh + 32 * Nh / 8,           # Z' read (+ accumulator RMW once per group)
+        "f3_transpose": 32 * Nh,
     }.get(name, None)
 
 

@@ -313,10 +313,11 @@ struct SplitPasses {
         std::vector<SplitGroups> norm, trans;
     };
     // F: the input spectrum (null for rec-only calls); acc: the accumulator
-    // (null for dec-only calls). The transposed frame needs fp64 buffers.
+    // (null for dec-only calls). F^T / accT live in double2 workspaces (the
+    // fp32 mode uses their front halves).
     SplitPasses(System& sys, Split3DLaunch<n, C>& l, const C* f, C* a) : s(sys), S3(l), F(f), acc(a) {
         grouped = s.knobs.group3d && n <= 192;
-        if (grouped && s.knobs.t3 && sizeof(C) == sizeof(double2))
+        if (grouped && s.knobs.t3)
             for (int b = s.lo; b < s.hi && !t3; ++b) t3 = s.bands3_host[static_cast<size_t>(b)].kind == 3;
         if (!t3) return;
         const size_t nT = static_cast<size_t>(S3.nT);
@@ -483,16 +484,17 @@ static void denoise3d_split_f32_t(System& s, const float* f, float* stack, float
     check_launch("k_f64_to_f32");
     s.w->inter.alloc(static_cast<size_t>(C) * K.nT);
     float2* Z = reinterpret_cast<float2*>(s.w->inter.p);
-    SplitPasses<n, float2> SP(s, S3, F32, acc32);  // shear groups, no transposed frame (fp64 buffers)
+    SplitPasses<n, float2> SP(s, S3, F32, acc32);
     for (int b0 = 0; b0 < nb; b0 += C) {
         const int cb = std::min(C, nb - b0);
         float* sb = stack ? stack + static_cast<size_t>(b0) * nr : nullptr;
         const auto ck = SP.plan(s.lo + b0, cb);
         SP.dec(Z, s.lo + b0, cb, ck);
-        S3.template mid<kMidFused>(Z, sb, nullptr, cb, delta, s.lo + b0);
+        S3.template mid<kMidFused>(Z, sb, nullptr, cb, delta, s.lo + b0, SP.tb());
         SP.rec(Z, s.lo + b0, cb, ck);
         SP.done_chunk(ck, cb);
     }
+    SP.fold();
     s.w->acc.alloc(static_cast<size_t>(K.nT));
     k_f32_to_f64<<<2048, 256, 0, st>>>(reinterpret_cast<const float*>(acc32), reinterpret_cast<double*>(s.w->acc.p),
                                        2 * K.nT);

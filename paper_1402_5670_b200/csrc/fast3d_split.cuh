@@ -295,7 +295,8 @@ enum SplitMid : int {
 // synchronised). A persistent variant that overlapped the next item's tile
 // load with the current item measured 6.7 % slower at 192^3
 // (profiles/r2b_ab_passB_persistent.log): the two resident CTAs per SM already
-// overlap each other's load and compute phases.
+// overlap each other's load and compute phases; so did an L2 bulk prefetch of
+// the tile one wave of CTAs ahead (2-3.5 % slower, r2b_ab_passB_l2_prefetch.log).
 template <int L, int MODE, bool STORE, class C>
 __device__ __forceinline__ void mid_item(C* __restrict__ tile, bool preloaded, int bx, int bi, C* __restrict__ Z,
                                          long long zbs, RealOf<C>* __restrict__ band, long long bbs,

@@ -66,12 +66,13 @@ def launches(path, out):
 PASS_KERNEL = {"f2_rows_fused": "k2_rows_fused", "f3_rows_fused": "k2_rows_fused",
                "f2_cols_dec": "k2_cols_dec", "f2_cols_rec": "k2_cols_rec",
                "f2_rows_c2r_thr": "k2_rows_c2r", "f3_axis1": "k3_lines_contig",
-               "f3s_dec": "k3s_dec", "f3s_mid": "k3s_mid", "f3s_rec": "k3s_rec"}
+               "f3s_dec": "k3s_dec", "f3s_mid": "k3s_mid", "f3s_rec": "k3s_rec",
+               "f3g_dec": "k3g_dec", "f3g_rec": "k3g_rec"}
 # kernels whose grid y is not the band count of the launch (band groups /
 # in-kernel band loops): bands per launch of the capture drivers
 # (tools/prof3d.py: a 12-band shard in one chunk; tools/prof2d.py: a lone
 # 512^2 frame, all 49 bands in one chunk)
-BANDS_OVERRIDE = {"k3s_dec": 12, "k3s_rec": 12, "k2_cols_dec": 49, "k2_cols_rec": 49}
+BANDS_OVERRIDE = {"k3s_dec": 12, "k3s_rec": 12, "k3g_dec": 12, "k3g_rec": 12, "k2_cols_dec": 49, "k2_cols_rec": 49}
 
 
 def traffic(rep, out, config):

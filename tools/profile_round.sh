@@ -24,6 +24,6 @@ python tools/prof2d.py denoise > $O/plain2_$R.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k2_rows_fused|k2_cols_dec|k2_cols_rec|k2_cols_sum" -s 8 -c 4 \
     -o $O/full2d_$R python tools/prof2d.py denoise > $O/ncu_full2d_$R.log 2>&1
 python tools/prof3d.py 192 > $O/plain3_$R.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k3s_" -s 3 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k3g_|k3s_" -s 3 -c 3 \
     -o $O/full3d_$R python tools/prof3d.py 192 > $O/ncu_full3d_$R.log 2>&1
 echo done
