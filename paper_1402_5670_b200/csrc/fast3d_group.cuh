@@ -21,6 +21,7 @@
 #pragma once
 
 #include "fast3d_split.cuh"
+#include "tma.cuh"
 
 namespace slb {
 
@@ -47,14 +48,21 @@ struct GroupShape {
     static_assert(S::AC_THREADS >= L, "one thread per output row i0 in the across-line DFTs");
     static constexpr size_t SC_BYTES = static_cast<size_t>(kMaxGroupLen) * S::P * sizeof(double);
     template <class C>
-    static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars
-        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES;
+    static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars (+ 1024-byte alignment for TMA)
+        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES + 1024;
     }
 #ifndef SLB_GROUP_A_MINB
     static constexpr int A_MINB = 2;
 #else
     static constexpr int A_MINB = SLB_GROUP_A_MINB;
 #endif
+#ifndef SLB_GROUP_TMA
+#define SLB_GROUP_TMA 1
+#endif
+    // pass A's Z tiles leave through TMA bulk tensor stores (fp64, 192: the
+    // quad-interleaved Z rows as a 5D tensor, 64-byte swizzled staging)
+    template <class C>
+    static constexpr bool TMA_STORE = SLB_GROUP_TMA && L == 192 && sizeof(C) == 16 && SplitLayout<L, C>::ZQUAD;
 #ifndef SLB_GROUP_C_MINB
     static constexpr int C_MINB = 2;
 #else
@@ -97,11 +105,13 @@ __device__ __forceinline__ double group_scalar(const FiltSynth3D& f, const BandD
 template <int L, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MINB)
     k3g_dec(const C* __restrict__ F, C* __restrict__ Z, long long zbs, FiltSynth3D filt,
-            const __grid_constant__ SplitGroups grp, const C* __restrict__ tw) {
+            const __grid_constant__ SplitGroups grp, const C* __restrict__ tw, const __grid_constant__ CUtensorMap zmap) {
     using S = SplitShape<L>;
     using R = RealOf<C>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
-    SLB_DYN_SMEM(C, tile);  // [2][n][LD] output tiles; the line buffers and the Y staging alias tile 0
+    constexpr bool TMA = GroupShape<L>::template TMA_STORE<C>;
+    SLB_DYN_SMEM(C, tile_raw);  // [2][n][LD] output tiles; the line buffers and the Y staging alias tile 0
+    C* tile = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023));
     R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);  // [len][P]
     const int gi = blockIdx.x;
     const int k2 = blockIdx.y / Q, q = blockIdx.y - k2 * Q;
@@ -141,6 +151,12 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
         // band bb writes tile (bb + 1) & 1: tile 0 (the Y staging) is first
         // rewritten at bb = 1, after the bb = 0 barrier every Y read precedes
         C* buf = tile + ((bb + 1) & 1) * S::AC_ELEMS;
+        if constexpr (TMA) {
+            if (bb >= 2) {  // the bulk store issued from this tile at bb - 2 has read it
+                if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                __syncthreads();
+            }
+        }
         if (i0 < n) {
             C v[P];
 #pragma unroll
@@ -150,7 +166,20 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
             }
             dft_small<P, +1>(v);
 #pragma unroll
-            for (int a = 0; a < P; ++a) buf[i0 * LD + a] = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
+            for (int a = 0; a < P; ++a) {
+                const C w = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
+                if constexpr (TMA)
+                    buf[sw64_slot(i0 * (P * 16) + a * 16)] = w;  // dense [i0][a], 64-byte swizzle
+                else
+                    buf[i0 * LD + a] = w;
+            }
+        }
+        if constexpr (TMA) {
+            // Z[slot][k2][i0][a/4][q][a%4] as the 5D tensor (a%4 re/im, q, a/4, i0, slot * H + k2)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0) tma_store_5d(&zmap, buf, 0, q, 0, 0, (b0 + bb - grp.zb0) * S::H + k2);
+            continue;
         }
         __syncthreads();
         // (32-byte STG.256 stores of a pairs measured 2 % slower here and in
@@ -159,6 +188,9 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
                zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) + (long long)si0 * n;
 #pragma unroll 4
         for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, buf[(si0 + T * j) * LD + sa]);
+    }
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes done before exit
     }
 }
 

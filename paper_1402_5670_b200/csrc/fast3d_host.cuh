@@ -232,8 +232,20 @@ struct Split3DLaunch {
         set_smem(k3g_dec<n, C>, G_SMEM);
         int nbands = 0;
         for (int i = 0; i < g.count; ++i) nbands += g.len[i];
+        CUtensorMap zmap{};
+        if constexpr (GroupShape<n>::template TMA_STORE<C>) {
+            // Z as the 5D tensor {re/im x a%4, q, a/4, i0, slot * H + k2} (zrow quads)
+            int slots = 0;
+            for (int i = 0; i < g.count; ++i) slots = std::max(slots, g.first[i] + g.len[i] - g.zb0);
+            const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(S::Q), static_cast<cuuint64_t>(S::P / 4),
+                                        static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(S::H) * slots};
+            const cuuint64_t strides[4] = {4 * sizeof(C), 4 * S::Q * sizeof(C), static_cast<cuuint64_t>(n) * sizeof(C),
+                                           static_cast<cuuint64_t>(n) * n * sizeof(C)};
+            const cuuint32_t box[5] = {8, 1, static_cast<cuuint32_t>(S::P / 4), static_cast<cuuint32_t>(n), 1};
+            zmap = tma_map_f64(Z, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+        }
         LaunchScope ls(s, "f3g_dec", st, nbands);
-        k3g_dec<n, C><<<dim3(g.count, S::H * S::Q), S::AC_THREADS, G_SMEM, st>>>(F, Z, nT, s.synth, g, tw);
+        k3g_dec<n, C><<<dim3(g.count, S::H * S::Q), S::AC_THREADS, G_SMEM, st>>>(F, Z, nT, s.synth, g, tw, zmap);
         check_launch("k3g_dec");
         }
     }
