@@ -48,8 +48,8 @@ struct GroupShape {
     static_assert(S::AC_THREADS >= L, "one thread per output row i0 in the across-line DFTs");
     static constexpr size_t SC_BYTES = static_cast<size_t>(kMaxGroupLen) * S::P * sizeof(double);
     template <class C>
-    static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars (+ 1024-byte alignment for TMA)
-        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES + 1024;
+    static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars + 2 mbarriers (+ 1024-byte alignment for TMA)
+        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES + 16 + 1024;
     }
 #ifndef SLB_GROUP_A_MINB
     static constexpr int A_MINB = 2;
@@ -200,12 +200,18 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
 template <int L, class C = double2>
 __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MINB)
     k3g_rec(const C* __restrict__ Z, long long zbs, C* __restrict__ acc, FiltSynth3D filt,
-            const __grid_constant__ SplitGroups grp, int accumulate, const C* __restrict__ tw, int bx0 = 0) {
+            const __grid_constant__ SplitGroups grp, int accumulate, const C* __restrict__ tw,
+            const __grid_constant__ CUtensorMap zmap, int bx0 = 0) {
     using S = SplitShape<L>;
     using R = RealOf<C>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
-    SLB_DYN_SMEM(C, tile);  // [2][n][LD] band tiles (cp.async double buffer)
+    // TMA: band tiles arrive by bulk tensor loads (dense [i0][a], 64-byte
+    // swizzle) on two mbarriers; otherwise cp.async into [n][LD] tiles
+    constexpr bool TMA = GroupShape<L>::template TMA_STORE<C>;
+    SLB_DYN_SMEM(C, tile_raw);  // [2][n][LD] band tiles (double buffer)
+    C* tile = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023));
     R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sc + kMaxGroupLen * P);
     const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
@@ -213,12 +219,26 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
     const int i0 = threadIdx.x;
     const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
     auto load = [&](int slot, C* buf) {
-        const C* z = Z + (long long)slot * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) +
-                     (long long)si0 * n;
+        if constexpr (TMA) {
+            if (threadIdx.x == 0)
+                tma_load_5d(&zmap, buf, bars + (buf == tile ? 0 : 1), static_cast<unsigned>(n * P * sizeof(C)), 0, q, 0, 0,
+                            slot * S::H + k2);
+        } else {
+            const C* z = Z + (long long)slot * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) +
+                         (long long)si0 * n;
 #pragma unroll 4
-        for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
-        asm volatile("cp.async.commit_group;" ::: "memory");
+            for (int j = 0; j < n / T; ++j) cp_async_c(buf + (si0 + T * j) * LD + sa, z + (long long)j * T * n);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
     };
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(bars, 1);
+            mbar_init(bars + 1, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     C ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
@@ -237,24 +257,32 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
         C* cur = tile;
         for (int bb = 0; bb < nbg; ++bb, ++it) {
             cur = tile + (it & 1) * S::AC_ELEMS;
-            if (it > 0) __syncthreads();  // tile (it + 1) & 1 is free (read by band it - 1 / the group end)
+            if constexpr (TMA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic use -> TMA refill
+            // tile (it + 1) & 1 is free (read by band it - 1 / the group end); with
+            // TMA this barrier also publishes the group's scalars at it = 0
+            if (it > 0 || TMA) __syncthreads();
             int nslot = -1;
             if (bb + 1 < nbg)
                 nslot = b0 + bb + 1 - grp.zb0;
             else if (gi + 1 < grp.count)
                 nslot = grp.first[gi + 1] - grp.zb0;
-            if (nslot >= 0) {
-                load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
-                asm volatile("cp.async.wait_group 1;" ::: "memory");  // band it landed, the next in flight
+            if constexpr (TMA) {
+                if (nslot >= 0) load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
+                mbar_wait_parity(bars + (it & 1), static_cast<unsigned>(it >> 1) & 1u);  // band it landed
             } else {
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                if (nslot >= 0) {
+                    load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");  // band it landed, the next in flight
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                __syncthreads();
             }
-            __syncthreads();
             if (i0 < n) {
                 C v[P];
 #pragma unroll
                 for (int a = 0; a < P; ++a) {
-                    const C u = cur[i0 * LD + a];
+                    const C u = TMA ? cur[sw64_slot(i0 * (P * 16) + a * 16)] : cur[i0 * LD + a];
                     v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
                 }
                 dft_small<P, -1>(v);

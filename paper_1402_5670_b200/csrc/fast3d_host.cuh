@@ -224,17 +224,11 @@ struct Split3DLaunch {
     }
     // shear-group passes (fast3d_group.cuh)
     static constexpr size_t G_SMEM = GroupShape<n>::template smem<C>();
-    void gdec(const C* F, C* Z, const SplitGroups& g) {
-        if constexpr (n > 192) {
-            throw SlError(SL_ERR_GENERIC, "shear-group passes: n <= 192");
-        } else {
-        if (g.count == 0) return;
-        set_smem(k3g_dec<n, C>, G_SMEM);
-        int nbands = 0;
-        for (int i = 0; i < g.count; ++i) nbands += g.len[i];
+    // the chunk's Z as the 5D tensor {re/im x a%4, q, a/4, i0, slot * H + k2}
+    // (quad-interleaved rows) for the TMA copies of the grouped passes A / C
+    static CUtensorMap zmap_of(const C* Z, const SplitGroups& g) {
         CUtensorMap zmap{};
         if constexpr (GroupShape<n>::template TMA_STORE<C>) {
-            // Z as the 5D tensor {re/im x a%4, q, a/4, i0, slot * H + k2} (zrow quads)
             int slots = 0;
             for (int i = 0; i < g.count; ++i) slots = std::max(slots, g.first[i] + g.len[i] - g.zb0);
             const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(S::Q), static_cast<cuuint64_t>(S::P / 4),
@@ -244,6 +238,17 @@ struct Split3DLaunch {
             const cuuint32_t box[5] = {8, 1, static_cast<cuuint32_t>(S::P / 4), static_cast<cuuint32_t>(n), 1};
             zmap = tma_map_f64(Z, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
         }
+        return zmap;
+    }
+    void gdec(const C* F, C* Z, const SplitGroups& g) {
+        if constexpr (n > 192) {
+            throw SlError(SL_ERR_GENERIC, "shear-group passes: n <= 192");
+        } else {
+        if (g.count == 0) return;
+        set_smem(k3g_dec<n, C>, G_SMEM);
+        int nbands = 0;
+        for (int i = 0; i < g.count; ++i) nbands += g.len[i];
+        const CUtensorMap zmap = zmap_of(Z, g);
         LaunchScope ls(s, "f3g_dec", st, nbands);
         k3g_dec<n, C><<<dim3(g.count, S::H * S::Q), S::AC_THREADS, G_SMEM, st>>>(F, Z, nT, s.synth, g, tw, zmap);
         check_launch("k3g_dec");
@@ -259,8 +264,9 @@ struct Split3DLaunch {
         int nbands = 0;
         for (int i = 0; i < g.count; ++i) nbands += g.len[i];
         LaunchScope ls(s, "f3g_rec", st, nbands);
+        const CUtensorMap zmap = zmap_of(Z, g);
         k3g_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, G_SMEM, st>>>(Z, nT, acc, s.synth, g, accumulate,
-                                                                                   tw, k2lo * S::Q);
+                                                                                   tw, zmap, k2lo * S::Q);
         check_launch("k3g_rec");
         }
     }

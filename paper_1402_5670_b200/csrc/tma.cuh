@@ -46,4 +46,31 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* m, const void* s
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// 5D bulk tensor load global -> smem, completing `bytes` on the mbarrier `bar`
+// (the issuing thread arms the barrier with the expected transaction count)
+__device__ __forceinline__ void tma_load_5d(const CUtensorMap* m, void* smem, uint64_t* bar, unsigned bytes, int c0,
+                                            int c1, int c2, int c3, int c4) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(sa),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(ba)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ba), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned phase) {
+    const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(ba),
+        "r"(phase)
+        : "memory");
+}
+
 }  // namespace slb
