@@ -10,8 +10,24 @@
 #pragma once
 
 #include "fast2d_host.cuh"
+#include "tma.cuh"
 
 namespace slb {
+
+// TMA tile load / store in the fused rows pass (fp64, 512): the tile [H][2V =
+// 8] has 128-byte rows, and tslot<4>'s XOR of the 16-byte slot with k & 7 is
+// exactly the TMA 128-byte swizzle, so the bulk tensor copies (two boxes of
+// HB <= 256 rows) land in the layout the per-line code already reads.
+#ifndef SLB_ROWS_TMA
+#define SLB_ROWS_TMA 1
+#endif
+template <int L, class C>
+struct RowsTma {
+    static constexpr bool ON = SLB_ROWS_TMA && L == 512 && sizeof(C) == 16 && 2 * RowCfg<L>::V == 8;
+    static constexpr int H = L / 2 + 1, HB = (H + 1) / 2;
+    static constexpr size_t TILE_BYTES = static_cast<size_t>(2 * HB) * 8 * sizeof(C);  // 2 boxes of HB 128-byte rows
+    static size_t smem(size_t plain) { return std::max(plain, TILE_BYTES) + 1024 + 16; }  // + alignment + mbarrier
+};
 
 // STORE = false: the stack is not materialised (sl_set_stack_output, band
 // null); a separate instantiation so the stack-writing variant keeps its
@@ -20,11 +36,15 @@ template <int L, bool STORE = true, class C = double2>
 __global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN_BLOCKS)
     k2_rows_fused(C* __restrict__ inter, long long ibs, RealOf<C>* __restrict__ band, long long bbs, int n0, int H,
                   RealOf<C> scale, const double* __restrict__ delta, int band0, const C* __restrict__ tw,
-                  long long izs = 0, long long bzs = 0) {
+                  const __grid_constant__ CUtensorMap tmap, int cstride, long long izs = 0, long long bzs = 0) {
     constexpr int T = FusedRowPlan<L>::T, E = FusedRowPlan<L>::E, V = RowCfg<L>::V;
     using R = RealOf<C>;
     constexpr int KPT = (L / 2 + 1 + T - 1) / T;
-    SLB_DYN_SMEM(C, tile);  // [H][2V] swizzled tile, then V line buffers
+    constexpr bool TMA = RowsTma<L, C>::ON;
+    SLB_DYN_SMEM(C, tile_raw);  // [H][2V] swizzled tile, then V line buffers
+    C* tile = TMA ? reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023)) : tile_raw;
+    [[maybe_unused]] uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(tile) + RowsTma<L, C>::TILE_BYTES);
+    [[maybe_unused]] const int slot = blockIdx.y + blockIdx.z * cstride;  // band slot of the intermediate (TMA z)
     const int r0 = blockIdx.x * 2 * V;
     inter += blockIdx.y * ibs + blockIdx.z * izs;  // blockIdx.z: frame of a lock-step batch
     // STORE = false keeps a (never taken) runtime test on the stores: ptxas
@@ -37,15 +57,30 @@ __global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN
     // thread -> fixed slot rr, k-rows strided by a compile-time step
     constexpr int KS = RowCfg<L>::FUSED_THREADS / (2 * V);
     const int rr = threadIdx.x % (2 * V);
+    if constexpr (TMA) {
+        constexpr int HB = RowsTma<L, C>::HB;
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();  // the barrier is initialised before anyone waits on it
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(bar, static_cast<unsigned>(RowsTma<L, C>::TILE_BYTES));
+            tma_load_3d(&tmap, tile, bar, 2 * r0, 0, slot);  // rows past n0 / k past H zero-fill
+            tma_load_3d(&tmap, tile + HB * 2 * V, bar, 2 * r0, HB, slot);
+        }
+        mbar_wait_parity(bar, 0);
+    } else {
 #pragma unroll 4
-    for (int k = threadIdx.x / (2 * V); k < H; k += KS) {
-        if (rr < nrows)
-            cp_async_c(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
-        else
-            tile[tslot<V>(k, rr)] = mkc<C>(0.0, 0.0);
+        for (int k = threadIdx.x / (2 * V); k < H; k += KS) {
+            if (rr < nrows)
+                cp_async_c(tile + tslot<V>(k, rr), inter + (long long)k * n0 + r0 + rr);
+            else
+                tile[tslot<V>(k, rr)] = mkc<C>(0.0, 0.0);
+        }
+        cp_async_wait_all();
+        __syncthreads();
     }
-    cp_async_wait_all();
-    __syncthreads();
     const int q = threadIdx.x / T, t = threadIdx.x - q * T;
     C x[E];
 #pragma unroll
@@ -112,6 +147,18 @@ __global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN
             tile[tslot<V>(k, 2 * q + 1)] = mkc<C>(R(0.5) * (zk[u].y + zm[u].y), R(0.5) * (zm[u].x - zk[u].x));
         }
     }
+    if constexpr (TMA) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            constexpr int HB = RowsTma<L, C>::HB;
+            tma_store_3d(&tmap, tile, 2 * r0, 0, slot);  // out-of-range rows / k are clipped
+            tma_store_3d(&tmap, tile + HB * 2 * V, 2 * r0, HB, slot);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        }
+        return;
+    }
     __syncthreads();
 #pragma unroll 4
     for (int k = threadIdx.x / (2 * V); k < H; k += KS)
@@ -119,14 +166,48 @@ __global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN
 }
 
 // rows pass of the fused denoise (band = null: the stack is not materialised)
+// the intermediate [slots][H][n0] complex as a 3D fp64 tensor for the TMA tile
+// copies (cached per buffer / shape: launches reuse a handful of workspaces)
+template <int L, class C>
+static CUtensorMap rows_tmap(C* inter, int n0, int H, long long slots) {
+    CUtensorMap m{};
+    if constexpr (RowsTma<L, C>::ON) {
+        static std::mutex mu;
+        static std::map<std::tuple<const void*, int, int, long long>, CUtensorMap> cache;
+        std::lock_guard<std::mutex> lk(mu);
+        const auto key = std::make_tuple(static_cast<const void*>(inter), n0, H, slots);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+        const cuuint64_t dims[3] = {2 * static_cast<cuuint64_t>(n0), static_cast<cuuint64_t>(H),
+                                    static_cast<cuuint64_t>(slots)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(n0) * sizeof(C),
+                                       static_cast<cuuint64_t>(n0) * H * sizeof(C)};
+        const cuuint32_t box[3] = {2 * 2 * RowCfg<L>::V, static_cast<cuuint32_t>(RowsTma<L, C>::HB), 1};
+        m = tma_map_f64(inter, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+        cache[key] = m;
+    }
+    return m;
+}
+
+// spectra of nhT complex values a workspace buffer holds
+template <class C>
+static long long ws_slots(const DBuf<double2>& b, long long nhT) {
+    return static_cast<long long>(b.n * sizeof(double2) / sizeof(C)) / nhT;
+}
+
+// inter: `slots` band spectra [H][n0] back to back (bands at ibs, frames at izs = cstride * ibs)
 template <int L, class C = double2>
 static void launch_rows_fused(dim3 grid, size_t tile_smem, cudaStream_t st, C* inter, long long ibs,
                               RealOf<C>* band, long long bbs, int n0, int H, double scale, const double* delta,
-                              int band0, const C* tw, long long izs, long long bzs) {
+                              int band0, const C* tw, long long izs, long long bzs, long long slots) {
     using RC = RowCfg<L>;
     auto* k = band ? k2_rows_fused<L, true, C> : k2_rows_fused<L, false, C>;
-    set_smem(k, tile_smem);
-    k<<<grid, RC::FUSED_THREADS, tile_smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, izs, bzs);
+    const int cstride = izs > 0 ? static_cast<int>(izs / ibs) : 0;
+    const size_t smem = RowsTma<L, C>::ON ? RowsTma<L, C>::smem(tile_smem) : tile_smem;
+    const CUtensorMap tm = rows_tmap<L, C>(inter, n0, H, slots);
+    set_smem(k, smem);
+    k<<<grid, RC::FUSED_THREADS, smem, st>>>(inter, ibs, band, bbs, n0, H, scale, delta, band0, tw, tm, cstride, izs,
+                                              bzs);
     check_launch("k2_rows_fused");
 }
 
@@ -188,7 +269,7 @@ static void denoise2d_fast_t(System& s, const RealOf<CX>* f, RealOf<CX>* stack, 
             LaunchScope ls(s, "f2_rows_fused", st, cb);
             launch_rows_fused<L1, CX>(dim3(row_blocks, cb), row_smem, st, ws_as<CX>(s.w->inter), nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
-                                  delta, s.lo + b0, tw1, 0, 0);
+                                  delta, s.lo + b0, tw1, 0, 0, ws_slots<CX>(s.w->inter, nhT));
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, cb);
@@ -273,7 +354,7 @@ static void denoise2d_fast_batch_t(System& s, const RealOf<CX>* f, long long ffs
             LaunchScope ls(s, "f2_rows_fused", st, static_cast<long long>(cb) * nf);
             launch_rows_fused<L1, CX>(dim3(row_blocks, cb, nf), row_smem, st, ws_as<CX>(s.w->inter), nhT,
                                   (stack ? stack + static_cast<size_t>(b0) * s.nreal : nullptr), s.nreal, n0, H, scale,
-                                  delta, s.lo + b0, tw1, izs, sfs);
+                                  delta, s.lo + b0, tw1, izs, sfs, ws_slots<CX>(s.w->inter, nhT));
         }
         {
             LaunchScope ls(s, "f2_cols_rec", st, static_cast<long long>(cb) * nf);

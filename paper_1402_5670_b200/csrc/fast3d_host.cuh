@@ -78,7 +78,7 @@ struct Fast3DLaunch {
         set_smem(k, row_smem);
         LaunchScope ls(s, "f3_rows_fused", st, nb);
         k<<<dim3(row_blocks, nb), RC::FUSED_THREADS, row_smem, st>>>(
-            inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw, 0, 0);
+            inter, nT, band, bbs, n * n, H, 1.0 / static_cast<double>(s.nreal), delta, band0, tw, CUtensorMap{}, 0, 0, 0);
         check_launch("k2_rows_fused");
     }
     template <int DIR>

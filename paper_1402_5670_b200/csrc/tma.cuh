@@ -59,6 +59,28 @@ __device__ __forceinline__ void tma_load_5d(const CUtensorMap* m, void* smem, ui
         "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(ba)
         : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes) : "memory");
+}
+// 3D bulk tensor load (the barrier armed separately with the total bytes)
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, void* smem, uint64_t* bar, int c0, int c1, int c2) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            sa),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(ba)
+        : "memory");
+}
+// 3D bulk tensor store (no commit: the caller commits the group)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* smem, int c0, int c1, int c2) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(sa)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     const unsigned ba = static_cast<unsigned>(__cvta_generic_to_shared(bar));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ba), "r"(count) : "memory");
