@@ -96,8 +96,10 @@ struct SplitShape {
     static constexpr bool B_SWZ = SLB_SPLIT_B_SWZ;
 #endif
 #ifndef SLB_SPLIT_B_MINB
-    // 192: 2 CTAs/SM at <= 128 registers (no spills) measured +1.3 % on pass B over 3 at <= 85 (72 B spilled)
-    static constexpr int B_MINB = L >= 256 ? 1 : (L == 192 ? 2 : 3);
+    // 192 (with the single-exchange rows, X1): 3 CTAs/SM at 80 registers, 128 B
+    // spilled, measured +3.4 % on the 3D step over 2 at 128 (without X1 the same
+    // cap spills 356 B and loses 10 %; profiles/r2b_ab_passB_minb3.log)
+    static constexpr int B_MINB = L >= 256 ? 1 : 3;
 #else
     static constexpr int B_MINB = SLB_SPLIT_B_MINB;
 #endif
