@@ -378,7 +378,9 @@ __device__ __forceinline__ void mirror_pairs_shfl(const C (&x)[E], C (&zk)[KPT],
 // fft192_a: 16-major in -> 12-major out (radix 12, exchange, radix 16);
 // fft192_b: 12-major in -> 16-major out (radix 16, exchange, radix 12).
 // Stockham stages as RegStage (w = e^{DIR 2 pi i / 192}); twiddle powers by a
-// running product (~15 ulp, far inside the 1e-10 budget). Exchange slots:
+// running product (~15 ulp, far inside the 1e-10 budget; 15 independent table
+// loads instead measured 6 % slower on the 3D step,
+// profiles/r2b_ab_fft192_twiddle_loads.log). Exchange slots:
 // e + e/24 for the radix-12 stores / 12-major loads, e ^ ((e >> 4) & 7) for the
 // radix-16 stores / 16-major loads (both conflict-free per quarter warp).
 __device__ __forceinline__ int swz192a(int e) { return e + static_cast<int>(static_cast<unsigned>(e) / 24u); }
