@@ -49,7 +49,7 @@ struct GroupShape {
     static constexpr size_t SC_BYTES = static_cast<size_t>(kMaxGroupLen) * S::P * sizeof(double);
     template <class C>
     static constexpr size_t smem() {  // two [n][LD] tiles + the band scalars + 2 mbarriers (+ 1024-byte alignment for TMA)
-        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES + 16 + 1024;
+        return 2 * S::AC_ELEMS * sizeof(C) + SC_BYTES + 16 + S::P * sizeof(C) + 1024;
     }
 #ifndef SLB_GROUP_A_MINB
     static constexpr int A_MINB = 2;
@@ -113,8 +113,12 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
     SLB_DYN_SMEM(C, tile_raw);  // [2][n][LD] output tiles; the line buffers and the Y staging alias tile 0
     C* tile = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023));
     R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);  // [len][P]
+    // the CTA's across-line DFT twiddles w_n^{a q} (q fixed per CTA): read as
+    // shared-memory broadcasts instead of per-band table loads through L1
+    C* twq = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(sc) + GroupShape<L>::SC_BYTES + 16);
     const int gi = blockIdx.x;
     const int k2 = blockIdx.y / Q, q = blockIdx.y - k2 * Q;
+    if (threadIdx.x < P) twq[threadIdx.x] = twiddle<+1>(tw, threadIdx.x * q);  // published by the post-FFT barrier
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
     const int b0 = grp.first[gi], nbg = grp.len[gi], type = grp.type[gi];
@@ -167,7 +171,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
             dft_small<P, +1>(v);
 #pragma unroll
             for (int a = 0; a < P; ++a) {
-                const C w = a == 0 ? v[0] : cmul(v[a], twiddle<+1>(tw, a * q));
+                const C w = a == 0 ? v[0] : cmul(v[a], twq[a]);
                 if constexpr (TMA)
                     buf[sw64_slot(i0 * (P * 16) + a * 16)] = w;  // dense [i0][a], 64-byte swizzle
                 else
@@ -212,6 +216,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
     C* tile = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023));
     R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);
     uint64_t* bars = reinterpret_cast<uint64_t*>(sc + kMaxGroupLen * P);
+    C* twq = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(sc) + GroupShape<L>::SC_BYTES + 16);
     const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
         }
         __syncthreads();
     }
+    if (threadIdx.x < P) twq[threadIdx.x] = twiddle<-1>(tw, threadIdx.x * q);  // published by the first band's barrier
     C ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
 #pragma unroll
                 for (int a = 0; a < P; ++a) {
                     const C u = TMA ? cur[sw64_slot(i0 * (P * 16) + a * 16)] : cur[i0 * LD + a];
-                    v[a] = a == 0 ? u : cmul(u, twiddle<-1>(tw, a * q));
+                    v[a] = a == 0 ? u : cmul(u, twq[a]);
                 }
                 dft_small<P, -1>(v);
 #pragma unroll
