@@ -54,6 +54,17 @@ __device__ __forceinline__ int tslot(int k, int rr) {
     return k * (2 * V) + (rr ^ (k & (2 * V - 1)));
 }
 
+// cols_dec: the FFTs' base twiddles loaded once per thread before the band
+// loop (they depend only on the thread index) instead of per band: cols_dec
+// -15 %; cols_rec (capped at 128 registers) spills with them and slows 38 %,
+// so it keeps the table loads (profiles/r2b_ab_cols_twiddle_preload.log)
+#ifndef SLB_COL_TWPRE
+#define SLB_COL_TWPRE 1
+#endif
+#ifndef SLB_COLREC_TWPRE
+#define SLB_COLREC_TWPRE 0
+#endif
+
 // CTA shapes: rows kernels take V = 256 / T row pairs (256 threads; smem =
 // [H][2V] tile + V line buffers); column kernels take 128 / T lines
 // (128 threads, L * 16 B each).
@@ -333,6 +344,8 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
     }
     const int g0 = blockIdx.y * G;
     const int gn = min(G, nb - g0);
+    [[maybe_unused]] TwPreK<ColPlan<L>, L, +1, C> twp;
+    if constexpr (SLB_COL_TWPRE) twp.load(tw, t);
     // psi of band b+1 is loaded while band b is in the FFT
     R p[E];
     {
@@ -353,7 +366,10 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, ColDec<L>::MIN_BLOCKS)
 #pragma unroll
             for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
-        reg_fft_p<ColPlan<L>, L, +1>(x, sm, t, tw);
+        if constexpr (SLB_COL_TWPRE)
+            reg_fft_pw<ColPlan<L>, L, +1>(x, sm, t, twp);
+        else
+            reg_fft_p<ColPlan<L>, L, +1>(x, sm, t, tw);
         if (valid) {
             C* o = inter + (long long)b * ibs + (long long)k1 * L;
 #pragma unroll
@@ -456,6 +472,8 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
             pn[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
     }
+    [[maybe_unused]] TwPreK<ColPlan<L>, L, -1, C> twp;
+    if constexpr (SLB_COLREC_TWPRE) twp.load(tw, t);
     constexpr bool CPA = ColRec<L>::CPA;
     C* stg = sm + LineBuf<L>::N;  // CPA: two staged lines [2][L] after the exchange buffer
     auto stage = [&](int b, int buf) {  // each thread copies exactly the elements it reads back
@@ -508,7 +526,10 @@ __global__ void __launch_bounds__(ColCfg<L>::THREADS, SLB_COLREC_MINB)
 #pragma unroll
             for (int m = 0; m < E; ++m) p[m] = valid ? __ldg(ps + t + T * m) : R(0);
         }
-        reg_fft_p<ColPlan<L>, L, -1>(x, sm, t, tw);
+        if constexpr (SLB_COLREC_TWPRE)
+            reg_fft_pw<ColPlan<L>, L, -1>(x, sm, t, twp);
+        else
+            reg_fft_p<ColPlan<L>, L, -1>(x, sm, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             C a = ColRec<L>::REGACC ? ar[m] : acc[t + T * m];

@@ -297,6 +297,16 @@ struct PlanNS<PL, 0> {
     static constexpr int value = 1;
 };
 
+// Base twiddle w^{jm} of butterfly q of stage S: a table load by default, or
+// a value the caller preloaded once (TwPreK: kernels that run many FFTs of the
+// same thread layout -- the twiddles depend only on the thread index)
+template <int DIR, class C>
+struct TwTable {
+    const C* __restrict__ tw;
+    template <int S>
+    __device__ __forceinline__ C get(int /*q*/, int idx) const { return twiddle<DIR>(tw, idx); }
+};
+
 template <int L, int DIR, int S, bool PAD, class C = double2, class PL = RegPlan<L>>
 struct RegStage {
     using P = PL;
@@ -308,6 +318,10 @@ struct RegStage {
     static_assert(E % R == 0, "radix must divide the per-thread element count");
 
     __device__ __forceinline__ static void run(C (&x)[E], C* sm, int t, const C* __restrict__ tw) {
+        run_w(x, sm, t, TwTable<DIR, C>{tw});
+    }
+    template <class TW>
+    __device__ __forceinline__ static void run_w(C (&x)[E], C* sm, int t, const TW& tws) {
 #pragma unroll
         for (int q = 0; q < B; ++q) {
             const int j = t + T * q;
@@ -316,7 +330,7 @@ struct RegStage {
                 // one table load per butterfly; w^2..w^(R-1) by complex products
                 // (error ~3 ulp, far inside the 1e-10 budget) instead of R-1
                 // loads through the L1 data pipe
-                const C w1 = twiddle<DIR>(tw, jm * (L / (NS * R)));
+                const C w1 = tws.template get<S>(q, jm * (L / (NS * R)));
                 C wp[R];
                 wp[1] = w1;
 #pragma unroll
@@ -345,9 +359,43 @@ struct RegStage {
                 for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD, L, sizeof(C)>(j + r * (L / R2))];
             }
             line_sync<T>();
-            RegStage<L, DIR, S + 1, PAD, C, PL>::run(x, sm, t, tw);
+            RegStage<L, DIR, S + 1, PAD, C, PL>::run_w(x, sm, t, tws);
         }
     }
+};
+
+// per-thread base twiddles of every stage s >= 1 (B butterflies each) for plan PL
+template <class PL, int S>
+struct PlanTwCount {
+    static constexpr int value = PlanTwCount<PL, S - 1>::value + PL::E / PL::R[S];
+};
+template <class PL>
+struct PlanTwCount<PL, 0> {
+    static constexpr int value = 0;
+};
+
+// base twiddles of plan PL / direction DIR for thread t, loaded once
+template <class PL, int L, int DIR, class C>
+struct TwPreK {
+    static constexpr int N = PlanTwCount<PL, PL::NST - 1>::value;
+    C w[N > 0 ? N : 1];
+    __device__ __forceinline__ void load(const C* __restrict__ tw, int t) {
+        fill<1>(tw, t);
+    }
+    template <int S>
+    __device__ __forceinline__ void fill(const C* __restrict__ tw, int t) {
+        if constexpr (S < PL::NST) {
+            constexpr int R = PL::R[S], B = PL::E / R, NS = PlanNS<PL, S>::value;
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+                const int jm = (t + PL::T * q) % NS;
+                w[PlanTwCount<PL, S - 1>::value + q] = twiddle<DIR>(tw, jm * (L / (NS * R)));
+            }
+            fill<S + 1>(tw, t);
+        }
+    }
+    template <int S>
+    __device__ __forceinline__ C get(int q, int) const { return w[PlanTwCount<PL, S - 1>::value + q]; }
 };
 
 // Mirror pairs of a line held in registers (x[m] = Z[t + T m] on the T lanes
@@ -437,6 +485,12 @@ template <class PL, int L, int DIR, bool PAD = true, class C>
 __device__ __forceinline__ void reg_fft_p(C (&x)[PL::E], C* sm, int t, const C* __restrict__ tw) {
     static_assert(PL::R[0] == RegPlan<L>::R[0], "line-buffer swizzle follows RegPlan<L>'s first radix");
     RegStage<L, DIR, 0, PAD, C, PL>::run(x, sm, t, tw);
+}
+// ... with the base twiddles preloaded once per thread (TwPreK)
+template <class PL, int L, int DIR, bool PAD = true, class C, class TW>
+__device__ __forceinline__ void reg_fft_pw(C (&x)[PL::E], C* sm, int t, const TW& tws) {
+    static_assert(PL::R[0] == RegPlan<L>::R[0], "line-buffer swizzle follows RegPlan<L>'s first radix");
+    RegStage<L, DIR, 0, PAD, C, PL>::run_w(x, sm, t, tws);
 }
 
 }  // namespace slb
