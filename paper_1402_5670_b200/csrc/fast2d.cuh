@@ -57,7 +57,9 @@ __device__ __forceinline__ int tslot(int k, int rr) {
 // cols_dec: the FFTs' base twiddles loaded once per thread before the band
 // loop (they depend only on the thread index) instead of per band: cols_dec
 // -15 %; cols_rec (capped at 128 registers) spills with them and slows 38 %,
-// so it keeps the table loads (profiles/r2b_ab_cols_twiddle_preload.log)
+// so it keeps the table loads (profiles/r2b_ab_cols_twiddle_preload.log; at 3
+// CTAs/SM without spills -35 %, r2b_ab_colrec_twpre_minb3.log; from a
+// shared-memory copy of the table -11 %, r2b_ab_colrec_twiddles_smem.log)
 #ifndef SLB_COL_TWPRE
 #define SLB_COL_TWPRE 1
 #endif
