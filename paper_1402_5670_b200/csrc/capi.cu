@@ -575,7 +575,9 @@ void denoise_lockstep(System& s, const double* in, int nframes, double* user_sta
         double* stk = group_stack(s, user_stack, f0, group, sfs);
         const int conc = s.concurrency;
         s.concurrency = std::max(conc, 4);  // full-machine band grouping (fast2d_cfg)
+        s.lockstep_cfg = true;
         denoise2d_fast_batch(s, in + off, s.nreal, nf, stk, sfs, out + off, s.nreal, s.delta.p, fst);
+        s.lockstep_cfg = false;
         s.concurrency = conc;
     });
 }
@@ -1437,7 +1439,9 @@ int sl_denoise_batch_f32_dev(sl_system* h, const float* in, int nframes, float* 
             }
             const int conc = s.concurrency;
             s.concurrency = std::max(conc, 4);
+            s.lockstep_cfg = true;
             denoise2d_fast_batch_f32(s, in + off, s.nreal, nf, stk, sfs, out + off, s.nreal, s.delta.p, fst);
+            s.lockstep_cfg = false;
             s.concurrency = conc;
         });
     });

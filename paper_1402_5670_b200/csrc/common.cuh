@@ -190,7 +190,7 @@ static int env_knob(const char* name, int dflt) {
 struct Knobs {
     int group = -1, chunk = -1, group1 = -1, group2 = -1, chunk1 = -1;  // 2D band grouping (fast2d_cfg)
     int g3 = -1, chunk3 = -1;                                          // 3D band group / chunk
-    int lockstep = 1, lockstep_frames = 2;                              // lock-step frame groups (device batch)
+    int lockstep = 1, lockstep_frames = 4;                              // lock-step frame groups (device batch)
     int host_pipe = -1, pipe_conc = -1, pipe_group = -1, pipe_head = -1, pipe_tail = -1, lockstep_host = 0;  // pipelined host batch (-1: auto)
     bool denoise_unfused = false, disable_fast2d = false, disable_fast3d = false;
     bool split3d = true;  // three-pass 3D kernels (fast3d_split.cuh); SLB_SPLIT3D=0 selects the five-pass ones
@@ -207,7 +207,7 @@ struct Knobs {
         k.g3 = env_knob("SLB_G3", -1);
         k.chunk3 = env_knob("SLB_CHUNK3", -1);
         k.lockstep = env_knob("SLB_LOCKSTEP", 1);
-        k.lockstep_frames = std::max(1, env_knob("SLB_LOCKSTEP_FRAMES", 2));
+        k.lockstep_frames = std::max(1, env_knob("SLB_LOCKSTEP_FRAMES", 4));
         k.host_pipe = env_knob("SLB_HOST_PIPE", -1);
         k.pipe_conc = env_knob("SLB_PIPE_CONC", -1);
         k.pipe_group = env_knob("SLB_PIPE_GROUP", -1);
@@ -290,6 +290,7 @@ struct System {
     Workspace* w = nullptr;
     int nstreams = 6;               // workspaces used by batched calls (measured: 6 best for 8-frame host batches)
     int concurrency = 1;            // frames in flight on other streams (set by batched calls)
+    bool lockstep_cfg = false;      // a lock-step frame group is being issued (fast2d_cfg: all bands in one group)
     bool materialize = true;        // fused denoise writes the thresholded stack (sl_set_stack_output)
     cudaEvent_t fork_ev = nullptr;
     cudaEvent_t last_ev = nullptr;  // completion of the previous call on this handle (any stream)

@@ -51,6 +51,16 @@ struct Fast2DCfg {
 // takes every band in one chunk (up to 256 MiB) so each pass is one
 // full-machine launch, G = 7 from 512^2 up.
 static Fast2DCfg fast2d_cfg(const System& s) {
+    if (s.lockstep_cfg) {
+        // lock-step frame groups (4 frames): every band in one chunk and one
+        // column group -- F and the accumulator stay in registers across all
+        // bands, one slot per frame (512^2 +3 %, 256^2 +7 %, 1024^2 +1 % over
+        // G = 28 / 64 MiB chunks; profiles/r2b_sweep_lockstep_r2c.log)
+        const int G = knob_or(s.knobs.group, std::max(1, s.nb()));
+        int C = knob_or(s.knobs.chunk, std::max(1, s.nb()));
+        C = std::max(G, (C / G) * G);
+        return {G, C};
+    }
     const bool conc = s.concurrency >= 4;
     const double per = static_cast<double>(s.H) * s.n[0] * sizeof(double2);
     if (!conc) {
