@@ -710,12 +710,13 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
         deltas(s, K, nK, sigma, scaled, st);
         // measured (tools/e2e_ab.sh, 8 frames of 512^2): 3 compute streams
         // 6250 frames/s, 1: 4800, 4: 6100, 5-6: 6220, per-frame fan-out: 6100
-        // schedule (profiles/r2_e2e_sweep.log): below 16 frames 3 compute streams of
-        // single frames; from 16 frames 4 streams of lock-step pairs after one
-        // single head frame (compute starts after one frame's H2D) -- e2e 0.92 of
-        // the device batch at 32 frames vs 0.88 with singles
+        // schedule (profiles/r2_e2e_sweep.log, r2b_sweep_e2e_pipe.log): below 16
+        // frames 3 compute streams of single frames; from 16 frames 3 streams of
+        // lock-step groups of 4 frames with every band in one group (as the
+        // device batch) after one single head frame (compute starts after one
+        // frame's H2D) -- e2e 0.90 of the device batch at 32 frames
         const bool many = nframes >= 16;
-        const int pipe = s.knobs.host_pipe >= 0 ? s.knobs.host_pipe : (s.fast2d ? (many ? 4 : 3) : 0);
+        const int pipe = s.knobs.host_pipe >= 0 ? s.knobs.host_pipe : (s.fast2d ? 3 : 0);
         const long long sfs = static_cast<long long>(s.nb()) * s.nreal;
         if (pipe > 0 && nframes > 1) {
             // pipelined: all H2D in frame order on one copy stream, the fused
@@ -730,9 +731,9 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             for (int k = 1; k <= P + 2; ++k) SL_CUDA(cudaStreamWaitEvent(s.ws[static_cast<size_t>(k)]->st, s.fork_ev, 0));
             const size_t fb = static_cast<size_t>(s.nreal) * sizeof(double);
             s.concurrency = s.knobs.pipe_conc >= 1 ? s.knobs.pipe_conc : P;  // band grouping of fast2d_cfg
-            // SLB_PIPE_GROUP = 2: lock-step frame pairs per compute stream (one
-            // launch per pass covers both frames, as in the device batch)
-            const int want_grp = s.knobs.pipe_group >= 1 ? s.knobs.pipe_group : (many ? 2 : 1);
+            // SLB_PIPE_GROUP: lock-step frame groups per compute stream (one
+            // launch per pass covers the group, as in the device batch)
+            const int want_grp = s.knobs.pipe_group >= 1 ? s.knobs.pipe_group : (many ? 4 : 1);
             const int head = s.knobs.pipe_head >= 0 ? s.knobs.pipe_head : (many ? 1 : 0);
             // the last `tail` frames alone too: the compute streams finish single
             // frames instead of pairs, so less D2H is left after the last kernel
@@ -759,10 +760,12 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
                     s.w = s.ws[static_cast<size_t>(1 + g % P)].get();
                     SL_CUDA(cudaStreamWaitEvent(s.w->st, ein, 0));
                     double* stk = group_stack(s, nullptr, 0, std::max(grp, nf), sfs);
-                    if (nf > 1)
+                    if (nf > 1) {
+                        s.lockstep_cfg = s.knobs.pipe_allbands != 0;  // all bands in one group (fast2d_cfg)
                         denoise2d_fast_batch(s, s.io_in.p + off, s.nreal, nf, stk, sfs, s.io_out.p + off, s.nreal,
                                              s.delta.p, s.w->st);
-                    else
+                        s.lockstep_cfg = false;
+                    } else
                         denoise(s, s.io_in.p + off, stk, s.io_out.p + off, s.delta.p, s.w->st);
                     SL_CUDA(cudaEventRecord(ec, s.w->st));
                     SL_CUDA(cudaStreamWaitEvent(cout, ec, 0));
@@ -771,6 +774,7 @@ int sl_denoise_batch_host(sl_system* h, const double* in, int nframes, double* o
             } catch (...) {
                 s.w = s.ws[0].get();
                 s.concurrency = 1;
+                s.lockstep_cfg = false;
                 throw;
             }
             s.w = s.ws[0].get();

@@ -191,7 +191,7 @@ struct Knobs {
     int group = -1, chunk = -1, group1 = -1, group2 = -1, chunk1 = -1;  // 2D band grouping (fast2d_cfg)
     int g3 = -1, chunk3 = -1;                                          // 3D band group / chunk
     int lockstep = 1, lockstep_frames = 4;                              // lock-step frame groups (device batch)
-    int host_pipe = -1, pipe_conc = -1, pipe_group = -1, pipe_head = -1, pipe_tail = -1, lockstep_host = 0;  // pipelined host batch (-1: auto)
+    int host_pipe = -1, pipe_conc = -1, pipe_group = -1, pipe_head = -1, pipe_tail = -1, lockstep_host = 0, pipe_allbands = 1;  // pipelined host batch (-1: auto)
     bool denoise_unfused = false, disable_fast2d = false, disable_fast3d = false;
     bool split3d = true;  // three-pass 3D kernels (fast3d_split.cuh); SLB_SPLIT3D=0 selects the five-pass ones
     bool group3d = true;  // shear-group passes A / C (fast3d_group.cuh); SLB_GROUP3D=0: one axis-0 FFT per band
@@ -214,6 +214,7 @@ struct Knobs {
         k.pipe_head = env_knob("SLB_PIPE_HEAD", -1);
         k.pipe_tail = env_knob("SLB_PIPE_TAIL", -1);
         k.lockstep_host = env_knob("SLB_LOCKSTEP_HOST", 0);
+        k.pipe_allbands = env_knob("SLB_PIPE_ALLBANDS", 1);
         k.denoise_unfused = std::getenv("SLB_DENOISE_UNFUSED") != nullptr;
         k.disable_fast2d = std::getenv("SLB_DISABLE_FAST2D") != nullptr;
         k.disable_fast3d = std::getenv("SLB_DISABLE_FAST3D") != nullptr;
