@@ -62,7 +62,16 @@ struct GroupShape {
     // pass A's Z tiles leave through TMA bulk tensor stores (fp64, 192: the
     // quad-interleaved Z rows as a 5D tensor, 64-byte swizzled staging)
     template <class C>
-    static constexpr bool TMA_STORE = SLB_GROUP_TMA && L == 192 && sizeof(C) == 16 && SplitLayout<L, C>::ZQUAD;
+    static constexpr bool TMA_STORE = SLB_GROUP_TMA && sizeof(C) == 16 &&
+                                      ((L == 192 && SplitLayout<L, C>::ZQUAD) || (L == 128 && !SplitLayout<L, C>::ZQUAD));
+    // slot of (i0, a) in a TMA-staged tile: dense [i0][a] rows of P * 16 bytes,
+    // 64-byte swizzle for 192 (quad rows), 128-byte for 128 (plain rows)
+    __device__ __forceinline__ static int tslot_tma(int i0, int a) {
+        if constexpr (L == 192)
+            return sw64_slot(i0 * (S::P * 16) + a * 16);
+        else
+            return sw128_slot(i0 * (S::P * 16) + a * 16);
+    }
 #ifndef SLB_GROUP_C_MINB
     static constexpr int C_MINB = 2;
 #else
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
             for (int a = 0; a < P; ++a) {
                 const C w = a == 0 ? v[0] : cmul(v[a], twq[a]);
                 if constexpr (TMA)
-                    buf[sw64_slot(i0 * (P * 16) + a * 16)] = w;  // dense [i0][a], 64-byte swizzle
+                    buf[GroupShape<L>::tslot_tma(i0, a)] = w;  // dense [i0][a], swizzled
                 else
                     buf[i0 * LD + a] = w;
             }
@@ -288,7 +297,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
                 C v[P];
 #pragma unroll
                 for (int a = 0; a < P; ++a) {
-                    const C u = TMA ? cur[sw64_slot(i0 * (P * 16) + a * 16)] : cur[i0 * LD + a];
+                    const C u = TMA ? cur[GroupShape<L>::tslot_tma(i0, a)] : cur[i0 * LD + a];
                     v[a] = a == 0 ? u : cmul(u, twq[a]);
                 }
                 dft_small<P, -1>(v);

@@ -231,12 +231,25 @@ struct Split3DLaunch {
         if constexpr (GroupShape<n>::template TMA_STORE<C>) {
             int slots = 0;
             for (int i = 0; i < g.count; ++i) slots = std::max(slots, g.first[i] + g.len[i] - g.zb0);
-            const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(S::Q), static_cast<cuuint64_t>(S::P / 4),
-                                        static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(S::H) * slots};
-            const cuuint64_t strides[4] = {4 * sizeof(C), 4 * S::Q * sizeof(C), static_cast<cuuint64_t>(n) * sizeof(C),
-                                           static_cast<cuuint64_t>(n) * n * sizeof(C)};
-            const cuuint32_t box[5] = {8, 1, static_cast<cuuint32_t>(S::P / 4), static_cast<cuuint32_t>(n), 1};
-            zmap = tma_map_f64(Z, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+            const cuuint64_t zs = static_cast<cuuint64_t>(S::H) * slots;
+            if constexpr (SplitLayout<n, C>::ZQUAD) {
+                // {re/im x a%4, q, a/4, i0, slot * H + k2}: quad-interleaved rows, 64-byte swizzle
+                const cuuint64_t dims[5] = {8, static_cast<cuuint64_t>(S::Q), static_cast<cuuint64_t>(S::P / 4),
+                                            static_cast<cuuint64_t>(n), zs};
+                const cuuint64_t strides[4] = {4 * sizeof(C), 4 * S::Q * sizeof(C), static_cast<cuuint64_t>(n) * sizeof(C),
+                                               static_cast<cuuint64_t>(n) * n * sizeof(C)};
+                const cuuint32_t box[5] = {8, 1, static_cast<cuuint32_t>(S::P / 4), static_cast<cuuint32_t>(n), 1};
+                zmap = tma_map_f64(Z, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B);
+            } else {
+                // {re/im x a, q, 1, i0, slot * H + k2}: plain [q][a] rows of P * 16 = 128 bytes, 128-byte swizzle
+                const cuuint64_t dims[5] = {2 * static_cast<cuuint64_t>(S::P), static_cast<cuuint64_t>(S::Q), 1,
+                                            static_cast<cuuint64_t>(n), zs};
+                const cuuint64_t strides[4] = {S::P * sizeof(C), static_cast<cuuint64_t>(n) * sizeof(C),
+                                               static_cast<cuuint64_t>(n) * sizeof(C),
+                                               static_cast<cuuint64_t>(n) * n * sizeof(C)};
+                const cuuint32_t box[5] = {2 * static_cast<cuuint32_t>(S::P), 1, 1, static_cast<cuuint32_t>(n), 1};
+                zmap = tma_map_f64(Z, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+            }
         }
         return zmap;
     }

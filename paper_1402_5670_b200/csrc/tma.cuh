@@ -34,6 +34,8 @@ static CUtensorMap tma_map_f64(const void* base, int rank, const cuuint64_t* dim
 // 16-byte slot of byte offset `b` inside a buffer written / read by a TMA copy
 // with 64-byte swizzle (bits [4,5] ^= bits [7,8]; the buffer is 1024-aligned)
 __device__ __forceinline__ int sw64_slot(int b) { return (b ^ (((b >> 7) & 3) << 4)) >> 4; }
+// ... with 128-byte swizzle (bits [4,6] ^= bits [7,9])
+__device__ __forceinline__ int sw128_slot(int b) { return (b ^ (((b >> 7) & 7) << 4)) >> 4; }
 
 // 5D bulk tensor store smem -> global (bulk async group of the calling thread)
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* m, const void* smem, int c0, int c1, int c2, int c3,
