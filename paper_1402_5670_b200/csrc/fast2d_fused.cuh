@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(RowCfg<L>::FUSED_THREADS, RowCfg<L>::FUSED_MIN
             tma_store_3d(&tmap, tile, 2 * r0, 0, slot);  // out-of-range rows / k are clipped
             tma_store_3d(&tmap, tile + HB * 2 * V, 2 * r0, HB, slot);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read before exit
         }
         return;
     }

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::A_MI
         for (int j = 0; j < n / T; ++j) __stcg(z + (long long)j * T * n, buf[(si0 + T * j) * LD + sa]);
     }
     if constexpr (TMA) {
-        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes done before exit
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem read before exit (stream order publishes the writes)
     }
 }
 
