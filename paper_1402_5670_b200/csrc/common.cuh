@@ -140,35 +140,6 @@ static LineCfg line_cfg(int L, bool strided) {
     return c;
 }
 
-// SMs of the current device (cached per device)
-static int sm_count() {
-    static std::mutex mu;
-    static std::map<int, int> cache;
-    int dev = 0;
-    SL_CUDA(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(dev);
-    if (it != cache.end()) return it->second;
-    int v = 0;
-    SL_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-    cache[dev] = v;
-    return v;
-}
-// resident CTAs per SM of a kernel at a block size / dynamic smem (cached)
-template <class K>
-static int resident_ctas(K kern, int threads, size_t smem) {
-    static std::mutex mu;
-    static std::map<std::pair<const void*, size_t>, int> cache;
-    std::lock_guard<std::mutex> lk(mu);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), smem * 4096 + static_cast<size_t>(threads));
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    int v = 0;
-    SL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, threads, smem));
-    cache[key] = std::max(1, v);
-    return cache[key];
-}
-
 template <class K>
 static void set_smem(K kern, size_t smem) {
     static std::mutex mu;

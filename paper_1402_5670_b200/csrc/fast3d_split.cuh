@@ -293,14 +293,13 @@ enum SplitMid : int {
 };
 
 // One pass-B work item (i0 = bx / (P/2), a pair, band bi) on the CTA's tile.
-// preloaded: the caller already staged the item's Z tile (cp.async, waited and
-// synchronised). A persistent variant that overlapped the next item's tile
-// load with the current item measured 6.7 % slower at 192^3
-// (profiles/r2b_ab_passB_persistent.log): the two resident CTAs per SM already
-// overlap each other's load and compute phases; so did an L2 bulk prefetch of
-// the tile one wave of CTAs ahead (2-3.5 % slower, r2b_ab_passB_l2_prefetch.log).
+// (A persistent variant that overlapped the next item's tile load with the
+// current item measured 6.7 % slower at 192^3, profiles/r2b_ab_passB_persistent.log:
+// the resident CTAs per SM already overlap each other's load and compute phases;
+// so did an L2 bulk prefetch of the tile one wave of CTAs ahead, 2-3.5 % slower,
+// r2b_ab_passB_l2_prefetch.log.)
 template <int L, int MODE, bool STORE, class C>
-__device__ __forceinline__ void mid_item(C* __restrict__ tile, bool preloaded, int bx, int bi, C* __restrict__ Z,
+__device__ __forceinline__ void mid_item(C* __restrict__ tile, int bx, int bi, C* __restrict__ Z,
                                          long long zbs, RealOf<C>* __restrict__ band, long long bbs,
                                          const RealOf<C>* __restrict__ bandin, RealOf<C> scale,
                                          const double* __restrict__ delta, int band0, const C* __restrict__ tw,
@@ -340,14 +339,12 @@ __device__ __forceinline__ void mid_item(C* __restrict__ tile, bool preloaded, i
                 for (int j = 0; j < Q; ++j) tile[bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, 2 * j + e)] = v[j];
             }
         } else {
-            if (!preloaded) {
-                // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
+            // KST k2-rows of 2Q slots per step (thread -> fixed slot, no per-element division)
 #pragma unroll 4
-                for (int k2 = sk2; k2 < H; k2 += KST)
-                    cp_async_c(tile + bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
-                cp_async_wait_all();
-                __syncthreads();
-            }
+            for (int k2 = sk2; k2 < H; k2 += KST)
+                cp_async_c(tile + bslot<Q, SplitLayout<L, C>::B_SWZ>(k2, sj), zb + (long long)k2 * n * n + (sj >> 1) * ZS + (sj & 1));
+            cp_async_wait_all();
+            __syncthreads();
             // length-Q DFT over q for each (k2, e), in place: slot 2q + e -> 2c + e
             for (int idx = threadIdx.x; idx < 2 * H; idx += S::B_THREADS) {
                 const int e = idx / H, k2 = idx - e * H;
@@ -488,7 +485,7 @@ __global__ void __launch_bounds__(SplitShape<L>::B_THREADS, SplitMinB<L, C>::val
             const RealOf<C>* __restrict__ bandin, RealOf<C> scale, const double* __restrict__ delta, int band0,
             const C* __restrict__ tw, const BandDesc3D* __restrict__ tb = nullptr) {
     SLB_DYN_SMEM(C, tile);  // [H][2Q] bslot<Q>; line buffers alias it
-    mid_item<L, MODE, STORE, C>(tile, false, blockIdx.x, blockIdx.y, Z, zbs, band, bbs, bandin, scale, delta, band0,
+    mid_item<L, MODE, STORE, C>(tile, blockIdx.x, blockIdx.y, Z, zbs, band, bbs, bandin, scale, delta, band0,
                                 tw, tb);
 }
 
