@@ -82,6 +82,18 @@ struct FusedRowPlan<512> {
     static constexpr int NST = 3;
 };
 #endif
+// 1024: 64 threads x 16 complex per line (radix 8, 8, 16: two exchanges
+// instead of the (8, 8, 4, 4) RegPlan's three): 2D 1024^2 x 64 +8 %
+// (profiles/r2b_ab_rows1024_plan.log; -DSLB_FUSEDPLAN1024_T128 restores 128 x 8)
+#ifndef SLB_FUSEDPLAN1024_T128
+template <>
+struct FusedRowPlan<1024> {
+    static constexpr int T = 64;
+    static constexpr int E = 16;
+    static constexpr int R[] = {8, 8, 16};
+    static constexpr int NST = 3;
+};
+#endif
 // plan of the 2D column kernels (k2_cols_dec / rec / sum): RegPlan<L> unless a
 // column-specific split is selected (A/B: -DSLB_COLPLAN512_T32)
 template <int L>

@@ -45,7 +45,8 @@ def test_cfg5_192_fused_denoise_vs_reference(cuda):
 
 
 def test_cfg2_512_lockstep_batch_vs_reference(cuda):
-    # the timed 2D step: 8 frames in lock-step pairs (G = 28), frame 3 = the cfg2 seed-7 frame
+    # the timed 2D step: 8 frames in lock-step groups of 4 (all bands in one
+    # group), frame 3 = the cfg2 seed-7 frame
     import torch
     g = golden("cfg2_denoise512_1122")
     s = P.build_system_2d(512, 512, P.ScaleProfile.from_levels([1, 1, 2, 2]))
@@ -60,7 +61,7 @@ def test_cfg2_512_lockstep_batch_vs_reference(cuda):
     np.testing.assert_array_equal(kept_fp_torch(stacks[3].reshape(49, -1)), g["kept_fp"])
     for i in range(8):
         one, st1 = P.denoise(ft[i], s, sch, return_stack=True)
-        # per-frame (G = 7) vs lock-step (G = 28): another summation association of the rec sum
+        # per-frame (G = 7) vs lock-step (G = 49): another summation association of the rec sum
         assert (torch.linalg.norm(den_b[i] - one) / torch.linalg.norm(one)).item() <= 1e-12
         assert torch.equal(stacks[i], st1)  # dec side: the same bits, the same support
     # the pipelined host batch (3 compute streams, G2 = 14 at 512^2) on the same frames
@@ -162,3 +163,31 @@ def test_in_library_nccl_single_rank(cuda):
     assert rel_l2(g2, P.denoise(fr[0], s2, sch2)) <= 1e-12
     s2.set_comm(None)
     s3.set_comm(None)
+
+
+def test_host_batch_groups_and_fused_rows_1024(cuda):
+    # from 16 frames the pipelined host batch runs lock-step groups of 4 on 3
+    # compute streams (all bands in one group); the fused rows pass at 1024 runs
+    # its own 64 x 16 line split. Both against the per-frame / unfused operators.
+    import torch
+    s = P.build_system_2d(512, 512, P.ScaleProfile.from_levels([1, 1, 2, 2]))
+    sch = P.ThresholdSchedule.defaults_2d(40.0)
+    frames = np.stack([P.add_gaussian_noise(P.cartoon(512), 40.0, 2000 + i) for i in range(18)])
+    host = P.denoise_batch(frames, s, sch)
+    dev = P.denoise_batch(torch.from_numpy(frames).to(cuda), s, sch).cpu().numpy()
+    for i in (0, 1, 5, 16, 17):
+        one = P.denoise(torch.from_numpy(frames[i]).to(cuda), s, sch).cpu().numpy()
+        assert rel_l2(host[i], one) <= 1e-12 and rel_l2(dev[i], one) <= 1e-12
+    s2 = P.build_system_2d(1024, 1024, P.ScaleProfile.from_levels([1, 1, 2, 2]))
+    x = torch.from_numpy(np.stack([P.add_gaussian_noise(P.cartoon(1024), 40.0, 3000 + i) for i in range(4)])).to(cuda)
+    den, stacks = P.denoise_batch(x, s2, sch, return_stacks=True)
+    for i in range(4):
+        # the unfused operators run the (8, 8, 4, 4) row plan, the fused rows
+        # (8, 8, 16): the same values to rounding; a coefficient within ~1e-16
+        # of its threshold could flip, so support is compared up to such ties
+        thr = P.forward_thresholded(x[i], s2, sch)
+        assert (torch.linalg.norm(stacks[i] - thr) / torch.linalg.norm(thr)).item() <= 1e-13
+        flips = torch.count_nonzero((thr != 0) != (stacks[i] != 0)).item()
+        assert flips <= 1e-8 * thr.numel()
+        ref = P.inverse(thr, s2)
+        assert (torch.linalg.norm(den[i] - ref) / torch.linalg.norm(ref)).item() <= 1e-12
