@@ -483,7 +483,7 @@ def run_workload(name, steps, warmup, ctx, want_cpu):
     fp64_peak = fp64_peak_tflops(clocks.get("sm_max_mhz"))
     R = R_full
     share = (1.0 / world) if is3d else 1.0  # per-GPU share of a volume's bands
-    group = 2 if (not is3d and frames > 1) else 1  # lock-step frame pairs in the device batch
+    group = min(4, frames) if (not is3d and frames > 1) else 1  # lock-step groups of 4 frames in the device batch
     fused_b = path_bytes(cfg, R, frames, "fused", group) * share
     lone_b = path_bytes(cfg, R, 1, "fused") * share
     unf_b = path_bytes(cfg, R, 1, "decrec") * share
