@@ -42,6 +42,9 @@ struct SplitGroups {
     unsigned char type[kMaxGroups];
 };
 
+#ifndef SLB_GROUP_C_TMA3
+#define SLB_GROUP_C_TMA3 1
+#endif
 template <int L>
 struct GroupShape {
     using S = SplitShape<L>;
@@ -71,6 +74,18 @@ struct GroupShape {
             return sw64_slot(i0 * (S::P * 16) + a * 16);
         else
             return sw128_slot(i0 * (S::P * 16) + a * 16);
+    }
+    // pass C: with TMA at 192 a three-stage ring of dense n x P tiles (two band
+    // tiles in flight while one is reduced); otherwise as smem()
+    template <class C>
+    static constexpr int C_STAGES = (SLB_GROUP_C_TMA3 && L == 192 && TMA_STORE<C>) ? 3 : 2;
+    template <class C>
+    __host__ __device__ static constexpr size_t c_stage_elems() {
+        return C_STAGES<C> == 3 ? static_cast<size_t>(L) * S::P : S::AC_ELEMS;
+    }
+    template <class C>
+    static constexpr size_t smem_c() {
+        return C_STAGES<C> * c_stage_elems<C>() * sizeof(C) + SC_BYTES + 32 + S::P * sizeof(C) + 1024;
     }
 #ifndef SLB_GROUP_C_MINB
     static constexpr int C_MINB = 2;
@@ -218,24 +233,29 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
     using S = SplitShape<L>;
     using R = RealOf<C>;
     constexpr int T = S::T, E = RegPlan<L>::E, P = S::P, Q = S::Q, LD = S::LD, n = L;
-    // TMA: band tiles arrive by bulk tensor loads (dense [i0][a], 64-byte
-    // swizzle) on two mbarriers; otherwise cp.async into [n][LD] tiles
+    // TMA: band tiles arrive by bulk tensor loads (dense [i0][a], swizzled) on
+    // mbarriers -- NST = 3 stages at 192 (two tiles in flight), else 2;
+    // without TMA cp.async into [n][LD] tiles
     constexpr bool TMA = GroupShape<L>::template TMA_STORE<C>;
-    SLB_DYN_SMEM(C, tile_raw);  // [2][n][LD] band tiles (double buffer)
+    constexpr int NST = GroupShape<L>::template C_STAGES<C>;
+    constexpr bool DENSE = NST == 3;  // group-end scratch in the dense swizzled layout (stages of exactly n P)
+    constexpr size_t STG = GroupShape<L>::template c_stage_elems<C>();
+    SLB_DYN_SMEM(C, tile_raw);  // [NST][stage] band tiles
     C* tile = reinterpret_cast<C*>((reinterpret_cast<uintptr_t>(tile_raw) + 1023) & ~uintptr_t(1023));
-    R* sc = reinterpret_cast<R*>(tile + 2 * S::AC_ELEMS);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sc + kMaxGroupLen * P);
-    C* twq = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(sc) + GroupShape<L>::SC_BYTES + 16);
+    R* sc = reinterpret_cast<R*>(tile + NST * STG);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(sc) + GroupShape<L>::SC_BYTES);
+    C* twq = reinterpret_cast<C*>(reinterpret_cast<unsigned char*>(sc) + GroupShape<L>::SC_BYTES + 32);
     const int bx = blockIdx.x + bx0;  // k2-slab launches (the multi-GPU reduce overlaps the last one)
     const int k2 = bx / Q, q = bx - k2 * Q;
     const int p = threadIdx.x / T, t = threadIdx.x - p * T;
     const int k1 = q + Q * p;
     const int i0 = threadIdx.x;
     const int sa = threadIdx.x % P, si0 = threadIdx.x / P;
-    auto load = [&](int slot, C* buf) {
+    auto load = [&](int slot, int stage) {
+        C* buf = tile + stage * STG;
         if constexpr (TMA) {
             if (threadIdx.x == 0)
-                tma_load_5d(&zmap, buf, bars + (buf == tile ? 0 : 1), static_cast<unsigned>(n * P * sizeof(C)), 0, q, 0, 0,
+                tma_load_5d(&zmap, buf, bars + stage, static_cast<unsigned>(n * P * sizeof(C)), 0, q, 0, 0,
                             slot * S::H + k2);
         } else {
             const C* z = Z + (long long)slot * zbs + (long long)k2 * n * n + zrow<P, Q, SplitLayout<L, C>::ZQUAD>(q, sa) +
@@ -245,10 +265,19 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
             asm volatile("cp.async.commit_group;" ::: "memory");
         }
     };
+    // Z slot of the band `ahead` bands after (gi, bb) in the launch's flat order, or -1
+    auto slot_ahead = [&](int gi, int bb, int ahead) {
+        bb += ahead;
+        while (gi < grp.count && bb >= grp.len[gi]) {
+            bb -= grp.len[gi];
+            ++gi;
+        }
+        return gi < grp.count ? grp.first[gi] + bb - grp.zb0 : -1;
+    };
     if constexpr (TMA) {
         if (threadIdx.x == 0) {
-            mbar_init(bars, 1);
-            mbar_init(bars + 1, 1);
+#pragma unroll
+            for (int st = 0; st < NST; ++st) mbar_init(bars + st, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
@@ -257,8 +286,13 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
     C ar[E];
 #pragma unroll
     for (int m = 0; m < E; ++m) ar[m] = mkc<C>(0.0, 0.0);
-    if (grp.count > 0) load(grp.first[0] - grp.zb0, tile);
-    int it = 0;  // flat band counter (tile it & 1)
+    // prologue: the first NST - 1 bands in flight
+#pragma unroll
+    for (int st = 0; st + 1 < NST; ++st) {
+        const int sl = slot_ahead(0, 0, st);
+        if (sl >= 0) load(sl, st);
+    }
+    int it = 0;  // flat band counter (stage it % NST)
     for (int gi = 0; gi < grp.count; ++gi) {
         const int b0 = grp.first[gi], nbg = grp.len[gi], type = grp.type[gi];
         // the previous group's scalars were last read before its closing barriers
@@ -271,22 +305,19 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
         for (int pp = 0; pp < P; ++pp) ag[pp] = mkc<C>(0.0, 0.0);
         C* cur = tile;
         for (int bb = 0; bb < nbg; ++bb, ++it) {
-            cur = tile + (it & 1) * S::AC_ELEMS;
+            const int stage = it % NST;
+            cur = tile + stage * STG;
             if constexpr (TMA) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic use -> TMA refill
-            // tile (it + 1) & 1 is free (read by band it - 1 / the group end); with
-            // TMA this barrier also publishes the group's scalars at it = 0
+            // stage (it + NST - 1) % NST is free (read by band it - 1 / the group
+            // end); with TMA this barrier also publishes the group's scalars at it = 0
             if (it > 0 || TMA) __syncthreads();
-            int nslot = -1;
-            if (bb + 1 < nbg)
-                nslot = b0 + bb + 1 - grp.zb0;
-            else if (gi + 1 < grp.count)
-                nslot = grp.first[gi + 1] - grp.zb0;
+            const int nslot = slot_ahead(gi, bb, NST - 1);
             if constexpr (TMA) {
-                if (nslot >= 0) load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
-                mbar_wait_parity(bars + (it & 1), static_cast<unsigned>(it >> 1) & 1u);  // band it landed
+                if (nslot >= 0) load(nslot, (it + NST - 1) % NST);
+                mbar_wait_parity(bars + stage, static_cast<unsigned>(it / NST) & 1u);  // band it landed
             } else {
                 if (nslot >= 0) {
-                    load(nslot, tile + ((it + 1) & 1) * S::AC_ELEMS);
+                    load(nslot, (it + 1) & 1);
                     asm volatile("cp.async.wait_group 1;" ::: "memory");  // band it landed, the next in flight
                 } else {
                     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -313,16 +344,24 @@ __global__ void __launch_bounds__(SplitShape<L>::AC_THREADS, GroupShape<L>::C_MI
         __syncthreads();  // every row read its last tile
         if (i0 < n) {
 #pragma unroll
-            for (int pp = 0; pp < P; ++pp) cur[i0 * LD + pp] = ag[pp];
+            for (int pp = 0; pp < P; ++pp) {
+                if constexpr (DENSE)
+                    cur[GroupShape<L>::tslot_tma(i0, pp)] = ag[pp];
+                else
+                    cur[i0 * LD + pp] = ag[pp];
+            }
         }
         __syncthreads();
         C x[E];
 #pragma unroll
-        for (int m = 0; m < E; ++m) x[m] = cur[(t + T * m) * LD + p];
+        for (int m = 0; m < E; ++m) x[m] = DENSE ? cur[GroupShape<L>::tslot_tma(t + T * m, p)] : cur[(t + T * m) * LD + p];
         __syncthreads();  // all lines gathered: the tile becomes the line buffers
         const BandDesc3D bd0 = filt.bands[b0];
         const GroupRow row = group_row(filt, bd0, type, k1, k2, n);
-        reg_fft<L, -1, S::PAD>(x, cur + p * S::LB, t, tw);
+        if constexpr (DENSE)
+            reg_fft_xor<L, -1>(x, cur + p * L, t, tw);  // P lines of exactly n slots fill the stage
+        else
+            reg_fft<L, -1, S::PAD>(x, cur + p * S::LB, t, tw);
 #pragma unroll
         for (int m = 0; m < E; ++m) {
             const R a = R(row.at(t + T * m));

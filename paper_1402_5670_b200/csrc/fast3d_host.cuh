@@ -272,13 +272,14 @@ struct Split3DLaunch {
             throw SlError(SL_ERR_GENERIC, "shear-group passes: n <= 192");
         } else {
         if (g.count == 0) return;
-        set_smem(k3g_rec<n, C>, G_SMEM);
+        constexpr size_t C_SMEM = GroupShape<n>::template smem_c<C>();
+        set_smem(k3g_rec<n, C>, C_SMEM);
         if (k2hi < 0) k2hi = S::H;
         int nbands = 0;
         for (int i = 0; i < g.count; ++i) nbands += g.len[i];
         LaunchScope ls(s, "f3g_rec", st, nbands);
         const CUtensorMap zmap = zmap_of(Z, g);
-        k3g_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, G_SMEM, st>>>(Z, nT, acc, s.synth, g, accumulate,
+        k3g_rec<n, C><<<dim3((k2hi - k2lo) * S::Q, 1), S::AC_THREADS, C_SMEM, st>>>(Z, nT, acc, s.synth, g, accumulate,
                                                                                    tw, zmap, k2lo * S::Q);
         check_launch("k3g_rec");
         }

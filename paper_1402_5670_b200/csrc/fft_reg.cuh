@@ -319,7 +319,9 @@ struct TwTable {
     __device__ __forceinline__ C get(int /*q*/, int idx) const { return twiddle<DIR>(tw, idx); }
 };
 
-template <int L, int DIR, int S, bool PAD, class C = double2, class PL = RegPlan<L>>
+// SWL: the length whose exchange swizzle the line buffer uses (0: the plain
+// XOR swizzle, L slots per line, for buffers sized exactly L)
+template <int L, int DIR, int S, bool PAD, class C = double2, class PL = RegPlan<L>, int SWL = L>
 struct RegStage {
     using P = PL;
     static constexpr int R = P::R[S];
@@ -359,7 +361,7 @@ struct RegStage {
                 const int jm = j % NS;
                 const int base = (j - jm) * R + jm;
 #pragma unroll
-                for (int r = 0; r < R; ++r) sm[swz<PAD, L, sizeof(C)>(base + r * NS)] = x[q + B * r];
+                for (int r = 0; r < R; ++r) sm[swz<PAD, SWL, sizeof(C)>(base + r * NS)] = x[q + B * r];
             }
             line_sync<T>();
             constexpr int R2 = P::R[S + 1];
@@ -368,10 +370,10 @@ struct RegStage {
             for (int q = 0; q < B2; ++q) {
                 const int j = t + T * q;
 #pragma unroll
-                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD, L, sizeof(C)>(j + r * (L / R2))];
+                for (int r = 0; r < R2; ++r) x[q + B2 * r] = sm[swz<PAD, SWL, sizeof(C)>(j + r * (L / R2))];
             }
             line_sync<T>();
-            RegStage<L, DIR, S + 1, PAD, C, PL>::run_w(x, sm, t, tws);
+            RegStage<L, DIR, S + 1, PAD, C, PL, SWL>::run_w(x, sm, t, tws);
         }
     }
 };
@@ -490,6 +492,11 @@ __device__ __forceinline__ void fft192_b(C (&x)[16], C* sm, int t, const C* __re
 template <int L, int DIR, bool PAD = true, class C>
 __device__ __forceinline__ void reg_fft(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
     RegStage<L, DIR, 0, PAD, C>::run(x, sm, t, tw);
+}
+// the same over an unpadded line buffer of exactly L slots (plain XOR swizzle)
+template <int L, int DIR, class C>
+__device__ __forceinline__ void reg_fft_xor(C (&x)[RegPlan<L>::E], C* sm, int t, const C* __restrict__ tw) {
+    RegStage<L, DIR, 0, false, C, RegPlan<L>, 0>::run(x, sm, t, tw);
 }
 // the same with an explicit plan (a kernel family may use another T / E split
 // of the same length; the first radix must match RegPlan<L>'s for the swizzle)
